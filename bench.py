@@ -1,0 +1,321 @@
+"""Rollout benchmark of the B200-native GRPO-rollout hot path (arXiv 2509.21792).
+
+Metric (BASELINE.json): rollout tokens/s, speedup vs AR decode, mean accept length tau.
+Workload (default, BASELINE configs[1] "c2"): Qwen2.5-1.5B-shaped target on the reference
+architecture (d=1536, L=28, H=12, d_ff=8960, V=151936) + 1-layer EAGLE-style draft,
+64 queries x group 8, 128-token synthetic prompts, 1024 new tokens, greedy, adaptive
+speculative decoding (Eqs. 1-3, alpha=2, K_max=10, L_max=6, C_peak=211). Random-init
+weights of that architecture drawn on the device (init_flat's distributions).
+
+One "step" = one full rollout (prefill + decode until every sequence finished).
+  value  = generated tokens / device time (CUDA events; prompts resident in HBM)
+  e2e    = generated tokens / wall time of the public C-ABI call sgb_rollout with host
+           prompts in and host tokens + features out (H2D/D2H inside the timed region)
+Multi-GPU (torchrun): data-parallel by query group, weak scaling -- every rank runs its own
+64x8 shard with global sequence ids; no collective on the data path; time = max over ranks.
+
+--impl reference times the reference's own CPU generate_dynamic_batch (oracle/_ref, the
+unmodified reference sources compiled here) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (V, d, L, H, dff, P, G, queries, max_new)
+    "c2": dict(V=151936, d=1536, L=28, H=12, dff=8960, P=128, G=8, Q=64, new=1024,
+               desc="Qwen2.5-1.5B-shaped target + 1-layer draft, 64 queries x group 8, 128-token prompts, "
+                    "1024 new tokens, greedy, adaptive spec (c_peak 211)"),
+    "c1": dict(V=512, d=256, L=2, H=4, dff=1024, P=32, G=4, Q=8, new=128,
+               desc="2-layer d=256 target + 1-layer draft, 8 queries x group 4, 32-token prompts, 128 new tokens"),
+}
+C_PEAK = 211  # analytic crossover s*F/(2*BW) at the measured sustained peaks
+
+
+def env_rank():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def model_cfg(w):
+    from oracle.oracle import ModelConfig  # plain config record (no oracle compute)
+    return ModelConfig(w["V"], w["d"], w["L"], w["H"], w["dff"], w["P"] + w["new"], 1)
+
+
+def make_prompts(w, rank):
+    """Uniform ids in [2, V) from a splitmix stream keyed by (run_seed=0, 0x9a01), SURVEY §8d;
+    rank r takes global queries [r*Q, (r+1)*Q)."""
+    from oracle.oracle import mix_key  # integer key derivation only
+    seed = mix_key(0, 0x9A01)
+    n = (rank + 1) * w["Q"] * w["P"]
+    with np.errstate(over="ignore"):
+        st = np.uint64(seed) + np.uint64(0x9E3779B97F4A7C15) * np.arange(2, n + 2, dtype=np.uint64)
+        z = (st ^ (st >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    toks = (z % np.uint64(w["V"] - 2) + np.uint64(2)).astype(np.int64)
+    toks = toks[rank * w["Q"] * w["P"]:].reshape(w["Q"], w["P"])
+    return [row.tolist() for row in toks]
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu, self.rows, self.proc = gpu, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) >= 9 for i in range(4)
+                          if r[5 + i].lower() in ("active", "0x1", "yes")})
+        loaded = [s for s in sm if s > 0.5 * (max(mx) if mx else 1)]
+        return {"sm_mhz": statistics.median(loaded or sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p["hbm_gbs"], p.get("bf16_tflops_sustained", p["bf16_tflops"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback"
+
+
+# ------------------------------------------------------------------------------ CPU legs
+def cpu_reference_sample(w, threads, new_tokens=8, prompt_len=16):
+    """The reference's own generate_dynamic_batch (oracle/_ref) on `threads` host threads,
+    one sequence per thread, at the full model shape (bounded sample). Returns dict."""
+    import ctypes as C
+    from oracle import refc as R
+    from oracle.oracle import ModelConfig
+    cfg = ModelConfig(w["V"], w["d"], w["L"], w["H"], w["dff"], w["P"] + w["new"], 1)
+    n = R.lib().sgref_param_count(C.byref(R.cfg_c(cfg)))
+    rng = np.random.default_rng(1)
+    flat = np.empty(n, np.float32)
+    for o in range(0, n, 1 << 26):
+        m = min(1 << 26, n - o)
+        flat[o:o + m] = rng.standard_normal(m, dtype=np.float32) * np.float32(0.02)
+    R.lib().sgref_model_new_weights.restype = C.c_void_p
+    h = R.lib().sgref_model_new_weights(C.byref(R.cfg_c(cfg)), flat.ctypes.data_as(C.POINTER(C.c_float)))
+    del flat
+    model = R.RefModel.__new__(R.RefModel)
+    model.cfg, model.h = cfg, h
+    draft = R.RefDraft(cfg, 1)
+    prompts = [p[:prompt_len] for p in make_prompts(w, 0)[:threads]]
+    return model, draft, prompts, dict(c_peak=C_PEAK, mode="vanilla", temperature=0.0, seed=7,
+                                       max_new_tokens=new_tokens)
+
+
+def run_cpu_sample(ctx, threads):
+    from oracle import refc as R
+    model, draft, prompts, kw = ctx
+    n, secs = R.generate_threaded(model, draft, prompts, 1, threads, **kw)
+    return n, secs
+
+
+def cpu_baseline(w, threads):
+    """rank 0, N=1 only: one bounded sample of the reference CPU path."""
+    from oracle import refc as R
+    if not R.available():
+        return {"value": None, "unit": "tokens/s", "cores": 0, "kind": "reference",
+                "sample": "oracle/_ref not built on this host"}
+    ctx = cpu_reference_sample(w, threads)
+    n, secs = run_cpu_sample(ctx, threads)
+    return {"value": n / secs, "unit": "tokens/s", "cores": threads, "kind": "reference",
+            "sample": f"{threads} sequences x (16-token prompt, 8 new tokens), vanilla greedy, full model shape, "
+                      f"{n} tokens in {secs:.1f}s (reference is single-threaded; one sequence per thread)"}
+
+
+def reference_arm(args, w):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return 0
+    from oracle import refc as R
+    threads = max(1, min(os.cpu_count() or 1, 64))
+    base = {"impl": "reference", "metric": "rollout tokens/s", "unit": "tokens/s", "n_gpus": args.gpus,
+            "higher_is_better": True, "scaling": "weak", "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{args.config}: {w['desc']}", "sample": "bounded CPU sample"}}
+    if not R.available():
+        base["unavailable"] = "oracle/_ref/libsgrpo_ref.so not built (needs /root/reference at build time)"
+        print(json.dumps(base))
+        return 0
+    ctx = cpu_reference_sample(w, threads)
+    for _ in range(args.warmup):
+        run_cpu_sample(ctx, threads)
+    tot_n, tot_s = 0, 0.0
+    for _ in range(args.steps):
+        n, s = run_cpu_sample(ctx, threads)
+        tot_n += n
+        tot_s += s
+    v = tot_n / tot_s
+    base.update(value=v, steps=args.steps, warmup=args.warmup, ms_per_step=1e3 * tot_s / args.steps,
+                vs_baseline=None,
+                cpu_baseline={"value": v, "unit": "tokens/s", "cores": threads, "kind": "reference",
+                              "sample": f"{threads} sequences x (16-token prompt, 8 new tokens) per step, vanilla "
+                                        f"greedy, full {args.config} shape, one sequence per host thread"},
+                e2e={"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0})
+    print(json.dumps(base))
+    return 0
+
+
+# ------------------------------------------------------------------------------ GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--mode", default="adaptive_spec", choices=["adaptive_spec", "vanilla"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-ar", action="store_true", help="skip the AR (vanilla) comparison rollout")
+    ap.add_argument("--max-new", type=int, default=0, help="override new tokens (profiling runs)")
+    args = ap.parse_args()
+    w = dict(WORKLOADS[args.config])
+    if args.max_new:
+        w["new"] = args.max_new
+    if args.impl == "reference":
+        return reference_arm(args, w)
+
+    rank, world, local = env_rank()
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2509_21792_b200 import capi
+    cfg = model_cfg(w)
+    n_seq = w["Q"] * w["G"]
+    eng = capi.Engine(cfg, 1, local, n_seq, max(2048, n_seq), 10, 6)
+    eng.init_random(1234)
+    prompts = make_prompts(w, rank)
+    gen = dict(c_peak=C_PEAK, alpha=2.0, k_max=10, l_max=6, temperature=0.0, seed=7, max_new_tokens=w["new"],
+               sid_offset=rank * n_seq)
+
+    def rollout(mode, prof=False):
+        t0 = time.perf_counter()
+        r = eng.generate(prompts, w["G"], mode=mode, want_features=True, **gen)
+        wall = time.perf_counter() - t0
+        return r, wall
+
+    for _ in range(args.warmup):
+        rollout(args.mode)
+    eng.read_profile(reset=True)
+    if dist:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    eng.profile(True)
+    dev_s, wall_s, toks, launches, acc, slots, h2d, d2h = 0.0, 0.0, 0, 0, 0, 0, 0, 0
+    spec_steps = 0
+    for _ in range(args.steps):
+        r, wall = rollout(args.mode)
+        dev_s += r.seconds
+        wall_s += wall
+        toks += r.generated()
+        launches += r.kernel_launches
+        acc += r.total_accepted
+        slots += r.total_verify_slots
+        h2d += r.h2d_bytes
+        d2h += r.d2h_bytes
+        spec_steps += sum(1 for s in r.steps if s[1] > 1)
+    eng.profile(False)
+    clk = clocks.stop()
+    prof = eng.read_profile(reset=True)
+    t_max, w_max, tok_all = dev_s, wall_s, toks
+    if dist:
+        import torch
+        t = torch.tensor([dev_s, wall_s], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        n = torch.tensor([toks], dtype=torch.float64)
+        dist.all_reduce(n, op=dist.ReduceOp.SUM)
+        t_max, w_max, tok_all = float(t[0]), float(t[1]), int(n[0])
+    ar = None
+    if not args.no_ar and args.mode != "vanilla":
+        if spec_steps == 0:
+            ar = {"value": tok_all / t_max, "unit": "tokens/s", "speedup": 1.0,
+                  "note": "every step had B_cur > C_peak, so Eqs. 1-3 planned N_verify=1 (AR) throughout"}
+        else:
+            r, _ = rollout("vanilla")
+            ar = {"value": r.generated() / r.seconds, "unit": "tokens/s"}
+            ar["speedup"] = (toks / dev_s) / ar["value"]
+    if rank != 0:
+        return 0
+    hbm, tf, src = measured_peaks()
+    att = prof["attention"]
+    ach = att["bytes"] / (att["ms"] * 1e-3) / 1e9 if att["ms"] else 0.0
+    total_ms = sum(v["ms"] for v in prof.values())
+    roofline = {"bound": "hbm", "kernel": "attn_split_kernel+attn_combine_kernel (tree/paged KV attention)",
+                "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s", "frac": round(ach / hbm, 4),
+                "traffic": None, "peak_source": src,
+                "share_of_step": round(att["ms"] / total_ms, 4) if total_ms else None,
+                "classes": {k: {"ms_per_step": round(v["ms"] / args.steps, 2),
+                                "GBps": round(v["bytes"] / (v["ms"] * 1e-3) / 1e9, 1) if v["ms"] else None,
+                                "TFLOPs": round(v["flops"] / (v["ms"] * 1e-3) / 1e12, 1) if v["ms"] else None,
+                                "launches": v["launches"]} for k, v in prof.items()}}
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(w, max(1, min(os.cpu_count() or 1, 64)))
+    line = {
+        "metric": "rollout tokens/s", "value": round(tok_all / t_max, 1), "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * t_max / args.steps, 1),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {w['desc']}", "mode": args.mode, "c_peak": C_PEAK,
+                   "sequences_per_gpu": n_seq, "new_tokens": w["new"], "prompt_len": w["P"],
+                   "l2": "inputs larger than L2 (KV cache ~100 GB per GPU at c2)",
+                   "parallelism": f"dp{world} (query groups)", "weights": "random init on device"},
+        "tau": round(acc / slots, 4) if slots else None, "spec_steps": spec_steps,
+        "speedup_vs_ar": ar["speedup"] if ar else None, "ar": ar,
+        "e2e": {"value": round(tok_all / w_max, 1), "unit": "tokens/s", "h2d_bytes_per_step": h2d // args.steps,
+                "d2h_bytes_per_step": d2h // args.steps},
+        "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk,
+    }
+    print(json.dumps(line))
+    eng.close()
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,140 @@
+/*
+ * sgrpo_b200.h -- C-ABI of the B200-native GRPO-rollout hot path (libsgrpo_b200.so).
+ *
+ * This is the drop-in boundary for the reference's C++ operator API (namespace sgrpo,
+ * /root/reference/proj). Every entry point below names the reference interface it
+ * replaces (file:line, relative to proj/). Arguments are plain pointers and sizes; host
+ * buffers in, host buffers out; no C++ or torch types cross the boundary.
+ *
+ * Errors: every function returns an int status (SGB_OK == 0). Non-zero codes map onto the
+ * exception types the reference throws:
+ *   SGB_EINVAL  1  std::invalid_argument   (empty input, bad token id, bad config, ...)
+ *   SGB_ERANGE  2  std::out_of_range       (position >= max_seq_len, cache capacity)
+ *   SGB_ERUNTIME 3 std::runtime_error      (non-finite logits, weights not uploaded)
+ *   SGB_EDOMAIN 4  std::domain_error       (NaN / all -inf logits in sampling)
+ *   SGB_ECUDA   5  CUDA failure -- there is NO CPU fallback
+ * sgb_last_error() returns the thread-local message of the last failure.
+ */
+#ifndef SGRPO_B200_H
+#define SGRPO_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SGB_ABI_VERSION 1
+
+/* ModelConfig (include/sgrpo/tinylm.hpp:16-37). */
+typedef struct sgb_model_config {
+    int vocab_size, d_model, n_layers, n_heads, d_ff, max_seq_len;
+    unsigned long long seed;
+} sgb_model_config;
+
+/* SchedParams + GenOptions (include/sgrpo/scheduler.hpp:34-58). */
+typedef struct sgb_gen_options {
+    double alpha;              /* Eq. 3 alpha (SchedParams.alpha)               */
+    int k_max, l_max, c_peak;  /* SchedParams                                    */
+    int mode;                  /* DecodeMode: 0 vanilla, 1 fixed_spec, 2 adaptive */
+    int early_term;            /* GenOptions.early_term                          */
+    double temperature;        /* GenOptions.temperature                         */
+    unsigned long long seed;   /* GenOptions.seed                                */
+    int max_new_tokens;        /* GenOptions.max_new_tokens (0: max_seq_len)     */
+    int fixed_n_verify, fixed_k_draft, fixed_l_draft; /* GenOptions.fixed        */
+    const int* seq_max_new;    /* optional per-sequence caps (c3 extension) or NULL */
+    int want_features;         /* copy SeqResult.features back                   */
+    int sid_offset;            /* global sid of this shard's first sequence (data-parallel ranks) */
+} sgb_gen_options;
+
+/* GenStats summary (scheduler.hpp:68-89) plus device measurements. */
+typedef struct sgb_rollout_stats {
+    long long total_accepted, total_verify_slots; /* tau = accepted / slots (scheduler.cpp:72-75) */
+    int n_steps;
+    long long target_forwards, draft_forwards, kernel_launches;
+    double seconds; /* device time of prefill + step loop, CUDA events (inputs resident) */
+    long long h2d_bytes, d2h_bytes; /* host<->device bytes moved by the call */
+} sgb_rollout_stats;
+
+typedef struct sgb_engine sgb_engine;
+
+const char* sgb_last_error(void);
+int sgb_version(void);
+int sgb_device_count(int* out);
+
+/* Engine: one per GPU. Owns bf16 weights, KV stores for max_seqs sequences of
+ * max_seq_len tokens, and activation buffers for max_rows rows per forward.
+ * k_max/l_max bound the speculation tree (SchedParams.k_max/l_max). */
+int sgb_engine_create(const sgb_model_config* cfg, int draft_layers, int device, int max_seqs, int max_rows,
+                      int k_max, int l_max, sgb_engine** out);
+int sgb_engine_destroy(sgb_engine* e);
+int sgb_param_counts(sgb_engine* e, size_t* target, size_t* draft);
+
+/* Weights in the reference's flat fp32 layout: init_model (tinylm.hpp:133-150) and
+ * init_draft (tinylm.hpp:172-189); also the SGRPOCK1 payload (src/tinylm.cpp:14-105). */
+int sgb_upload_target(sgb_engine* e, const float* flat, size_t n);
+int sgb_upload_draft(sgb_engine* e, const float* flat, size_t n);
+int sgb_download_draft(sgb_engine* e, float* flat, size_t n);
+/* Benchmark weights drawn on the device with init_flat's distributions (not bit-identical). */
+int sgb_init_random(sgb_engine* e, unsigned long long seed);
+
+/* ---- per-op parity entry points -------------------------------------------------- */
+/* KvCacheT reset / len / gather_tail (tinylm.hpp:232-269). slot = engine sequence slot. */
+int sgb_cache_reset(sgb_engine* e, int slot, int draft);
+int sgb_cache_len(sgb_engine* e, int slot, int draft, int* out);
+int sgb_cache_read(sgb_engine* e, int slot, int draft, float* k, float* v); /* [layers][len][d] */
+int sgb_cache_gather_tail(sgb_engine* e, int slot, int base, const int* keep, int n);
+
+/* forward_target<T> (tinylm.hpp:422-463): mask NULL = causal; rows are appended to the
+ * slot's cache. logits [rows][vocab], hidden [rows][d]. */
+int sgb_forward_target(sgb_engine* e, int slot, const int* tokens, const int* positions, int rows,
+                       const unsigned char* mask, float* logits, float* hidden);
+/* forward_draft_rows<T> (tinylm.hpp:502-563) with cache = the slot's draft cache. */
+int sgb_forward_draft_rows(sgb_engine* e, int slot, const int* tokens, const float* prev_features,
+                           const int* positions, int rows, int extend_cache, float* features, float* logits);
+/* sample_token<T> (tinylm.hpp:591-628) per row with key mix_key(seeds[i], key_pos[i])
+ * (the key verify derives, drafttree.cpp:184-190). */
+int sgb_sample_rows(sgb_engine* e, const float* logits, int rows, int vocab, double temperature,
+                    const unsigned long long* seeds, const int* key_pos, int* out);
+/* log_softmax_row<double> + topk_tokens (nn.hpp:172-180, drafttree.cpp:20-30). */
+int sgb_topk_logsoftmax(sgb_engine* e, const float* logits, int rows, int vocab, int k, int* tokens,
+                        double* log_probs);
+
+/* expand_tree_with + rerank_candidates + build_tree_mask (drafttree.cpp:34-168) on the
+ * device, with the draft logits of each expanded node supplied by a callback (the
+ * reference's ExpandFn, drafttree.hpp:33). Outputs: nodes (tok/par/dep/lp/conf, capacity
+ * cap), selected node ids [n_sel] and mask [n_sel][n_sel]. */
+typedef void (*sgb_logits_fn)(void* ctx, int n_front, const int* node_ids, const int* node_tok,
+                              const int* node_par, int n_nodes, float* logits_out);
+int sgb_build_tree(sgb_engine* e, int root_token, int k_draft, int l_draft, int n_verify, sgb_logits_fn fn,
+                   void* ctx, int cap, int* tok, int* par, int* dep, double* lp, double* conf, int* n_nodes,
+                   int* sel, int* n_sel, unsigned char* mask);
+
+/* ---- the hot path ------------------------------------------------------------------ */
+/* generate_dynamic_batch (include/sgrpo/scheduler.hpp:99-102, src/scheduler.cpp:236-354).
+ * prompts: concatenated token ids, prompt_lens[n_prompts]; g = group size.
+ * Outputs (sequence order = global sid = prompt_idx*g + r):
+ *   tokens [n_prompts*g][max_seq_len] (row i holds lens[i] tokens), lens, prompt_len, hit_eos,
+ *   features [n_prompts*g][max_seq_len-1][d] (optional, NULL to skip).
+ * Per-step GenStats records (b_cur, n_verify, k_draft, l_draft, accepted) go to
+ * step_rec[5*i..] for i < min(n_steps, step_cap). */
+int sgb_rollout(sgb_engine* e, const int* prompts, const int* prompt_lens, int n_prompts, int g,
+                const sgb_gen_options* opt, int* tokens, int* lens, int* prompt_len, int* hit_eos, float* features,
+                int* step_rec, int step_cap, sgb_rollout_stats* stats);
+
+/* Kernel-class profiler: CUDA events around every launch on the engine's stream.
+ * Classes: 0 GEMM (tcgen05), 1 attention, 2 row ops (LN/reduce/GELU/scatter), 3 LM head,
+ * 4 sampling, 5 tree/walk, 6 KV commit. Per class: device ms, algorithmic bytes/flops, launches. */
+int sgb_profile_enable(sgb_engine* e, int on);
+int sgb_profile_read(sgb_engine* e, int n_cls, double* ms, double* bytes, double* flops, long long* launches,
+                     int reset);
+
+/* tcgen05 GEMM self-test: out[M][N] = bf16(x)[M][K] . bf16(w)[N][K]^T (K-major). */
+int sgb_debug_gemm(const float* w, const float* x, int M, int N, int K, float* out, int* splits_out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SGRPO_B200_H */

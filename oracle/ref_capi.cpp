@@ -523,3 +523,27 @@ int sgref_save_draft_checkpoint(void* draft, const char* path) {
 }
 
 }  // extern "C"
+
+// Model with the reference's layout (tinylm.hpp:133-150) and caller-supplied weights,
+// skipping init_flat's sequential Box-Muller (33 s at the 1.5B shape); used only by the
+// CPU-baseline leg of bench.py, whose timing does not depend on weight values.
+extern "C" void* sgref_model_new_weights(const CfgC* c, const float* flat) {
+    Model* m = nullptr;
+    int rc = guarded([&] {
+        ModelConfig cfg = to_cfg(c);
+        cfg.validate();
+        m = new Model();
+        m->config = cfg;
+        detail::LayoutBuilder lb;
+        const int d = cfg.d_model;
+        m->tok_emb = lb.add("tok_emb", cfg.vocab_size, d, Init::normal);
+        m->pos_emb = lb.add("pos_emb", cfg.max_seq_len, d, Init::pos_emb);
+        for (int l = 0; l < cfg.n_layers; ++l) m->layers.push_back(lb.add_layer(d, cfg.d_ff));
+        m->lnf_g = lb.add("lnf_g", 1, d, Init::ones);
+        m->lnf_b = lb.add("lnf_b", 1, d, Init::zeros);
+        m->lm_head = lb.add("lm_head", d, cfg.vocab_size, Init::normal);
+        m->layout = lb.specs;
+        m->flat.assign(flat, flat + lb.total);
+    });
+    return rc == 0 ? m : nullptr;
+}

@@ -1,0 +1,313 @@
+"""ctypes binding of libsgrpo_b200.so (include/sgrpo_b200.h).
+
+Host-side mirror of the reference's operator API for the rollout path: the same
+names (forward_target, forward_draft_rows, sample_token, expand/rerank/verify,
+generate_dynamic_batch), argument meaning and error behaviour -- C-ABI status codes are
+re-raised as the Python equivalents of the reference's exception types:
+  invalid_argument -> ValueError, out_of_range -> IndexError,
+  runtime_error -> RuntimeError, domain_error -> ArithmeticError.
+There is no CPU fallback: if the shared library is missing this module raises at import.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libsgrpo_b200.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2509_21792_b200.build` "
+                      "(there is no CPU fallback)")
+
+_lib = C.CDLL(LIB_PATH)
+
+
+class ModelConfigC(C.Structure):
+    _fields_ = [("vocab_size", C.c_int), ("d_model", C.c_int), ("n_layers", C.c_int), ("n_heads", C.c_int),
+                ("d_ff", C.c_int), ("max_seq_len", C.c_int), ("seed", C.c_ulonglong)]
+
+
+class GenOptionsC(C.Structure):
+    _fields_ = [("alpha", C.c_double), ("k_max", C.c_int), ("l_max", C.c_int), ("c_peak", C.c_int),
+                ("mode", C.c_int), ("early_term", C.c_int), ("temperature", C.c_double), ("seed", C.c_ulonglong),
+                ("max_new_tokens", C.c_int), ("fixed_n_verify", C.c_int), ("fixed_k_draft", C.c_int),
+                ("fixed_l_draft", C.c_int), ("seq_max_new", C.POINTER(C.c_int)), ("want_features", C.c_int),
+                ("sid_offset", C.c_int)]
+
+
+class RolloutStatsC(C.Structure):
+    _fields_ = [("total_accepted", C.c_longlong), ("total_verify_slots", C.c_longlong), ("n_steps", C.c_int),
+                ("target_forwards", C.c_longlong), ("draft_forwards", C.c_longlong),
+                ("kernel_launches", C.c_longlong), ("seconds", C.c_double), ("h2d_bytes", C.c_longlong),
+                ("d2h_bytes", C.c_longlong)]
+
+
+LOGITS_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int),
+                        C.c_int, C.POINTER(C.c_float))
+
+_lib.sgb_last_error.restype = C.c_char_p
+_lib.sgb_engine_create.argtypes = [C.POINTER(ModelConfigC), C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                   C.POINTER(C.c_void_p)]
+_lib.sgb_engine_destroy.argtypes = [C.c_void_p]
+
+EXPORTED = ["sgb_last_error", "sgb_version", "sgb_device_count", "sgb_engine_create", "sgb_engine_destroy",
+            "sgb_param_counts", "sgb_upload_target", "sgb_upload_draft", "sgb_download_draft", "sgb_init_random",
+            "sgb_cache_reset", "sgb_cache_len", "sgb_cache_read", "sgb_cache_gather_tail", "sgb_forward_target",
+            "sgb_forward_draft_rows", "sgb_sample_rows", "sgb_topk_logsoftmax", "sgb_build_tree", "sgb_rollout",
+            "sgb_debug_gemm", "sgb_profile_enable", "sgb_profile_read"]
+
+KERNEL_CLASSES = ["gemm_tcgen05", "attention", "rowops", "lm_head", "sample", "tree", "kv_commit"]
+
+_EXC = {1: ValueError, 2: IndexError, 3: RuntimeError, 4: ArithmeticError, 5: RuntimeError}
+
+
+def _check(rc: int):
+    if rc != 0:
+        raise _EXC.get(rc, RuntimeError)(_lib.sgb_last_error().decode())
+
+
+def _p(a, ct):
+    return None if a is None else a.ctypes.data_as(C.POINTER(ct))
+
+
+def lib():
+    return _lib
+
+
+def device_count() -> int:
+    n = C.c_int()
+    _check(_lib.sgb_device_count(C.byref(n)))
+    return n.value
+
+
+def debug_gemm(w: np.ndarray, x: np.ndarray):
+    """out = bf16(x) @ bf16(w).T via the tcgen05 GEMM; returns (out, splits)."""
+    w = np.ascontiguousarray(w, np.float32)
+    x = np.ascontiguousarray(x, np.float32)
+    N, K = w.shape
+    M = x.shape[0]
+    out = np.zeros((M, N), np.float32)
+    sp = C.c_int()
+    _check(_lib.sgb_debug_gemm(_p(w, C.c_float), _p(x, C.c_float), M, N, K, _p(out, C.c_float), C.byref(sp)))
+    return out, sp.value
+
+
+MODES = {"vanilla": 0, "fixed_spec": 1, "adaptive_spec": 2}
+
+
+@dataclass
+class Rollout:
+    """BatchState (scheduler.hpp:91-94) + measurements."""
+    tokens: List[List[int]]
+    prompt_len: List[int]
+    hit_eos: List[bool]
+    features: Optional[List[np.ndarray]]
+    steps: List[tuple]  # (b_cur, n_verify, k_draft, l_draft, accepted)
+    total_accepted: int
+    total_verify_slots: int
+    target_forwards: int
+    draft_forwards: int
+    kernel_launches: int
+    seconds: float
+    h2d_bytes: int = 0
+    d2h_bytes: int = 0
+
+    def tau(self) -> float:
+        if self.total_verify_slots == 0:
+            raise ArithmeticError("tau: no verification steps logged")
+        return self.total_accepted / self.total_verify_slots
+
+    def generated(self) -> int:
+        return sum(len(t) - p for t, p in zip(self.tokens, self.prompt_len))
+
+
+class Engine:
+    """One GPU's rollout engine (sgb_engine)."""
+
+    def __init__(self, cfg, draft_layers: int = 1, device: int = 0, max_seqs: int = 64, max_rows: int = 512,
+                 k_max: int = 10, l_max: int = 6):
+        self.cfg = cfg
+        c = ModelConfigC(cfg.vocab_size, cfg.d_model, cfg.n_layers, cfg.n_heads, cfg.d_ff, cfg.max_seq_len,
+                         getattr(cfg, "seed", 0))
+        h = C.c_void_p()
+        _check(_lib.sgb_engine_create(C.byref(c), draft_layers, device, max_seqs, max_rows, k_max, l_max,
+                                      C.byref(h)))
+        self.h = h
+        t, d = C.c_size_t(), C.c_size_t()
+        _check(_lib.sgb_param_counts(self.h, C.byref(t), C.byref(d)))
+        self.n_target, self.n_draft = t.value, d.value
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.sgb_engine_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- weights
+    def upload_target(self, flat):
+        f = np.ascontiguousarray(flat, np.float32)
+        _check(_lib.sgb_upload_target(self.h, _p(f, C.c_float), C.c_size_t(f.size)))
+
+    def upload_draft(self, flat):
+        f = np.ascontiguousarray(flat, np.float32)
+        _check(_lib.sgb_upload_draft(self.h, _p(f, C.c_float), C.c_size_t(f.size)))
+
+    def download_draft(self) -> np.ndarray:
+        out = np.zeros(self.n_draft, np.float32)
+        _check(_lib.sgb_download_draft(self.h, _p(out, C.c_float), C.c_size_t(out.size)))
+        return out
+
+    def init_random(self, seed: int):
+        _check(_lib.sgb_init_random(self.h, C.c_ulonglong(seed)))
+
+    # ---- per-op parity entry points
+    def cache_reset(self, slot: int, draft: bool = False):
+        _check(_lib.sgb_cache_reset(self.h, slot, int(draft)))
+
+    def cache_len(self, slot: int, draft: bool = False) -> int:
+        n = C.c_int()
+        _check(_lib.sgb_cache_len(self.h, slot, int(draft), C.byref(n)))
+        return n.value
+
+    def cache_read(self, slot: int, draft: bool = False):
+        n = self.cache_len(slot, draft)
+        L = self.cfg.n_layers if not draft else self.draft_layers
+        k = np.zeros((L, n, self.cfg.d_model), np.float32)
+        v = np.zeros_like(k)
+        _check(_lib.sgb_cache_read(self.h, slot, int(draft), _p(k, C.c_float), _p(v, C.c_float)))
+        return k, v
+
+    draft_layers = 1
+
+    def cache_gather_tail(self, slot: int, base: int, keep: Sequence[int]):
+        kp = np.ascontiguousarray(keep, np.int32)
+        _check(_lib.sgb_cache_gather_tail(self.h, slot, base, _p(kp, C.c_int), kp.size))
+
+    def forward_target(self, slot: int, tokens, positions, mask=None):
+        t = np.ascontiguousarray(tokens, np.int32)
+        p = np.ascontiguousarray(positions, np.int32)
+        n = t.size
+        m = None if mask is None else np.ascontiguousarray(mask, np.uint8).reshape(-1)
+        logits = np.zeros((n, self.cfg.vocab_size), np.float32)
+        hidden = np.zeros((n, self.cfg.d_model), np.float32)
+        _check(_lib.sgb_forward_target(self.h, slot, _p(t, C.c_int), _p(p, C.c_int), n, _p(m, C.c_ubyte),
+                                       _p(logits, C.c_float), _p(hidden, C.c_float)))
+        return logits, hidden
+
+    def forward_draft_rows(self, slot: int, tokens, prev_features, positions, extend_cache=True):
+        t = np.ascontiguousarray(tokens, np.int32)
+        p = np.ascontiguousarray(positions, np.int32)
+        f = np.ascontiguousarray(prev_features, np.float32)
+        n = t.size
+        feats = np.zeros((n, self.cfg.d_model), np.float32)
+        logits = np.zeros((n, self.cfg.vocab_size), np.float32)
+        _check(_lib.sgb_forward_draft_rows(self.h, slot, _p(t, C.c_int), _p(f, C.c_float), _p(p, C.c_int), n,
+                                           int(extend_cache), _p(feats, C.c_float), _p(logits, C.c_float)))
+        return feats, logits
+
+    def sample_rows(self, logits, temperature: float, seeds, key_pos):
+        lg = np.ascontiguousarray(logits, np.float32)
+        rows, V = lg.shape
+        s = np.ascontiguousarray(seeds, np.uint64)
+        kp = np.ascontiguousarray(key_pos, np.int32)
+        out = np.zeros(rows, np.int32)
+        _check(_lib.sgb_sample_rows(self.h, _p(lg, C.c_float), rows, V, C.c_double(temperature),
+                                    _p(s, C.c_ulonglong), _p(kp, C.c_int), _p(out, C.c_int)))
+        return out
+
+    def topk_logsoftmax(self, logits, k: int):
+        lg = np.ascontiguousarray(logits, np.float32)
+        rows, V = lg.shape
+        kk = min(k, V)
+        tok = np.zeros((rows, kk), np.int32)
+        lp = np.zeros((rows, kk), np.float64)
+        _check(_lib.sgb_topk_logsoftmax(self.h, _p(lg, C.c_float), rows, V, k, _p(tok, C.c_int),
+                                        _p(lp, C.c_double)))
+        return tok, lp
+
+    def build_tree(self, root_token: int, k: int, l: int, n_verify: int, logits_fn, cap: int = 1024):
+        """logits_fn(node_ids, node_tok, node_par) -> [len(node_ids)][V] draft logits."""
+        V = self.cfg.vocab_size
+
+        def cb(ctx, n_front, ids, tok, par, n_nodes, out):
+            nid = [ids[i] for i in range(n_front)]
+            tk = [tok[i] for i in range(n_nodes)]
+            pr = [par[i] for i in range(n_nodes)]
+            lg = np.ascontiguousarray(logits_fn(nid, tk, pr), np.float32).reshape(-1)
+            C.memmove(out, lg.ctypes.data, lg.nbytes)
+
+        cbf = LOGITS_FN(cb)
+        tok = np.zeros(cap, np.int32)
+        par = np.zeros(cap, np.int32)
+        dep = np.zeros(cap, np.int32)
+        lp = np.zeros(cap, np.float64)
+        conf = np.zeros(cap, np.float64)
+        sel = np.zeros(cap, np.int32)
+        mask = np.zeros(cap * cap, np.uint8)
+        nn, ns = C.c_int(), C.c_int()
+        _check(_lib.sgb_build_tree(self.h, root_token, k, l, n_verify, cbf, None, cap, _p(tok, C.c_int),
+                                   _p(par, C.c_int), _p(dep, C.c_int), _p(lp, C.c_double), _p(conf, C.c_double),
+                                   C.byref(nn), _p(sel, C.c_int), C.byref(ns), _p(mask, C.c_ubyte)))
+        n, s = nn.value, ns.value
+        return dict(tok=tok[:n], par=par[:n], dep=dep[:n], lp=lp[:n], conf=conf[:n], sel=sel[:s],
+                    mask=mask[:s * s].reshape(s, s))
+
+    # ---- the hot path: generate_dynamic_batch
+    def generate(self, prompts: Sequence[Sequence[int]], g: int, c_peak: int, alpha: float = 2.0,
+                 k_max: int = 10, l_max: int = 6, mode: str = "vanilla", early_term: bool = True,
+                 temperature: float = 0.0, seed: int = 0, max_new_tokens: int = 0, fixed=(1, 0, 0),
+                 seq_max_new: Optional[Sequence[int]] = None, want_features: bool = True,
+                 max_steps_record: int = 1 << 16, sid_offset: int = 0) -> Rollout:
+        T, d = self.cfg.max_seq_len, self.cfg.d_model
+        n_p = len(prompts)
+        ns = n_p * g
+        plens = np.array([len(p) for p in prompts], np.int32)
+        flat = np.ascontiguousarray(np.concatenate([np.asarray(p, np.int32) for p in prompts])
+                                    if n_p else np.zeros(0, np.int32), np.int32)
+        smn = None if seq_max_new is None else np.ascontiguousarray(seq_max_new, np.int32)
+        opt = GenOptionsC(alpha, k_max, l_max, c_peak, MODES[mode], int(early_term), temperature, seed,
+                          max_new_tokens, fixed[0], fixed[1], fixed[2], _p(smn, C.c_int), int(want_features),
+                          sid_offset)
+        toks = np.zeros((max(ns, 1), T), np.int32)
+        lens = np.zeros(max(ns, 1), np.int32)
+        pl = np.zeros(max(ns, 1), np.int32)
+        eos = np.zeros(max(ns, 1), np.int32)
+        feats = np.zeros((max(ns, 1), T - 1, d), np.float32) if want_features else None
+        rec = np.zeros(5 * max_steps_record, np.int32)
+        st = RolloutStatsC()
+        _check(_lib.sgb_rollout(self.h, _p(flat, C.c_int), _p(plens, C.c_int), n_p, g, C.byref(opt),
+                                _p(toks, C.c_int), _p(lens, C.c_int), _p(pl, C.c_int), _p(eos, C.c_int),
+                                _p(feats, C.c_float), _p(rec, C.c_int), max_steps_record, C.byref(st)))
+        nst = min(st.n_steps, max_steps_record)
+        return Rollout(
+            tokens=[toks[i, :lens[i]].tolist() for i in range(ns)], prompt_len=pl[:ns].tolist(),
+            hit_eos=[bool(x) for x in eos[:ns]],
+            features=[feats[i, :lens[i] - 1] for i in range(ns)] if want_features else None,
+            steps=[tuple(int(x) for x in rec[5 * i:5 * i + 5]) for i in range(nst)],
+            total_accepted=st.total_accepted, total_verify_slots=st.total_verify_slots,
+            target_forwards=st.target_forwards, draft_forwards=st.draft_forwards,
+            kernel_launches=st.kernel_launches, seconds=st.seconds, h2d_bytes=st.h2d_bytes,
+            d2h_bytes=st.d2h_bytes)
+
+    # ---- kernel-class profiler
+    def profile(self, on: bool = True):
+        _check(_lib.sgb_profile_enable(self.h, int(on)))
+
+    def read_profile(self, reset: bool = True) -> dict:
+        n = len(KERNEL_CLASSES)
+        ms, by, fl = np.zeros(n), np.zeros(n), np.zeros(n)
+        la = np.zeros(n, np.int64)
+        _check(_lib.sgb_profile_read(self.h, n, _p(ms, C.c_double), _p(by, C.c_double), _p(fl, C.c_double),
+                                     _p(la, C.c_longlong), int(reset)))
+        return {k: dict(ms=float(ms[i]), bytes=float(by[i]), flops=float(fl[i]), launches=int(la[i]))
+                for i, k in enumerate(KERNEL_CLASSES)}

@@ -1,0 +1,283 @@
+// The drop-in boundary: extern "C" entry points declared in include/sgrpo_b200.h.
+// Each translates exceptions to the status codes of util.h and records a thread-local
+// message (sgb_last_error), mirroring the reference's exception types
+// (SURVEY.md §8b). There is no CPU fallback: every compute entry point runs CUDA.
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/sgrpo_b200.h"
+#include "engine.h"
+#include "gemm.h"
+#include "util.h"
+
+struct sgb_engine {
+    std::unique_ptr<sgb::Engine> eng;
+};
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return sgb::SGB_OK;
+    } catch (const sgb::CudaError& e) {
+        g_err = e.what();
+        return sgb::SGB_ECUDA;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return sgb::SGB_EINVAL;
+    } catch (const std::out_of_range& e) {
+        g_err = e.what();
+        return sgb::SGB_ERANGE;
+    } catch (const std::domain_error& e) {
+        g_err = e.what();
+        return sgb::SGB_EDOMAIN;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return sgb::SGB_ERUNTIME;
+    }
+}
+
+sgb::Engine& E(sgb_engine* e) {
+    if (!e || !e->eng) throw std::invalid_argument("null engine");
+    return *e->eng;
+}
+}  // namespace
+
+extern "C" {
+
+const char* sgb_last_error(void) { return g_err.c_str(); }
+
+int sgb_version(void) { return SGB_ABI_VERSION; }
+
+int sgb_device_count(int* out) {
+    return guarded([&] { SGB_CUDA(cudaGetDeviceCount(out)); });
+}
+
+int sgb_engine_create(const sgb_model_config* c, int draft_layers, int device, int max_seqs, int max_rows, int k_max,
+                      int l_max, sgb_engine** out) {
+    return guarded([&] {
+        if (!c || !out) throw std::invalid_argument("null argument");
+        sgb::ModelDims d;
+        d.vocab = c->vocab_size;
+        d.d = c->d_model;
+        d.layers = c->n_layers;
+        d.heads = c->n_heads;
+        d.dff = c->d_ff;
+        d.max_seq = c->max_seq_len;
+        auto* h = new sgb_engine;
+        try {
+            h->eng = std::make_unique<sgb::Engine>(d, draft_layers, device, max_seqs, max_rows, k_max, l_max);
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
+int sgb_engine_destroy(sgb_engine* e) {
+    return guarded([&] { delete e; });
+}
+
+int sgb_param_counts(sgb_engine* e, size_t* target, size_t* draft) {
+    return guarded([&] {
+        *target = E(e).target_param_count();
+        *draft = E(e).draft_param_count();
+    });
+}
+
+int sgb_upload_target(sgb_engine* e, const float* flat, size_t n) {
+    return guarded([&] { E(e).upload_target(flat, n); });
+}
+int sgb_upload_draft(sgb_engine* e, const float* flat, size_t n) {
+    return guarded([&] { E(e).upload_draft(flat, n); });
+}
+int sgb_download_draft(sgb_engine* e, float* flat, size_t n) {
+    return guarded([&] { E(e).download_draft(flat, n); });
+}
+int sgb_init_random(sgb_engine* e, unsigned long long seed) {
+    return guarded([&] { E(e).init_random(seed); });
+}
+
+int sgb_cache_reset(sgb_engine* e, int slot, int draft) {
+    return guarded([&] { E(e).cache_reset(slot, draft != 0); });
+}
+int sgb_cache_len(sgb_engine* e, int slot, int draft, int* out) {
+    return guarded([&] { *out = E(e).cache_len(slot, draft != 0); });
+}
+int sgb_cache_read(sgb_engine* e, int slot, int draft, float* k, float* v) {
+    return guarded([&] { E(e).cache_read(slot, draft != 0, k, v); });
+}
+int sgb_cache_gather_tail(sgb_engine* e, int slot, int base, const int* keep, int n) {
+    return guarded([&] { E(e).cache_gather_tail(slot, base, keep, n); });
+}
+
+int sgb_forward_target(sgb_engine* e, int slot, const int* tokens, const int* positions, int rows,
+                       const unsigned char* mask, float* logits, float* hidden) {
+    return guarded([&] { E(e).forward_target(slot, tokens, positions, rows, mask, logits, hidden); });
+}
+
+int sgb_forward_draft_rows(sgb_engine* e, int slot, const int* tokens, const float* prev_features,
+                           const int* positions, int rows, int extend_cache, float* features, float* logits) {
+    return guarded(
+        [&] { E(e).forward_draft(slot, tokens, prev_features, positions, rows, extend_cache != 0, features, logits); });
+}
+
+int sgb_sample_rows(sgb_engine* e, const float* logits, int rows, int vocab, double temperature,
+                    const unsigned long long* seeds, const int* key_pos, int* out) {
+    return guarded([&] { E(e).emit(logits, rows, vocab, temperature, seeds, key_pos, out); });
+}
+
+int sgb_topk_logsoftmax(sgb_engine* e, const float* logits, int rows, int vocab, int k, int* tokens,
+                        double* log_probs) {
+    return guarded([&] { E(e).topk_logsoftmax(logits, rows, vocab, k, tokens, log_probs); });
+}
+
+int sgb_build_tree(sgb_engine* e, int root_token, int k_draft, int l_draft, int n_verify, sgb_logits_fn fn,
+                   void* ctx, int cap, int* tok, int* par, int* dep, double* lp, double* conf, int* n_nodes, int* sel,
+                   int* n_sel, unsigned char* mask) {
+    return guarded([&] {
+        auto t = E(e).debug_tree_cb(root_token, k_draft, l_draft, n_verify, fn, ctx);
+        const int n = static_cast<int>(t.tok.size());
+        if (n > cap) throw std::invalid_argument("build_tree: capacity");
+        std::copy(t.tok.begin(), t.tok.end(), tok);
+        std::copy(t.par.begin(), t.par.end(), par);
+        std::copy(t.dep.begin(), t.dep.end(), dep);
+        std::copy(t.lp.begin(), t.lp.end(), lp);
+        std::copy(t.conf.begin(), t.conf.end(), conf);
+        std::copy(t.sel.begin(), t.sel.end(), sel);
+        if (mask) std::copy(t.mask.begin(), t.mask.end(), mask);
+        *n_nodes = n;
+        *n_sel = static_cast<int>(t.sel.size());
+    });
+}
+
+int sgb_rollout(sgb_engine* e, const int* prompts, const int* prompt_lens, int n_prompts, int g,
+                const sgb_gen_options* opt, int* tokens, int* lens, int* prompt_len, int* hit_eos, float* features,
+                int* step_rec, int step_cap, sgb_rollout_stats* stats) {
+    return guarded([&] {
+        sgb::Engine& en = E(e);
+        if (!opt) throw std::invalid_argument("null options");
+        if (n_prompts < 0) throw std::invalid_argument("generate: negative prompt count");
+        sgb::RolloutArgs a;
+        size_t off = 0;
+        for (int i = 0; i < n_prompts; ++i) {
+            if (prompt_lens[i] < 0) throw std::invalid_argument("generate: negative prompt length");
+            a.prompts.emplace_back(prompts + off, prompts + off + prompt_lens[i]);
+            off += prompt_lens[i];
+        }
+        a.g = g;
+        a.alpha = opt->alpha;
+        a.k_max = opt->k_max;
+        a.l_max = opt->l_max;
+        a.c_peak = opt->c_peak;
+        a.mode = opt->mode;
+        if (a.mode < 0 || a.mode > 2) throw std::invalid_argument("unknown decode mode");
+        a.early_term = opt->early_term != 0;
+        a.temperature = opt->temperature;
+        a.seed = opt->seed;
+        a.max_new_tokens = opt->max_new_tokens;
+        a.fixed = sgb::SpecCfg{opt->fixed_n_verify, opt->fixed_k_draft, opt->fixed_l_draft};
+        if (opt->seq_max_new) a.seq_max_new.assign(opt->seq_max_new, opt->seq_max_new + n_prompts * g);
+        a.want_features = features != nullptr && opt->want_features;
+        a.sid_offset = opt->sid_offset;
+        sgb::RolloutResult r = en.rollout(a);
+        const int T = en.dims().max_seq, d = en.dims().d;
+        const int ns = static_cast<int>(r.tokens.size());
+        for (int s = 0; s < ns; ++s) {
+            if (tokens) std::copy(r.tokens[s].begin(), r.tokens[s].end(), tokens + static_cast<size_t>(s) * T);
+            if (lens) lens[s] = static_cast<int>(r.tokens[s].size());
+            if (prompt_len) prompt_len[s] = r.prompt_len[s];
+            if (hit_eos) hit_eos[s] = r.hit_eos[s];
+            if (features && a.want_features)
+                std::copy(r.features[s].begin(), r.features[s].end(),
+                          features + static_cast<size_t>(s) * (T - 1) * d);
+        }
+        if (step_rec) {
+            const int n = std::min(step_cap, static_cast<int>(r.steps.size()));
+            for (int i = 0; i < n; ++i) {
+                step_rec[5 * i] = r.steps[i].b_cur;
+                step_rec[5 * i + 1] = r.steps[i].n_verify;
+                step_rec[5 * i + 2] = r.steps[i].k_draft;
+                step_rec[5 * i + 3] = r.steps[i].l_draft;
+                step_rec[5 * i + 4] = r.steps[i].accepted;
+            }
+        }
+        if (stats) {
+            stats->total_accepted = r.total_accepted;
+            stats->total_verify_slots = r.total_verify_slots;
+            stats->n_steps = static_cast<int>(r.steps.size());
+            stats->target_forwards = r.target_forwards;
+            stats->draft_forwards = r.draft_forwards;
+            stats->kernel_launches = r.kernel_launches;
+            stats->seconds = r.seconds;
+            stats->h2d_bytes = r.h2d_bytes;
+            stats->d2h_bytes = r.d2h_bytes;
+        }
+    });
+}
+
+int sgb_profile_enable(sgb_engine* e, int on) {
+    return guarded([&] { E(e).set_profiling(on != 0); });
+}
+
+int sgb_profile_read(sgb_engine* e, int n_cls, double* ms, double* bytes, double* flops, long long* launches,
+                     int reset) {
+    return guarded([&] {
+        sgb::KernelProfile kp[sgb::kNumCls];
+        E(e).read_profile(kp, sgb::kNumCls, reset != 0);
+        for (int i = 0; i < n_cls && i < sgb::kNumCls; ++i) {
+            if (ms) ms[i] = kp[i].ms;
+            if (bytes) bytes[i] = kp[i].bytes;
+            if (flops) flops[i] = kp[i].flops;
+            if (launches) launches[i] = kp[i].launches;
+        }
+    });
+}
+
+int sgb_debug_gemm(const float* w, const float* x, int M, int N, int K, float* out, int* splits_out) {
+    return guarded([&] {
+        if (M <= 0 || N <= 0 || K <= 0) throw std::invalid_argument("debug_gemm: bad shape");
+        std::vector<__nv_bfloat16> wb(static_cast<size_t>(N) * K), xb(static_cast<size_t>(M) * K);
+        for (size_t i = 0; i < wb.size(); ++i) wb[i] = __float2bfloat16(w[i]);
+        for (size_t i = 0; i < xb.size(); ++i) xb[i] = __float2bfloat16(x[i]);
+        __nv_bfloat16 *dw = nullptr, *dx = nullptr;
+        float* dp = nullptr;
+        const int cap = ((M + 255) / 256) * 256;
+        SGB_CUDA(cudaMalloc(&dw, wb.size() * 2));
+        SGB_CUDA(cudaMalloc(&dx, static_cast<size_t>(cap) * K * 2));
+        SGB_CUDA(cudaMemset(dx, 0, static_cast<size_t>(cap) * K * 2));
+        SGB_CUDA(cudaMemcpy(dw, wb.data(), wb.size() * 2, cudaMemcpyHostToDevice));
+        SGB_CUDA(cudaMemcpy(dx, xb.data(), xb.size() * 2, cudaMemcpyHostToDevice));
+        sgb::GemmWeight gw;
+        gw.init(dw, N, K);
+        sgb::GemmAct ga;
+        ga.init(dx, cap, K);
+        const size_t np = static_cast<size_t>(gw.splits) * M * N;
+        SGB_CUDA(cudaMalloc(&dp, np * 4));
+        sgb::gemm_launch(gw, ga, dp, M, 0);
+        SGB_KCHECK();
+        SGB_CUDA(cudaDeviceSynchronize());
+        std::vector<float> part(np);
+        SGB_CUDA(cudaMemcpy(part.data(), dp, np * 4, cudaMemcpyDeviceToHost));
+        for (size_t i = 0; i < static_cast<size_t>(M) * N; ++i) {
+            float s = part[i];
+            for (int k = 1; k < gw.splits; ++k) s += part[static_cast<size_t>(k) * M * N + i];
+            out[i] = s;
+        }
+        if (splits_out) *splits_out = gw.splits;
+        cudaFree(dw);
+        cudaFree(dx);
+        cudaFree(dp);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,1262 @@
+// Engine: device weights, KV stores, batched forward passes and the rollout step loop.
+//
+// The rollout is generate_dynamic_batch (src/scheduler.cpp:236-354) restated for a GPU:
+// the reference runs one forward per *sequence* per step (scheduler.cpp:322-328); here one
+// step is ONE batched target forward over the flattened trees of all live sequences, plus
+// one batched draft catch-up forward and (L-1) batched draft-level forwards. All tree
+// decisions run in device kernels (tree.cu); the host only plans the step (Eqs. 1-3,
+// scheduler.cpp:14-54 -- pure integer work that needs the live count B_cur) and reads back
+// one small per-sequence result vector per step.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <stdexcept>
+#include <string>
+
+#include "common.cuh"
+#include "engine.h"
+#include "util.h"
+
+namespace sgb {
+
+namespace {
+
+
+template <class T>
+T* dalloc(size_t n) {
+    T* p = nullptr;
+    if (n == 0) n = 1;
+    SGB_CUDA(cudaMalloc(&p, n * sizeof(T)));
+    return p;
+}
+
+template <class T>
+void h2d(T* dst, const T* src, size_t n, cudaStream_t st) {
+    if (n) SGB_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(T), cudaMemcpyHostToDevice, st));
+}
+template <class T>
+void d2h(T* dst, const T* src, size_t n, cudaStream_t st) {
+    if (n) SGB_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(T), cudaMemcpyDeviceToHost, st));
+}
+
+int tree_cap(int k, int l) { return 1 + k + std::max(0, l - 1) * k * k; }  // drafttree.cpp:11-15
+
+// Eqs. 1-3 (scheduler.cpp:26-54).
+SpecCfg plan(int c_peak, int b, double alpha, int k_max, int l_max) {
+    if (c_peak < 1 || b < 1) throw std::invalid_argument("compute_n_verify: c_peak, b >= 1");
+    if (alpha <= 0) throw std::invalid_argument("compute_l_draft: alpha must be positive");
+    SpecCfg c;
+    c.n_verify = std::max(1, c_peak / b);
+    c.k_draft = std::max(0, std::min(c.n_verify - 1, k_max));
+    if (c.k_draft == 0) {
+        c.l_draft = 0;
+    } else {
+        const int raw = static_cast<int>(std::floor(std::log2(static_cast<double>(c.n_verify) / alpha)));
+        c.l_draft = std::max(1, std::min(raw, l_max));
+    }
+    if (c.l_draft > l_max) throw std::invalid_argument("spec config: l_draft exceeds l_max");
+    return c;
+}
+
+void validate_spec(const SpecCfg& c, double alpha, int k_max, int l_max, int c_peak) {  // scheduler.cpp:14-24
+    if (c.n_verify < 1) throw std::invalid_argument("spec config: n_verify must be >= 1");
+    if (c.k_draft < 0 || c.l_draft < 0) throw std::invalid_argument("spec config: k_draft/l_draft must be >= 0");
+    if (c.k_draft > std::max(0, c.n_verify - 1))
+        throw std::invalid_argument("spec config: k_draft must be <= n_verify - 1");
+    if (c.k_draft > k_max) throw std::invalid_argument("spec config: k_draft exceeds k_max");
+    if (c.l_draft > l_max) throw std::invalid_argument("spec config: l_draft exceeds l_max");
+    if (alpha <= 0) throw std::invalid_argument("spec config: alpha must be positive");
+    if (c_peak < 1) throw std::invalid_argument("spec config: c_peak must be >= 1");
+}
+
+uint64_t splitmix_host(uint64_t& s) {
+    uint64_t z = (s += 0x9e3779b97f4a7c15ULL);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+uint64_t mix_key_host(uint64_t a, uint64_t b) {  // rng.hpp:17-20
+    uint64_t s = a ^ (b + 0x9e3779b97f4a7c15ULL + (a << 6) + (a >> 2));
+    return splitmix_host(s);
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ layouts
+FlatLayout FlatLayout::target(const ModelDims& m) {
+    FlatLayout f;
+    size_t o = 0;
+    const size_t d = m.d;
+    auto add = [&](size_t n) {
+        size_t r = o;
+        o += n;
+        return r;
+    };
+    f.tok_emb = add(static_cast<size_t>(m.vocab) * d);
+    f.pos_emb = add(static_cast<size_t>(m.max_seq) * d);
+    for (int l = 0; l < m.layers; ++l) {
+        L x;
+        x.ln1_g = add(d);
+        x.ln1_b = add(d);
+        x.wq = add(d * d);
+        x.wk = add(d * d);
+        x.wv = add(d * d);
+        x.wo = add(d * d);
+        x.ln2_g = add(d);
+        x.ln2_b = add(d);
+        x.w1 = add(d * m.dff);
+        x.w2 = add(d * m.dff);
+        f.layers.push_back(x);
+    }
+    f.lnf_g = add(d);
+    f.lnf_b = add(d);
+    f.lm_head = add(d * m.vocab);
+    f.total = o;
+    return f;
+}
+
+FlatLayout FlatLayout::draft(const ModelDims& m, int n_layers) {
+    FlatLayout f;
+    size_t o = 0;
+    const size_t d = m.d;
+    auto add = [&](size_t n) {
+        size_t r = o;
+        o += n;
+        return r;
+    };
+    f.w_fuse = add(2 * d * d);
+    for (int l = 0; l < n_layers; ++l) {
+        L x;
+        x.ln1_g = add(d);
+        x.ln1_b = add(d);
+        x.wq = add(d * d);
+        x.wk = add(d * d);
+        x.wv = add(d * d);
+        x.wo = add(d * d);
+        x.ln2_g = add(d);
+        x.ln2_b = add(d);
+        x.w1 = add(d * m.dff);
+        x.w2 = add(d * m.dff);
+        f.layers.push_back(x);
+    }
+    f.lnf_g = add(d);
+    f.lnf_b = add(d);
+    f.total = o;
+    return f;
+}
+
+// ------------------------------------------------------------------ construction
+Engine::Engine(const ModelDims& dims, int draft_layers, int device, int max_seqs, int max_rows, int k_max, int l_max)
+    : dims_(dims), dlayers_(draft_layers), device_(device), max_seqs_(max_seqs), k_max_(k_max), l_max_(l_max) {
+    if (dims.vocab < 4 || dims.d <= 0 || dims.layers <= 0 || dims.heads <= 0 || dims.dff <= 0)
+        throw std::invalid_argument("model dims must be positive (vocab >= 4)");
+    if (dims.d % dims.heads) throw std::invalid_argument("d_model must be divisible by n_heads");
+    if (dims.max_seq < 8) throw std::invalid_argument("max_seq_len must be >= 8");
+    const int dh = dims.d / dims.heads;
+    if (dh != 64 && dh != 128 && dh != 256) throw std::invalid_argument("head dim must be 64, 128 or 256");
+    if (dims.d % 8 || dims.dff % 8) throw std::invalid_argument("d_model and d_ff must be multiples of 8");
+    if (draft_layers <= 0) throw std::invalid_argument("draft n_layers must be positive");
+    if (k_max < 0 || k_max > 16) throw std::invalid_argument("engine k_max must be in [0, 16]");
+    if (l_max < 0 || l_max + 1 > kMaxChain) throw std::invalid_argument("engine l_max must be in [0, 7]");
+    if (max_seqs < 1) throw std::invalid_argument("max_seqs must be >= 1");
+    max_rows_ = std::max(256, ((max_rows + 255) / 256) * 256);
+    SGB_CUDA(cudaSetDevice(device));
+    SGB_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+    SGB_CUDA(cudaEventCreate(&ev0_));
+    SGB_CUDA(cudaEventCreate(&ev1_));
+    tlay_ = FlatLayout::target(dims);
+    dlay_ = FlatLayout::draft(dims, draft_layers);
+
+    const size_t d = dims.d, V = dims.vocab, T = dims.max_seq, F = dims.dff, S = max_seqs, R = max_rows_;
+    const int ds = 1 + std::max(0, l_max - 1) * std::max(1, k_max);
+    // weights
+    const size_t per_layer_bf = 4 * d * d + 2 * d * F;
+    tw_ = dalloc<__nv_bfloat16>(dims.layers * per_layer_bf + V * d);
+    dw_ = dalloc<__nv_bfloat16>(draft_layers * per_layer_bf + 2 * d * d);
+    tsmall_ = dalloc<float>(V * d + T * d + dims.layers * 4 * d + 2 * d);
+    dmaster_ = dalloc<float>(dlay_.total);
+    // KV stores
+    tkv_.layers = dims.layers;
+    tkv_.seq_stride = T;
+    tkv_.scratch_base = static_cast<long long>(S) * T;
+    tkv_.n_slots = tkv_.scratch_base + R;
+    tkv_.K = dalloc<__nv_bfloat16>(static_cast<size_t>(tkv_.n_slots) * d * dims.layers);
+    tkv_.V = dalloc<__nv_bfloat16>(static_cast<size_t>(tkv_.n_slots) * d * dims.layers);
+    dkv_.layers = draft_layers;
+    dkv_.seq_stride = T;
+    dkv_.scratch_base = static_cast<long long>(S) * T;
+    dkv_.n_slots = dkv_.scratch_base + static_cast<long long>(S) * ds;
+    dkv_.K = dalloc<__nv_bfloat16>(static_cast<size_t>(dkv_.n_slots) * d * draft_layers);
+    dkv_.V = dalloc<__nv_bfloat16>(static_cast<size_t>(dkv_.n_slots) * d * draft_layers);
+    // sequences
+    ss_.max_seq = static_cast<int>(T);
+    ss_.tokens = dalloc<int>(S * T);
+    ss_.len = dalloc<int>(S);
+    ss_.finished = dalloc<int>(S);
+    ss_.hit_eos = dalloc<int>(S);
+    ss_.seed = dalloc<unsigned long long>(S);
+    feats_ = dalloc<float>(S * T * d);
+    dfeat_ = dalloc<float>(S * ds * d);
+    tr_.tmax = tree_cap(std::max(1, k_max), std::max(1, l_max));
+    if (tr_.tmax > 1024) throw std::invalid_argument("tree capacity exceeds 1024 nodes (k_max, l_max too large)");
+    tr_.ds = ds;
+    const size_t TM = static_cast<size_t>(tr_.tmax) * S;
+    tr_.tok = dalloc<int>(TM);
+    tr_.par = dalloc<int>(TM);
+    tr_.dep = dalloc<int>(TM);
+    tr_.lp = dalloc<double>(TM);
+    tr_.conf = dalloc<double>(TM);
+    tr_.fslot = dalloc<int>(TM);
+    tr_.sel = dalloc<int>(TM);
+    tr_.n_nodes = dalloc<int>(S);
+    tr_.lvl_start = dalloc<int>(S);
+    tr_.lvl_cnt = dalloc<int>(S);
+    tr_.frontier = dalloc<int>(S * 16);
+    cache_len_t_.assign(S, 0);
+    cache_len_d_.assign(S, 0);
+    // activations
+    x_ = dalloc<float>(R * d);
+    q_ = dalloc<float>(R * d);
+    y_ = dalloc<float>(R * d);
+    featin_ = dalloc<float>(R * d);
+    a_ = dalloc<__nv_bfloat16>(R * d);
+    att_ = dalloc<__nv_bfloat16>(R * d);
+    a2_ = dalloc<__nv_bfloat16>(R * d);
+    h_ = dalloc<__nv_bfloat16>(R * F);
+    fuse_ = dalloc<__nv_bfloat16>(R * 2 * d);
+    act_a_.init(a_, static_cast<int>(R), static_cast<int>(d));
+    act_att_.init(att_, static_cast<int>(R), static_cast<int>(d));
+    act_a2_.init(a2_, static_cast<int>(R), static_cast<int>(d));
+    act_h_.init(h_, static_cast<int>(R), static_cast<int>(F));
+    act_fuse_.init(fuse_, static_cast<int>(R), static_cast<int>(2 * d));
+    size_t pe = 0;
+    auto upd = [&](int N, int K) { pe = std::max(pe, static_cast<size_t>(gemm_splits(N, K)) * N); };
+    upd(3 * d, d);
+    upd(d, d);
+    upd(F, d);
+    upd(d, F);
+    upd(d, 2 * d);
+    if (gemm_splits(V, d) > 1) upd(V, d);
+    part_elems_ = pe * R;
+    part_ = dalloc<float>(part_elems_);
+    logits_ = dalloc<float>(R * V);
+    max_vlen_cap_ = static_cast<int>(T) + kMaxChain;
+    const int ns = attn_splits_for(max_vlen_cap_);
+    pacc_ = dalloc<float>(R * d * ns);
+    pml_ = dalloc<float>(R * dims.heads * ns * 2);
+    alloc_rows();
+    SGB_CUDA(cudaMallocHost(&h_result_, sizeof(int) * (2 * S + 4)));
+    SGB_CUDA(cudaMemset(err_, 0, sizeof(int)));
+    SGB_CUDA(cudaDeviceSynchronize());
+}
+
+void Engine::alloc_rows() {
+    const size_t R = max_rows_, S = max_seqs_;
+    rows_.tok = dalloc<int>(R);
+    rows_.pos = dalloc<int>(R);
+    rows_.kv_dst = dalloc<long long>(R);
+    rows_.ctx_base = dalloc<long long>(R);
+    rows_.ctx_len = dalloc<int>(R);
+    rows_.chain_len = dalloc<int>(R);
+    rows_.chain = dalloc<long long>(R * kMaxChain);
+    rows_.feat_off = dalloc<long long>(R);
+    rows_.out_off = dalloc<long long>(R);
+    rows_.key_pos = dalloc<int>(R);
+    rows_.seed = dalloc<unsigned long long>(R);
+    rows_.par_row = dalloc<int>(R);
+    lm_idx_ = dalloc<int>(R);
+    topk_tok_ = dalloc<int>(R * 16);
+    topk_lp_ = dalloc<double>(R * 16);
+    emitted_ = dalloc<int>(R);
+    acc_rows_ = dalloc<int>(S * kMaxChain);
+    result_ = dalloc<int>(2 * S);
+    err_ = dalloc<int>(1);
+    steps_ = dalloc<StepSeqDev>(S);
+    drow_ = dalloc<int>(S * std::max(1, l_max_));
+    misc_i_ = dalloc<int>(4 * R + 4 * S);
+    misc_l_ = dalloc<long long>(2 * R + 2 * S);
+    mask_dbg_ = dalloc<unsigned char>(1024 * 1024);
+}
+
+Engine::~Engine() {
+    cudaSetDevice(device_);
+    cudaStreamSynchronize(st_);
+    void* ptrs[] = {tw_, dw_, tsmall_, dmaster_, tkv_.K, tkv_.V, dkv_.K, dkv_.V, ss_.tokens, ss_.len, ss_.finished,
+                    ss_.hit_eos, ss_.seed, feats_, dfeat_, tr_.tok, tr_.par, tr_.dep, tr_.lp, tr_.conf, tr_.fslot,
+                    tr_.sel, tr_.n_nodes, tr_.lvl_start, tr_.lvl_cnt, tr_.frontier, x_, q_, y_, featin_, a_, att_,
+                    a2_, h_, fuse_, part_, logits_, pacc_, pml_, rows_.tok, rows_.pos, rows_.kv_dst,
+                    rows_.ctx_base, rows_.ctx_len, rows_.chain_len, rows_.chain, rows_.feat_off, rows_.out_off,
+                    rows_.key_pos, rows_.seed, rows_.par_row, lm_idx_, topk_tok_, topk_lp_, emitted_, acc_rows_,
+                    result_, err_, steps_, drow_, misc_i_, misc_l_, mask_dbg_};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    if (h_result_) cudaFreeHost(h_result_);
+    if (ev0_) cudaEventDestroy(ev0_);
+    if (ev1_) cudaEventDestroy(ev1_);
+    if (st_) cudaStreamDestroy(st_);
+}
+
+// ------------------------------------------------------------------ weights
+void Engine::convert_target(const float* stg) {
+    const int d = dims_.d, F = dims_.dff, V = dims_.vocab, T = dims_.max_seq;
+    float* sm = tsmall_;
+    SGB_CUDA(cudaMemcpyAsync(sm, stg + tlay_.tok_emb, sizeof(float) * V * d, cudaMemcpyDeviceToDevice, st_));
+    tok_emb_ = sm;
+    sm += static_cast<size_t>(V) * d;
+    SGB_CUDA(cudaMemcpyAsync(sm, stg + tlay_.pos_emb, sizeof(float) * T * d, cudaMemcpyDeviceToDevice, st_));
+    pos_emb_ = sm;
+    sm += static_cast<size_t>(T) * d;
+    __nv_bfloat16* w = tw_;
+    tL_.assign(dims_.layers, LayerDev{});
+    for (int l = 0; l < dims_.layers; ++l) {
+        const auto& o = tlay_.layers[l];
+        LayerDev& L = tL_[l];
+        const size_t ln[4] = {o.ln1_g, o.ln1_b, o.ln2_g, o.ln2_b};
+        const float** dst[4] = {&L.ln1_g, &L.ln1_b, &L.ln2_g, &L.ln2_b};
+        for (int i = 0; i < 4; ++i) {
+            SGB_CUDA(cudaMemcpyAsync(sm, stg + ln[i], sizeof(float) * d, cudaMemcpyDeviceToDevice, st_));
+            *dst[i] = sm;
+            sm += d;
+        }
+        __nv_bfloat16* qkv = w;
+        launch_transpose_to_bf16(stg + o.wq, d, d, qkv, d, st_);
+        launch_transpose_to_bf16(stg + o.wk, d, d, qkv + static_cast<size_t>(d) * d, d, st_);
+        launch_transpose_to_bf16(stg + o.wv, d, d, qkv + 2 * static_cast<size_t>(d) * d, d, st_);
+        w += 3 * static_cast<size_t>(d) * d;
+        __nv_bfloat16* wo = w;
+        launch_transpose_to_bf16(stg + o.wo, d, d, wo, d, st_);
+        w += static_cast<size_t>(d) * d;
+        __nv_bfloat16* w1 = w;
+        launch_transpose_to_bf16(stg + o.w1, d, F, w1, d, st_);
+        w += static_cast<size_t>(d) * F;
+        __nv_bfloat16* w2 = w;
+        launch_transpose_to_bf16(stg + o.w2, F, d, w2, F, st_);
+        w += static_cast<size_t>(d) * F;
+        L.qkv.init(qkv, 3 * d, d);
+        L.wo.init(wo, d, d);
+        L.w1.init(w1, F, d);
+        L.w2.init(w2, d, F);
+    }
+    SGB_CUDA(cudaMemcpyAsync(sm, stg + tlay_.lnf_g, sizeof(float) * d, cudaMemcpyDeviceToDevice, st_));
+    lnf_g_ = sm;
+    sm += d;
+    SGB_CUDA(cudaMemcpyAsync(sm, stg + tlay_.lnf_b, sizeof(float) * d, cudaMemcpyDeviceToDevice, st_));
+    lnf_b_ = sm;
+    launch_transpose_to_bf16(stg + tlay_.lm_head, d, V, w, d, st_);
+    lm_head_.init(w, V, d);
+    SGB_CUDA(cudaStreamSynchronize(st_));
+    target_ready_ = true;
+}
+
+void Engine::convert_draft() {
+    const int d = dims_.d, F = dims_.dff;
+    const float* m = dmaster_;
+    __nv_bfloat16* w = dw_;
+    launch_transpose_to_bf16(m + dlay_.w_fuse, 2 * d, d, w, 2 * d, st_);
+    w_fuse_.init(w, d, 2 * d);
+    w += 2 * static_cast<size_t>(d) * d;
+    dL_.assign(dlayers_, LayerDev{});
+    for (int l = 0; l < dlayers_; ++l) {
+        const auto& o = dlay_.layers[l];
+        LayerDev& L = dL_[l];
+        L.ln1_g = m + o.ln1_g;
+        L.ln1_b = m + o.ln1_b;
+        L.ln2_g = m + o.ln2_g;
+        L.ln2_b = m + o.ln2_b;
+        __nv_bfloat16* qkv = w;
+        launch_transpose_to_bf16(m + o.wq, d, d, qkv, d, st_);
+        launch_transpose_to_bf16(m + o.wk, d, d, qkv + static_cast<size_t>(d) * d, d, st_);
+        launch_transpose_to_bf16(m + o.wv, d, d, qkv + 2 * static_cast<size_t>(d) * d, d, st_);
+        w += 3 * static_cast<size_t>(d) * d;
+        __nv_bfloat16* wo = w;
+        launch_transpose_to_bf16(m + o.wo, d, d, wo, d, st_);
+        w += static_cast<size_t>(d) * d;
+        __nv_bfloat16* w1 = w;
+        launch_transpose_to_bf16(m + o.w1, d, F, w1, d, st_);
+        w += static_cast<size_t>(d) * F;
+        __nv_bfloat16* w2 = w;
+        launch_transpose_to_bf16(m + o.w2, F, d, w2, F, st_);
+        w += static_cast<size_t>(d) * F;
+        L.qkv.init(qkv, 3 * d, d);
+        L.wo.init(wo, d, d);
+        L.w1.init(w1, F, d);
+        L.w2.init(w2, d, F);
+    }
+    dlnf_g_ = m + dlay_.lnf_g;
+    dlnf_b_ = m + dlay_.lnf_b;
+    SGB_CUDA(cudaStreamSynchronize(st_));
+    draft_ready_ = true;
+}
+
+void Engine::upload_target(const float* flat, size_t n) {
+    if (n != tlay_.total) throw std::invalid_argument("upload_target: param count mismatch");
+    float* stg = dalloc<float>(n);
+    SGB_CUDA(cudaMemcpy(stg, flat, n * sizeof(float), cudaMemcpyHostToDevice));
+    convert_target(stg);
+    cudaFree(stg);
+}
+
+void Engine::upload_draft(const float* flat, size_t n) {
+    if (n != dlay_.total) throw std::invalid_argument("upload_draft: param count mismatch");
+    SGB_CUDA(cudaMemcpy(dmaster_, flat, n * sizeof(float), cudaMemcpyHostToDevice));
+    convert_draft();
+}
+
+void Engine::download_draft(float* flat, size_t n) {
+    if (n != dlay_.total) throw std::invalid_argument("download_draft: param count mismatch");
+    SGB_CUDA(cudaStreamSynchronize(st_));
+    SGB_CUDA(cudaMemcpy(flat, dmaster_, n * sizeof(float), cudaMemcpyDeviceToHost));
+}
+
+// Same distributions as init_flat (tinylm.hpp:83-109) but drawn by a device counter RNG,
+// so large benchmark models initialise in milliseconds (not reference-identical values).
+void Engine::init_random(uint64_t seed) {
+    const int d = dims_.d, F = dims_.dff, V = dims_.vocab, T = dims_.max_seq;
+    float* stg = dalloc<float>(tlay_.total);
+    uint64_t s = seed;
+    auto nrm = [&](size_t off, size_t n, float sd) { launch_init_normal(stg + off, n, splitmix_host(s), sd, st_); };
+    auto one = [&](size_t off, size_t n, float v) { launch_fill(stg + off, n, v, st_); };
+    const float res_t = static_cast<float>(0.02 / std::sqrt(2.0 * dims_.layers));
+    nrm(tlay_.tok_emb, static_cast<size_t>(V) * d, 0.02f);
+    nrm(tlay_.pos_emb, static_cast<size_t>(T) * d, 0.01f);
+    for (const auto& o : tlay_.layers) {
+        one(o.ln1_g, d, 1.f);
+        one(o.ln1_b, d, 0.f);
+        one(o.ln2_g, d, 1.f);
+        one(o.ln2_b, d, 0.f);
+        nrm(o.wq, static_cast<size_t>(d) * d, 0.02f);
+        nrm(o.wk, static_cast<size_t>(d) * d, 0.02f);
+        nrm(o.wv, static_cast<size_t>(d) * d, 0.02f);
+        nrm(o.wo, static_cast<size_t>(d) * d, res_t);
+        nrm(o.w1, static_cast<size_t>(d) * F, 0.02f);
+        nrm(o.w2, static_cast<size_t>(d) * F, res_t);
+    }
+    one(tlay_.lnf_g, d, 1.f);
+    one(tlay_.lnf_b, d, 0.f);
+    nrm(tlay_.lm_head, static_cast<size_t>(d) * V, 0.02f);
+    convert_target(stg);
+    cudaFree(stg);
+    const float res_d = static_cast<float>(0.02 / std::sqrt(2.0 * dlayers_));
+    float* m = dmaster_;
+    launch_init_normal(m + dlay_.w_fuse, 2 * static_cast<size_t>(d) * d, splitmix_host(s), 0.02f, st_);
+    for (const auto& o : dlay_.layers) {
+        launch_fill(m + o.ln1_g, d, 1.f, st_);
+        launch_fill(m + o.ln1_b, d, 0.f, st_);
+        launch_fill(m + o.ln2_g, d, 1.f, st_);
+        launch_fill(m + o.ln2_b, d, 0.f, st_);
+        launch_init_normal(m + o.wq, static_cast<size_t>(d) * d, splitmix_host(s), 0.02f, st_);
+        launch_init_normal(m + o.wk, static_cast<size_t>(d) * d, splitmix_host(s), 0.02f, st_);
+        launch_init_normal(m + o.wv, static_cast<size_t>(d) * d, splitmix_host(s), 0.02f, st_);
+        launch_init_normal(m + o.wo, static_cast<size_t>(d) * d, splitmix_host(s), res_d, st_);
+        launch_init_normal(m + o.w1, static_cast<size_t>(d) * F, splitmix_host(s), 0.02f, st_);
+        launch_init_normal(m + o.w2, static_cast<size_t>(d) * F, splitmix_host(s), res_d, st_);
+    }
+    launch_fill(m + dlay_.lnf_g, d, 1.f, st_);
+    launch_fill(m + dlay_.lnf_b, d, 0.f, st_);
+    convert_draft();
+}
+
+// ------------------------------------------------------------------ forward
+void Engine::lm_head(const __nv_bfloat16*, const GemmAct& act, int R, float* out) {
+    const double K = dims_.d, N = dims_.vocab;
+    const int e0 = pbeg();
+    if (lm_head_.splits == 1) {
+        gemm_launch(lm_head_, act, out, R, st_);
+        count();
+    } else {
+        gemm_launch(lm_head_, act, part_, R, st_);
+        launch_reduce_plain(part_, lm_head_.splits, R, dims_.vocab, out, st_);
+        count(2);
+    }
+    pend(kClsLmHead, e0, N * K * 2 + R * K * 2 + R * N * 4.0, 2.0 * R * N * K);
+}
+
+void Engine::gemm(const GemmWeight& w, const GemmAct& a, int M) {
+    const int e0 = pbeg();
+    gemm_launch(w, a, part_, M, st_);
+    pend(kClsGemm, e0, 2.0 * w.N * w.K + 2.0 * M * w.K + 4.0 * w.splits * M * w.N, 2.0 * M * w.N * w.K);
+    count();
+}
+
+void Engine::forward(const Fwd& f) {
+    const int M = f.M, d = dims_.d, F = dims_.dff, H = dims_.heads;
+    if (M <= 0) return;
+    if (M > max_rows_) throw std::invalid_argument("forward: rows exceed engine max_rows");
+    if (f.max_vlen > max_vlen_cap_) throw std::out_of_range("forward: context beyond capacity");
+    if (!target_ready_ || (f.draft && !draft_ready_)) throw std::runtime_error("weights not uploaded");
+    const std::vector<LayerDev>& L = f.draft ? dL_ : tL_;
+    KvStore& kv = f.draft ? dkv_ : tkv_;
+    const AttnRowsDev ar{rows_.ctx_base, rows_.ctx_len, rows_.chain_len, rows_.chain};
+    const double row_bytes = static_cast<double>(M) * d * 4;
+    int e0 = pbeg();
+    if (!f.draft) {
+        launch_embed_ln(rows_.tok, rows_.pos, M, d, tok_emb_, pos_emb_, L[0].ln1_g, L[0].ln1_b, x_, a_, st_);
+        pend(kClsRow, e0, 3 * row_bytes, 0);
+        count();
+    } else {
+        launch_gather_fuse(rows_.tok, rows_.feat_off, f.feat_base, tok_emb_, M, d, fuse_, st_);
+        pend(kClsRow, e0, 3 * row_bytes, 0);
+        count();
+        gemm(w_fuse_, act_fuse_, M);
+        e0 = pbeg();
+        launch_reduce_residual_ln(part_, w_fuse_.splits, M, d, x_, false, pos_emb_, rows_.pos, L[0].ln1_g,
+                                  L[0].ln1_b, a_, nullptr, st_);
+        pend(kClsRow, e0, (w_fuse_.splits + 2.5) * row_bytes, 0);
+        count();
+    }
+    const size_t lstride = static_cast<size_t>(kv.n_slots) * d;
+    const double attn_bytes = f.attn_kv_unique * d * 4.0 + row_bytes * 1.5;
+    const double attn_flops = 4.0 * f.attn_row_keys * d;
+    for (size_t l = 0; l < L.size(); ++l) {
+        const LayerDev& W = L[l];
+        __nv_bfloat16* Kl = kv.K + l * lstride;
+        __nv_bfloat16* Vl = kv.V + l * lstride;
+        gemm(W.qkv, act_a_, M);
+        e0 = pbeg();
+        launch_reduce_qkv(part_, W.qkv.splits, M, d, q_, Kl, Vl, rows_.kv_dst, st_);
+        pend(kClsRow, e0, (3.0 * W.qkv.splits + 2.0) * row_bytes, 0);
+        e0 = pbeg();
+        launch_attention(q_, Kl, Vl, ar, M, H, d, f.max_vlen, pacc_, pml_, att_, st_);
+        pend(kClsAttn, e0, attn_bytes, attn_flops);
+        gemm(W.wo, act_att_, M);
+        e0 = pbeg();
+        launch_reduce_residual_ln(part_, W.wo.splits, M, d, x_, true, nullptr, nullptr, W.ln2_g, W.ln2_b, a_,
+                                  nullptr, st_);
+        pend(kClsRow, e0, (W.wo.splits + 2.5) * row_bytes, 0);
+        gemm(W.w1, act_a_, M);
+        e0 = pbeg();
+        launch_reduce_gelu(part_, W.w1.splits, M, F, h_, st_);
+        pend(kClsRow, e0, (4.0 * W.w1.splits + 2.0) * M * F, 0);
+        gemm(W.w2, act_h_, M);
+        const bool last = l + 1 == L.size();
+        const float* g = last ? (f.draft ? dlnf_g_ : lnf_g_) : L[l + 1].ln1_g;
+        const float* b = last ? (f.draft ? dlnf_b_ : lnf_b_) : L[l + 1].ln1_b;
+        e0 = pbeg();
+        launch_reduce_residual_ln(part_, W.w2.splits, M, d, x_, true, nullptr, nullptr, g, b, a_,
+                                  last ? f.y_out : nullptr, st_);
+        pend(kClsRow, e0, (W.w2.splits + 2.5 + (last ? 1 : 0)) * row_bytes, 0);
+        count(6);
+    }
+    if (f.logits) {
+        if (f.lm_idx) {
+            launch_gather_rows_bf16(a_, f.lm_idx, f.lm_rows, d, a2_, st_);
+            count();
+            lm_head(a2_, act_a2_, f.lm_rows, f.logits_out);
+        } else {
+            lm_head(a_, act_a_, M, f.logits_out);
+        }
+    }
+}
+
+// ------------------------------------------------------------------ profiler (CUDA events)
+int Engine::pbeg() {
+    if (!prof_) return -1;
+    if (ev_used_ >= static_cast<int>(evs_.size())) {
+        cudaEvent_t e;
+        SGB_CUDA(cudaEventCreate(&e));
+        evs_.push_back(e);
+    }
+    SGB_CUDA(cudaEventRecord(evs_[ev_used_], st_));
+    return ev_used_++;
+}
+
+void Engine::pend(int cls, int e0, double bytes, double flops) {
+    if (!prof_ || e0 < 0) return;
+    const int e1 = pbeg();
+    precs_.push_back(PRec{cls, e0, e1, bytes, flops});
+}
+
+void Engine::pflush() {
+    if (precs_.empty()) {
+        ev_used_ = 0;
+        return;
+    }
+    SGB_CUDA(cudaStreamSynchronize(st_));
+    for (const PRec& r : precs_) {
+        float ms = 0.f;
+        SGB_CUDA(cudaEventElapsedTime(&ms, evs_[r.e0], evs_[r.e1]));
+        KernelProfile& k = prof_cls_[r.cls];
+        k.ms += ms;
+        k.launches += 1;
+        k.bytes += r.bytes;
+        k.flops += r.flops;
+    }
+    precs_.clear();
+    ev_used_ = 0;
+}
+
+void Engine::set_profiling(bool on) {
+    pflush();
+    prof_ = on;
+}
+
+void Engine::read_profile(KernelProfile* out, int n, bool reset) {
+    pflush();
+    for (int i = 0; i < n && i < kNumCls; ++i) out[i] = prof_cls_[i];
+    if (reset)
+        for (auto& k : prof_cls_) k = KernelProfile{};
+}
+
+void Engine::upload_rows_host(int M, const std::vector<int>& tok, const std::vector<int>& pos,
+                              const std::vector<long long>& kv_dst, const std::vector<long long>& ctx_base,
+                              const std::vector<int>& ctx_len, const std::vector<int>& chain_len,
+                              const std::vector<long long>& chain, const std::vector<long long>* feat_off) {
+    if (!tok.empty()) h2d(rows_.tok, tok.data(), M, st_);
+    h2d(rows_.pos, pos.data(), M, st_);
+    h2d(rows_.kv_dst, kv_dst.data(), M, st_);
+    h2d(rows_.ctx_base, ctx_base.data(), M, st_);
+    h2d(rows_.ctx_len, ctx_len.data(), M, st_);
+    h2d(rows_.chain_len, chain_len.data(), M, st_);
+    if (!chain.empty()) h2d(rows_.chain, chain.data(), static_cast<size_t>(M) * kMaxChain, st_);
+    if (feat_off) h2d(rows_.feat_off, feat_off->data(), M, st_);
+}
+
+// ------------------------------------------------------------------ per-op parity entry points
+void Engine::cache_reset(int slot, bool draft) {
+    if (slot < 0 || slot >= max_seqs_) throw std::invalid_argument("cache slot out of range");
+    (draft ? cache_len_d_ : cache_len_t_)[slot] = 0;
+}
+int Engine::cache_len(int slot, bool draft) const {
+    if (slot < 0 || slot >= max_seqs_) throw std::invalid_argument("cache slot out of range");
+    return (draft ? cache_len_d_ : cache_len_t_)[slot];
+}
+
+void Engine::cache_read(int slot, bool draft, float* k, float* v) {
+    const KvStore& kv = draft ? dkv_ : tkv_;
+    const int len = cache_len(slot, draft), d = dims_.d;
+    std::vector<__nv_bfloat16> tmp(static_cast<size_t>(len) * d);
+    SGB_CUDA(cudaStreamSynchronize(st_));
+    for (int l = 0; l < kv.layers; ++l) {
+        for (int w = 0; w < 2; ++w) {
+            const __nv_bfloat16* src = (w ? kv.V : kv.K) + (static_cast<size_t>(l) * kv.n_slots + slot * kv.seq_stride) * d;
+            SGB_CUDA(cudaMemcpy(tmp.data(), src, tmp.size() * 2, cudaMemcpyDeviceToHost));
+            float* dst = (w ? v : k) + static_cast<size_t>(l) * len * d;
+            for (size_t i = 0; i < tmp.size(); ++i) dst[i] = __bfloat162float(tmp[i]);
+        }
+    }
+}
+
+void Engine::cache_gather_tail(int slot, int base, const int* keep, int n) {  // tinylm.hpp:254-268
+    int& len = cache_len_t_.at(slot);
+    if (base < 0 || base > len) throw std::invalid_argument("gather_tail: base beyond length");
+    for (int i = 0; i < n; ++i) {
+        if (keep[i] < 0 || base + keep[i] >= len || (i > 0 && keep[i] <= keep[i - 1]))
+            throw std::invalid_argument("gather_tail: keep must be strictly increasing and in range");
+    }
+    const int d = dims_.d;
+    for (int l = 0; l < tkv_.layers; ++l)
+        for (int i = 0; i < n; ++i) {
+            if (keep[i] == i) continue;
+            for (int w = 0; w < 2; ++w) {
+                __nv_bfloat16* P = (w ? tkv_.V : tkv_.K) + (static_cast<size_t>(l) * tkv_.n_slots + slot * tkv_.seq_stride) * d;
+                SGB_CUDA(cudaMemcpyAsync(P + static_cast<size_t>(base + i) * d, P + static_cast<size_t>(base + keep[i]) * d,
+                                         d * 2, cudaMemcpyDeviceToDevice, st_));
+            }
+        }
+    len = base + n;
+    SGB_CUDA(cudaStreamSynchronize(st_));
+}
+
+void Engine::forward_target(int slot, const int* tokens, const int* positions, int rows, const unsigned char* mask,
+                            float* logits, float* hidden) {  // tinylm.hpp:422-463
+    if (rows <= 0) throw std::invalid_argument("forward_target: empty input");
+    for (int i = 0; i < rows; ++i) {
+        if (tokens[i] < 0 || tokens[i] >= dims_.vocab)
+            throw std::invalid_argument("forward_target: token id out of range");
+        if (positions[i] < 0 || positions[i] >= dims_.max_seq)
+            throw std::out_of_range("forward_target: position beyond max_seq_len");
+    }
+    int& len = cache_len_t_.at(slot);
+    if (len + rows > dims_.max_seq) throw std::out_of_range("forward_target: cache capacity");
+    const long long base = static_cast<long long>(slot) * tkv_.seq_stride;
+    std::vector<int> tok(tokens, tokens + rows), pos(positions, positions + rows), cl(rows), chl(rows, 0);
+    std::vector<long long> kvd(rows), cb(rows, base), ch(static_cast<size_t>(rows) * kMaxChain, 0);
+    for (int i = 0; i < rows; ++i) {
+        if (!mask) {
+            kvd[i] = base + len + i;
+            cl[i] = len + i + 1;
+        } else {
+            kvd[i] = tkv_.scratch_base + i;
+            cl[i] = len;
+            int c = 0;
+            for (int j = 0; j < rows; ++j)
+                if (mask[static_cast<size_t>(i) * rows + j]) {
+                    if (c >= kMaxChain) throw std::invalid_argument("forward_target: mask row exceeds tree depth");
+                    ch[static_cast<size_t>(i) * kMaxChain + c++] = tkv_.scratch_base + j;
+                }
+            chl[i] = c;
+        }
+    }
+    upload_rows_host(rows, tok, pos, kvd, cb, cl, chl, ch, nullptr);
+    Fwd f;
+    f.M = rows;
+    f.y_out = y_;
+    f.logits = true;
+    f.logits_out = logits_;
+    f.max_vlen = len + rows;
+    f.attn_kv_unique = len + rows;
+    f.attn_row_keys = static_cast<double>(rows) * (len + rows);
+    forward(f);
+    if (mask) {  // extend the cache by every forwarded row (tinylm.hpp:405-412)
+        const int d = dims_.d;
+        for (int l = 0; l < tkv_.layers; ++l)
+            for (int w = 0; w < 2; ++w) {
+                __nv_bfloat16* P = (w ? tkv_.V : tkv_.K) + static_cast<size_t>(l) * tkv_.n_slots * d;
+                SGB_CUDA(cudaMemcpyAsync(P + (base + len) * d, P + tkv_.scratch_base * d,
+                                         static_cast<size_t>(rows) * d * 2, cudaMemcpyDeviceToDevice, st_));
+            }
+    }
+    len += rows;
+    if (logits) d2h(logits, logits_, static_cast<size_t>(rows) * dims_.vocab, st_);
+    if (hidden) d2h(hidden, y_, static_cast<size_t>(rows) * dims_.d, st_);
+    SGB_CUDA(cudaStreamSynchronize(st_));
+}
+
+void Engine::forward_draft(int slot, const int* tokens, const float* prev_feat, const int* positions, int rows,
+                           bool extend, float* feats, float* logits) {  // tinylm.hpp:502-563
+    if (rows <= 0) throw std::invalid_argument("forward_draft: empty input");
+    for (int i = 0; i < rows; ++i) {
+        if (tokens[i] < 0 || tokens[i] >= dims_.vocab)
+            throw std::invalid_argument("forward_draft: token id out of range");
+        if (positions[i] < 0 || positions[i] >= dims_.max_seq)
+            throw std::out_of_range("forward_draft: position beyond max_seq_len");
+    }
+    int& len = cache_len_d_.at(slot);
+    if (len + rows > dims_.max_seq) throw std::out_of_range("forward_draft: cache capacity");
+    if (!extend && rows > kMaxChain) throw std::invalid_argument("forward_draft: read-only rows exceed chain");
+    const long long base = static_cast<long long>(slot) * dkv_.seq_stride;
+    std::vector<int> tok(tokens, tokens + rows), pos(positions, positions + rows), cl(rows), chl(rows, 0);
+    std::vector<long long> kvd(rows), cb(rows, base), ch(static_cast<size_t>(rows) * kMaxChain, 0), fo(rows);
+    for (int i = 0; i < rows; ++i) {
+        fo[i] = static_cast<long long>(i) * dims_.d;
+        if (extend) {
+            kvd[i] = base + len + i;
+            cl[i] = len + i + 1;
+        } else {
+            kvd[i] = dkv_.scratch_base + i;
+            cl[i] = len;
+            for (int j = 0; j <= i; ++j) ch[static_cast<size_t>(i) * kMaxChain + j] = dkv_.scratch_base + j;
+            chl[i] = i + 1;
+        }
+    }
+    upload_rows_host(rows, tok, pos, kvd, cb, cl, chl, ch, &fo);
+    h2d(featin_, prev_feat, static_cast<size_t>(rows) * dims_.d, st_);
+    Fwd f;
+    f.M = rows;
+    f.draft = true;
+    f.feat_base = featin_;
+    f.y_out = y_;
+    f.logits = true;
+    f.logits_out = logits_;
+    f.max_vlen = len + rows;
+    f.attn_kv_unique = len + rows;
+    f.attn_row_keys = static_cast<double>(rows) * (len + rows);
+    forward(f);
+    if (extend) len += rows;
+    if (logits) d2h(logits, logits_, static_cast<size_t>(rows) * dims_.vocab, st_);
+    if (feats) d2h(feats, y_, static_cast<size_t>(rows) * dims_.d, st_);
+    SGB_CUDA(cudaStreamSynchronize(st_));
+}
+
+void Engine::emit(const float* logits, int rows, int vocab, double temperature, const unsigned long long* seeds,
+                  const int* key_pos, int* out) {
+    if (vocab != dims_.vocab) throw std::invalid_argument("emit: vocab mismatch");
+    if (rows <= 0 || rows > max_rows_) throw std::invalid_argument("emit: bad row count");
+    if (temperature < 0) throw std::invalid_argument("sample_token: negative temperature");
+    h2d(logits_, logits, static_cast<size_t>(rows) * vocab, st_);
+    h2d(rows_.seed, seeds, rows, st_);
+    h2d(rows_.key_pos, key_pos, rows, st_);
+    SGB_CUDA(cudaMemsetAsync(err_, 0, sizeof(int), st_));
+    launch_emit(logits_, vocab, nullptr, rows_.seed, rows_.key_pos, rows, temperature, emitted_, err_, st_);
+    d2h(out, emitted_, rows, st_);
+    int err = 0;
+    d2h(&err, err_, 1, st_);
+    SGB_CUDA(cudaStreamSynchronize(st_));
+    if (err & 2) throw std::domain_error("sample_token: NaN logit");
+    if (err & 4) throw std::domain_error("sample_token: all logits are -inf");
+}
+
+void Engine::topk_logsoftmax(const float* logits, int rows, int vocab, int k, int* tok, double* lp) {
+    if (vocab != dims_.vocab) throw std::invalid_argument("topk: vocab mismatch");
+    if (rows <= 0 || rows > max_rows_) throw std::invalid_argument("topk: bad row count");
+    k = std::min(k, vocab);
+    h2d(logits_, logits, static_cast<size_t>(rows) * vocab, st_);
+    launch_topk_lsm(logits_, vocab, rows, k, topk_tok_, topk_lp_, st_);
+    d2h(tok, topk_tok_, static_cast<size_t>(rows) * k, st_);
+    d2h(lp, topk_lp_, static_cast<size_t>(rows) * k, st_);
+    SGB_CUDA(cudaStreamSynchronize(st_));
+}
+
+Engine::DebugTree Engine::debug_tree_cb(int root_token, int k, int l, int n_verify,
+                                        void (*fn)(void*, int, const int*, const int*, const int*, int, float*),
+                                        void* ctx) {
+    const int V = dims_.vocab;
+    if (k < 0 || l < 0) throw std::invalid_argument("expand_tree: negative k_draft or l_draft");
+    if (n_verify < 1) throw std::invalid_argument("rerank_candidates: n_verify must be >= 1");
+    if (k > k_max_ || l > l_max_) throw std::invalid_argument("debug_tree: k/l beyond engine capacity");
+    const int ke = (k == 0 || l == 0) ? 0 : std::min(k, V);
+    const int le = ke == 0 ? 0 : l;
+    const int nodes = ke ? tree_cap(ke, le) : 1;
+    StepSeqDev sd{0, 0, ke, le, std::min(n_verify, nodes), 0, ke ? 0 : -1, dims_.max_seq};
+    h2d(ss_.tokens, &root_token, 1, st_);
+    h2d(steps_, &sd, 1, st_);
+    std::vector<float> lg(static_cast<size_t>(std::max(1, ke)) * V);
+    if (ke) {
+        int id0 = 0, t0 = root_token, p0 = -1;
+        fn(ctx, 1, &id0, &t0, &p0, 1, lg.data());
+        h2d(logits_, lg.data(), V, st_);
+        launch_topk_lsm(logits_, V, 1, ke, topk_tok_, topk_lp_, st_);
+    }
+    launch_tree_root(1, steps_, ss_, tr_, topk_tok_, topk_lp_, std::max(1, ke), st_);
+    const int zero = 0;
+    h2d(drow_, &zero, 1, st_);
+    for (int level = 2; level <= le; ++level) {
+        launch_tree_frontier(1, level, steps_, drow_, ss_, tr_, rows_, dkv_.seq_stride, dkv_.scratch_base, dims_.d,
+                             st_);
+        int n = 0;
+        d2h(&n, tr_.n_nodes, 1, st_);
+        SGB_CUDA(cudaStreamSynchronize(st_));
+        std::vector<int> fr(ke), tok(n), par(n);
+        d2h(fr.data(), tr_.frontier, ke, st_);
+        d2h(tok.data(), tr_.tok, n, st_);
+        d2h(par.data(), tr_.par, n, st_);
+        SGB_CUDA(cudaStreamSynchronize(st_));
+        fn(ctx, ke, fr.data(), tok.data(), par.data(), n, lg.data());
+        h2d(logits_, lg.data(), static_cast<size_t>(ke) * V, st_);
+        launch_topk_lsm(logits_, V, ke, ke, topk_tok_, topk_lp_, st_);
+        launch_tree_expand(1, level, steps_, drow_, tr_, topk_tok_, topk_lp_, st_);
+    }
+    SGB_CUDA(cudaMemsetAsync(mask_dbg_, 0, static_cast<size_t>(sd.nsel) * sd.nsel, st_));
+    SGB_CUDA(cudaMemsetAsync(err_, 0, sizeof(int), st_));
+    launch_tree_select(1, steps_, ss_, tr_, rows_, tkv_.seq_stride, tkv_.scratch_base, mask_dbg_, err_, st_);
+    DebugTree out;
+    int n = 0;
+    d2h(&n, tr_.n_nodes, 1, st_);
+    SGB_CUDA(cudaStreamSynchronize(st_));
+    out.tok.resize(n);
+    out.par.resize(n);
+    out.dep.resize(n);
+    out.lp.resize(n);
+    out.conf.resize(n);
+    out.sel.resize(sd.nsel);
+    out.mask.resize(static_cast<size_t>(sd.nsel) * sd.nsel);
+    d2h(out.tok.data(), tr_.tok, n, st_);
+    d2h(out.par.data(), tr_.par, n, st_);
+    d2h(out.dep.data(), tr_.dep, n, st_);
+    d2h(out.lp.data(), tr_.lp, n, st_);
+    d2h(out.conf.data(), tr_.conf, n, st_);
+    d2h(out.sel.data(), tr_.sel, sd.nsel, st_);
+    d2h(out.mask.data(), mask_dbg_, out.mask.size(), st_);
+    int err = 0;
+    d2h(&err, err_, 1, st_);
+    SGB_CUDA(cudaStreamSynchronize(st_));
+    if (err & 8) throw std::invalid_argument("build_tree_mask: closure violation");
+    return out;
+}
+
+// ------------------------------------------------------------------ the rollout
+RolloutResult Engine::rollout(const RolloutArgs& a) {
+    const ModelDims& mc = dims_;
+    const int d = mc.d, V = mc.vocab, T = mc.max_seq;
+    // validation (scheduler.cpp:240-249)
+    if (a.prompts.empty()) throw std::invalid_argument("generate: prompts must be non-empty");
+    if (a.g < 1) throw std::invalid_argument("generate: g must be >= 1");
+    if (a.c_peak < 1) throw std::invalid_argument("generate: c_peak must be >= 1");
+    for (const auto& pr : a.prompts) {
+        if (pr.empty()) throw std::invalid_argument("generate: zero-length prompt");
+        if (static_cast<int>(pr.size()) > T - 1)
+            throw std::invalid_argument("generate: prompt longer than max_seq_len - 1");
+        for (int t : pr)
+            if (t < 0 || t >= V) throw std::invalid_argument("forward_target: token id out of range");
+    }
+    if (a.mode == 1) validate_spec(a.fixed, a.alpha, a.k_max, a.l_max, a.c_peak);
+    if (a.k_max > k_max_ || a.l_max > l_max_)
+        throw std::invalid_argument("generate: k_max/l_max exceed the engine's tree capacity");
+    if (a.temperature < 0) throw std::invalid_argument("sample_token: negative temperature");
+    if (!target_ready_ || !draft_ready_) throw std::runtime_error("weights not uploaded");
+    const int P = static_cast<int>(a.prompts.size());
+    const int n_seqs = P * a.g;
+    if (n_seqs > max_seqs_) throw std::invalid_argument("generate: more sequences than engine max_seqs");
+    if (!a.seq_max_new.empty() && static_cast<int>(a.seq_max_new.size()) != n_seqs)
+        throw std::invalid_argument("generate: seq_max_new size mismatch");
+
+    RolloutResult res;
+    const long long launches0 = launches_;
+    SGB_CUDA(cudaMemsetAsync(err_, 0, sizeof(int), st_));
+
+    // ---------------- sequence setup
+    std::vector<int> len(n_seqs), len_cap(n_seqs), fin(n_seqs, 0), dft_len(n_seqs, 0), plen(n_seqs);
+    std::vector<unsigned long long> seeds(n_seqs);
+    for (int pi = 0; pi < P; ++pi)
+        for (int r = 0; r < a.g; ++r) {
+            const int sid = pi * a.g + r;
+            const int q = static_cast<int>(a.prompts[pi].size());
+            plen[sid] = q;
+            seeds[sid] = mix_key_host(a.seed, static_cast<uint64_t>(sid + a.sid_offset) + 1);
+            const int mn = a.seq_max_new.empty() ? a.max_new_tokens : a.seq_max_new[sid];
+            len_cap[sid] = mn > 0 ? std::min(T, q + mn) : T;
+            h2d(ss_.tokens + static_cast<size_t>(sid) * T, a.prompts[pi].data(), q, st_);
+        }
+    h2d(ss_.seed, seeds.data(), n_seqs, st_);
+    for (const auto& pr : a.prompts) res.h2d_bytes += static_cast<long long>(pr.size()) * sizeof(int);
+    SGB_CUDA(cudaEventRecord(ev0_, st_));  // inputs resident in HBM from here on
+
+    // ---------------- prefill: one forward per chunk of distinct prompts (scheduler.cpp:259-294)
+    {
+        int pi = 0;
+        while (pi < P) {
+            int rows = 0, pe = pi;
+            while (pe < P && rows + static_cast<int>(a.prompts[pe].size()) <= max_rows_) rows += a.prompts[pe++].size();
+            if (pe == pi) throw std::invalid_argument("generate: prompt longer than engine max_rows");
+            std::vector<int> tok, pos, cl, chl, last_rows;
+            std::vector<long long> kvd, cb;
+            int maxq = 0;
+            for (int p2 = pi; p2 < pe; ++p2) {
+                const int s0 = p2 * a.g;
+                const int q = static_cast<int>(a.prompts[p2].size());
+                maxq = std::max(maxq, q);
+                for (int t = 0; t < q; ++t) {
+                    tok.push_back(a.prompts[p2][t]);
+                    pos.push_back(t);
+                    kvd.push_back(static_cast<long long>(s0) * T + t);
+                    cb.push_back(static_cast<long long>(s0) * T);
+                    cl.push_back(t + 1);
+                    chl.push_back(0);
+                }
+                last_rows.push_back(static_cast<int>(tok.size()) - 1);
+            }
+            upload_rows_host(rows, tok, pos, kvd, cb, cl, chl, {}, nullptr);
+            const int np = pe - pi;
+            h2d(lm_idx_, last_rows.data(), np, st_);
+            Fwd f;
+            f.M = rows;
+            f.y_out = y_;
+            f.logits = true;
+            f.lm_rows = np;
+            f.lm_idx = lm_idx_;
+            f.logits_out = logits_;
+            f.max_vlen = maxq;
+            f.attn_kv_unique = rows;
+            for (int p2 = pi; p2 < pe; ++p2) {
+                const double q = static_cast<double>(a.prompts[p2].size());
+                f.attn_row_keys += q * (q + 1) / 2;
+            }
+            forward(f);
+            res.target_forwards++;
+            // features of every member: feats[s][t] = hidden[row]
+            std::vector<int> src_row;
+            std::vector<long long> dst_off;
+            std::vector<int> srcs, dsts, pl, ems, emseq, emq, emcap, emrow, emkey;
+            std::vector<unsigned long long> emseed;
+            int row0 = 0;
+            for (int p2 = pi; p2 < pe; ++p2) {
+                const int q = static_cast<int>(a.prompts[p2].size());
+                for (int r = 0; r < a.g; ++r) {
+                    const int s = p2 * a.g + r;
+                    for (int t = 0; t < q; ++t) {
+                        src_row.push_back(row0 + t);
+                        dst_off.push_back((static_cast<long long>(s) * T + t) * d);
+                    }
+                    if (r > 0) {
+                        srcs.push_back(p2 * a.g);
+                        dsts.push_back(s);
+                        pl.push_back(q);
+                    }
+                    emseq.push_back(s);
+                    emq.push_back(q);
+                    emcap.push_back(len_cap[s]);
+                    emrow.push_back(p2 - pi);
+                    emseed.push_back(seeds[s]);
+                    emkey.push_back(q);
+                }
+                row0 += q;
+            }
+            const int nr = static_cast<int>(src_row.size());
+            for (int off = 0; off < nr; off += max_rows_) {  // chunk the copy descriptors
+                const int c = std::min(max_rows_, nr - off);
+                h2d(misc_i_, src_row.data() + off, c, st_);
+                h2d(misc_l_, dst_off.data() + off, c, st_);
+                launch_copy_rows_f32(y_, misc_i_, misc_l_, c, d, feats_, st_);
+                count();
+                SGB_CUDA(cudaStreamSynchronize(st_));
+            }
+            if (!srcs.empty()) {
+                const int n = static_cast<int>(srcs.size());
+                int* b = misc_i_;
+                h2d(b, srcs.data(), n, st_);
+                h2d(b + n, dsts.data(), n, st_);
+                h2d(b + 2 * n, pl.data(), n, st_);
+                launch_copy_kv_prefix(b, b + n, b + 2 * n, n, maxq, tkv_.layers, d, tkv_.K, tkv_.V, tkv_.n_slots,
+                                      tkv_.seq_stride, st_);
+                count();
+                SGB_CUDA(cudaStreamSynchronize(st_));
+            }
+            const int ne = static_cast<int>(emseq.size());
+            int* b = misc_i_;
+            h2d(b, emrow.data(), ne, st_);
+            h2d(b + ne, emkey.data(), ne, st_);
+            h2d(rows_.seed, emseed.data(), ne, st_);
+            launch_emit(logits_, V, b, rows_.seed, b + ne, ne, a.temperature, emitted_, err_, st_);
+            h2d(b + 2 * ne, emseq.data(), ne, st_);
+            h2d(b + 3 * ne, emq.data(), ne, st_);
+            h2d(lm_idx_, emcap.data(), ne, st_);
+            launch_prefill_commit(ne, b + 2 * ne, b + 3 * ne, lm_idx_, emitted_, ss_, st_);
+            count(2);
+            SGB_CUDA(cudaStreamSynchronize(st_));
+            pi = pe;
+        }
+        std::vector<int> t1(n_seqs), f1(n_seqs);
+        d2h(t1.data(), ss_.len, n_seqs, st_);
+        d2h(f1.data(), ss_.finished, n_seqs, st_);
+        SGB_CUDA(cudaStreamSynchronize(st_));
+        for (int s = 0; s < n_seqs; ++s) {
+            len[s] = t1[s];
+            fin[s] = f1[s];
+        }
+    }
+
+    // ---------------- step loop (scheduler.cpp:299-341)
+    std::vector<StepSeqDev> hs;
+    std::vector<int> drow, live;
+    for (int step = 0;; ++step) {
+        live.clear();
+        for (int s = 0; s < n_seqs; ++s)
+            if (!fin[s]) live.push_back(s);
+        const int B = static_cast<int>(live.size());
+        if (B == 0) break;
+        const int eff_b = a.early_term ? B : n_seqs;
+        SpecCfg cfg;
+        if (a.mode == 0) cfg = SpecCfg{1, 0, 0};
+        else if (a.mode == 1) cfg = a.fixed;
+        else cfg = plan(a.c_peak, eff_b, a.alpha, a.k_max, a.l_max);
+
+        // per-sequence shapes (scheduler.cpp:125-133)
+        hs.assign(B, StepSeqDev{});
+        int vrows = 0, n_spec = 0, max_l = 0, max_p = 0, kstep = 0;
+        for (int i = 0; i < B; ++i) {
+            const int s = live[i];
+            const int p = len[s] - 1;
+            int l_eff = std::min(cfg.l_draft, len_cap[s] - 1 - p);
+            int k_eff = l_eff >= 1 ? std::min(cfg.k_draft, V) : 0;
+            if (k_eff == 0) l_eff = 0;
+            const int nodes = k_eff ? tree_cap(k_eff, l_eff) : 1;
+            StepSeqDev& e = hs[i];
+            e.seq = s;
+            e.p = p;
+            e.k = k_eff;
+            e.l = l_eff;
+            e.nsel = std::min(cfg.n_verify, nodes);
+            e.vrow_off = vrows;
+            e.root_row = k_eff ? n_spec++ : -1;
+            e.len_cap = len_cap[s];
+            vrows += e.nsel;
+            max_l = std::max(max_l, l_eff);
+            max_p = std::max(max_p, p);
+            if (k_eff) kstep = k_eff;
+        }
+        if (vrows > max_rows_) throw std::invalid_argument("generate: verify rows exceed engine max_rows");
+        h2d(steps_, hs.data(), B, st_);
+        StepStat stat;
+        stat.b_cur = B;
+        stat.n_verify = cfg.n_verify;
+        stat.k_draft = cfg.k_draft;
+        stat.l_draft = cfg.l_draft;
+        stat.rows = vrows;
+
+        if (n_spec > 0) {
+            // ---- draft catch-up over committed pairs (t_j, f_{j-1}), j = dft_len+1..p (scheduler.cpp:137-157)
+            struct CU {
+                int s, j, spec;
+            };
+            std::vector<CU> cu;
+            for (int i = 0; i < B; ++i)
+                if (hs[i].k) {
+                    const int s = hs[i].seq;
+                    for (int j = dft_len[s] + 1; j <= hs[i].p; ++j) cu.push_back({s, j, hs[i].root_row});
+                }
+            const int ncu = static_cast<int>(cu.size());
+            for (int off = 0; off < ncu; off += max_rows_) {
+                const int M = std::min(max_rows_, ncu - off);
+                std::vector<int> seq(M), pos(M), cl(M), chl(M, 0), lastr, lasts;
+                std::vector<long long> kvd(M), cb(M), fo(M), dsto;
+                int maxj = 0;
+                for (int r = 0; r < M; ++r) {
+                    const CU& c = cu[off + r];
+                    seq[r] = c.s;
+                    pos[r] = c.j;
+                    kvd[r] = static_cast<long long>(c.s) * T + (c.j - 1);
+                    cb[r] = static_cast<long long>(c.s) * T;
+                    cl[r] = c.j;
+                    fo[r] = (static_cast<long long>(c.s) * T + (c.j - 1)) * d;
+                    maxj = std::max(maxj, c.j);
+                    const bool last = (off + r + 1 == ncu) || cu[off + r + 1].s != c.s;
+                    if (last) {
+                        lastr.push_back(r);
+                        lasts.push_back(c.spec);
+                        dsto.push_back((static_cast<long long>(c.s) * tr_.ds + 0) * d);
+                    }
+                }
+                upload_rows_host(M, {}, pos, kvd, cb, cl, chl, {}, &fo);
+                h2d(misc_i_, seq.data(), M, st_);
+                launch_gather_tokens(misc_i_, rows_.pos, M, ss_, rows_.tok, st_);
+                count();
+                Fwd f;
+                f.M = M;
+                f.draft = true;
+                f.feat_base = feats_;
+                f.y_out = y_;
+                f.max_vlen = maxj;
+                for (int r = 0; r < M; ++r) f.attn_row_keys += pos[r];
+                for (size_t t = 0; t < lastr.size(); ++t) f.attn_kv_unique += pos[lastr[t]];
+                forward(f);
+                res.draft_forwards++;
+                stat.draft_rows += M;
+                const int nl = static_cast<int>(lastr.size());
+                if (nl) {
+                    h2d(lm_idx_, lastr.data(), nl, st_);
+                    h2d(misc_l_, dsto.data(), nl, st_);
+                    launch_copy_rows_f32(y_, lm_idx_, misc_l_, nl, d, dfeat_, st_);  // root features
+                    launch_gather_rows_bf16(a_, lm_idx_, nl, d, a2_ + static_cast<size_t>(lasts[0]) * d, st_);
+                    count(2);
+                }
+                SGB_CUDA(cudaStreamSynchronize(st_));
+            }
+            for (int i = 0; i < B; ++i)
+                if (hs[i].k) dft_len[hs[i].seq] = hs[i].p;
+            // root logits -> level 1
+            lm_head(a2_, act_a2_, n_spec, logits_);
+            launch_topk_lsm(logits_, V, n_spec, kstep, topk_tok_, topk_lp_, st_);
+            launch_tree_root(B, steps_, ss_, tr_, topk_tok_, topk_lp_, kstep, st_);
+            count(2);
+            // levels 2..L: one batched draft forward per level
+            if (max_l >= 2) {
+                drow.assign(static_cast<size_t>(max_l - 1) * B, -1);
+                std::vector<int> lvl_rows(max_l + 1, 0);
+                for (int level = 2; level <= max_l; ++level) {
+                    int r = 0;
+                    for (int i = 0; i < B; ++i)
+                        if (hs[i].k && hs[i].l >= level) {
+                            drow[static_cast<size_t>(level - 2) * B + i] = r;
+                            r += hs[i].k;
+                        }
+                    lvl_rows[level] = r;
+                }
+                h2d(drow_, drow.data(), drow.size(), st_);
+                for (int level = 2; level <= max_l; ++level) {
+                    const int R = lvl_rows[level];
+                    if (R == 0) break;
+                    if (R > max_rows_) throw std::invalid_argument("generate: draft rows exceed engine max_rows");
+                    const int* dro = drow_ + static_cast<size_t>(level - 2) * B;
+                    launch_tree_frontier(B, level, steps_, dro, ss_, tr_, rows_, dkv_.seq_stride, dkv_.scratch_base,
+                                         d, st_);
+                    count();
+                    Fwd f;
+                    f.M = R;
+                    f.draft = true;
+                    f.feat_base = dfeat_;
+                    f.y_out = y_;
+                    f.logits = true;
+                    f.logits_out = logits_;
+                    f.max_vlen = max_p + level;
+                    for (int i = 0; i < B; ++i)
+                        if (hs[i].k && hs[i].l >= level) {
+                            f.attn_kv_unique += hs[i].p + level - 1;
+                            f.attn_row_keys += static_cast<double>(hs[i].k) * (hs[i].p + level - 1);
+                        }
+                    forward(f);
+                    res.draft_forwards++;
+                    stat.draft_rows += R;
+                    launch_copy_rows_f32(y_, nullptr, rows_.out_off, R, d, dfeat_, st_);
+                    launch_topk_lsm(logits_, V, R, kstep, topk_tok_, topk_lp_, st_);
+                    launch_tree_expand(B, level, steps_, dro, tr_, topk_tok_, topk_lp_, st_);
+                    count(3);
+                }
+            }
+        } else {
+            launch_tree_root(B, steps_, ss_, tr_, topk_tok_, topk_lp_, 1, st_);
+            count();
+        }
+
+        // ---- rerank + mask -> verify rows; one batched target forward (scheduler.cpp:208-217)
+        int pe0 = pbeg();
+        launch_tree_select(B, steps_, ss_, tr_, rows_, tkv_.seq_stride, tkv_.scratch_base, nullptr, err_, st_);
+        pend(kClsTree, pe0, 0, 0);
+        count();
+        Fwd f;
+        f.M = vrows;
+        f.y_out = y_;
+        f.logits = true;
+        f.logits_out = logits_;
+        f.max_vlen = max_p + max_l + 1;
+        for (int i = 0; i < B; ++i) {
+            f.attn_kv_unique += hs[i].p + hs[i].nsel;
+            f.attn_row_keys += static_cast<double>(hs[i].nsel) * (hs[i].p + 1);
+        }
+        forward(f);
+        res.target_forwards++;
+        // ---- acceptance, walk, commit (scheduler.cpp:219-231)
+        pe0 = pbeg();
+        launch_emit(logits_, V, nullptr, rows_.seed, rows_.key_pos, vrows, a.temperature, emitted_, err_, st_);
+        pend(kClsSample, pe0, 4.0 * vrows * V, 0);
+        pe0 = pbeg();
+        launch_walk_commit(B, steps_, ss_, tr_, rows_, emitted_, acc_rows_, result_, st_);
+        pend(kClsTree, pe0, 0, 0);
+        pe0 = pbeg();
+        launch_commit_kv(B, steps_, acc_rows_, result_, tkv_.layers, d, tkv_.K, tkv_.V, tkv_.n_slots, tkv_.seq_stride,
+                         tkv_.scratch_base, y_, feats_, T, st_);
+        pend(kClsCommit, pe0, 0, 0);
+        count(3);
+        d2h(h_result_, result_, 2 * B, st_);
+        d2h(h_result_ + 2 * B, err_, 1, st_);
+        SGB_CUDA(cudaStreamSynchronize(st_));
+        const int err = h_result_[2 * B];
+        if (err & 1) throw std::runtime_error("forward_target: non-finite logits");
+        if (err & 8) throw std::invalid_argument("build_tree_mask: closure violation");
+        pflush();
+        for (int i = 0; i < B; ++i) {
+            const int s = live[i];
+            const int acc = h_result_[2 * i];
+            len[s] += acc;
+            fin[s] = h_result_[2 * i + 1];
+            stat.accepted += acc;
+            res.events.push_back(step);
+            res.events.push_back(s);
+            res.events.push_back(acc);
+        }
+        res.steps.push_back(stat);
+        res.total_accepted += stat.accepted;
+        res.total_verify_slots += B;
+    }
+    SGB_CUDA(cudaEventRecord(ev1_, st_));
+
+    // ---------------- results (scheduler.cpp:343-353)
+    std::vector<int> h_eos(n_seqs);
+    d2h(h_eos.data(), ss_.hit_eos, n_seqs, st_);
+    res.tokens.resize(n_seqs);
+    res.prompt_len = plen;
+    for (int s = 0; s < n_seqs; ++s) {
+        res.tokens[s].resize(len[s]);
+        d2h(res.tokens[s].data(), ss_.tokens + static_cast<size_t>(s) * T, len[s], st_);
+    }
+    if (a.want_features) {
+        res.features.resize(n_seqs);
+        for (int s = 0; s < n_seqs; ++s) {
+            res.features[s].resize(static_cast<size_t>(len[s] - 1) * d);
+            d2h(res.features[s].data(), feats_ + static_cast<size_t>(s) * T * d, res.features[s].size(), st_);
+        }
+    }
+    SGB_CUDA(cudaStreamSynchronize(st_));
+    res.hit_eos = h_eos;
+    for (int s = 0; s < n_seqs; ++s) {
+        res.d2h_bytes += static_cast<long long>(len[s]) * sizeof(int);
+        if (a.want_features) res.d2h_bytes += static_cast<long long>(len[s] - 1) * d * sizeof(float);
+    }
+    float ms = 0.f;
+    SGB_CUDA(cudaEventElapsedTime(&ms, ev0_, ev1_));
+    res.seconds = ms * 1e-3;
+    res.kernel_launches = launches_ - launches0;
+    return res;
+}
+
+}  // namespace sgb

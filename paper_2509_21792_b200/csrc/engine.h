@@ -1,0 +1,225 @@
+// Host engine of the B200 rollout: device-resident weights, paged-by-sequence KV stores,
+// and the step loop of generate_dynamic_batch (scheduler.cpp:236-354) expressed as
+// batched sm_100a kernels. One Engine per GPU; the C-ABI (capi.cpp) owns it.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "gemm.h"
+#include "kernels.h"
+
+namespace sgb {
+
+struct ModelDims {
+    int vocab = 0, d = 0, layers = 0, heads = 0, dff = 0, max_seq = 0;
+};
+
+struct LayerDev {
+    GemmWeight qkv, wo, w1, w2;
+    const float *ln1_g = nullptr, *ln1_b = nullptr, *ln2_g = nullptr, *ln2_b = nullptr;
+};
+
+// Offsets of the reference's flat parameter layout (tinylm.hpp:58-81, 133-189).
+struct FlatLayout {
+    size_t tok_emb = 0, pos_emb = 0, lnf_g = 0, lnf_b = 0, lm_head = 0, w_fuse = 0, total = 0;
+    struct L {
+        size_t ln1_g, ln1_b, wq, wk, wv, wo, ln2_g, ln2_b, w1, w2;
+    };
+    std::vector<L> layers;
+    static FlatLayout target(const ModelDims& m);
+    static FlatLayout draft(const ModelDims& m, int n_layers);
+};
+
+struct KvStore {
+    __nv_bfloat16* K = nullptr;
+    __nv_bfloat16* V = nullptr;
+    int layers = 0;
+    long long n_slots = 0;       // per layer
+    long long seq_stride = 0;    // slots per sequence region
+    long long scratch_base = 0;  // first scratch slot
+    long long layer_stride() const { return n_slots; }
+};
+
+struct SpecCfg {
+    int n_verify = 1, k_draft = 0, l_draft = 0;
+};
+
+struct RolloutArgs {
+    std::vector<std::vector<int>> prompts;
+    int g = 1;
+    double alpha = 2.0;
+    int k_max = 10, l_max = 6, c_peak = 1;
+    int mode = 0;  // 0 vanilla, 1 fixed_spec, 2 adaptive_spec (scheduler.hpp:46)
+    bool early_term = true;
+    double temperature = 0.0;
+    uint64_t seed = 0;
+    int max_new_tokens = 0;
+    SpecCfg fixed;
+    std::vector<int> seq_max_new;  // optional per-sequence caps (c3 extension)
+    bool want_features = true;
+    int sid_offset = 0;  // global sid of local sequence 0 (seed parity under sharding)
+};
+
+struct StepStat {
+    int b_cur = 0, n_verify = 0, k_draft = 0, l_draft = 0, accepted = 0, rows = 0, draft_rows = 0;
+};
+
+// Per kernel-class device time (CUDA events on the launching stream) and algorithmic work.
+enum KernelClass { kClsGemm = 0, kClsAttn, kClsRow, kClsLmHead, kClsSample, kClsTree, kClsCommit, kNumCls };
+struct KernelProfile {
+    double ms = 0, bytes = 0, flops = 0;
+    long long launches = 0;
+};
+
+struct RolloutResult {
+    std::vector<std::vector<int>> tokens;
+    std::vector<int> prompt_len, hit_eos;
+    std::vector<std::vector<float>> features;
+    std::vector<StepStat> steps;
+    std::vector<int> events;  // (step, seq, accepted) triples
+    long long total_accepted = 0, total_verify_slots = 0;
+    long long target_forwards = 0, draft_forwards = 0, kernel_launches = 0;
+    double seconds = 0;  // device time of the step loop incl. prefill (CUDA events)
+    long long h2d_bytes = 0, d2h_bytes = 0;
+};
+
+class Engine {
+   public:
+    Engine(const ModelDims& dims, int draft_layers, int device, int max_seqs, int max_rows, int k_max, int l_max);
+    ~Engine();
+    Engine(const Engine&) = delete;
+    Engine& operator=(const Engine&) = delete;
+
+    const ModelDims& dims() const { return dims_; }
+    int draft_layers() const { return dlayers_; }
+    size_t target_param_count() const { return tlay_.total; }
+    size_t draft_param_count() const { return dlay_.total; }
+
+    void upload_target(const float* flat, size_t n);  // host fp32, reference layout
+    void upload_draft(const float* flat, size_t n);
+    void init_random(uint64_t seed);                  // benchmark weights (device RNG)
+    void download_draft(float* flat, size_t n);
+
+    // ---- per-op parity entry points (host in / host out)
+    void cache_reset(int slot, bool draft);
+    int cache_len(int slot, bool draft) const;
+    void cache_read(int slot, bool draft, float* k, float* v);  // [layers][len][d]
+    void cache_gather_tail(int slot, int base, const int* keep, int n);
+    void forward_target(int slot, const int* tokens, const int* positions, int rows, const unsigned char* mask,
+                        float* logits, float* hidden);
+    void forward_draft(int slot, const int* tokens, const float* prev_feat, const int* positions, int rows, bool extend,
+                       float* feats, float* logits);
+    void emit(const float* logits, int rows, int vocab, double temperature, const unsigned long long* seeds,
+              const int* key_pos, int* out);
+    void topk_logsoftmax(const float* logits, int rows, int vocab, int k, int* tok, double* lp);
+
+    // ---- the rollout (generate_dynamic_batch drop-in)
+    RolloutResult rollout(const RolloutArgs& args);
+
+    // device-resident state of the last rollout (for the draft update)
+    const float* d_feats() const { return feats_; }
+    const int* d_tokens() const { return ss_.tokens; }
+    cudaStream_t stream() const { return st_; }
+    long long launches() const { return launches_; }
+    void set_profiling(bool on);
+    void read_profile(KernelProfile* out, int n, bool reset);
+
+    // debug tree driver (tests): expands one tree on device with host-supplied logits
+    struct DebugTree {
+        std::vector<int> tok, par, dep, sel;
+        std::vector<double> lp, conf;
+        std::vector<unsigned char> mask;
+    };
+    DebugTree debug_tree_cb(int root_token, int k, int l, int n_verify,
+                            void (*fn)(void* ctx, int n_front, const int* node_ids, const int* tok, const int* par,
+                                       int n_nodes, float* logits_out),
+                            void* ctx);
+
+   private:
+    struct Fwd {
+        int M = 0;
+        bool draft = false;
+        const float* feat_base = nullptr;  // draft fuse features
+        float* y_out = nullptr;            // final LN fp32 [M][d]
+        bool logits = false;
+        int lm_rows = 0;
+        const int* lm_idx = nullptr;  // subset of rows for the LM head (nullptr = all)
+        float* logits_out = nullptr;
+        int max_vlen = 0;
+        double attn_kv_unique = 0;  // distinct KV tokens read per layer (roofline bytes)
+        double attn_row_keys = 0;   // sum over rows of keys attended (roofline flops)
+    };
+    void forward(const Fwd& f);
+    void convert_target(const float* staging);
+    void convert_draft();
+    void alloc_rows();
+    void upload_rows_host(int M, const std::vector<int>& tok, const std::vector<int>& pos,
+                          const std::vector<long long>& kv_dst, const std::vector<long long>& ctx_base,
+                          const std::vector<int>& ctx_len, const std::vector<int>& chain_len,
+                          const std::vector<long long>& chain, const std::vector<long long>* feat_off);
+    void lm_head(const __nv_bfloat16* a_rows, const GemmAct& act, int R, float* logits);
+    void count(int n = 1) { launches_ += n; }
+    void gemm(const GemmWeight& w, const GemmAct& a, int M);
+    int pbeg();
+    void pend(int cls, int e0, double bytes, double flops);
+    void pflush();
+    struct PRec {
+        int cls, e0, e1;
+        double bytes, flops;
+    };
+    bool prof_ = false;
+    std::vector<cudaEvent_t> evs_;
+    int ev_used_ = 0;
+    std::vector<PRec> precs_;
+    KernelProfile prof_cls_[kNumCls];
+
+    ModelDims dims_;
+    int dlayers_, device_, max_seqs_, max_rows_, k_max_, l_max_;
+    cudaStream_t st_ = nullptr;
+    FlatLayout tlay_, dlay_;
+
+    // weights
+    std::vector<LayerDev> tL_, dL_;
+    __nv_bfloat16 *tw_ = nullptr, *dw_ = nullptr;  // bf16 weight arenas
+    float* tsmall_ = nullptr;                      // target fp32: tok_emb | pos_emb | LN params
+    float* dmaster_ = nullptr;                     // draft fp32 flat (master weights)
+    const float *tok_emb_ = nullptr, *pos_emb_ = nullptr, *lnf_g_ = nullptr, *lnf_b_ = nullptr;
+    const float *dlnf_g_ = nullptr, *dlnf_b_ = nullptr;
+    GemmWeight lm_head_, w_fuse_;
+    bool target_ready_ = false, draft_ready_ = false;
+
+    // kv + sequence state
+    KvStore tkv_, dkv_;
+    SeqStateDev ss_{};
+    float* feats_ = nullptr;  // [S][max_seq][d]
+    float* dfeat_ = nullptr;  // [S][ds][d]
+    TreeDev tr_{};
+    std::vector<int> cache_len_t_, cache_len_d_;
+
+    // activations
+    float *x_ = nullptr, *q_ = nullptr, *y_ = nullptr, *part_ = nullptr, *logits_ = nullptr, *featin_ = nullptr;
+    float *pacc_ = nullptr, *pml_ = nullptr;
+    __nv_bfloat16 *a_ = nullptr, *att_ = nullptr, *h_ = nullptr, *fuse_ = nullptr, *a2_ = nullptr;
+    GemmAct act_a_, act_att_, act_h_, act_fuse_, act_a2_;
+    size_t part_elems_ = 0;
+    int max_vlen_cap_ = 0;
+    // row descriptors
+    RowsDev rows_{};
+    int* lm_idx_ = nullptr;
+    int *topk_tok_ = nullptr, *emitted_ = nullptr, *acc_rows_ = nullptr, *result_ = nullptr, *err_ = nullptr;
+    double* topk_lp_ = nullptr;
+    StepSeqDev* steps_ = nullptr;
+    int* drow_ = nullptr;
+    int* misc_i_ = nullptr;
+    long long* misc_l_ = nullptr;
+    unsigned char* mask_dbg_ = nullptr;
+    int *h_result_ = nullptr;  // pinned
+    long long launches_ = 0;
+    cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
+};
+
+}  // namespace sgb

@@ -1,0 +1,127 @@
+// Launchers of the sm_100a kernels (rowops.cu, attention.cu, sample.cu, tree.cu).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstddef>
+
+namespace sgb {
+
+constexpr int kMaxChain = 8;  // l_max + 1 (root + tree depth) per attention row
+
+// Per-row attention metadata (see attention.cu).
+struct AttnRowsDev {
+    const long long* ctx_base;     // [M] global KV slot of virtual index 0
+    const int* ctx_len;            // [M] contiguous prefix length
+    const int* chain_len;          // [M] number of chain (tree-path) slots
+    const long long* chain_slots;  // [M][kMaxChain] global KV slots, root-first
+};
+
+// ---- rowops.cu
+void launch_embed_ln(const int* tokens, const int* positions, int M, int d, const float* tok_emb, const float* pos_emb,
+                     const float* g, const float* b, float* x, __nv_bfloat16* a, cudaStream_t st);
+void launch_reduce_residual_ln(const float* P, int S, int M, int d, float* x, bool accumulate, const float* pos_emb,
+                               const int* positions, const float* g, const float* b, __nv_bfloat16* a, float* y,
+                               cudaStream_t st);
+void launch_reduce_gelu(const float* P, int S, int M, int N, __nv_bfloat16* out, cudaStream_t st);
+void launch_reduce_plain(const float* P, int S, int M, int N, float* out, cudaStream_t st);
+void launch_reduce_qkv(const float* P, int S, int M, int d, float* q, __nv_bfloat16* kc, __nv_bfloat16* vc,
+                       const long long* kv_dst, cudaStream_t st);
+void launch_gather_fuse(const int* tokens, const long long* feat_off, const float* feat_base, const float* tok_emb,
+                        int R, int d, __nv_bfloat16* out, cudaStream_t st);
+void launch_transpose_to_bf16(const float* src, int in, int out_dim, __nv_bfloat16* dst, int dst_ld, cudaStream_t st);
+void launch_gather_rows_bf16(const __nv_bfloat16* src, const int* idx, int R, int d, __nv_bfloat16* dst,
+                             cudaStream_t st);
+void launch_init_normal(float* out, size_t n, unsigned long long seed, float std_, cudaStream_t st);
+void launch_fill(float* out, size_t n, float v, cudaStream_t st);
+
+// ---- attention.cu
+int attn_splits_for(int max_virtual_len);
+void launch_attention(const float* q, const __nv_bfloat16* K, const __nv_bfloat16* V, const AttnRowsDev& rows, int M,
+                      int H, int d, int max_virtual_len, float* part_acc, float* part_ml, __nv_bfloat16* out,
+                      cudaStream_t st);
+
+// ---- sample.cu
+void launch_emit(const float* logits, int V, const int* row_idx, const unsigned long long* seeds, const int* key_pos,
+                 int R, double temperature, int* out, int* err, cudaStream_t st);
+void launch_topk_lsm(const float* logits, int V, int R, int k, int* out_tok, double* out_lp, cudaStream_t st);
+
+// ---- tree.cu
+// Per-step descriptor of the live sequences (index i = live order), uploaded once a step.
+struct StepSeqDev {
+    int seq;        // global sequence slot
+    int p;          // root position (= tokens.size()-1)
+    int k, l;       // k_eff, l_eff (scheduler.cpp:127-133)
+    int nsel;       // rows this sequence verifies
+    int vrow_off;   // first verify row
+    int root_row;   // row of this sequence's root logits in the draft top-k output (-1: no draft)
+    int len_cap;
+};
+
+struct TreeDev {
+    int tmax;                 // node capacity per sequence
+    int ds;                   // draft feature / scratch slots per sequence
+    int* tok;                 // [S][tmax]
+    int* par;                 // [S][tmax]
+    int* dep;                 // [S][tmax]
+    double* lp;               // [S][tmax]
+    double* conf;             // [S][tmax]
+    int* fslot;               // [S][tmax] draft feature slot of expanded nodes
+    int* n_nodes;             // [S]
+    int* lvl_start;           // [S]
+    int* lvl_cnt;             // [S]
+    int* frontier;            // [S][16]
+    int* sel;                 // [S][tmax] selected node ids (ascending)
+};
+
+struct SeqStateDev {
+    int* tokens;                  // [S][max_seq]
+    int* len;                     // [S]
+    int* finished;                // [S]
+    int* hit_eos;                 // [S]
+    unsigned long long* seed;     // [S]
+    int max_seq;
+};
+
+// Rows of a forward pass (inputs the forward consumes + attention metadata).
+struct RowsDev {
+    int* tok;              // [M]
+    int* pos;              // [M]
+    long long* kv_dst;     // [M]
+    long long* ctx_base;   // [M]
+    int* ctx_len;          // [M]
+    int* chain_len;        // [M]
+    long long* chain;      // [M][kMaxChain]
+    long long* feat_off;   // [M] draft: offset of the previous feature (fuse input)
+    long long* out_off;    // [M] draft: destination offset of the output feature
+    int* key_pos;          // [M] verify: sampling key position
+    unsigned long long* seed;  // [M] verify: sequence seed
+    int* par_row;          // [M] verify: parent row within the sequence (-1 root)
+};
+
+void launch_tree_root(int B, const StepSeqDev* steps, const SeqStateDev& ss, const TreeDev& tr, const int* topk_tok,
+                      const double* topk_lp, int kmax_row, cudaStream_t st);
+void launch_tree_frontier(int B, int level, const StepSeqDev* steps, const int* drow_off, const SeqStateDev& ss,
+                          const TreeDev& tr, const RowsDev& rows, long long dcache_stride, long long dscratch_base,
+                          int d, cudaStream_t st);
+void launch_tree_expand(int B, int level, const StepSeqDev* steps, const int* drow_off, const TreeDev& tr,
+                        const int* topk_tok, const double* topk_lp, cudaStream_t st);
+void launch_tree_select(int B, const StepSeqDev* steps, const SeqStateDev& ss, const TreeDev& tr, const RowsDev& rows,
+                        long long tcache_stride, long long tscratch_base, unsigned char* mask_dbg, int* err,
+                        cudaStream_t st);
+void launch_walk_commit(int B, const StepSeqDev* steps, const SeqStateDev& ss, const TreeDev& tr, const RowsDev& rows,
+                        const int* emitted, int* acc_rows, int* result, cudaStream_t st);
+void launch_commit_kv(int B, const StepSeqDev* steps, const int* acc_rows, const int* result, int layers, int d,
+                      __nv_bfloat16* K, __nv_bfloat16* V, long long layer_stride, long long tcache_stride,
+                      long long tscratch_base, const float* hidden, float* feats, int max_seq, cudaStream_t st);
+void launch_copy_rows_f32(const float* src, const int* src_row, const long long* dst_off, int R, int d, float* dst,
+                          cudaStream_t st);
+void launch_copy_kv_prefix(const int* src_seq, const int* dst_seq, const int* plen, int n, int max_plen, int layers,
+                           int d, __nv_bfloat16* K, __nv_bfloat16* V, long long layer_stride, long long seq_stride,
+                           cudaStream_t st);
+void launch_prefill_commit(int n, const int* seqs, const int* qlen, const int* len_cap, const int* emitted,
+                           const SeqStateDev& ss, cudaStream_t st);
+void launch_gather_tokens(const int* seq, const int* pos, int R, const SeqStateDev& ss, int* out, cudaStream_t st);
+
+}  // namespace sgb
