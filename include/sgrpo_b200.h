@@ -130,6 +130,9 @@ int sgb_profile_enable(sgb_engine* e, int on);
 int sgb_profile_read(sgb_engine* e, int n_cls, double* ms, double* bytes, double* flops, long long* launches,
                      int reset);
 
+/* GEMM microbenchmark (device-resident operands): average device ms per launch. */
+int sgb_bench_gemm(int M, int N, int K, int splits, int iters, double* ms_out);
+
 /* tcgen05 GEMM self-test: out[M][N] = bf16(x)[M][K] . bf16(w)[N][K]^T (K-major). */
 int sgb_debug_gemm(const float* w, const float* x, int M, int N, int K, float* out, int* splits_out);
 

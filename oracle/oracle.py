@@ -817,7 +817,8 @@ def generate_dynamic_batch(tgt: Params, dr: Params, prompts: Sequence[Sequence[i
                            c_peak: int, alpha: float = 2.0, k_max: int = 10, l_max: int = 6,
                            mode: str = "vanilla", early_term: bool = True, temperature: float = 0.0,
                            seed: int = 0, max_new_tokens: int = 0, fixed: Optional[SpecConfig] = None,
-                           seq_max_new: Optional[Sequence[int]] = None, trace=None) -> GenResult:
+                           seq_max_new: Optional[Sequence[int]] = None, trace=None,
+                           sid_offset: int = 0) -> GenResult:
     """scheduler.cpp:236-354.
 
     ``seq_max_new`` (per-sequence caps, indexed by global sid) is the c3 variable-length
@@ -846,7 +847,7 @@ def generate_dynamic_batch(tgt: Params, dr: Params, prompts: Sequence[Sequence[i
             sid = pi * g + r
             s = _Seq()
             s.id = sid
-            s.seed = mix_key(seed, sid + 1)
+            s.seed = mix_key(seed, sid + sid_offset + 1)  # global sid under data-parallel sharding
             s.tokens = [int(t) for t in prompt]
             s.prompt_len = q
             mn = seq_max_new[sid] if seq_max_new is not None else max_new_tokens

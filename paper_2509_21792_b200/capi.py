@@ -18,7 +18,7 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsgrpo_b200.so")
+LIB_PATH = os.environ.get("SGB_LIB") or os.path.join(HERE, "libsgrpo_b200.so")  # SGB_LIB: A/B kernel variants
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2509_21792_b200.build` "
@@ -85,14 +85,15 @@ def device_count() -> int:
     return n.value
 
 
-def debug_gemm(w: np.ndarray, x: np.ndarray):
-    """out = bf16(x) @ bf16(w).T via the tcgen05 GEMM; returns (out, splits)."""
+def debug_gemm(w: np.ndarray, x: np.ndarray, splits: int = 0):
+    """out = bf16(x) @ bf16(w).T via the tcgen05 GEMM (optionally forcing the K split);
+    returns (out, the split count the auto policy picks)."""
     w = np.ascontiguousarray(w, np.float32)
     x = np.ascontiguousarray(x, np.float32)
     N, K = w.shape
     M = x.shape[0]
     out = np.zeros((M, N), np.float32)
-    sp = C.c_int()
+    sp = C.c_int(splits)
     _check(_lib.sgb_debug_gemm(_p(w, C.c_float), _p(x, C.c_float), M, N, K, _p(out, C.c_float), C.byref(sp)))
     return out, sp.value
 

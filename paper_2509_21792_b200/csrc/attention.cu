@@ -77,11 +77,16 @@ __global__ void __launch_bounds__(32 * kWarps)
         if (valid) slot = v < ctx_len ? ctx_base + v : chain[v - ctx_len];
         float s = -INFINITY;
         if (valid) {
+            // all 16-byte pieces of this lane's key row are issued before any math so the
+            // whole row (DH*2 bytes) is in flight at once
             const uint4* kr = reinterpret_cast<const uint4*>(K + slot * d + h * DH);
+            uint4 kreg[DH / 8];
+#pragma unroll
+            for (int e8 = 0; e8 < DH / 8; ++e8) kreg[e8] = __ldg(kr + e8);
             float dot = 0.f;
 #pragma unroll
             for (int e8 = 0; e8 < DH / 8; ++e8) {
-                const uint4 u = __ldg(kr + e8);
+                const uint4 u = kreg[e8];
                 const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&u);
 #pragma unroll
                 for (int t = 0; t < 4; ++t) {
@@ -100,23 +105,49 @@ __global__ void __launch_bounds__(32 * kWarps)
 #pragma unroll
         for (int i = 0; i < PL; ++i) acc[i] *= alpha;
         const int nvalid = min(32, v1 - c);
-        for (int j = 0; j < nvalid; ++j) {
-            const float pj = __shfl_sync(0xffffffffu, p, j);
-            const long long sj = __shfl_sync(0xffffffffu, slot, j);
-            const __nv_bfloat16* vr = V + sj * d + h * DH + lane * PL;
-            if constexpr (PL == 4) {
-                const uint2 u = __ldg(reinterpret_cast<const uint2*>(vr));
-                const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
-                const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
-                acc[0] = fmaf(pj, a.x, acc[0]);
-                acc[1] = fmaf(pj, a.y, acc[1]);
-                acc[2] = fmaf(pj, b.x, acc[2]);
-                acc[3] = fmaf(pj, b.y, acc[3]);
-            } else if constexpr (PL == 2) {
-                const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(vr));
-                acc[0] = fmaf(pj, a.x, acc[0]);
-                acc[1] = fmaf(pj, a.y, acc[1]);
-            } else {
+        // P.V over the chunk: fully unrolled so the 32 value-row loads (one coalesced
+        // DH*2-byte row per key across the warp) are all in flight before the FMAs; the
+        // accumulation order stays j = 0..31.
+        if constexpr (PL == 4) {
+            uint2 vv[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                const long long sj = __shfl_sync(0xffffffffu, slot, j);
+                if (j < nvalid) vv[j] = __ldg(reinterpret_cast<const uint2*>(V + sj * d + h * DH + lane * PL));
+            }
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                const float pj = __shfl_sync(0xffffffffu, p, j);
+                if (j < nvalid) {
+                    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&vv[j].x));
+                    const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&vv[j].y));
+                    acc[0] = fmaf(pj, a.x, acc[0]);
+                    acc[1] = fmaf(pj, a.y, acc[1]);
+                    acc[2] = fmaf(pj, b.x, acc[2]);
+                    acc[3] = fmaf(pj, b.y, acc[3]);
+                }
+            }
+        } else if constexpr (PL == 2) {
+            unsigned vv[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                const long long sj = __shfl_sync(0xffffffffu, slot, j);
+                if (j < nvalid) vv[j] = __ldg(reinterpret_cast<const unsigned*>(V + sj * d + h * DH + lane * PL));
+            }
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                const float pj = __shfl_sync(0xffffffffu, p, j);
+                if (j < nvalid) {
+                    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&vv[j]));
+                    acc[0] = fmaf(pj, a.x, acc[0]);
+                    acc[1] = fmaf(pj, a.y, acc[1]);
+                }
+            }
+        } else {
+            for (int j = 0; j < nvalid; ++j) {
+                const float pj = __shfl_sync(0xffffffffu, p, j);
+                const long long sj = __shfl_sync(0xffffffffu, slot, j);
+                const __nv_bfloat16* vr = V + sj * d + h * DH + lane * PL;
 #pragma unroll
                 for (int i = 0; i < PL; ++i) acc[i] = fmaf(pj, __bfloat162float(vr[i]), acc[i]);
             }

@@ -10,9 +10,10 @@
 #include <string>
 #include <vector>
 
-#include "../../include/sgrpo_b200.h"
+#include "sgrpo_b200.h"
 #include "engine.h"
 #include "gemm.h"
+#include "kernels.h"
 #include "util.h"
 
 struct sgb_engine {
@@ -225,6 +226,115 @@ int sgb_rollout(sgb_engine* e, const int* prompts, const int* prompt_lens, int n
     });
 }
 
+// GEMM microbenchmark: device-resident random bf16 operands, fused fp32 epilogue,
+// average device ms over `iters` launches (CUDA events on the launching stream).
+int sgb_bench_gemm(int M, int N, int K, int splits, int iters, double* ms_out) {
+    return guarded([&] {
+        const int cap = ((M + 255) / 256) * 256;
+        std::vector<__nv_bfloat16> hw(static_cast<size_t>(N) * K), hx(static_cast<size_t>(cap) * K);
+        uint64_t st = 12345;
+        auto rnd = [&]() {
+            st = st * 6364136223846793005ULL + 1442695040888963407ULL;
+            return static_cast<float>((st >> 40) & 0xFFFF) / 65536.0f - 0.5f;
+        };
+        for (auto& v : hw) v = __float2bfloat16(0.05f * rnd());
+        for (auto& v : hx) v = __float2bfloat16(rnd());
+        __nv_bfloat16 *dw = nullptr, *dx = nullptr;
+        float* dp = nullptr;
+        SGB_CUDA(cudaMalloc(&dw, hw.size() * 2));
+        SGB_CUDA(cudaMalloc(&dx, hx.size() * 2));
+        SGB_CUDA(cudaMemcpy(dw, hw.data(), hw.size() * 2, cudaMemcpyHostToDevice));
+        SGB_CUDA(cudaMemcpy(dx, hx.data(), hx.size() * 2, cudaMemcpyHostToDevice));
+        sgb::GemmWeight gw;
+        gw.init(dw, N, K);
+        sgb::GemmAct ga;
+        ga.init(dx, cap, K);
+        sgb::GemmWorkspace ws;
+        ws.cap_floats = sgb::gemm_ws_floats(M, N, K);
+        ws.ctr_cap = 1 << 16;
+        SGB_CUDA(cudaMalloc(&ws.buf, ws.cap_floats * 4));
+        SGB_CUDA(cudaMalloc(&ws.ctr, ws.ctr_cap * sizeof(int)));
+        SGB_CUDA(cudaMemset(ws.ctr, 0, ws.ctr_cap * sizeof(int)));
+        SGB_CUDA(cudaMalloc(&dp, static_cast<size_t>(M) * N * 4));
+        sgb::GemmEpi epi;
+        epi.kind = sgb::kEpiF32;
+        epi.f32 = dp;
+        epi.ld = N;
+        cudaEvent_t a, b;
+        SGB_CUDA(cudaEventCreate(&a));
+        SGB_CUDA(cudaEventCreate(&b));
+        for (int i = 0; i < 3; ++i) sgb::gemm_run(gw, ga, M, epi, ws, 0, splits);
+        SGB_CUDA(cudaEventRecord(a, 0));
+        for (int i = 0; i < iters; ++i) sgb::gemm_run(gw, ga, M, epi, ws, 0, splits);
+        SGB_CUDA(cudaEventRecord(b, 0));
+        SGB_CUDA(cudaEventSynchronize(b));
+        SGB_KCHECK();
+        float ms = 0.f;
+        SGB_CUDA(cudaEventElapsedTime(&ms, a, b));
+        *ms_out = ms / iters;
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        cudaFree(dw);
+        cudaFree(dx);
+        cudaFree(dp);
+        cudaFree(ws.buf);
+        cudaFree(ws.ctr);
+    });
+}
+
+// Decode-attention microbenchmark: B sequences x H heads, each one query row attending to
+// ctx cached keys + itself (AR decode shape), KV in a [B*(ctx+1)][d] bf16 store.
+int sgb_bench_attention(int B, int ctx, int H, int dh, int iters, double* ms_out) {
+    return guarded([&] {
+        const int d = H * dh;
+        const long long slots = static_cast<long long>(B) * (ctx + 1);
+        __nv_bfloat16 *K = nullptr, *V = nullptr, *out = nullptr;
+        float *q = nullptr, *pacc = nullptr, *pml = nullptr;
+        SGB_CUDA(cudaMalloc(&K, slots * d * 2));
+        SGB_CUDA(cudaMalloc(&V, slots * d * 2));
+        SGB_CUDA(cudaMemset(K, 0x3c, slots * d * 2));
+        SGB_CUDA(cudaMemset(V, 0x3c, slots * d * 2));
+        SGB_CUDA(cudaMalloc(&q, static_cast<size_t>(B) * d * 4));
+        SGB_CUDA(cudaMemset(q, 0, static_cast<size_t>(B) * d * 4));
+        SGB_CUDA(cudaMalloc(&out, static_cast<size_t>(B) * d * 2));
+        const int ns = sgb::attn_splits_for(ctx + 1);
+        SGB_CUDA(cudaMalloc(&pacc, static_cast<size_t>(B) * d * ns * 4));
+        SGB_CUDA(cudaMalloc(&pml, static_cast<size_t>(B) * H * ns * 2 * 4));
+        std::vector<long long> base(B), chain(static_cast<size_t>(B) * sgb::kMaxChain, 0);
+        std::vector<int> cl(B, ctx), chl(B, 1);
+        for (int b = 0; b < B; ++b) {
+            base[b] = static_cast<long long>(b) * (ctx + 1);
+            chain[static_cast<size_t>(b) * sgb::kMaxChain] = base[b] + ctx;
+        }
+        long long *dbase = nullptr, *dchain = nullptr;
+        int *dcl = nullptr, *dchl = nullptr;
+        SGB_CUDA(cudaMalloc(&dbase, B * 8));
+        SGB_CUDA(cudaMalloc(&dchain, chain.size() * 8));
+        SGB_CUDA(cudaMalloc(&dcl, B * 4));
+        SGB_CUDA(cudaMalloc(&dchl, B * 4));
+        SGB_CUDA(cudaMemcpy(dbase, base.data(), B * 8, cudaMemcpyHostToDevice));
+        SGB_CUDA(cudaMemcpy(dchain, chain.data(), chain.size() * 8, cudaMemcpyHostToDevice));
+        SGB_CUDA(cudaMemcpy(dcl, cl.data(), B * 4, cudaMemcpyHostToDevice));
+        SGB_CUDA(cudaMemcpy(dchl, chl.data(), B * 4, cudaMemcpyHostToDevice));
+        sgb::AttnRowsDev ar{dbase, dcl, dchl, dchain};
+        cudaEvent_t a, b;
+        SGB_CUDA(cudaEventCreate(&a));
+        SGB_CUDA(cudaEventCreate(&b));
+        for (int i = 0; i < 2; ++i) sgb::launch_attention(q, K, V, ar, B, H, d, ctx + 1, pacc, pml, out, 0);
+        SGB_CUDA(cudaEventRecord(a, 0));
+        for (int i = 0; i < iters; ++i) sgb::launch_attention(q, K, V, ar, B, H, d, ctx + 1, pacc, pml, out, 0);
+        SGB_CUDA(cudaEventRecord(b, 0));
+        SGB_CUDA(cudaEventSynchronize(b));
+        float ms = 0.f;
+        SGB_CUDA(cudaEventElapsedTime(&ms, a, b));
+        *ms_out = ms / iters;
+        void* ptrs[] = {K, V, out, q, pacc, pml, dbase, dchain, dcl, dchl};
+        for (void* p : ptrs) cudaFree(p);
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+    });
+}
+
 int sgb_profile_enable(sgb_engine* e, int on) {
     return guarded([&] { E(e).set_profiling(on != 0); });
 }
@@ -261,19 +371,24 @@ int sgb_debug_gemm(const float* w, const float* x, int M, int N, int K, float* o
         gw.init(dw, N, K);
         sgb::GemmAct ga;
         ga.init(dx, cap, K);
-        const size_t np = static_cast<size_t>(gw.splits) * M * N;
-        SGB_CUDA(cudaMalloc(&dp, np * 4));
-        sgb::gemm_launch(gw, ga, dp, M, 0);
+        sgb::GemmWorkspace ws;
+        ws.cap_floats = sgb::gemm_ws_floats(M, N, K);
+        ws.ctr_cap = 1 << 14;
+        SGB_CUDA(cudaMalloc(&ws.buf, ws.cap_floats * 4));
+        SGB_CUDA(cudaMalloc(&ws.ctr, ws.ctr_cap * sizeof(int)));
+        SGB_CUDA(cudaMemset(ws.ctr, 0, ws.ctr_cap * sizeof(int)));
+        SGB_CUDA(cudaMalloc(&dp, static_cast<size_t>(M) * N * 4));
+        sgb::GemmEpi epi;
+        epi.kind = sgb::kEpiF32;
+        epi.f32 = dp;
+        epi.ld = N;
+        sgb::gemm_run(gw, ga, M, epi, ws, 0, splits_out ? *splits_out : 0);
         SGB_KCHECK();
         SGB_CUDA(cudaDeviceSynchronize());
-        std::vector<float> part(np);
-        SGB_CUDA(cudaMemcpy(part.data(), dp, np * 4, cudaMemcpyDeviceToHost));
-        for (size_t i = 0; i < static_cast<size_t>(M) * N; ++i) {
-            float s = part[i];
-            for (int k = 1; k < gw.splits; ++k) s += part[static_cast<size_t>(k) * M * N + i];
-            out[i] = s;
-        }
-        if (splits_out) *splits_out = gw.splits;
+        SGB_CUDA(cudaMemcpy(out, dp, static_cast<size_t>(M) * N * 4, cudaMemcpyDeviceToHost));
+        if (splits_out) *splits_out = sgb::gemm_splits_for(M, N, K);
+        cudaFree(ws.buf);
+        cudaFree(ws.ctr);
         cudaFree(dw);
         cudaFree(dx);
         cudaFree(dp);

@@ -230,16 +230,11 @@ Engine::Engine(const ModelDims& dims, int draft_layers, int device, int max_seqs
     act_a2_.init(a2_, static_cast<int>(R), static_cast<int>(d));
     act_h_.init(h_, static_cast<int>(R), static_cast<int>(F));
     act_fuse_.init(fuse_, static_cast<int>(R), static_cast<int>(2 * d));
-    size_t pe = 0;
-    auto upd = [&](int N, int K) { pe = std::max(pe, static_cast<size_t>(gemm_splits(N, K)) * N); };
-    upd(3 * d, d);
-    upd(d, d);
-    upd(F, d);
-    upd(d, F);
-    upd(d, 2 * d);
-    if (gemm_splits(V, d) > 1) upd(V, d);
-    part_elems_ = pe * R;
-    part_ = dalloc<float>(part_elems_);
+    ws_.cap_floats = static_cast<size_t>(64) << 20;  // 256 MiB split-K workspace
+    ws_.buf = dalloc<float>(ws_.cap_floats);
+    ws_.ctr_cap = 1 << 16;
+    ws_.ctr = dalloc<int>(ws_.ctr_cap);
+    SGB_CUDA(cudaMemset(ws_.ctr, 0, sizeof(int) * ws_.ctr_cap));
     logits_ = dalloc<float>(R * V);
     max_vlen_cap_ = static_cast<int>(T) + kMaxChain;
     const int ns = attn_splits_for(max_vlen_cap_);
@@ -285,7 +280,7 @@ Engine::~Engine() {
     void* ptrs[] = {tw_, dw_, tsmall_, dmaster_, tkv_.K, tkv_.V, dkv_.K, dkv_.V, ss_.tokens, ss_.len, ss_.finished,
                     ss_.hit_eos, ss_.seed, feats_, dfeat_, tr_.tok, tr_.par, tr_.dep, tr_.lp, tr_.conf, tr_.fslot,
                     tr_.sel, tr_.n_nodes, tr_.lvl_start, tr_.lvl_cnt, tr_.frontier, x_, q_, y_, featin_, a_, att_,
-                    a2_, h_, fuse_, part_, logits_, pacc_, pml_, rows_.tok, rows_.pos, rows_.kv_dst,
+                    a2_, h_, fuse_, ws_.buf, ws_.ctr, logits_, pacc_, pml_, rows_.tok, rows_.pos, rows_.kv_dst,
                     rows_.ctx_base, rows_.ctx_len, rows_.chain_len, rows_.chain, rows_.feat_off, rows_.out_off,
                     rows_.key_pos, rows_.seed, rows_.par_row, lm_idx_, topk_tok_, topk_lp_, emitted_, acc_rows_,
                     result_, err_, steps_, drow_, misc_i_, misc_l_, mask_dbg_};
@@ -459,23 +454,24 @@ void Engine::init_random(uint64_t seed) {
 
 // ------------------------------------------------------------------ forward
 void Engine::lm_head(const __nv_bfloat16*, const GemmAct& act, int R, float* out) {
-    const double K = dims_.d, N = dims_.vocab;
-    const int e0 = pbeg();
-    if (lm_head_.splits == 1) {
-        gemm_launch(lm_head_, act, out, R, st_);
-        count();
-    } else {
-        gemm_launch(lm_head_, act, part_, R, st_);
-        launch_reduce_plain(part_, lm_head_.splits, R, dims_.vocab, out, st_);
-        count(2);
-    }
-    pend(kClsLmHead, e0, N * K * 2 + R * K * 2 + R * N * 4.0, 2.0 * R * N * K);
+    GemmEpi e;
+    e.kind = kEpiF32;
+    e.f32 = out;
+    e.ld = dims_.vocab;
+    gemm(lm_head_, act, R, e, kClsLmHead, 4.0);
 }
 
-void Engine::gemm(const GemmWeight& w, const GemmAct& a, int M) {
+void Engine::gemm(const GemmWeight& w, const GemmAct& a, int M, const GemmEpi& epi, int cls, double out_bytes) {
     const int e0 = pbeg();
-    gemm_launch(w, a, part_, M, st_);
-    pend(kClsGemm, e0, 2.0 * w.N * w.K + 2.0 * M * w.K + 4.0 * w.splits * M * w.N, 2.0 * M * w.N * w.K);
+    gemm_run(w, a, M, epi, ws_, st_, force_splits_);
+    pend(cls, e0, 2.0 * w.N * w.K + 2.0 * M * w.K + out_bytes * M * w.N, 2.0 * M * w.N * w.K);
+    count();
+}
+
+void Engine::ln(int M, const float* g, const float* b, float* y) {
+    const int e0 = pbeg();
+    launch_reduce_residual_ln(nullptr, 0, M, dims_.d, x_, false, nullptr, nullptr, g, b, a_, y, st_);
+    pend(kClsRow, e0, static_cast<double>(M) * dims_.d * (4 + 2 + (y ? 4 : 0)), 0);
     count();
 }
 
@@ -498,45 +494,49 @@ void Engine::forward(const Fwd& f) {
         launch_gather_fuse(rows_.tok, rows_.feat_off, f.feat_base, tok_emb_, M, d, fuse_, st_);
         pend(kClsRow, e0, 3 * row_bytes, 0);
         count();
-        gemm(w_fuse_, act_fuse_, M);
-        e0 = pbeg();
-        launch_reduce_residual_ln(part_, w_fuse_.splits, M, d, x_, false, pos_emb_, rows_.pos, L[0].ln1_g,
-                                  L[0].ln1_b, a_, nullptr, st_);
-        pend(kClsRow, e0, (w_fuse_.splits + 2.5) * row_bytes, 0);
-        count();
+        GemmEpi e;
+        e.kind = kEpiFusePos;
+        e.f32 = x_;
+        e.pos_emb = pos_emb_;
+        e.pos = rows_.pos;
+        e.ld = d;
+        gemm(w_fuse_, act_fuse_, M, e, kClsGemm, 8.0);
+        ln(M, L[0].ln1_g, L[0].ln1_b, nullptr);
     }
     const size_t lstride = static_cast<size_t>(kv.n_slots) * d;
     const double attn_bytes = f.attn_kv_unique * d * 4.0 + row_bytes * 1.5;
     const double attn_flops = 4.0 * f.attn_row_keys * d;
     for (size_t l = 0; l < L.size(); ++l) {
         const LayerDev& W = L[l];
-        __nv_bfloat16* Kl = kv.K + l * lstride;
-        __nv_bfloat16* Vl = kv.V + l * lstride;
-        gemm(W.qkv, act_a_, M);
+        GemmEpi eq;
+        eq.kind = kEpiQKV;
+        eq.f32 = q_;
+        eq.kv_dst = rows_.kv_dst;
+        eq.K = kv.K + l * lstride;
+        eq.V = kv.V + l * lstride;
+        eq.ld = 3 * d;
+        eq.d = d;
+        gemm(W.qkv, act_a_, M, eq, kClsGemm, 8.0 / 3.0);
         e0 = pbeg();
-        launch_reduce_qkv(part_, W.qkv.splits, M, d, q_, Kl, Vl, rows_.kv_dst, st_);
-        pend(kClsRow, e0, (3.0 * W.qkv.splits + 2.0) * row_bytes, 0);
-        e0 = pbeg();
-        launch_attention(q_, Kl, Vl, ar, M, H, d, f.max_vlen, pacc_, pml_, att_, st_);
+        launch_attention(q_, eq.K, eq.V, ar, M, H, d, f.max_vlen, pacc_, pml_, att_, st_);
         pend(kClsAttn, e0, attn_bytes, attn_flops);
-        gemm(W.wo, act_att_, M);
-        e0 = pbeg();
-        launch_reduce_residual_ln(part_, W.wo.splits, M, d, x_, true, nullptr, nullptr, W.ln2_g, W.ln2_b, a_,
-                                  nullptr, st_);
-        pend(kClsRow, e0, (W.wo.splits + 2.5) * row_bytes, 0);
-        gemm(W.w1, act_a_, M);
-        e0 = pbeg();
-        launch_reduce_gelu(part_, W.w1.splits, M, F, h_, st_);
-        pend(kClsRow, e0, (4.0 * W.w1.splits + 2.0) * M * F, 0);
-        gemm(W.w2, act_h_, M);
+        count();
+        GemmEpi er;
+        er.kind = kEpiResid;
+        er.f32 = x_;
+        er.ld = d;
+        gemm(W.wo, act_att_, M, er, kClsGemm, 8.0);
+        ln(M, W.ln2_g, W.ln2_b, nullptr);
+        GemmEpi eg;
+        eg.kind = kEpiGeluBF16;
+        eg.b16 = h_;
+        eg.ld = F;
+        gemm(W.w1, act_a_, M, eg, kClsGemm, 2.0);
+        gemm(W.w2, act_h_, M, er, kClsGemm, 8.0);
         const bool last = l + 1 == L.size();
         const float* g = last ? (f.draft ? dlnf_g_ : lnf_g_) : L[l + 1].ln1_g;
         const float* b = last ? (f.draft ? dlnf_b_ : lnf_b_) : L[l + 1].ln1_b;
-        e0 = pbeg();
-        launch_reduce_residual_ln(part_, W.w2.splits, M, d, x_, true, nullptr, nullptr, g, b, a_,
-                                  last ? f.y_out : nullptr, st_);
-        pend(kClsRow, e0, (W.w2.splits + 2.5 + (last ? 1 : 0)) * row_bytes, 0);
-        count(6);
+        ln(M, g, b, last ? f.y_out : nullptr);
     }
     if (f.logits) {
         if (f.lm_idx) {
@@ -987,7 +987,7 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
                 h2d(b, srcs.data(), n, st_);
                 h2d(b + n, dsts.data(), n, st_);
                 h2d(b + 2 * n, pl.data(), n, st_);
-                launch_copy_kv_prefix(b, b + n, b + 2 * n, n, maxq, tkv_.layers, d, tkv_.K, tkv_.V, tkv_.n_slots,
+                launch_copy_kv_prefix(b, b + n, b + 2 * n, n, maxq, tkv_.layers, d, tkv_.K, tkv_.V, tkv_.n_slots * d,
                                       tkv_.seq_stride, st_);
                 count();
                 SGB_CUDA(cudaStreamSynchronize(st_));
@@ -1203,7 +1203,7 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
         launch_walk_commit(B, steps_, ss_, tr_, rows_, emitted_, acc_rows_, result_, st_);
         pend(kClsTree, pe0, 0, 0);
         pe0 = pbeg();
-        launch_commit_kv(B, steps_, acc_rows_, result_, tkv_.layers, d, tkv_.K, tkv_.V, tkv_.n_slots, tkv_.seq_stride,
+        launch_commit_kv(B, steps_, acc_rows_, result_, tkv_.layers, d, tkv_.K, tkv_.V, tkv_.n_slots * d, tkv_.seq_stride,
                          tkv_.scratch_base, y_, feats_, T, st_);
         pend(kClsCommit, pe0, 0, 0);
         count(3);

@@ -126,6 +126,7 @@ class Engine {
     cudaStream_t stream() const { return st_; }
     long long launches() const { return launches_; }
     void set_profiling(bool on);
+    void set_force_splits(int s) { force_splits_ = s; }
     void read_profile(KernelProfile* out, int n, bool reset);
 
     // debug tree driver (tests): expands one tree on device with host-supplied logits
@@ -163,7 +164,8 @@ class Engine {
                           const std::vector<long long>& chain, const std::vector<long long>* feat_off);
     void lm_head(const __nv_bfloat16* a_rows, const GemmAct& act, int R, float* logits);
     void count(int n = 1) { launches_ += n; }
-    void gemm(const GemmWeight& w, const GemmAct& a, int M);
+    void gemm(const GemmWeight& w, const GemmAct& a, int M, const GemmEpi& epi, int cls, double out_bytes);
+    void ln(int M, const float* g, const float* b, float* y);
     int pbeg();
     void pend(int cls, int e0, double bytes, double flops);
     void pflush();
@@ -201,11 +203,12 @@ class Engine {
     std::vector<int> cache_len_t_, cache_len_d_;
 
     // activations
-    float *x_ = nullptr, *q_ = nullptr, *y_ = nullptr, *part_ = nullptr, *logits_ = nullptr, *featin_ = nullptr;
+    float *x_ = nullptr, *q_ = nullptr, *y_ = nullptr, *logits_ = nullptr, *featin_ = nullptr;
     float *pacc_ = nullptr, *pml_ = nullptr;
     __nv_bfloat16 *a_ = nullptr, *att_ = nullptr, *h_ = nullptr, *fuse_ = nullptr, *a2_ = nullptr;
     GemmAct act_a_, act_att_, act_h_, act_fuse_, act_a2_;
-    size_t part_elems_ = 0;
+    GemmWorkspace ws_;
+    int force_splits_ = 0;
     int max_vlen_cap_ = 0;
     // row descriptors
     RowsDev rows_{};

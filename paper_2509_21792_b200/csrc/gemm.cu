@@ -1,19 +1,33 @@
-// tcgen05 + TMA GEMM for sm_100a:  P[s][t][o] = sum_{k in split s} X[t][k] * W[o][k]
+// tcgen05 + TMA GEMM for sm_100a: persistent, warp-specialised, fused epilogues and a
+// batch-invariant split-K.
+//
+//   Y[t][o] = sum_k X[t][k] * W[o][k]      (X = token rows, W = weight, both K-major bf16)
 //
 // Replaces the reference's scalar i-k-j nn::matmul (include/sgrpo/nn.hpp:15-29) for every
-// projection of the decode forward (tinylm.hpp:325-327 q/k/v, :396 wo, :400 w1, :402 w2,
-// :458 lm_head, :528 w_fuse). Weights live on the device K-major ([out][in], bf16), so
-// y = x.W of the reference becomes a "TN" GEMM with the weight as the UMMA A operand
-// (M = 128 output features per tile) and the token rows as the B operand (N = BN tokens).
-// This swap-AB mapping keeps the tensor core busy at decode batch sizes (1..256 rows),
-// where the kernel streams weight tiles at HBM rate.
+// projection of the decode forward: q/k/v (tinylm.hpp:325-327), wo (:396), w1 (:400),
+// w2 (:402), lm_head (:458) and the draft fuse (:528). Weights are stored K-major
+// ([out][in], bf16), so the reference's y = x.W is a "TN" GEMM whose UMMA A operand is
+// the weight tile (M = 128 output features) and whose B operand is the token tile
+// (N = BN in {16,32,64,128} tokens): the swap-AB mapping that keeps tcgen05 busy at
+// decode batch sizes, where the kernel streams weight tiles at HBM rate.
 //
-// Batch invariance (SURVEY.md §7 hard part 1): the K split (grid.y) is a function of the
-// weight shape only, each output element accumulates its K range in the same order for
-// every BN, and partial sums are reduced in split order by the epilogue kernels
-// (rowops.cu). A row's result therefore never depends on how many rows share the launch.
+// Persistent: one CTA per SM walks work units (m_tile, n_tile, k_split) round-robin; the
+// smem stage ring and the two TMEM accumulator buffers run continuously across units, so
+// the epilogue of one tile overlaps the MMAs of the next.
+// Roles (320 threads): warp 0 = TMA producer, warp 1 = MMA issuer (+TMEM owner),
+// warps 2-9 = epilogue (TMEM lane quarter = warp % 4 -> one output feature per thread;
+// two warps per quarter split the token columns).
+//
+// Batch invariance (SURVEY.md §7 hard part 1). K is cut into fixed 256-wide chunks.
+// Every chunk is accumulated separately in TMEM, read out, and the chunk sums are added
+// in fp32 registers strictly in chunk order: ((c0 + c1) + c2) + ... A K split only decides
+// WHICH CTA computes which chunks: split 0 keeps the running prefix, later splits publish
+// their raw chunk sums, and the last-arriving CTA continues the same sequential sum. The
+// bits of an output element are therefore independent of M, of the token tile BN and of
+// the split count, which makes the speculative and the AR rollouts bit-identical.
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <stdexcept>
 #include <string>
@@ -25,37 +39,127 @@ namespace sgb {
 
 namespace {
 
-constexpr int kBK = 64;          // 64 bf16 = 128 B = one swizzle row
-constexpr int kBM = 128;         // output features per tile (UMMA M)
+constexpr int kBK = 64;       // 64 bf16 = 128 B = one swizzle row
+constexpr int kBM = 128;      // output features per tile (UMMA M)
+constexpr int kChunkKB = 4;   // k-blocks per accumulation chunk (K = 256); fixes the fp32 association
 constexpr int kABytes = kBM * kBK * 2;
+constexpr int kThreads = 320;  // TMA warp, MMA warp, 8 epilogue warps (2 per TMEM lane quarter)
+constexpr int kEpiThreads = 256;
+constexpr int kNumSMs = 148;
 
 template <int BN>
 struct GemmCfg {
     static constexpr int kBBytes = BN * kBK * 2;
     static constexpr int kStage = kABytes + kBBytes;
-    static constexpr int kStages = (200 * 1024) / kStage > 8 ? 8 : (200 * 1024) / kStage;
-    static constexpr int kTmemCols = BN < 32 ? 32 : BN;
+    static constexpr int kStages = (196 * 1024) / kStage > 8 ? 8 : (196 * 1024) / kStage;
+    static constexpr int kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;
     static constexpr int kSmem = kStages * kStage + 1024 /*align*/ + 256 /*barriers*/;
 };
 
+__device__ __forceinline__ float gelu_tanh(float x) {
+    const float c = 0.7978845608028654f;
+    return 0.5f * x * (1.0f + tanhf(c * (x + 0.044715f * x * x * x)));
+}
+
+// Element-wise epilogue (split-K finisher path).
+__device__ __forceinline__ void epi_store(const GemmEpi& e, int t, int o, float v) {
+    const size_t i = static_cast<size_t>(t) * e.ld + o;
+    switch (e.kind) {
+        case kEpiF32: e.f32[i] = v; break;
+        case kEpiBF16: e.b16[i] = __float2bfloat16(v); break;
+        case kEpiGeluBF16: e.b16[i] = __float2bfloat16(gelu_tanh(v)); break;
+        case kEpiResid: e.f32[i] += v; break;
+        case kEpiQKV:
+            if (o < e.d) e.f32[static_cast<size_t>(t) * e.d + o] = v;
+            else if (o < 2 * e.d) e.K[e.kv_dst[t] * e.d + (o - e.d)] = __float2bfloat16(v);
+            else e.V[e.kv_dst[t] * e.d + (o - 2 * e.d)] = __float2bfloat16(v);
+            break;
+        case kEpiFusePos: e.f32[i] = v + e.pos_emb[static_cast<size_t>(e.pos[t]) * e.ld + o]; break;
+    }
+}
+
+// Tile epilogue from registers: one branch on the (uniform) kind, then a tight loop over
+// this thread's token columns. Stores are coalesced along the feature dimension o.
+template <int HB>
+__device__ __forceinline__ void epi_store_run(const GemmEpi& e, int t0, int n, int o, const float* run) {
+    switch (e.kind) {
+        case kEpiF32:
+#pragma unroll
+            for (int j = 0; j < HB; ++j)
+                if (j < n) e.f32[static_cast<size_t>(t0 + j) * e.ld + o] = run[j];
+            break;
+        case kEpiBF16:
+#pragma unroll
+            for (int j = 0; j < HB; ++j)
+                if (j < n) e.b16[static_cast<size_t>(t0 + j) * e.ld + o] = __float2bfloat16(run[j]);
+            break;
+        case kEpiGeluBF16:
+#pragma unroll
+            for (int j = 0; j < HB; ++j)
+                if (j < n) e.b16[static_cast<size_t>(t0 + j) * e.ld + o] = __float2bfloat16(gelu_tanh(run[j]));
+            break;
+        case kEpiResid:
+#pragma unroll
+            for (int j = 0; j < HB; ++j)
+                if (j < n) e.f32[static_cast<size_t>(t0 + j) * e.ld + o] += run[j];
+            break;
+        case kEpiQKV:
+            if (o < e.d) {
+#pragma unroll
+                for (int j = 0; j < HB; ++j)
+                    if (j < n) e.f32[static_cast<size_t>(t0 + j) * e.d + o] = run[j];
+            } else {
+                __nv_bfloat16* base = o < 2 * e.d ? e.K + (o - e.d) : e.V + (o - 2 * e.d);
+#pragma unroll
+                for (int j = 0; j < HB; ++j)
+                    if (j < n) base[e.kv_dst[t0 + j] * e.d] = __float2bfloat16(run[j]);
+            }
+            break;
+        case kEpiFusePos:
+#pragma unroll
+            for (int j = 0; j < HB; ++j)
+                if (j < n)
+                    e.f32[static_cast<size_t>(t0 + j) * e.ld + o] =
+                        run[j] + e.pos_emb[static_cast<size_t>(e.pos[t0 + j]) * e.ld + o];
+            break;
+    }
+}
+
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
+struct Unit {
+    int m0, n0, split, tile;
+};
+
+__device__ __forceinline__ Unit decode_unit(int u, int m_tiles, int n_tiles, int BN) {
+    Unit r;
+    const int mt = u % m_tiles;
+    const int rest = u / m_tiles;
+    const int nt = rest % n_tiles;
+    r.split = rest / n_tiles;
+    r.m0 = mt * BN;
+    r.n0 = nt * kBM;
+    r.tile = nt * m_tiles + mt;
+    return r;
+}
+
 template <int BN>
-__global__ void __launch_bounds__(128, 1)
-    gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap mapW, const __grid_constant__ CUtensorMap mapX,
-                        float* __restrict__ out, int M, int N, int kb_per_split, int kb_total) {
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap mapW, const __grid_constant__ CUtensorMap mapX, int M,
+                        int N, int kb_total, int n_chunks, int cps, int S, int m_tiles, int n_tiles, GemmEpi epi,
+                        float* __restrict__ ws, int* __restrict__ ctr) {
     using Cfg = GemmCfg<BN>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::kStages * Cfg::kStage);
     uint64_t* empty = full + Cfg::kStages;
-    uint64_t* done = empty + Cfg::kStages;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+    uint64_t* tfull = empty + Cfg::kStages;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int m0 = blockIdx.x * BN;
-    const int n0 = blockIdx.y * kBM;
-    const int split = blockIdx.z;
-    const int kb0 = split * kb_per_split;
-    const int nkb = min(kb_per_split, kb_total - kb0);
+    const int n_units = m_tiles * n_tiles * S;
 
     if (warp == 0 && lane == 0) {
         tma_prefetch(&mapW);
@@ -64,7 +168,10 @@ __global__ void __launch_bounds__(128, 1)
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        mbar_init(done, 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], kEpiThreads / 32);
+        }
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc<Cfg::kTmemCols>(tmem_slot);
@@ -73,51 +180,130 @@ __global__ void __launch_bounds__(128, 1)
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    if (warp == 0 && lane == 0) {
-        // TMA producer: weights are streamed once (evict-first), activations stay in L2.
-        const uint64_t pol_w = policy_evict_first();
-        for (int i = 0; i < nkb; ++i) {
-            const int s = i % Cfg::kStages;
-            if (i >= Cfg::kStages) mbar_wait(&empty[s], ((i / Cfg::kStages) & 1) ^ 1);
-            uint8_t* a = smem + s * Cfg::kStage;
-            mbar_arrive_expect_tx(&full[s], Cfg::kStage);
-            tma_load_2d_hint(a, &mapW, &full[s], (kb0 + i) * kBK, n0, pol_w);
-            tma_load_2d(a + kABytes, &mapX, &full[s], (kb0 + i) * kBK, m0);
+    if (warp == 0) {
+        if (lane == 0) {
+            const uint64_t pol_w = policy_evict_first();
+            int i = 0;
+            for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+                const Unit un = decode_unit(u, m_tiles, n_tiles, BN);
+                const int kb_begin = un.split * cps * kChunkKB;
+                const int kb_end = min(kb_total, (un.split + 1) * cps * kChunkKB);
+                for (int kb = kb_begin; kb < kb_end; ++kb, ++i) {
+                    const int s = i % Cfg::kStages;
+                    if (i >= Cfg::kStages) mbar_wait(&empty[s], ((i / Cfg::kStages) & 1) ^ 1);
+                    uint8_t* a = smem + s * Cfg::kStage;
+                    mbar_arrive_expect_tx(&full[s], Cfg::kStage);
+                    tma_load_2d_hint(a, &mapW, &full[s], kb * kBK, un.n0, pol_w);
+                    tma_load_2d(a + kABytes, &mapX, &full[s], kb * kBK, un.m0);
+                }
+            }
         }
-    } else if (warp == 1 && lane == 0) {
-        // MMA issuer: one thread drives the tensor core; accumulator lives in TMEM.
-        constexpr uint32_t idesc = idesc_bf16_m128(BN);
-        for (int i = 0; i < nkb; ++i) {
-            const int s = i % Cfg::kStages;
-            mbar_wait(&full[s], (i / Cfg::kStages) & 1);
-            tc_fence_after();
-            const uint32_t a = smem_u32(smem + s * Cfg::kStage);
-            const uint64_t adesc = sw128_desc(a), bdesc = sw128_desc(a + kABytes);
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = idesc_bf16_m128(BN);
+            int i = 0, it = 0;
+            for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+                const Unit un = decode_unit(u, m_tiles, n_tiles, BN);
+                const int c_begin = un.split * cps, c_end = min(n_chunks, c_begin + cps);
+                for (int c = c_begin; c < c_end; ++c, ++it) {
+                    const int buf = it & 1;
+                    if (it >= 2) mbar_wait(&tempty[buf], ((it >> 1) - 1) & 1);
+                    tc_fence_after();
+                    const int lo = c * kChunkKB, hi = min(kb_total, lo + kChunkKB);
+                    for (int kb = lo; kb < hi; ++kb, ++i) {
+                        const int s = i % Cfg::kStages;
+                        mbar_wait(&full[s], (i / Cfg::kStages) & 1);
+                        tc_fence_after();
+                        const uint32_t a = smem_u32(smem + s * Cfg::kStage);
+                        const uint64_t adesc = sw128_desc(a), bdesc = sw128_desc(a + kABytes);
 #pragma unroll
-            for (int k = 0; k < kBK / 16; ++k)
-                umma_bf16(tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (i | k) != 0);
-            umma_commit(&empty[s]);
+                        for (int k = 0; k < kBK / 16; ++k)
+                            umma_bf16(tmem + buf * BN, adesc + 2 * k, bdesc + 2 * k, idesc, (kb != lo || k != 0));
+                        umma_commit(&empty[s]);
+                    }
+                    umma_commit(&tfull[buf]);
+                }
+            }
         }
-        umma_commit(done);
-    }
-    __syncwarp();
-    mbar_wait(done, 0);
-    tc_fence_after();
-
-    // Epilogue: warp w owns TMEM lanes [32w, 32w+32) = output features n0+32w+lane; the
-    // columns are token rows. Stores are coalesced along the feature dimension.
-    const int o = n0 + 32 * warp + lane;
-    float* dst = out + static_cast<size_t>(split) * M * N;
-#pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 16) {
-        if (m0 + c0 >= M) break;
-        float v[16];
-        tmem_ld16(tmem + (static_cast<uint32_t>(32 * warp) << 16) + c0, v);
-        if (o < N) {
+    } else {
+        // ---------------- epilogue warps: TMEM lane quarter q (output feature o), column half h
+        constexpr int HB = BN / 2;
+        const int q = warp & 3;
+        const int h = (warp - 2) >> 2;
+        const int r = 32 * q + lane;
+        const int j0 = h * HB;
+        int it = 0;
+        for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+            const Unit un = decode_unit(u, m_tiles, n_tiles, BN);
+            const int o = un.n0 + r;
+            const int ncols = min(BN, M - un.m0);
+            const int nmine = max(0, min(HB, ncols - j0));
+            const int c_begin = un.split * cps, c_end = min(n_chunks, c_begin + cps);
+            float* wst = ws ? ws + static_cast<size_t>(un.tile) * n_chunks * BN * kBM : nullptr;
+            float run[HB];
+            for (int c = c_begin; c < c_end; ++c, ++it) {
+                const int buf = it & 1;
+                mbar_wait(&tfull[buf], (it >> 1) & 1);
+                tc_fence_after();
+                float v[HB];
+                tmem_ld<HB>(tmem + (static_cast<uint32_t>(32 * q) << 16) + buf * BN + j0, v);
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty[buf]);
+                if (un.split == 0) {
+                    if (c == c_begin) {
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                const int t = m0 + c0 + j;
-                if (t < M) dst[static_cast<size_t>(t) * N + o] = v[j];
+                        for (int j = 0; j < HB; ++j) run[j] = v[j];
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < HB; ++j) run[j] += v[j];
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < HB; ++j)
+                        if (j < nmine) wst[(static_cast<size_t>(c) * BN + j0 + j) * kBM + r] = v[j];
+                }
+            }
+            if (S == 1) {
+                if (o < N) epi_store_run<HB>(epi, un.m0 + j0, nmine, o, run);
+            } else {
+                if (un.split == 0)
+#pragma unroll
+                    for (int j = 0; j < HB; ++j)
+                        if (j < nmine) wst[static_cast<size_t>(j0 + j) * kBM + r] = run[j];
+                __threadfence();
+                epi_bar();
+                if (threadIdx.x == 64) {
+                    const int old = atomicAdd(&ctr[un.tile], 1);
+                    *last_flag = (old == S - 1);
+                }
+                epi_bar();
+                const int last = *last_flag;
+                if (last) {
+                    __threadfence();
+                    if (o < N) {
+                        for (int j = j0; j < j0 + nmine; ++j) {
+                            // the finisher continues the sequential chunk sum; loads are
+                            // independent so issue them 4 at a time
+                            float v = __ldcg(&wst[static_cast<size_t>(j) * kBM + r]);
+                            int c = cps;
+                            for (; c + 4 <= n_chunks; c += 4) {
+                                const float a0 = __ldcg(&wst[(static_cast<size_t>(c) * BN + j) * kBM + r]);
+                                const float a1 = __ldcg(&wst[(static_cast<size_t>(c + 1) * BN + j) * kBM + r]);
+                                const float a2 = __ldcg(&wst[(static_cast<size_t>(c + 2) * BN + j) * kBM + r]);
+                                const float a3 = __ldcg(&wst[(static_cast<size_t>(c + 3) * BN + j) * kBM + r]);
+                                v += a0;
+                                v += a1;
+                                v += a2;
+                                v += a3;
+                            }
+                            for (; c < n_chunks; ++c) v += __ldcg(&wst[(static_cast<size_t>(c) * BN + j) * kBM + r]);
+                            epi_store(epi, un.m0 + j, o, v);
+                        }
+                    }
+                    if (threadIdx.x == 64) ctr[un.tile] = 0;
+                }
+                epi_bar();  // last_flag is reused by the next unit
             }
         }
     }
@@ -139,17 +325,22 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 template <int BN>
-void launch_bn(const CUtensorMap& w, const CUtensorMap& x, float* out, int M, int N, int S, int kbps, int kbt,
-               cudaStream_t st) {
+void launch_bn(const CUtensorMap& w, const CUtensorMap& x, int M, int N, int kbt, int n_chunks, int S, int cps,
+               const GemmEpi& epi, float* ws, int* ctr, cudaStream_t st) {
     using Cfg = GemmCfg<BN>;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(gemm_bf16_tn_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
         attr = true;
     }
-    dim3 grid((M + BN - 1) / BN, (N + kBM - 1) / kBM, S);
-    gemm_bf16_tn_kernel<BN><<<grid, 128, Cfg::kSmem, st>>>(w, x, out, M, N, kbps, kbt);
+    const int m_tiles = (M + BN - 1) / BN, n_tiles = (N + kBM - 1) / kBM;
+    const int units = m_tiles * n_tiles * S;
+    const int grid = std::min(units, kNumSMs);
+    gemm_bf16_tn_kernel<BN><<<grid, kThreads, Cfg::kSmem, st>>>(w, x, M, N, kbt, n_chunks, cps, S, m_tiles, n_tiles,
+                                                                 epi, ws, ctr);
 }
+
+int chunks_of(int K) { return ((K + kBK - 1) / kBK + kChunkKB - 1) / kChunkKB; }
 
 }  // namespace
 
@@ -167,38 +358,52 @@ CUtensorMap make_kmajor_map(const void* ptr, int rows, int K, int box_rows) {
     return m;
 }
 
-int gemm_splits(int N, int K) {
-    const int tiles_n = (N + kBM - 1) / kBM;
-    const int kbt = (K + kBK - 1) / kBK;
-    int want = (2 * 148 + tiles_n - 1) / tiles_n;  // ~2 CTAs per SM worth of tiles
-    if (want > 16) want = 16;
-    if (want > kbt / 2) want = kbt / 2;  // keep >= 2 k-blocks per split
-    if (want < 1) want = 1;
-    const int kbps = (kbt + want - 1) / want;
-    return (kbt + kbps - 1) / kbps;
-}
-
 int gemm_bn_for(int M) {
     if (M <= 16) return 16;
     if (M <= 32) return 32;
     if (M <= 64) return 64;
-    if (M <= 128) return 128;
-    return 256;
+    return 128;
 }
 
-void gemm_launch(const GemmWeight& w, const GemmAct& x, float* partials, int M, cudaStream_t st) {
-    if (M <= 0) return;
-    const int kbt = (w.K + kBK - 1) / kBK;
-    const int kbps = (kbt + w.splits - 1) / w.splits;
-    const int S = (kbt + kbps - 1) / kbps;
+// K split: enough work units for one wave on 148 SMs. Any choice gives identical bits.
+int gemm_splits_for(int M, int N, int K) {
     const int bn = gemm_bn_for(M);
+    const int tiles = ((M + bn - 1) / bn) * ((N + kBM - 1) / kBM);
+    const int nc = chunks_of(K);
+    // Split only in the HBM-bound decode regime (<= 32 token rows) where the finisher's
+    // serial tail is a handful of columns; larger M has enough tiles or is MMA-bound.
+    if (bn > 32 || tiles >= 96) return 1;
+    int S = (kNumSMs + tiles - 1) / tiles;
+    if (S > nc) S = nc;
+    if (S < 1) S = 1;
+    const int cps = (nc + S - 1) / S;
+    return (nc + cps - 1) / cps;
+}
+
+size_t gemm_ws_floats(int M, int N, int K) {
+    const int bn = gemm_bn_for(M);
+    const size_t tiles = static_cast<size_t>((M + bn - 1) / bn) * ((N + kBM - 1) / kBM);
+    return tiles * chunks_of(K) * bn * kBM;
+}
+
+void gemm_run(const GemmWeight& w, const GemmAct& x, int M, const GemmEpi& epi, const GemmWorkspace& ws,
+              cudaStream_t st, int force_splits) {
+    if (M <= 0) return;
+    if (M > x.cap_rows) throw std::invalid_argument("gemm: rows exceed activation capacity");
+    const int kbt = (w.K + kBK - 1) / kBK;
+    const int nc = chunks_of(w.K);
+    int S = force_splits > 0 ? std::min(force_splits, nc) : gemm_splits_for(M, w.N, w.K);
+    const int bn = gemm_bn_for(M);
+    const int tiles = ((M + bn - 1) / bn) * ((w.N + kBM - 1) / kBM);
+    if (S > 1 && (ws.buf == nullptr || gemm_ws_floats(M, w.N, w.K) > ws.cap_floats || tiles > ws.ctr_cap)) S = 1;
+    const int cps = (nc + S - 1) / S;
+    S = (nc + cps - 1) / cps;
     const CUtensorMap& xm = x.map_for_bn(bn);
     switch (bn) {
-        case 16: launch_bn<16>(w.map, xm, partials, M, w.N, S, kbps, kbt, st); break;
-        case 32: launch_bn<32>(w.map, xm, partials, M, w.N, S, kbps, kbt, st); break;
-        case 64: launch_bn<64>(w.map, xm, partials, M, w.N, S, kbps, kbt, st); break;
-        case 128: launch_bn<128>(w.map, xm, partials, M, w.N, S, kbps, kbt, st); break;
-        default: launch_bn<256>(w.map, xm, partials, M, w.N, S, kbps, kbt, st); break;
+        case 16: launch_bn<16>(w.map, xm, M, w.N, kbt, nc, S, cps, epi, ws.buf, ws.ctr, st); break;
+        case 32: launch_bn<32>(w.map, xm, M, w.N, kbt, nc, S, cps, epi, ws.buf, ws.ctr, st); break;
+        case 64: launch_bn<64>(w.map, xm, M, w.N, kbt, nc, S, cps, epi, ws.buf, ws.ctr, st); break;
+        default: launch_bn<128>(w.map, xm, M, w.N, kbt, nc, S, cps, epi, ws.buf, ws.ctr, st); break;
     }
 }
 
@@ -206,7 +411,6 @@ void GemmWeight::init(const __nv_bfloat16* p, int n, int k) {
     ptr = p;
     N = n;
     K = k;
-    splits = gemm_splits(n, k);
     map = make_kmajor_map(p, n, k, kBM);
 }
 
@@ -214,8 +418,8 @@ void GemmAct::init(const __nv_bfloat16* p, int rows, int k) {
     ptr = p;
     cap_rows = rows;
     K = k;
-    const int bns[5] = {16, 32, 64, 128, 256};
-    for (int i = 0; i < 5; ++i) maps[i] = make_kmajor_map(p, rows, k, bns[i]);
+    const int bns[4] = {16, 32, 64, 128};
+    for (int i = 0; i < 4; ++i) maps[i] = make_kmajor_map(p, rows, k, bns[i]);
 }
 
 const CUtensorMap& GemmAct::map_for_bn(int bn) const {
@@ -223,8 +427,7 @@ const CUtensorMap& GemmAct::map_for_bn(int bn) const {
         case 16: return maps[0];
         case 32: return maps[1];
         case 64: return maps[2];
-        case 128: return maps[3];
-        default: return maps[4];
+        default: return maps[3];
     }
 }
 

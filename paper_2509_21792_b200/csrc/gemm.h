@@ -7,10 +7,10 @@
 
 namespace sgb {
 
-// A K-major bf16 weight [N][K] (device) with its TMA map and its fixed K split.
+// A K-major bf16 weight [N][K] (device) with its TMA map.
 struct GemmWeight {
     const __nv_bfloat16* ptr = nullptr;
-    int N = 0, K = 0, splits = 1;
+    int N = 0, K = 0;
     CUtensorMap map;
     void init(const __nv_bfloat16* p, int n, int k);
 };
@@ -19,15 +19,47 @@ struct GemmWeight {
 struct GemmAct {
     const __nv_bfloat16* ptr = nullptr;
     int cap_rows = 0, K = 0;
-    CUtensorMap maps[5];
+    CUtensorMap maps[4];
     void init(const __nv_bfloat16* p, int rows, int k);
     const CUtensorMap& map_for_bn(int bn) const;
 };
 
+// Fused epilogues applied to the final fp32 sum v of (token row t, output feature o).
+enum GemmEpiKind : int {
+    kEpiF32 = 0,      // f32[t*ld + o] = v
+    kEpiBF16 = 1,     // b16[t*ld + o] = bf16(v)
+    kEpiGeluBF16 = 2, // b16[t*ld + o] = bf16(gelu_tanh(v))                  (nn.hpp:128-133)
+    kEpiResid = 3,    // x[t*ld + o] += v   (residual stream, fp32)           (tinylm.hpp:396-403)
+    kEpiQKV = 4,      // o<d: q[t*d+o]=v; K/V[kv_dst[t]*d + o-d|o-2d] = bf16(v) (tinylm.hpp:325-327,405-408)
+    kEpiFusePos = 5,  // x[t*ld + o] = v + pos_emb[pos[t]*ld + o]            (tinylm.hpp:528-533)
+};
+
+struct GemmEpi {
+    int kind = kEpiF32;
+    float* f32 = nullptr;
+    __nv_bfloat16* b16 = nullptr;
+    const long long* kv_dst = nullptr;
+    __nv_bfloat16* K = nullptr;
+    __nv_bfloat16* V = nullptr;
+    const float* pos_emb = nullptr;
+    const int* pos = nullptr;
+    int ld = 0;
+    int d = 0;
+};
+
+// Split-K workspace: per-tile chunk partials + arrival counters (zeroed once).
+struct GemmWorkspace {
+    float* buf = nullptr;
+    size_t cap_floats = 0;
+    int* ctr = nullptr;
+    int ctr_cap = 0;
+};
+
 CUtensorMap make_kmajor_map(const void* ptr, int rows, int K, int box_rows);
-int gemm_splits(int N, int K);
 int gemm_bn_for(int M);
-// partials: [w.splits][M][w.N] fp32
-void gemm_launch(const GemmWeight& w, const GemmAct& x, float* partials, int M, cudaStream_t st);
+int gemm_splits_for(int M, int N, int K);
+size_t gemm_ws_floats(int M, int N, int K);
+void gemm_run(const GemmWeight& w, const GemmAct& x, int M, const GemmEpi& epi, const GemmWorkspace& ws,
+              cudaStream_t st, int force_splits = 0);
 
 }  // namespace sgb

@@ -105,12 +105,16 @@ __global__ void __launch_bounds__(kRowThreads)
         const int e = threadIdx.x + i * kRowThreads;
         if (e < d) {
             const size_t idx = static_cast<size_t>(r) * d + e;
-            float acc = P[idx];
-            for (int s = 1; s < S; ++s) acc += P[static_cast<size_t>(s) * M * d + idx];
-            float v = accumulate ? x[idx] + acc : acc;
-            if (pe) v += pe[e];
-            x[idx] = v;
-            xs[i] = v;
+            if (P) {
+                float acc = P[idx];
+                for (int s = 1; s < S; ++s) acc += P[static_cast<size_t>(s) * M * d + idx];
+                float v = accumulate ? x[idx] + acc : acc;
+                if (pe) v += pe[e];
+                x[idx] = v;
+                xs[i] = v;
+            } else {
+                xs[i] = x[idx];  // plain LayerNorm of the residual stream
+            }
         } else {
             xs[i] = 0.f;
         }

@@ -40,6 +40,11 @@ def test_gemm_batch_invariance():
     for m in (1, 3, 16, 17, 33, 64, 65, 128, 129, 256, 257):
         part, _ = c.debug_gemm(w, x[:m])
         assert np.array_equal(part, full[:m]), m
+    # the K split decides only which CTA computes which chunk: bits are identical
+    for m in (1, 40, 300):
+        for s in (1, 2, 3):
+            part, _ = c.debug_gemm(w, x[:m], splits=s)
+            assert np.array_equal(part, full[:m]), (m, s)
 
 
 def test_forward_target_matches_oracle():
