@@ -12,15 +12,23 @@
 // same token see the *same* key sequence in the same order -- the tree mask of
 // build_tree_mask (drafttree.cpp:145-168) is exactly "keys = ancestors-or-self".
 //
-// Kernel: one warp per (row, head, split of 256 virtual positions). Inside a split the
-// warp walks 32-position chunks aligned to absolute virtual indices; each lane scores one
-// key (bf16 K row, fp32 dot against the fp32 query), the warp does an online-softmax
-// update per chunk, and the lane owning head dims [lane*DH/32, ...) accumulates P.V.
-// Splits are merged by attn_combine_kernel in split order. Chunk and split boundaries
-// depend only on the virtual index, so results are bit-identical between the AR path
-// and the tree path (batch invariance, SURVEY.md §7 hard part 1).
+// Kernel (B200): one CTA per (row, run of 64-key blocks), ALL heads of the row. The K and
+// V rows of a 16-key chunk are contiguous in the store ([slot][d], heads interleaved as
+// in the reference), so one elected thread moves each chunk with a single bulk DMA
+// (cp.async.bulk, mbarrier completion) into a 2-stage shared-memory ring: the kernel is a
+// pure HBM stream with no per-lane address math on the load side. Tree-path keys come
+// from the scratch slots with one bulk copy per key. One consumer warp per head (two
+// heads per warp above 16 heads) computes coalesced conflict-free dot products from
+// smem, an online softmax per chunk, and P.V with each lane owning DH/32 dims.
 //
-// Roofline: HBM-bound on K/V reads (2*ctx*DH*2 bytes per (row,head)); see DESIGN.md.
+// Determinism / batch invariance (SURVEY.md §7 hard part 1): every 64-key block yields
+// its own partial (m, l, acc) from a fresh state, with chunk boundaries fixed in virtual
+// index; attn_combine_kernel merges a row's block partials strictly in block order. How
+// many blocks a CTA walks (a launch-shape choice) never changes the bits, so the AR
+// and the tree rows of the same token produce identical outputs.
+//
+// Roofline: HBM-bound on K/V reads, 4*d bytes per key per layer.
+#include <algorithm>
 #include <cfloat>
 
 #include "common.cuh"
@@ -31,192 +39,257 @@ namespace sgb {
 
 namespace {
 
-constexpr int kSplit = 256;
-constexpr int kWarps = 4;
+constexpr int kBlock = 64;  // keys per softmax partial (fixed: part of the numerics)
+constexpr int kStages = 2;
 
-template <int DH>
-__global__ void __launch_bounds__(32 * kWarps)
-    attn_split_kernel(const float* __restrict__ q, const __nv_bfloat16* __restrict__ K,
-                      const __nv_bfloat16* __restrict__ V, AttnRowsDev rows, int H, int d, int n_splits,
-                      float scale, float* __restrict__ part_acc, float* __restrict__ part_ml) {
-    constexpr int PL = DH / 32;  // dims per lane in P.V
-    __shared__ __align__(16) float qs[kWarps][DH];
+SGB_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+// KPC keys per chunk (fixed per d), HPW heads per consumer warp.
+template <int DH, int KPC, int HPW>
+__global__ void __launch_bounds__(1024, 1)
+    attn_block_kernel(const float* __restrict__ q, const __nv_bfloat16* __restrict__ K,
+                      const __nv_bfloat16* __restrict__ V, AttnRowsDev rows, int H, int d, int nb_max,
+                      int blocks_per_cta, float scale, float* __restrict__ part_acc, float* __restrict__ part_ml) {
+    constexpr int PL = DH / 32;      // P.V dims per lane
+    constexpr int LPR = DH / 8;      // lanes per key row in the score pass (16 B each)
+    constexpr int RPI = 32 / LPR;    // key rows per score instruction
+    constexpr int NIT = KPC / RPI;   // score instructions per chunk
+    constexpr int CPB = kBlock / KPC;
+    extern __shared__ __align__(128) uint8_t smem[];
+    const size_t stage_bytes = static_cast<size_t>(KPC) * d * 2;  // one of K or V
+    __nv_bfloat16* Ks = reinterpret_cast<__nv_bfloat16*>(smem);
+    __nv_bfloat16* Vs = reinterpret_cast<__nv_bfloat16*>(smem + kStages * stage_bytes);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + 2 * kStages * stage_bytes);
+    uint64_t* empty = full + kStages;
+
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int sp = blockIdx.x;
-    const int h = blockIdx.y * kWarps + warp;
-    const int r = blockIdx.z;
-    if (h >= H) return;
+    const int n_cons = (H + HPW - 1) / HPW;
+    const int r = blockIdx.y;
     const int ctx_len = rows.ctx_len[r];
-    const int chain_len = rows.chain_len[r];
-    const int Lv = ctx_len + chain_len;
+    const int Lv = ctx_len + rows.chain_len[r];
     const long long ctx_base = rows.ctx_base[r];
     const long long* chain = rows.chain_slots + static_cast<size_t>(r) * kMaxChain;
-    const size_t pidx = (static_cast<size_t>(r) * H + h) * n_splits + sp;
-    const int v0 = sp * kSplit;
-    if (v0 >= Lv) {
+    const int nb_row = (Lv + kBlock - 1) / kBlock;
+    const int b0 = blockIdx.x * blocks_per_cta;
+    const int b1 = min(nb_row, b0 + blocks_per_cta);
+    if (b0 >= nb_row) return;
+    const int k_begin = b0 * kBlock, k_end = min(Lv, b1 * kBlock);
+    const int n_chunks = (k_end - k_begin + KPC - 1) / KPC;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], n_cons);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+
+    if (warp == n_cons) {
+        // ---------------- producer: bulk DMA of K/V chunks into the smem ring
         if (lane == 0) {
-            part_ml[2 * pidx] = -INFINITY;
-            part_ml[2 * pidx + 1] = 0.f;
+            for (int i = 0; i < n_chunks; ++i) {
+                const int s = i % kStages;
+                if (i >= kStages) mbar_wait(&empty[s], ((i / kStages) & 1) ^ 1);
+                const int v0 = k_begin + i * KPC;
+                const int v1 = min(k_end, v0 + KPC);
+                const int nctx = max(0, min(v1, ctx_len) - v0);
+                const int nch = (v1 - v0) - nctx;
+                const uint32_t row_bytes = static_cast<uint32_t>(d) * 2;
+                mbar_arrive_expect_tx(&full[s], 2u * row_bytes * (nctx + nch));
+                __nv_bfloat16* kd = Ks + static_cast<size_t>(s) * KPC * d;
+                __nv_bfloat16* vd = Vs + static_cast<size_t>(s) * KPC * d;
+                if (nctx > 0) {
+                    const size_t src = static_cast<size_t>(ctx_base + v0) * d;
+                    bulk_g2s(kd, K + src, row_bytes * nctx, &full[s]);
+                    bulk_g2s(vd, V + src, row_bytes * nctx, &full[s]);
+                }
+                for (int j = 0; j < nch; ++j) {
+                    const size_t src = static_cast<size_t>(chain[v0 + nctx + j - ctx_len]) * d;
+                    bulk_g2s(kd + static_cast<size_t>(nctx + j) * d, K + src, row_bytes, &full[s]);
+                    bulk_g2s(vd + static_cast<size_t>(nctx + j) * d, V + src, row_bytes, &full[s]);
+                }
+            }
         }
         return;
     }
-    const int v1 = min(Lv, v0 + kSplit);
-    const float* qrow = q + static_cast<size_t>(r) * d + h * DH;
-    for (int e = lane; e < DH; e += 32) qs[warp][e] = qrow[e];
-    __syncwarp();
+    if (warp > n_cons) return;
 
-    float m = -INFINITY, l = 0.f;
-    float acc[PL];
+    // ---------------- consumers: warp `warp` owns heads warp*HPW .. +HPW-1
+    const int piece = lane % LPR, sub = lane / LPR;
+    float qreg[HPW][8];
+    float m[HPW], l[HPW], acc[HPW][PL];
 #pragma unroll
-    for (int i = 0; i < PL; ++i) acc[i] = 0.f;
-
-    for (int c = v0; c < v1; c += 32) {
-        const int v = c + lane;
-        const bool valid = v < v1;
-        long long slot = 0;
-        if (valid) slot = v < ctx_len ? ctx_base + v : chain[v - ctx_len];
-        float s = -INFINITY;
-        if (valid) {
-            // all 16-byte pieces of this lane's key row are issued before any math so the
-            // whole row (DH*2 bytes) is in flight at once
-            const uint4* kr = reinterpret_cast<const uint4*>(K + slot * d + h * DH);
-            uint4 kreg[DH / 8];
+    for (int hh = 0; hh < HPW; ++hh) {
+        const int h = warp * HPW + hh;
+        const float* qrow = q + static_cast<size_t>(r) * d + min(h, H - 1) * DH;
 #pragma unroll
-            for (int e8 = 0; e8 < DH / 8; ++e8) kreg[e8] = __ldg(kr + e8);
-            float dot = 0.f;
+        for (int t = 0; t < 8; ++t) qreg[hh][t] = qrow[piece * 8 + t];
+    }
+    for (int i = 0; i < n_chunks; ++i) {
+        const int s = i % kStages;
+        const int v0 = k_begin + i * KPC;
+        const int nvalid = min(KPC, k_end - v0);
+        const bool block_start = ((v0 - k_begin) % kBlock) == 0;
+        mbar_wait(&full[s], (i / kStages) & 1);
+        const __nv_bfloat16* kc = Ks + static_cast<size_t>(s) * KPC * d;
+        const __nv_bfloat16* vc = Vs + static_cast<size_t>(s) * KPC * d;
 #pragma unroll
-            for (int e8 = 0; e8 < DH / 8; ++e8) {
-                const uint4 u = kreg[e8];
+        for (int hh = 0; hh < HPW; ++hh) {
+            const int h = warp * HPW + hh;
+            if (h >= H) break;
+            if (block_start) {
+                m[hh] = -INFINITY;
+                l[hh] = 0.f;
+#pragma unroll
+                for (int e = 0; e < PL; ++e) acc[hh][e] = 0.f;
+            }
+            // scores: RPI rows per LDS.128 instruction, LPR-lane butterfly per row
+            float sc = -INFINITY;
+#pragma unroll
+            for (int it = 0; it < NIT; ++it) {
+                const int key = it * RPI + sub;
+                const uint4 u = *reinterpret_cast<const uint4*>(kc + static_cast<size_t>(key) * d + h * DH + piece * 8);
                 const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+                float dot = 0.f;
 #pragma unroll
                 for (int t = 0; t < 4; ++t) {
                     const float2 f = __bfloat1622float2(b2[t]);
-                    dot = fmaf(qs[warp][e8 * 8 + 2 * t], f.x, dot);
-                    dot = fmaf(qs[warp][e8 * 8 + 2 * t + 1], f.y, dot);
+                    dot = fmaf(qreg[hh][2 * t], f.x, dot);
+                    dot = fmaf(qreg[hh][2 * t + 1], f.y, dot);
+                }
+#pragma unroll
+                for (int o = LPR / 2; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+#pragma unroll
+                for (int rr = 0; rr < RPI; ++rr) {
+                    const float dr = __shfl_sync(0xffffffffu, dot, rr * LPR);
+                    if (lane == it * RPI + rr && lane < nvalid) sc = dr * scale;
                 }
             }
-            s = dot * scale;
-        }
-        const float cm = warp_max(s);
-        const float nm = fmaxf(m, cm);
-        const float alpha = (m == -INFINITY) ? 0.f : expf(m - nm);
-        const float p = valid ? expf(s - nm) : 0.f;
-        l = l * alpha + warp_sum(p);
+            const float cm = warp_max(sc);
+            const float nm = fmaxf(m[hh], cm);
+            const float alpha = (m[hh] == -INFINITY) ? 0.f : expf(m[hh] - nm);
+            const float p = (lane < nvalid) ? expf(sc - nm) : 0.f;
+            l[hh] = l[hh] * alpha + warp_sum(p);
 #pragma unroll
-        for (int i = 0; i < PL; ++i) acc[i] *= alpha;
-        const int nvalid = min(32, v1 - c);
-        // P.V over the chunk: fully unrolled so the 32 value-row loads (one coalesced
-        // DH*2-byte row per key across the warp) are all in flight before the FMAs; the
-        // accumulation order stays j = 0..31.
-        if constexpr (PL == 4) {
-            uint2 vv[32];
+            for (int e = 0; e < PL; ++e) acc[hh][e] *= alpha;
+            m[hh] = nm;
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-                const long long sj = __shfl_sync(0xffffffffu, slot, j);
-                if (j < nvalid) vv[j] = __ldg(reinterpret_cast<const uint2*>(V + sj * d + h * DH + lane * PL));
-            }
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
+            for (int j = 0; j < KPC; ++j) {
                 const float pj = __shfl_sync(0xffffffffu, p, j);
                 if (j < nvalid) {
-                    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&vv[j].x));
-                    const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&vv[j].y));
-                    acc[0] = fmaf(pj, a.x, acc[0]);
-                    acc[1] = fmaf(pj, a.y, acc[1]);
-                    acc[2] = fmaf(pj, b.x, acc[2]);
-                    acc[3] = fmaf(pj, b.y, acc[3]);
+                    const __nv_bfloat16* vr = vc + static_cast<size_t>(j) * d + h * DH + lane * PL;
+                    if constexpr (PL == 4) {
+                        const uint2 u = *reinterpret_cast<const uint2*>(vr);
+                        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+                        const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+                        acc[hh][0] = fmaf(pj, a.x, acc[hh][0]);
+                        acc[hh][1] = fmaf(pj, a.y, acc[hh][1]);
+                        acc[hh][2] = fmaf(pj, b.x, acc[hh][2]);
+                        acc[hh][3] = fmaf(pj, b.y, acc[hh][3]);
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < PL; e += 2) {
+                            const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(vr + e));
+                            acc[hh][e] = fmaf(pj, a.x, acc[hh][e]);
+                            acc[hh][e + 1] = fmaf(pj, a.y, acc[hh][e + 1]);
+                        }
+                    }
                 }
             }
-        } else if constexpr (PL == 2) {
-            unsigned vv[32];
+            // end of a 64-key block (or of the row): publish the block partial
+            const bool block_end = (((v0 + KPC - k_begin) % kBlock) == 0) || (v0 + KPC >= k_end);
+            if (block_end) {
+                const int b = v0 / kBlock;
+                const size_t pidx = (static_cast<size_t>(r) * nb_max + b) * H + h;
+                float* pa = part_acc + pidx * DH + lane * PL;
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-                const long long sj = __shfl_sync(0xffffffffu, slot, j);
-                if (j < nvalid) vv[j] = __ldg(reinterpret_cast<const unsigned*>(V + sj * d + h * DH + lane * PL));
-            }
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-                const float pj = __shfl_sync(0xffffffffu, p, j);
-                if (j < nvalid) {
-                    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&vv[j]));
-                    acc[0] = fmaf(pj, a.x, acc[0]);
-                    acc[1] = fmaf(pj, a.y, acc[1]);
+                for (int e = 0; e < PL; ++e) pa[e] = acc[hh][e];
+                if (lane == 0) {
+                    part_ml[2 * pidx] = m[hh];
+                    part_ml[2 * pidx + 1] = l[hh];
                 }
-            }
-        } else {
-            for (int j = 0; j < nvalid; ++j) {
-                const float pj = __shfl_sync(0xffffffffu, p, j);
-                const long long sj = __shfl_sync(0xffffffffu, slot, j);
-                const __nv_bfloat16* vr = V + sj * d + h * DH + lane * PL;
-#pragma unroll
-                for (int i = 0; i < PL; ++i) acc[i] = fmaf(pj, __bfloat162float(vr[i]), acc[i]);
             }
         }
-        m = nm;
-    }
-    float* pa = part_acc + pidx * DH + lane * PL;
-#pragma unroll
-    for (int i = 0; i < PL; ++i) pa[i] = acc[i];
-    if (lane == 0) {
-        part_ml[2 * pidx] = m;
-        part_ml[2 * pidx + 1] = l;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
     }
 }
 
-// Merge the splits of one (row, head) in split order -> bf16 attention output.
+// Merge a row's 64-key block partials strictly in block order -> bf16 attention output.
 template <int DH>
-__global__ void attn_combine_kernel(const float* __restrict__ part_acc, const float* __restrict__ part_ml, int H,
-                                    int n_splits, __nv_bfloat16* __restrict__ out, int d) {
+__global__ void attn_combine_kernel(const float* __restrict__ part_acc, const float* __restrict__ part_ml,
+                                    AttnRowsDev rows, int H, int nb_max, __nv_bfloat16* __restrict__ out, int d) {
     const int r = blockIdx.x, h = blockIdx.y;
-    const size_t base = (static_cast<size_t>(r) * H + h) * n_splits;
-    float M = -INFINITY;
-    for (int s = 0; s < n_splits; ++s) M = fmaxf(M, part_ml[2 * (base + s)]);
-    float L = 0.f;
-    for (int s = 0; s < n_splits; ++s) {
-        const float ms = part_ml[2 * (base + s)];
-        if (ms != -INFINITY) L += part_ml[2 * (base + s) + 1] * expf(ms - M);
-    }
+    const int Lv = rows.ctx_len[r] + rows.chain_len[r];
+    const int nb = (Lv + kBlock - 1) / kBlock;
     for (int e = threadIdx.x; e < DH; e += blockDim.x) {
-        float o = 0.f;
-        for (int s = 0; s < n_splits; ++s) {
-            const float ms = part_ml[2 * (base + s)];
-            if (ms != -INFINITY) o += part_acc[(base + s) * DH + e] * expf(ms - M);
+        size_t pidx = static_cast<size_t>(r) * nb_max * H + h;
+        float M = part_ml[2 * pidx], L = part_ml[2 * pidx + 1], A = part_acc[pidx * DH + e];
+        for (int b = 1; b < nb; ++b) {
+            pidx = (static_cast<size_t>(r) * nb_max + b) * H + h;
+            const float mb = part_ml[2 * pidx], lb = part_ml[2 * pidx + 1], ab = part_acc[pidx * DH + e];
+            const float Mn = fmaxf(M, mb);
+            const float ca = expf(M - Mn), cb = expf(mb - Mn);
+            L = L * ca + lb * cb;
+            A = A * ca + ab * cb;
+            M = Mn;
         }
-        out[static_cast<size_t>(r) * d + h * DH + e] = __float2bfloat16(o / L);
+        out[static_cast<size_t>(r) * d + h * DH + e] = __float2bfloat16(A / L);
     }
+}
+
+template <int DH, int KPC, int HPW>
+void launch_impl(const float* q, const __nv_bfloat16* K, const __nv_bfloat16* V, const AttnRowsDev& rows, int M,
+                 int H, int d, int nb_max, float* part_acc, float* part_ml, __nv_bfloat16* out, cudaStream_t st) {
+    const size_t smem = 2 * kStages * static_cast<size_t>(KPC) * d * 2 + 64;
+    static size_t attr = 0;
+    if (attr < smem) {
+        cudaFuncSetAttribute(attn_block_kernel<DH, KPC, HPW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
+        attr = smem;
+    }
+    // enough CTAs for ~4 waves on 148 SMs; the blocks-per-CTA choice does not affect results
+    const long long total_blocks = static_cast<long long>(M) * nb_max;
+    int bpc = static_cast<int>((total_blocks + 148 * 4 - 1) / (148 * 4));
+    bpc = std::max(1, std::min(bpc, nb_max));
+    const int n_cons = (H + HPW - 1) / HPW;
+    dim3 grid((nb_max + bpc - 1) / bpc, M);
+    attn_block_kernel<DH, KPC, HPW><<<grid, 32 * (n_cons + 1), smem, st>>>(q, K, V, rows, H, d, nb_max, bpc,
+                                                                         1.0f / sqrtf(static_cast<float>(DH)),
+                                                                         part_acc, part_ml);
+    SGB_KCHECK();
+    attn_combine_kernel<DH><<<dim3(M, H), DH, 0, st>>>(part_acc, part_ml, rows, H, nb_max, out, d);
 }
 
 }  // namespace
 
-int attn_splits_for(int max_virtual_len) { return (max_virtual_len + kSplit - 1) / kSplit; }
+int attn_splits_for(int max_virtual_len) { return (max_virtual_len + kBlock - 1) / kBlock; }
 
 void launch_attention(const float* q, const __nv_bfloat16* K, const __nv_bfloat16* V, const AttnRowsDev& rows, int M,
                       int H, int d, int max_virtual_len, float* part_acc, float* part_ml, __nv_bfloat16* out,
                       cudaStream_t st) {
     if (M <= 0) return;
     const int dh = d / H;
-    const int ns = attn_splits_for(max_virtual_len);
-    const float scale = 1.0f / sqrtf(static_cast<float>(dh));
-    dim3 grid(ns, (H + kWarps - 1) / kWarps, M);
-    switch (dh) {
-        case 64:
-            attn_split_kernel<64><<<grid, 32 * kWarps, 0, st>>>(q, K, V, rows, H, d, ns, scale, part_acc, part_ml);
-            SGB_KCHECK();
-            attn_combine_kernel<64><<<dim3(M, H), 64, 0, st>>>(part_acc, part_ml, H, ns, out, d);
-            break;
-        case 128:
-            attn_split_kernel<128><<<grid, 32 * kWarps, 0, st>>>(q, K, V, rows, H, d, ns, scale, part_acc, part_ml);
-            SGB_KCHECK();
-            attn_combine_kernel<128><<<dim3(M, H), 128, 0, st>>>(part_acc, part_ml, H, ns, out, d);
-            break;
-        case 256:
-            attn_split_kernel<256><<<grid, 32 * kWarps, 0, st>>>(q, K, V, rows, H, d, ns, scale, part_acc, part_ml);
-            SGB_KCHECK();
-            attn_combine_kernel<256><<<dim3(M, H), 128, 0, st>>>(part_acc, part_ml, H, ns, out, d);
-            break;
-        default:
-            throw std::invalid_argument("attention: head dim must be 64, 128 or 256");
-    }
+    const int nb = attn_splits_for(max_virtual_len);
+    // chunk size KPC is fixed per model width (2 stages x (K+V) must fit in shared memory);
+    // it is part of the numerics, never a function of the batch
+    if (H > 32) throw std::invalid_argument("attention: at most 32 heads");
+    const int kpc = d <= 1664 ? 16 : (d <= 3328 ? 8 : 4);
+    const bool two = H > 16;
+#define SGB_ATT(DH_, KPC_, HPW_) launch_impl<DH_, KPC_, HPW_>(q, K, V, rows, M, H, d, nb, part_acc, part_ml, out, st)
+    if (dh == 128 && kpc == 16) { if (two) SGB_ATT(128, 16, 2); else SGB_ATT(128, 16, 1); }
+    else if (dh == 128 && kpc == 8) { if (two) SGB_ATT(128, 8, 2); else SGB_ATT(128, 8, 1); }
+    else if (dh == 128 && kpc == 4) { if (two) SGB_ATT(128, 4, 2); else SGB_ATT(128, 4, 1); }
+    else if (dh == 64 && kpc == 16) { if (two) SGB_ATT(64, 16, 2); else SGB_ATT(64, 16, 1); }
+    else if (dh == 64 && kpc == 8) { if (two) SGB_ATT(64, 8, 2); else SGB_ATT(64, 8, 1); }
+#undef SGB_ATT
+    else throw std::invalid_argument("attention: head dim must be 64 or 128");
     SGB_KCHECK();
 }
 
