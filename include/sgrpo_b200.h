@@ -130,6 +130,33 @@ int sgb_profile_enable(sgb_engine* e, int on);
 int sgb_profile_read(sgb_engine* e, int n_cls, double* ms, double* bytes, double* flops, long long* launches,
                      int reset);
 
+/* ---- online draft learning ------------------------------------------------------------ */
+/* AdamW hyper-parameters (grpo.hpp:97-103) and loss weights (draft_update, grpo.hpp:115-116). */
+typedef struct sgb_adamw {
+    double lr, beta1, beta2, eps, weight_decay;
+    double w_feat, w_tok;
+    long long rows_total; /* > 0: global row normaliser for a data-parallel shard (grpo.hpp:286-290) */
+    int apply_step;       /* 0: loss + gradient only */
+} sgb_adamw;
+
+/* DraftLossTerms (grpo.hpp:79-84) + device seconds. */
+typedef struct sgb_draft_terms {
+    double feature_loss, token_loss, total;
+    long long rows;
+    double seconds;
+} sgb_draft_terms;
+
+/* draft_update (grpo.cpp:177-186 -> draft_loss_grad grpo.hpp:278-344 -> AdamW::step
+ * grpo.cpp:142-161) on sequences given by the host: tokens concatenated, lens[n_seqs],
+ * features concatenated ((len-1)*d per sequence). grad_out (optional) receives the fp32
+ * gradient in the reference flat draft layout. The AdamW moments live in the engine. */
+int sgb_draft_update(sgb_engine* e, int n_seqs, const int* tokens, const int* lens, const float* features,
+                     const sgb_adamw* opt, float* grad_out, sgb_draft_terms* terms);
+/* Same, on the sequences of the engine's last sgb_rollout, read straight from HBM. */
+int sgb_draft_update_last(sgb_engine* e, const sgb_adamw* opt, float* grad_out, sgb_draft_terms* terms);
+/* Reset the AdamW moments and step counter (a fresh AdamW object). */
+int sgb_adamw_reset(sgb_engine* e);
+
 /* GEMM microbenchmark (device-resident operands): average device ms per launch. */
 int sgb_bench_gemm(int M, int N, int K, int splits, int iters, double* ms_out);
 

@@ -312,3 +312,43 @@ class Engine:
                                      _p(la, C.c_longlong), int(reset)))
         return {k: dict(ms=float(ms[i]), bytes=float(by[i]), flops=float(fl[i]), launches=int(la[i]))
                 for i, k in enumerate(KERNEL_CLASSES)}
+
+
+class AdamWC(C.Structure):
+    _fields_ = [("lr", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double),
+                ("weight_decay", C.c_double), ("w_feat", C.c_double), ("w_tok", C.c_double),
+                ("rows_total", C.c_longlong), ("apply_step", C.c_int)]
+
+
+class DraftTermsC(C.Structure):
+    _fields_ = [("feature_loss", C.c_double), ("token_loss", C.c_double), ("total", C.c_double),
+                ("rows", C.c_longlong), ("seconds", C.c_double)]
+
+
+def _draft_update(self, seqs=None, lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.0, w_feat=1.0,
+                  w_tok=0.1, rows_total=0, apply_step=True, want_grad=False):
+    """draft_update (grpo.cpp:177-186). seqs: list of (tokens, features[(len-1), d]) or None for
+    the engine's last rollout (read from HBM). Returns (feature_loss, token_loss, total, rows,
+    seconds) and the fp32 gradient (reference flat layout) if want_grad."""
+    opt = AdamWC(lr, beta1, beta2, eps, weight_decay, w_feat, w_tok, rows_total, int(apply_step))
+    terms = DraftTermsC()
+    grad = np.zeros(self.n_draft, np.float32) if want_grad else None
+    if seqs is None:
+        _check(_lib.sgb_draft_update_last(self.h, C.byref(opt), _p(grad, C.c_float), C.byref(terms)))
+    else:
+        toks = np.ascontiguousarray(np.concatenate([np.asarray(t, np.int32) for t, _ in seqs]), np.int32)
+        lens = np.array([len(t) for t, _ in seqs], np.int32)
+        feats = np.ascontiguousarray(np.concatenate([np.asarray(f, np.float32).reshape(-1) for _, f in seqs]),
+                                     np.float32)
+        _check(_lib.sgb_draft_update(self.h, len(seqs), _p(toks, C.c_int), _p(lens, C.c_int), _p(feats, C.c_float),
+                                     C.byref(opt), _p(grad, C.c_float), C.byref(terms)))
+    return (terms.feature_loss, terms.token_loss, terms.total, terms.rows, terms.seconds), grad
+
+
+def _adamw_reset(self):
+    _check(_lib.sgb_adamw_reset(self.h))
+
+
+Engine.draft_update = _draft_update
+Engine.adamw_reset = _adamw_reset
+EXPORTED += ["sgb_draft_update", "sgb_draft_update_last", "sgb_adamw_reset"]

@@ -226,6 +226,55 @@ int sgb_rollout(sgb_engine* e, const int* prompts, const int* prompt_lens, int n
     });
 }
 
+static sgb::Engine::DraftUpdateArgs draft_args(const sgb_adamw* o, float* grad_out) {
+    if (!o) throw std::invalid_argument("null AdamW options");
+    sgb::Engine::DraftUpdateArgs a;
+    a.lr = o->lr;
+    a.beta1 = o->beta1;
+    a.beta2 = o->beta2;
+    a.eps = o->eps;
+    a.weight_decay = o->weight_decay;
+    a.w_feat = o->w_feat;
+    a.w_tok = o->w_tok;
+    a.rows_total = o->rows_total;
+    a.apply_step = o->apply_step != 0;
+    a.grad_out = grad_out;
+    return a;
+}
+
+static void fill_terms(const sgb::Engine::DraftLossTerms& t, sgb_draft_terms* out) {
+    if (!out) return;
+    out->feature_loss = t.feature_loss;
+    out->token_loss = t.token_loss;
+    out->total = t.total;
+    out->rows = t.rows;
+    out->seconds = t.seconds;
+}
+
+int sgb_draft_update(sgb_engine* e, int n_seqs, const int* tokens, const int* lens, const float* features,
+                     const sgb_adamw* opt, float* grad_out, sgb_draft_terms* terms) {
+    return guarded([&] {
+        auto a = draft_args(opt, grad_out);
+        a.n_seqs = n_seqs;
+        a.tokens = tokens;
+        a.lens = lens;
+        a.features = features;
+        fill_terms(E(e).draft_update(a), terms);
+    });
+}
+
+int sgb_draft_update_last(sgb_engine* e, const sgb_adamw* opt, float* grad_out, sgb_draft_terms* terms) {
+    return guarded([&] {
+        auto a = draft_args(opt, grad_out);
+        a.use_last_rollout = true;
+        fill_terms(E(e).draft_update(a), terms);
+    });
+}
+
+int sgb_adamw_reset(sgb_engine* e) {
+    return guarded([&] { E(e).adamw_reset(); });
+}
+
 // GEMM microbenchmark: device-resident random bf16 operands, fused fp32 epilogue,
 // average device ms over `iters` launches (CUDA events on the launching stream).
 int sgb_bench_gemm(int M, int N, int K, int splits, int iters, double* ms_out) {

@@ -1248,6 +1248,7 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
     }
     SGB_CUDA(cudaStreamSynchronize(st_));
     res.hit_eos = h_eos;
+    last_lens_ = len;  // the draft update can consume this rollout straight from HBM
     for (int s = 0; s < n_seqs; ++s) {
         res.d2h_bytes += static_cast<long long>(len[s]) * sizeof(int);
         if (a.want_features) res.d2h_bytes += static_cast<long long>(len[s] - 1) * d * sizeof(float);

@@ -129,6 +129,31 @@ class Engine {
     void set_force_splits(int s) { force_splits_ = s; }
     void read_profile(KernelProfile* out, int n, bool reset);
 
+    // ---- online draft learning (draft_update, grpo.cpp:177-186)
+    struct DraftUpdateArgs {
+        // sequences: either host data (tokens/lens/features) or the last rollout (device-resident)
+        bool use_last_rollout = false;
+        int n_seqs = 0;
+        const int* tokens = nullptr;      // concatenated
+        const int* lens = nullptr;        // [n_seqs]
+        const float* features = nullptr;  // concatenated (len-1)*d per sequence
+        double lr = 1e-3, beta1 = 0.9, beta2 = 0.999, eps = 1e-8, weight_decay = 0.0;
+        double w_feat = 1.0, w_tok = 0.1;
+        long long rows_total = 0;  // > 0: global row normaliser (data-parallel shard)
+        bool apply_step = true;    // false: only compute loss + gradient (grad_out)
+        float* grad_out = nullptr; // optional host copy of the gradient (reference flat layout)
+        // optional hook run on the device gradient before the AdamW step (NCCL all-reduce)
+        void (*grad_hook)(float* dgrad, size_t n, cudaStream_t st, void* ctx) = nullptr;
+        void* hook_ctx = nullptr;
+    };
+    struct DraftLossTerms {
+        double feature_loss = 0, token_loss = 0, total = 0;
+        long long rows = 0;
+        double seconds = 0;
+    };
+    DraftLossTerms draft_update(const DraftUpdateArgs& a);
+    void adamw_reset();
+
     // debug tree driver (tests): expands one tree on device with host-supplied logits
     struct DebugTree {
         std::vector<int> tok, par, dep, sel;
@@ -222,6 +247,27 @@ class Engine {
     unsigned char* mask_dbg_ = nullptr;
     int *h_result_ = nullptr;  // pinned
     long long launches_ = 0;
+
+    // ---- training state (allocated on the first draft_update)
+    struct Train {
+        bool ready = false;
+        int rmax = 0, lc = 0, smax = 0;
+        float *x0, *xmid, *xfin, *fhat, *dlnf, *dx, *dxmid, *dx0, *ctx, *dctx, *da, *qkv, *dqkv, *fch, *dhg, *dgb;
+        float *lse, *Drow, *mu1, *rs1, *mu2, *rs2, *muf, *rsf, *logits, *sc, *grad, *m, *v, *feat_in;
+        __nv_bfloat16 *fuse, *a1, *a2, *ctx_b, *fhat_b, *dx_b, *dxmid_b, *hg, *dfch_b, *dqkv_b, *dlog, *tA, *tB;
+        __nv_bfloat16 *dflat_b, *wqkv_ref, *lm_ref;
+        int *tok, *pos, *next, *seq_first, *seq_last;
+        long long *prev_off, *tgt_off;
+        double* loss_row;
+        long long adam_t = 0;
+        size_t feat_cap = 0;
+        GemmAct act_fuse, act_a1, act_a2, act_ctx, act_hg, act_dx, act_dxmid, act_dfch, act_dqkv, act_dlog;
+        GemmWeight w2_ref, w1_ref, wo_ref, wqkv_ref_w, lm_ref_w;
+    } tr2_;
+    std::vector<int> last_lens_;  // token counts of the last rollout's sequences
+    void train_alloc();
+    void train_refresh_ref_weights();
+    void wgrad(const __nv_bfloat16* dyT, int N, const __nv_bfloat16* xT, int Kfeat, int Rp, float* grad_dst, int ld);
     cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
 };
 
