@@ -55,6 +55,8 @@ __global__ void __launch_bounds__(1024, 1)
     attn_block_kernel(const float* __restrict__ q, const __nv_bfloat16* __restrict__ K,
                       const __nv_bfloat16* __restrict__ V, AttnRowsDev rows, int H, int d, int nb_max,
                       int blocks_per_cta, float scale, float* __restrict__ part_acc, float* __restrict__ part_ml) {
+    pdl_wait();
+    pdl_trigger();
     constexpr int PL = DH / 32;      // P.V dims per lane
     constexpr int LPR = DH / 8;      // lanes per key row in the score pass (16 B each)
     constexpr int RPI = 32 / LPR;    // key rows per score instruction
@@ -225,6 +227,8 @@ __global__ void __launch_bounds__(1024, 1)
 template <int DH>
 __global__ void attn_combine_kernel(const float* __restrict__ part_acc, const float* __restrict__ part_ml,
                                     AttnRowsDev rows, int H, int nb_max, __nv_bfloat16* __restrict__ out, int d) {
+    pdl_wait();
+    pdl_trigger();
     const int r = blockIdx.x, h = blockIdx.y;
     const int Lv = rows.ctx_len[r] + rows.chain_len[r];
     const int nb = (Lv + kBlock - 1) / kBlock;
@@ -260,11 +264,11 @@ void launch_impl(const float* q, const __nv_bfloat16* K, const __nv_bfloat16* V,
     bpc = std::max(1, std::min(bpc, nb_max));
     const int n_cons = (H + HPW - 1) / HPW;
     dim3 grid((nb_max + bpc - 1) / bpc, M);
-    attn_block_kernel<DH, KPC, HPW><<<grid, 32 * (n_cons + 1), smem, st>>>(q, K, V, rows, H, d, nb_max, bpc,
+    launch_pdl(attn_block_kernel<DH, KPC, HPW>, grid, dim3(32 * (n_cons + 1)), smem, st, q, K, V, rows, H, d, nb_max, bpc,
                                                                          1.0f / sqrtf(static_cast<float>(DH)),
                                                                          part_acc, part_ml);
     SGB_KCHECK();
-    attn_combine_kernel<DH><<<dim3(M, H), DH, 0, st>>>(part_acc, part_ml, rows, H, nb_max, out, d);
+    launch_pdl(attn_combine_kernel<DH>, dim3(M, H), dim3(DH), 0, st, part_acc, part_ml, rows, H, nb_max, out, d);
 }
 
 }  // namespace

@@ -8,6 +8,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #define SGB_DEV __device__ __forceinline__
 
 namespace sgb {
@@ -173,6 +175,29 @@ SGB_DEV void tmem_ld(uint32_t taddr, float* v) {
     else if constexpr (N == 16) tmem_ld16(taddr, v);
     else if constexpr (N == 32) tmem_ld_x32(taddr, v);
     else tmem_ld_x64(taddr, v);
+}
+
+// ------------------------------------------------------------------ programmatic dependent launch
+// Every decode-path kernel is launched with programmatic stream serialization: the next
+// kernel's CTAs are scheduled while this one drains, run their prologue, and block in
+// pdl_wait() until all prior grids have completed and their writes are visible.
+SGB_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+SGB_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 // ------------------------------------------------------------------ warp helpers

@@ -8,7 +8,7 @@
 // w2 (:402), lm_head (:458) and the draft fuse (:528). Weights are stored K-major
 // ([out][in], bf16), so the reference's y = x.W is a "TN" GEMM whose UMMA A operand is
 // the weight tile (M = 128 output features) and whose B operand is the token tile
-// (N = BN in {16,32,64,128} tokens): the swap-AB mapping that keeps tcgen05 busy at
+// (N = BN in {16,32,64,128,256} tokens): the swap-AB mapping that keeps tcgen05 busy at
 // decode batch sizes, where the kernel streams weight tiles at HBM rate.
 //
 // Persistent: one CTA per SM walks work units (m_tile, n_tile, k_split) round-robin; the
@@ -18,7 +18,7 @@
 // warps 2-9 = epilogue (TMEM lane quarter = warp % 4 -> one output feature per thread;
 // two warps per quarter split the token columns).
 //
-// Batch invariance (SURVEY.md §7 hard part 1). K is cut into fixed 256-wide chunks.
+// Batch invariance (SURVEY.md §7 hard part 1). K is cut into fixed 1024-wide chunks.
 // Every chunk is accumulated separately in TMEM, read out, and the chunk sums are added
 // in fp32 registers strictly in chunk order: ((c0 + c1) + c2) + ... A K split only decides
 // WHICH CTA computes which chunks: split 0 keeps the running prefix, later splits publish
@@ -41,7 +41,7 @@ namespace {
 
 constexpr int kBK = 64;       // 64 bf16 = 128 B = one swizzle row
 constexpr int kBM = 128;      // output features per tile (UMMA M)
-constexpr int kChunkKB = 4;   // k-blocks per accumulation chunk (K = 256); fixes the fp32 association
+constexpr int kChunkKB = 16;  // k-blocks per accumulation chunk (K = 1024); fixes the fp32 association
 constexpr int kABytes = kBM * kBK * 2;
 constexpr int kThreads = 320;  // TMA warp, MMA warp, 8 epilogue warps (2 per TMEM lane quarter)
 constexpr int kEpiThreads = 256;
@@ -179,6 +179,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    // PDL: the prologue above overlapped the previous kernel; from here on we touch its outputs
+    pdl_wait();
+    pdl_trigger();
 
     if (warp == 0) {
         if (lane == 0) {
@@ -245,24 +248,29 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int buf = it & 1;
                 mbar_wait(&tfull[buf], (it >> 1) & 1);
                 tc_fence_after();
-                float v[HB];
-                tmem_ld<HB>(tmem + (static_cast<uint32_t>(32 * q) << 16) + buf * BN + j0, v);
+                // read the chunk out of TMEM in pieces of <= 64 columns (register budget)
+                constexpr int PC = HB < 64 ? HB : (HB == 64 ? 64 : 32);
+#pragma unroll
+                for (int p0 = 0; p0 < HB; p0 += PC) {
+                    float v[PC];
+                    tmem_ld<PC>(tmem + (static_cast<uint32_t>(32 * q) << 16) + buf * BN + j0 + p0, v);
+                    if (un.split == 0) {
+                        if (c == c_begin) {
+#pragma unroll
+                            for (int j = 0; j < PC; ++j) run[p0 + j] = v[j];
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < PC; ++j) run[p0 + j] += v[j];
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < PC; ++j)
+                            if (p0 + j < nmine) wst[(static_cast<size_t>(c) * BN + j0 + p0 + j) * kBM + r] = v[j];
+                    }
+                }
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&tempty[buf]);
-                if (un.split == 0) {
-                    if (c == c_begin) {
-#pragma unroll
-                        for (int j = 0; j < HB; ++j) run[j] = v[j];
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < HB; ++j) run[j] += v[j];
-                    }
-                } else {
-#pragma unroll
-                    for (int j = 0; j < HB; ++j)
-                        if (j < nmine) wst[(static_cast<size_t>(c) * BN + j0 + j) * kBM + r] = v[j];
-                }
             }
             if (S == 1) {
                 if (o < N) epi_store_run<HB>(epi, un.m0 + j0, nmine, o, run);
@@ -282,23 +290,27 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (last) {
                     __threadfence();
                     if (o < N) {
-                        for (int j = j0; j < j0 + nmine; ++j) {
-                            // the finisher continues the sequential chunk sum; loads are
-                            // independent so issue them 4 at a time
-                            float v = __ldcg(&wst[static_cast<size_t>(j) * kBM + r]);
-                            int c = cps;
-                            for (; c + 4 <= n_chunks; c += 4) {
-                                const float a0 = __ldcg(&wst[(static_cast<size_t>(c) * BN + j) * kBM + r]);
-                                const float a1 = __ldcg(&wst[(static_cast<size_t>(c + 1) * BN + j) * kBM + r]);
-                                const float a2 = __ldcg(&wst[(static_cast<size_t>(c + 2) * BN + j) * kBM + r]);
-                                const float a3 = __ldcg(&wst[(static_cast<size_t>(c + 3) * BN + j) * kBM + r]);
-                                v += a0;
-                                v += a1;
-                                v += a2;
-                                v += a3;
+                        // The finisher continues the sequential chunk sum. Columns are
+                        // independent, so 8 of them are processed together (8 loads in
+                        // flight per chunk) while each column keeps its strict chunk order.
+                        for (int jb = j0; jb < j0 + nmine; jb += 8) {
+                            float v[8];
+#pragma unroll
+                            for (int u = 0; u < 8; ++u)
+                                v[u] = (jb + u < j0 + nmine) ? __ldcg(&wst[static_cast<size_t>(jb + u) * kBM + r]) : 0.f;
+                            for (int c = cps; c < n_chunks; ++c) {
+                                float a[8];
+#pragma unroll
+                                for (int u = 0; u < 8; ++u)
+                                    a[u] = (jb + u < j0 + nmine)
+                                               ? __ldcg(&wst[(static_cast<size_t>(c) * BN + jb + u) * kBM + r])
+                                               : 0.f;
+#pragma unroll
+                                for (int u = 0; u < 8; ++u) v[u] += a[u];
                             }
-                            for (; c < n_chunks; ++c) v += __ldcg(&wst[(static_cast<size_t>(c) * BN + j) * kBM + r]);
-                            epi_store(epi, un.m0 + j, o, v);
+#pragma unroll
+                            for (int u = 0; u < 8; ++u)
+                                if (jb + u < j0 + nmine) epi_store(epi, un.m0 + jb + u, o, v[u]);
                         }
                     }
                     if (threadIdx.x == 64) ctr[un.tile] = 0;
@@ -336,8 +348,8 @@ void launch_bn(const CUtensorMap& w, const CUtensorMap& x, int M, int N, int kbt
     const int m_tiles = (M + BN - 1) / BN, n_tiles = (N + kBM - 1) / kBM;
     const int units = m_tiles * n_tiles * S;
     const int grid = std::min(units, kNumSMs);
-    gemm_bf16_tn_kernel<BN><<<grid, kThreads, Cfg::kSmem, st>>>(w, x, M, N, kbt, n_chunks, cps, S, m_tiles, n_tiles,
-                                                                 epi, ws, ctr);
+    launch_pdl(gemm_bf16_tn_kernel<BN>, dim3(grid), dim3(kThreads), Cfg::kSmem, st, w, x, M, N, kbt, n_chunks, cps, S,
+               m_tiles, n_tiles, epi, ws, ctr);
 }
 
 int chunks_of(int K) { return ((K + kBK - 1) / kBK + kChunkKB - 1) / kChunkKB; }
@@ -362,7 +374,7 @@ int gemm_bn_for(int M) {
     if (M <= 16) return 16;
     if (M <= 32) return 32;
     if (M <= 64) return 64;
-    return 128;
+    return 128;  // BN=256 (kernel instantiated) spills the epilogue's running sums at 320 threads
 }
 
 // K split: enough work units for one wave on 148 SMs. Any choice gives identical bits.
@@ -372,7 +384,7 @@ int gemm_splits_for(int M, int N, int K) {
     const int nc = chunks_of(K);
     // Split only in the HBM-bound decode regime (<= 32 token rows) where the finisher's
     // serial tail is a handful of columns; larger M has enough tiles or is MMA-bound.
-    if (bn > 32 || tiles >= 96) return 1;
+    if (tiles >= 96 || (bn > 32 && (tiles >= 74 || nc < 4))) return 1;
     int S = (kNumSMs + tiles - 1) / tiles;
     if (S > nc) S = nc;
     if (S < 1) S = 1;
@@ -403,7 +415,8 @@ void gemm_run(const GemmWeight& w, const GemmAct& x, int M, const GemmEpi& epi, 
         case 16: launch_bn<16>(w.map, xm, M, w.N, kbt, nc, S, cps, epi, ws.buf, ws.ctr, st); break;
         case 32: launch_bn<32>(w.map, xm, M, w.N, kbt, nc, S, cps, epi, ws.buf, ws.ctr, st); break;
         case 64: launch_bn<64>(w.map, xm, M, w.N, kbt, nc, S, cps, epi, ws.buf, ws.ctr, st); break;
-        default: launch_bn<128>(w.map, xm, M, w.N, kbt, nc, S, cps, epi, ws.buf, ws.ctr, st); break;
+        case 128: launch_bn<128>(w.map, xm, M, w.N, kbt, nc, S, cps, epi, ws.buf, ws.ctr, st); break;
+        default: launch_bn<256>(w.map, xm, M, w.N, kbt, nc, S, cps, epi, ws.buf, ws.ctr, st); break;
     }
 }
 
@@ -418,8 +431,8 @@ void GemmAct::init(const __nv_bfloat16* p, int rows, int k) {
     ptr = p;
     cap_rows = rows;
     K = k;
-    const int bns[4] = {16, 32, 64, 128};
-    for (int i = 0; i < 4; ++i) maps[i] = make_kmajor_map(p, rows, k, bns[i]);
+    const int bns[5] = {16, 32, 64, 128, 256};
+    for (int i = 0; i < 5; ++i) maps[i] = make_kmajor_map(p, rows, k, bns[i]);
 }
 
 const CUtensorMap& GemmAct::map_for_bn(int bn) const {
@@ -427,7 +440,8 @@ const CUtensorMap& GemmAct::map_for_bn(int bn) const {
         case 16: return maps[0];
         case 32: return maps[1];
         case 64: return maps[2];
-        default: return maps[3];
+        case 128: return maps[3];
+        default: return maps[4];
     }
 }
 

@@ -19,7 +19,7 @@ struct GemmWeight {
 struct GemmAct {
     const __nv_bfloat16* ptr = nullptr;
     int cap_rows = 0, K = 0;
-    CUtensorMap maps[4];
+    CUtensorMap maps[5];
     void init(const __nv_bfloat16* p, int rows, int k);
     const CUtensorMap& map_for_bn(int bn) const;
 };

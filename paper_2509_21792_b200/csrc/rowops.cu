@@ -75,6 +75,8 @@ __global__ void __launch_bounds__(kRowThreads) embed_ln_kernel(const int* __rest
                                                              const float* __restrict__ pos_emb,
                                                              const float* __restrict__ g, const float* __restrict__ b,
                                                              float* __restrict__ x, __nv_bfloat16* __restrict__ a) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ float red[kRowThreads / 32];
     const int r = blockIdx.x;
     const float* te = tok_emb + static_cast<size_t>(tokens[r]) * d;
@@ -96,6 +98,8 @@ __global__ void __launch_bounds__(kRowThreads)
                               const float* __restrict__ pos_emb, const int* __restrict__ positions,
                               const float* __restrict__ g, const float* __restrict__ b, __nv_bfloat16* __restrict__ a,
                               float* __restrict__ y) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ float red[kRowThreads / 32];
     const int r = blockIdx.x;
     float xs[PER];
@@ -176,6 +180,8 @@ __global__ void reduce_qkv_kernel(const float* __restrict__ P, int S, int M, int
 __global__ void gather_fuse_kernel(const int* __restrict__ tokens, const long long* __restrict__ feat_off,
                                    const float* __restrict__ feat_base, const float* __restrict__ tok_emb, int d,
                                    __nv_bfloat16* __restrict__ out) {
+    pdl_wait();
+    pdl_trigger();
     const int r = blockIdx.x;
     const float* te = tok_emb + static_cast<size_t>(tokens[r]) * d;
     const float* fe = feat_base + feat_off[r];
@@ -204,6 +210,8 @@ __global__ void transpose_to_bf16_kernel(const float* __restrict__ src, int in, 
 
 __global__ void gather_rows_bf16_kernel(const __nv_bfloat16* __restrict__ src, const int* __restrict__ idx, int d,
                                         __nv_bfloat16* __restrict__ dst) {
+    pdl_wait();
+    pdl_trigger();
     const int r = blockIdx.x;
     const __nv_bfloat16* s = src + static_cast<size_t>(idx[r]) * d;
     for (int e = threadIdx.x; e < d; e += blockDim.x) dst[static_cast<size_t>(r) * d + e] = s[e];
@@ -249,12 +257,12 @@ void launch_embed_ln(const int* tokens, const int* positions, int M, int d, cons
                      const float* g, const float* b, float* x, __nv_bfloat16* a, cudaStream_t st) {
     if (M <= 0) return;
     if (d > kMaxPerThread * kRowThreads) throw std::invalid_argument("d_model too large");
-#define ARGS M, kRowThreads, 0, st >>> (tokens, positions, d, tok_emb, pos_emb, g, b, x, a
-    if (d <= 256) embed_ln_kernel<1><<<ARGS);
-    else if (d <= 1024) embed_ln_kernel<4><<<ARGS);
-    else if (d <= 2048) embed_ln_kernel<8><<<ARGS);
-    else if (d <= 4096) embed_ln_kernel<16><<<ARGS);
-    else embed_ln_kernel<kMaxPerThread><<<ARGS);
+#define ARGS , dim3(M), dim3(kRowThreads), 0, st, tokens, positions, d, tok_emb, pos_emb, g, b, x, a
+    if (d <= 256) launch_pdl(embed_ln_kernel<1> ARGS);
+    else if (d <= 1024) launch_pdl(embed_ln_kernel<4> ARGS);
+    else if (d <= 2048) launch_pdl(embed_ln_kernel<8> ARGS);
+    else if (d <= 4096) launch_pdl(embed_ln_kernel<16> ARGS);
+    else launch_pdl(embed_ln_kernel<kMaxPerThread> ARGS);
 #undef ARGS
     SGB_KCHECK();
 }
@@ -263,12 +271,12 @@ void launch_reduce_residual_ln(const float* P, int S, int M, int d, float* x, bo
                                const int* positions, const float* g, const float* b, __nv_bfloat16* a, float* y,
                                cudaStream_t st) {
     if (M <= 0) return;
-#define ARGS M, kRowThreads, 0, st >>> (P, S, M, d, x, accumulate ? 1 : 0, pos_emb, positions, g, b, a, y
-    if (d <= 256) reduce_residual_ln_kernel<1><<<ARGS);
-    else if (d <= 1024) reduce_residual_ln_kernel<4><<<ARGS);
-    else if (d <= 2048) reduce_residual_ln_kernel<8><<<ARGS);
-    else if (d <= 4096) reduce_residual_ln_kernel<16><<<ARGS);
-    else reduce_residual_ln_kernel<kMaxPerThread><<<ARGS);
+#define ARGS , dim3(M), dim3(kRowThreads), 0, st, P, S, M, d, x, accumulate ? 1 : 0, pos_emb, positions, g, b, a, y
+    if (d <= 256) launch_pdl(reduce_residual_ln_kernel<1> ARGS);
+    else if (d <= 1024) launch_pdl(reduce_residual_ln_kernel<4> ARGS);
+    else if (d <= 2048) launch_pdl(reduce_residual_ln_kernel<8> ARGS);
+    else if (d <= 4096) launch_pdl(reduce_residual_ln_kernel<16> ARGS);
+    else launch_pdl(reduce_residual_ln_kernel<kMaxPerThread> ARGS);
 #undef ARGS
     SGB_KCHECK();
 }
@@ -295,7 +303,7 @@ void launch_reduce_qkv(const float* P, int S, int M, int d, float* q, __nv_bfloa
 void launch_gather_fuse(const int* tokens, const long long* feat_off, const float* feat_base, const float* tok_emb,
                         int R, int d, __nv_bfloat16* out, cudaStream_t st) {
     if (R <= 0) return;
-    gather_fuse_kernel<<<R, 256, 0, st>>>(tokens, feat_off, feat_base, tok_emb, d, out);
+    launch_pdl(gather_fuse_kernel, dim3(R), dim3(256), 0, st, tokens, feat_off, feat_base, tok_emb, d, out);
     SGB_KCHECK();
 }
 
@@ -309,7 +317,7 @@ void launch_transpose_to_bf16(const float* src, int in, int out_dim, __nv_bfloat
 void launch_gather_rows_bf16(const __nv_bfloat16* src, const int* idx, int R, int d, __nv_bfloat16* dst,
                              cudaStream_t st) {
     if (R <= 0) return;
-    gather_rows_bf16_kernel<<<R, 256, 0, st>>>(src, idx, d, dst);
+    launch_pdl(gather_rows_bf16_kernel, dim3(R), dim3(256), 0, st, src, idx, d, dst);
     SGB_KCHECK();
 }
 

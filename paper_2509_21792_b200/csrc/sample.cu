@@ -57,6 +57,8 @@ __global__ void __launch_bounds__(kT) emit_kernel(const float* __restrict__ logi
                                                   const int* __restrict__ row_idx, const unsigned long long* __restrict__ seeds,
                                                   const int* __restrict__ key_pos, double temperature,
                                                   int* __restrict__ out, int* __restrict__ err) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ VI shv[kT / 32];
     __shared__ double shd[kT / 32];
     __shared__ double chunk_sum[kT];
@@ -131,6 +133,8 @@ __global__ void __launch_bounds__(kT) emit_kernel(const float* __restrict__ logi
 // Fused log-softmax (fp64) + top-k, k <= 16.
 __global__ void __launch_bounds__(kT) topk_lsm_kernel(const float* __restrict__ logits, int V, int k,
                                                       int* __restrict__ out_tok, double* __restrict__ out_lp) {
+    pdl_wait();
+    pdl_trigger();
     constexpr int KM = 16;
     __shared__ VI cand[kT][KM];
     __shared__ VI shv[kT / 32];
@@ -204,14 +208,14 @@ __global__ void __launch_bounds__(kT) topk_lsm_kernel(const float* __restrict__ 
 void launch_emit(const float* logits, int V, const int* row_idx, const unsigned long long* seeds, const int* key_pos,
                  int R, double temperature, int* out, int* err, cudaStream_t st) {
     if (R <= 0) return;
-    emit_kernel<<<R, kT, 0, st>>>(logits, V, row_idx, seeds, key_pos, temperature, out, err);
+    launch_pdl(emit_kernel, dim3(R), dim3(kT), 0, st, logits, V, row_idx, seeds, key_pos, temperature, out, err);
     SGB_KCHECK();
 }
 
 void launch_topk_lsm(const float* logits, int V, int R, int k, int* out_tok, double* out_lp, cudaStream_t st) {
     if (R <= 0) return;
     if (k < 1 || k > 16) throw std::invalid_argument("top-k must be in [1, 16]");
-    topk_lsm_kernel<<<R, kT, 0, st>>>(logits, V, k, out_tok, out_lp);
+    launch_pdl(topk_lsm_kernel, dim3(R), dim3(kT), 0, st, logits, V, k, out_tok, out_lp);
     SGB_KCHECK();
 }
 

@@ -35,6 +35,8 @@ __device__ __forceinline__ bool node_better(double ca, int ta, int ia, double cb
 
 __global__ void tree_root_kernel(int B, const StepSeqDev* __restrict__ steps, SeqStateDev ss, TreeDev tr,
                                  const int* __restrict__ topk_tok, const double* __restrict__ topk_lp, int kk) {
+    pdl_wait();
+    pdl_trigger();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= B) return;
     const StepSeqDev st = steps[i];
@@ -65,6 +67,8 @@ __global__ void tree_root_kernel(int B, const StepSeqDev* __restrict__ steps, Se
 __global__ void tree_frontier_kernel(int B, int level, const StepSeqDev* __restrict__ steps,
                                      const int* __restrict__ drow_off, SeqStateDev ss, TreeDev tr, RowsDev rows,
                                      long long dcache_stride, long long dscratch_base, int d) {
+    pdl_wait();
+    pdl_trigger();
     const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (i >= B) return;
@@ -121,6 +125,8 @@ __global__ void tree_frontier_kernel(int B, int level, const StepSeqDev* __restr
 __global__ void tree_expand_kernel(int B, int level, const StepSeqDev* __restrict__ steps,
                                    const int* __restrict__ drow_off, TreeDev tr, const int* __restrict__ topk_tok,
                                    const double* __restrict__ topk_lp) {
+    pdl_wait();
+    pdl_trigger();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= B) return;
     const StepSeqDev st = steps[i];
@@ -154,6 +160,8 @@ constexpr int kTmaxCap = 1024;
 __global__ void __launch_bounds__(kSelT)
     tree_select_kernel(int B, const StepSeqDev* __restrict__ steps, SeqStateDev ss, TreeDev tr, RowsDev rows,
                        long long tcache_stride, long long tscratch_base, unsigned char* mask_dbg, int* err) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ double sconf[kTmaxCap];
     __shared__ int spar[kTmaxCap], sdep[kTmaxCap], ssel[kTmaxCap], spos[kTmaxCap];
     const int i = blockIdx.x;
@@ -212,6 +220,8 @@ __global__ void __launch_bounds__(kSelT)
 __global__ void walk_commit_kernel(int B, const StepSeqDev* __restrict__ steps, SeqStateDev ss, TreeDev tr,
                                    RowsDev rows, const int* __restrict__ emitted, int* __restrict__ acc_rows,
                                    int* __restrict__ result) {
+    pdl_wait();
+    pdl_trigger();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= B) return;
     const StepSeqDev st = steps[i];
@@ -260,6 +270,8 @@ __global__ void commit_kv_kernel(const StepSeqDev* __restrict__ steps, const int
                                  __nv_bfloat16* __restrict__ V, long long layer_stride, long long tcache_stride,
                                  long long tscratch_base, const float* __restrict__ hidden, float* __restrict__ feats,
                                  int max_seq) {
+    pdl_wait();
+    pdl_trigger();
     const int i = blockIdx.x, j = blockIdx.y, layer = blockIdx.z;
     if (j >= result[2 * i]) return;
     const StepSeqDev st = steps[i];
@@ -284,6 +296,8 @@ __global__ void commit_kv_kernel(const StepSeqDev* __restrict__ steps, const int
 
 __global__ void copy_rows_f32_kernel(const float* __restrict__ src, const int* __restrict__ src_row,
                                      const long long* __restrict__ dst_off, int d, float* __restrict__ dst) {
+    pdl_wait();
+    pdl_trigger();
     const int r = blockIdx.x;
     const float* s = src + static_cast<size_t>(src_row ? src_row[r] : r) * d;
     float* o = dst + dst_off[r];
@@ -293,6 +307,8 @@ __global__ void copy_rows_f32_kernel(const float* __restrict__ src, const int* _
 __global__ void copy_kv_prefix_kernel(const int* __restrict__ src_seq, const int* __restrict__ dst_seq,
                                       const int* __restrict__ plen, int d, __nv_bfloat16* __restrict__ K,
                                       __nv_bfloat16* __restrict__ V, long long layer_stride, long long seq_stride) {
+    pdl_wait();
+    pdl_trigger();
     const int pr = blockIdx.x, layer = blockIdx.y, t = blockIdx.z;
     if (t >= plen[pr]) return;
     const size_t lo = static_cast<size_t>(layer) * layer_stride;
@@ -310,6 +326,8 @@ __global__ void copy_kv_prefix_kernel(const int* __restrict__ src_seq, const int
 
 __global__ void prefill_commit_kernel(int n, const int* __restrict__ seqs, const int* __restrict__ qlen,
                                       const int* __restrict__ len_cap, const int* __restrict__ emitted, SeqStateDev ss) {
+    pdl_wait();
+    pdl_trigger();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int s = seqs[i], q = qlen[i], t = emitted[i];
@@ -322,6 +340,8 @@ __global__ void prefill_commit_kernel(int n, const int* __restrict__ seqs, const
 
 __global__ void gather_tokens_kernel(const int* __restrict__ seq, const int* __restrict__ pos, int R, SeqStateDev ss,
                                      int* __restrict__ out) {
+    pdl_wait();
+    pdl_trigger();
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r < R) out[r] = ss.tokens[static_cast<size_t>(seq[r]) * ss.max_seq + pos[r]];
 }
@@ -331,7 +351,7 @@ __global__ void gather_tokens_kernel(const int* __restrict__ seq, const int* __r
 void launch_tree_root(int B, const StepSeqDev* steps, const SeqStateDev& ss, const TreeDev& tr, const int* topk_tok,
                       const double* topk_lp, int kk, cudaStream_t st) {
     if (B <= 0) return;
-    tree_root_kernel<<<(B + 127) / 128, 128, 0, st>>>(B, steps, ss, tr, topk_tok, topk_lp, kk);
+    launch_pdl(tree_root_kernel, (B + 127) / 128, 128, 0, st, B, steps, ss, tr, topk_tok, topk_lp, kk);
     SGB_KCHECK();
 }
 
@@ -339,7 +359,7 @@ void launch_tree_frontier(int B, int level, const StepSeqDev* steps, const int* 
                           const TreeDev& tr, const RowsDev& rows, long long dcache_stride, long long dscratch_base,
                           int d, cudaStream_t st) {
     if (B <= 0) return;
-    tree_frontier_kernel<<<(B + 3) / 4, 128, 0, st>>>(B, level, steps, drow_off, ss, tr, rows, dcache_stride,
+    launch_pdl(tree_frontier_kernel, (B + 3) / 4, 128, 0, st, B, level, steps, drow_off, ss, tr, rows, dcache_stride,
                                                       dscratch_base, d);
     SGB_KCHECK();
 }
@@ -347,7 +367,7 @@ void launch_tree_frontier(int B, int level, const StepSeqDev* steps, const int* 
 void launch_tree_expand(int B, int level, const StepSeqDev* steps, const int* drow_off, const TreeDev& tr,
                         const int* topk_tok, const double* topk_lp, cudaStream_t st) {
     if (B <= 0) return;
-    tree_expand_kernel<<<(B + 127) / 128, 128, 0, st>>>(B, level, steps, drow_off, tr, topk_tok, topk_lp);
+    launch_pdl(tree_expand_kernel, (B + 127) / 128, 128, 0, st, B, level, steps, drow_off, tr, topk_tok, topk_lp);
     SGB_KCHECK();
 }
 
@@ -356,14 +376,14 @@ void launch_tree_select(int B, const StepSeqDev* steps, const SeqStateDev& ss, c
                         cudaStream_t st) {
     if (B <= 0) return;
     if (tr.tmax > kTmaxCap) throw std::invalid_argument("tree capacity exceeds 1024 nodes");
-    tree_select_kernel<<<B, kSelT, 0, st>>>(B, steps, ss, tr, rows, tcache_stride, tscratch_base, mask_dbg, err);
+    launch_pdl(tree_select_kernel, B, kSelT, 0, st, B, steps, ss, tr, rows, tcache_stride, tscratch_base, mask_dbg, err);
     SGB_KCHECK();
 }
 
 void launch_walk_commit(int B, const StepSeqDev* steps, const SeqStateDev& ss, const TreeDev& tr, const RowsDev& rows,
                         const int* emitted, int* acc_rows, int* result, cudaStream_t st) {
     if (B <= 0) return;
-    walk_commit_kernel<<<(B + 127) / 128, 128, 0, st>>>(B, steps, ss, tr, rows, emitted, acc_rows, result);
+    launch_pdl(walk_commit_kernel, (B + 127) / 128, 128, 0, st, B, steps, ss, tr, rows, emitted, acc_rows, result);
     SGB_KCHECK();
 }
 
@@ -372,7 +392,7 @@ void launch_commit_kv(int B, const StepSeqDev* steps, const int* acc_rows, const
                       long long tscratch_base, const float* hidden, float* feats, int max_seq, cudaStream_t st) {
     if (B <= 0) return;
     dim3 grid(B, kMaxChain, layers);
-    commit_kv_kernel<<<grid, 128, 0, st>>>(steps, acc_rows, result, d, K, V, layer_stride, tcache_stride,
+    launch_pdl(commit_kv_kernel, grid, 128, 0, st, steps, acc_rows, result, d, K, V, layer_stride, tcache_stride,
                                            tscratch_base, hidden, feats, max_seq);
     SGB_KCHECK();
 }
@@ -380,7 +400,7 @@ void launch_commit_kv(int B, const StepSeqDev* steps, const int* acc_rows, const
 void launch_copy_rows_f32(const float* src, const int* src_row, const long long* dst_off, int R, int d, float* dst,
                           cudaStream_t st) {
     if (R <= 0) return;
-    copy_rows_f32_kernel<<<R, 256, 0, st>>>(src, src_row, dst_off, d, dst);
+    launch_pdl(copy_rows_f32_kernel, R, 256, 0, st, src, src_row, dst_off, d, dst);
     SGB_KCHECK();
 }
 
@@ -388,7 +408,7 @@ void launch_copy_kv_prefix(const int* src_seq, const int* dst_seq, const int* pl
                            int d, __nv_bfloat16* K, __nv_bfloat16* V, long long layer_stride, long long seq_stride,
                            cudaStream_t st) {
     if (n <= 0 || max_plen <= 0) return;
-    copy_kv_prefix_kernel<<<dim3(n, layers, max_plen), 128, 0, st>>>(src_seq, dst_seq, plen, d, K, V, layer_stride,
+    launch_pdl(copy_kv_prefix_kernel, dim3(n, layers, max_plen), 128, 0, st, src_seq, dst_seq, plen, d, K, V, layer_stride,
                                                                      seq_stride);
     SGB_KCHECK();
 }
@@ -396,13 +416,13 @@ void launch_copy_kv_prefix(const int* src_seq, const int* dst_seq, const int* pl
 void launch_prefill_commit(int n, const int* seqs, const int* qlen, const int* len_cap, const int* emitted,
                            const SeqStateDev& ss, cudaStream_t st) {
     if (n <= 0) return;
-    prefill_commit_kernel<<<(n + 127) / 128, 128, 0, st>>>(n, seqs, qlen, len_cap, emitted, ss);
+    launch_pdl(prefill_commit_kernel, (n + 127) / 128, 128, 0, st, n, seqs, qlen, len_cap, emitted, ss);
     SGB_KCHECK();
 }
 
 void launch_gather_tokens(const int* seq, const int* pos, int R, const SeqStateDev& ss, int* out, cudaStream_t st) {
     if (R <= 0) return;
-    gather_tokens_kernel<<<(R + 127) / 128, 128, 0, st>>>(seq, pos, R, ss, out);
+    launch_pdl(gather_tokens_kernel, (R + 127) / 128, 128, 0, st, seq, pos, R, ss, out);
     SGB_KCHECK();
 }
 
