@@ -137,7 +137,17 @@ typedef struct sgb_adamw {
     double w_feat, w_tok;
     long long rows_total; /* > 0: global row normaliser for a data-parallel shard (grpo.hpp:286-290) */
     int apply_step;       /* 0: loss + gradient only */
+    int allreduce_grad;   /* 1: NCCL all-reduce (sum) of the gradient over the engine's DP group */
 } sgb_adamw;
+
+/* ---- data parallelism over NVLink: one engine per GPU / process ------------- */
+/* NCCL unique id (128 bytes) created on rank 0 and shared by the caller's launcher. */
+int sgb_nccl_unique_id(unsigned char* id128);
+/* Join the data-parallel group (ncclCommInitRank) on the engine's device. */
+int sgb_nccl_init(sgb_engine* e, int rank, int world, const unsigned char* id128);
+/* C2: in-place sum over ranks of small host vectors (rollout statistics, row counts). */
+int sgb_allreduce_sum_f64(sgb_engine* e, double* vals, int n);
+int sgb_allreduce_sum_i64(sgb_engine* e, long long* vals, int n);
 
 /* DraftLossTerms (grpo.hpp:79-84) + device seconds. */
 typedef struct sgb_draft_terms {

@@ -317,7 +317,7 @@ class Engine:
 class AdamWC(C.Structure):
     _fields_ = [("lr", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double),
                 ("weight_decay", C.c_double), ("w_feat", C.c_double), ("w_tok", C.c_double),
-                ("rows_total", C.c_longlong), ("apply_step", C.c_int)]
+                ("rows_total", C.c_longlong), ("apply_step", C.c_int), ("allreduce_grad", C.c_int)]
 
 
 class DraftTermsC(C.Structure):
@@ -326,11 +326,14 @@ class DraftTermsC(C.Structure):
 
 
 def _draft_update(self, seqs=None, lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.0, w_feat=1.0,
-                  w_tok=0.1, rows_total=0, apply_step=True, want_grad=False):
+                  w_tok=0.1, rows_total=0, apply_step=True, want_grad=False, allreduce_grad=False):
     """draft_update (grpo.cpp:177-186). seqs: list of (tokens, features[(len-1), d]) or None for
-    the engine's last rollout (read from HBM). Returns (feature_loss, token_loss, total, rows,
-    seconds) and the fp32 gradient (reference flat layout) if want_grad."""
-    opt = AdamWC(lr, beta1, beta2, eps, weight_decay, w_feat, w_tok, rows_total, int(apply_step))
+    the engine's last rollout (read from HBM). rows_total: global row normaliser of a data-parallel
+    shard (grpo.hpp:286-290); allreduce_grad: NCCL sum of the gradient over the DP group (C1).
+    Returns (feature_loss, token_loss, total, rows, seconds) and the fp32 gradient (reference flat
+    layout) if want_grad."""
+    opt = AdamWC(lr, beta1, beta2, eps, weight_decay, w_feat, w_tok, rows_total, int(apply_step),
+                 int(allreduce_grad))
     terms = DraftTermsC()
     grad = np.zeros(self.n_draft, np.float32) if want_grad else None
     if seqs is None:
@@ -352,3 +355,32 @@ def _adamw_reset(self):
 Engine.draft_update = _draft_update
 Engine.adamw_reset = _adamw_reset
 EXPORTED += ["sgb_draft_update", "sgb_draft_update_last", "sgb_adamw_reset"]
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_ubyte * 128)()
+    _check(_lib.sgb_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def _nccl_init(self, rank: int, world: int, uid: bytes):
+    buf = (C.c_ubyte * 128).from_buffer_copy(uid)
+    _check(_lib.sgb_nccl_init(self.h, rank, world, buf))
+
+
+def _allreduce_f64(self, vals):
+    a = np.ascontiguousarray(vals, np.float64).copy()
+    _check(_lib.sgb_allreduce_sum_f64(self.h, _p(a, C.c_double), a.size))
+    return a
+
+
+def _allreduce_i64(self, vals):
+    a = np.ascontiguousarray(vals, np.int64).copy()
+    _check(_lib.sgb_allreduce_sum_i64(self.h, _p(a, C.c_longlong), a.size))
+    return a
+
+
+Engine.nccl_init = _nccl_init
+Engine.allreduce_f64 = _allreduce_f64
+Engine.allreduce_i64 = _allreduce_i64
+EXPORTED += ["sgb_nccl_unique_id", "sgb_nccl_init", "sgb_allreduce_sum_f64", "sgb_allreduce_sum_i64"]

@@ -8,7 +8,10 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <unordered_map>
 #include <vector>
+
+#include <nccl.h>
 
 #include "sgrpo_b200.h"
 #include "engine.h"
@@ -52,6 +55,43 @@ sgb::Engine& E(sgb_engine* e) {
 }
 }  // namespace
 
+// ---------------------------------------------------------------- data parallel (NCCL)
+namespace {
+struct DpGroup {
+    ncclComm_t comm = nullptr;
+    int rank = 0, world = 1;
+    double* dbuf = nullptr;
+};
+std::unordered_map<const sgb_engine*, DpGroup>& groups() {
+    static std::unordered_map<const sgb_engine*, DpGroup> g;
+    return g;
+}
+void nccl_check(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess) throw std::runtime_error(std::string(what) + ": " + ncclGetErrorString(r));
+}
+DpGroup& group_of(sgb_engine* e) {
+    auto it = groups().find(e);
+    if (it == groups().end() || !it->second.comm) throw std::invalid_argument("engine has no NCCL group (sgb_nccl_init)");
+    return it->second;
+}
+// gradient all-reduce hook run by draft_update before the AdamW step (C1)
+void grad_allreduce_hook(float* g, size_t n, cudaStream_t st, void* ctx) {
+    DpGroup* dg = static_cast<DpGroup*>(ctx);
+    nccl_check(ncclAllReduce(g, g, n, ncclFloat, ncclSum, dg->comm, st), "ncclAllReduce(grad)");
+}
+}  // namespace
+
+template <class T>
+void allreduce_host(sgb_engine* e, T* vals, int n, ncclDataType_t type) {
+    DpGroup& g = group_of(e);
+    if (n < 0 || static_cast<size_t>(n) * sizeof(T) > 4096 * sizeof(double)) throw std::invalid_argument("allreduce size");
+    cudaStream_t st = E(e).stream();
+    SGB_CUDA(cudaMemcpyAsync(g.dbuf, vals, n * sizeof(T), cudaMemcpyHostToDevice, st));
+    nccl_check(ncclAllReduce(g.dbuf, g.dbuf, n, type, ncclSum, g.comm, st), "ncclAllReduce");
+    SGB_CUDA(cudaMemcpyAsync(vals, g.dbuf, n * sizeof(T), cudaMemcpyDeviceToHost, st));
+    SGB_CUDA(cudaStreamSynchronize(st));
+}
+
 extern "C" {
 
 const char* sgb_last_error(void) { return g_err.c_str(); }
@@ -85,7 +125,15 @@ int sgb_engine_create(const sgb_model_config* c, int draft_layers, int device, i
 }
 
 int sgb_engine_destroy(sgb_engine* e) {
-    return guarded([&] { delete e; });
+    return guarded([&] {
+        auto it = groups().find(e);
+        if (it != groups().end()) {
+            if (it->second.comm) ncclCommDestroy(it->second.comm);
+            if (it->second.dbuf) cudaFree(it->second.dbuf);
+            groups().erase(it);
+        }
+        delete e;
+    });
 }
 
 int sgb_param_counts(sgb_engine* e, size_t* target, size_t* draft) {
@@ -226,6 +274,38 @@ int sgb_rollout(sgb_engine* e, const int* prompts, const int* prompt_lens, int n
     });
 }
 
+
+int sgb_nccl_unique_id(unsigned char* id128) {
+    return guarded([&] {
+        ncclUniqueId id;
+        nccl_check(ncclGetUniqueId(&id), "ncclGetUniqueId");
+        static_assert(sizeof(id) == 128, "NCCL unique id size");
+        std::memcpy(id128, &id, 128);
+    });
+}
+
+int sgb_nccl_init(sgb_engine* e, int rank, int world, const unsigned char* id128) {
+    return guarded([&] {
+        E(e);
+        ncclUniqueId id;
+        std::memcpy(&id, id128, 128);
+        DpGroup g;
+        g.rank = rank;
+        g.world = world;
+        nccl_check(ncclCommInitRank(&g.comm, world, id, rank), "ncclCommInitRank");
+        SGB_CUDA(cudaMalloc(&g.dbuf, 4096 * sizeof(double)));
+        groups()[e] = g;
+    });
+}
+
+
+int sgb_allreduce_sum_f64(sgb_engine* e, double* vals, int n) {
+    return guarded([&] { allreduce_host(e, vals, n, ncclFloat64); });
+}
+int sgb_allreduce_sum_i64(sgb_engine* e, long long* vals, int n) {
+    return guarded([&] { allreduce_host(e, vals, n, ncclInt64); });
+}
+
 static sgb::Engine::DraftUpdateArgs draft_args(const sgb_adamw* o, float* grad_out) {
     if (!o) throw std::invalid_argument("null AdamW options");
     sgb::Engine::DraftUpdateArgs a;
@@ -255,6 +335,10 @@ int sgb_draft_update(sgb_engine* e, int n_seqs, const int* tokens, const int* le
                      const sgb_adamw* opt, float* grad_out, sgb_draft_terms* terms) {
     return guarded([&] {
         auto a = draft_args(opt, grad_out);
+        if (opt->allreduce_grad) {
+            a.grad_hook = grad_allreduce_hook;
+            a.hook_ctx = &group_of(e);
+        }
         a.n_seqs = n_seqs;
         a.tokens = tokens;
         a.lens = lens;
@@ -266,6 +350,10 @@ int sgb_draft_update(sgb_engine* e, int n_seqs, const int* tokens, const int* le
 int sgb_draft_update_last(sgb_engine* e, const sgb_adamw* opt, float* grad_out, sgb_draft_terms* terms) {
     return guarded([&] {
         auto a = draft_args(opt, grad_out);
+        if (opt->allreduce_grad) {
+            a.grad_hook = grad_allreduce_hook;
+            a.hook_ctx = &group_of(e);
+        }
         a.use_last_rollout = true;
         fill_terms(E(e).draft_update(a), terms);
     });

@@ -1,0 +1,28 @@
+"""Low-concurrency regime at the c2 shape: per-step device time of AR vs speculative steps
+for B sequences (diagnostic for the concurrency-sweep tail)."""
+import json
+import sys
+
+sys.path.insert(0, '.')
+from bench import WORKLOADS, make_prompts, model_cfg  # noqa: E402
+from paper_2509_21792_b200 import capi  # noqa: E402
+
+w = dict(WORKLOADS["c2"])
+cfg = model_cfg(w)
+eng = capi.Engine(cfg, 1, 0, 64, 2048, 10, 6)
+eng.init_random(1234)
+prompts = make_prompts(w, 0)
+for B in [int(x) for x in (sys.argv[1:] or ["1", "4", "16", "64"])]:
+    pr = prompts[:B]
+    for mode in ("vanilla", "adaptive_spec"):
+        kw = dict(c_peak=211, temperature=0.0, seed=7, max_new_tokens=48, want_features=False)
+        eng.generate(pr, 1, mode=mode, **kw)  # warm
+        eng.profile(True)
+        r = eng.generate(pr, 1, mode=mode, **kw)
+        eng.profile(False)
+        prof = eng.read_profile(reset=True)
+        n = len(r.steps)
+        print(json.dumps(dict(B=B, mode=mode, steps=n, ms_per_step=round(1e3 * r.seconds / n, 3), tau=round(r.tau(), 3),
+                              tok_s=round(r.generated() / r.seconds, 1), nkl=r.steps[-1][1:4],
+                              launches_per_step=round(r.kernel_launches / n, 1),
+                              cls_ms_per_step={k: round(v["ms"] / n, 3) for k, v in prof.items()})))
