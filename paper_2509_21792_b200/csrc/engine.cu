@@ -236,6 +236,12 @@ Engine::Engine(const ModelDims& dims, int draft_layers, int device, int max_seqs
     ws_.ctr = dalloc<int>(ws_.ctr_cap);
     SGB_CUDA(cudaMemset(ws_.ctr, 0, sizeof(int) * ws_.ctr_cap));
     logits_ = dalloc<float>(R * V);
+    rsc_.rows = static_cast<int>(R);
+    rsc_.bytes = row_scratch_bytes(static_cast<int>(R), static_cast<int>(V));
+    rsc_.buf = dalloc<unsigned char>(rsc_.bytes);
+    rsc_.ctr = dalloc<int>(R);
+    rsc_.rowmax = dalloc<float>(R);
+    SGB_CUDA(cudaMemset(rsc_.ctr, 0, sizeof(int) * R));
     max_vlen_cap_ = static_cast<int>(T) + kMaxChain;
     const int ns = attn_splits_for(max_vlen_cap_);
     pacc_ = dalloc<float>(R * d * ns);
@@ -283,7 +289,7 @@ Engine::~Engine() {
                     a2_, h_, fuse_, ws_.buf, ws_.ctr, logits_, pacc_, pml_, rows_.tok, rows_.pos, rows_.kv_dst,
                     rows_.ctx_base, rows_.ctx_len, rows_.chain_len, rows_.chain, rows_.feat_off, rows_.out_off,
                     rows_.key_pos, rows_.seed, rows_.par_row, lm_idx_, topk_tok_, topk_lp_, emitted_, acc_rows_,
-                    result_, err_, steps_, drow_, misc_i_, misc_l_, mask_dbg_};
+                    result_, err_, steps_, drow_, misc_i_, misc_l_, mask_dbg_, rsc_.buf, rsc_.ctr, rsc_.rowmax};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (h_result_) cudaFreeHost(h_result_);
@@ -768,7 +774,7 @@ void Engine::emit(const float* logits, int rows, int vocab, double temperature, 
     h2d(rows_.seed, seeds, rows, st_);
     h2d(rows_.key_pos, key_pos, rows, st_);
     SGB_CUDA(cudaMemsetAsync(err_, 0, sizeof(int), st_));
-    launch_emit(logits_, vocab, nullptr, rows_.seed, rows_.key_pos, rows, temperature, emitted_, err_, st_);
+    launch_emit(logits_, vocab, nullptr, rows_.seed, rows_.key_pos, rows, temperature, emitted_, err_, rsc_, st_);
     d2h(out, emitted_, rows, st_);
     int err = 0;
     d2h(&err, err_, 1, st_);
@@ -782,7 +788,7 @@ void Engine::topk_logsoftmax(const float* logits, int rows, int vocab, int k, in
     if (rows <= 0 || rows > max_rows_) throw std::invalid_argument("topk: bad row count");
     k = std::min(k, vocab);
     h2d(logits_, logits, static_cast<size_t>(rows) * vocab, st_);
-    launch_topk_lsm(logits_, vocab, rows, k, topk_tok_, topk_lp_, st_);
+    launch_topk_lsm(logits_, vocab, rows, k, topk_tok_, topk_lp_, rsc_, st_);
     d2h(tok, topk_tok_, static_cast<size_t>(rows) * k, st_);
     d2h(lp, topk_lp_, static_cast<size_t>(rows) * k, st_);
     SGB_CUDA(cudaStreamSynchronize(st_));
@@ -806,7 +812,7 @@ Engine::DebugTree Engine::debug_tree_cb(int root_token, int k, int l, int n_veri
         int id0 = 0, t0 = root_token, p0 = -1;
         fn(ctx, 1, &id0, &t0, &p0, 1, lg.data());
         h2d(logits_, lg.data(), V, st_);
-        launch_topk_lsm(logits_, V, 1, ke, topk_tok_, topk_lp_, st_);
+        launch_topk_lsm(logits_, V, 1, ke, topk_tok_, topk_lp_, rsc_, st_);
     }
     launch_tree_root(1, steps_, ss_, tr_, topk_tok_, topk_lp_, std::max(1, ke), st_);
     const int zero = 0;
@@ -824,7 +830,7 @@ Engine::DebugTree Engine::debug_tree_cb(int root_token, int k, int l, int n_veri
         SGB_CUDA(cudaStreamSynchronize(st_));
         fn(ctx, ke, fr.data(), tok.data(), par.data(), n, lg.data());
         h2d(logits_, lg.data(), static_cast<size_t>(ke) * V, st_);
-        launch_topk_lsm(logits_, V, ke, ke, topk_tok_, topk_lp_, st_);
+        launch_topk_lsm(logits_, V, ke, ke, topk_tok_, topk_lp_, rsc_, st_);
         launch_tree_expand(1, level, steps_, drow_, tr_, topk_tok_, topk_lp_, st_);
     }
     SGB_CUDA(cudaMemsetAsync(mask_dbg_, 0, static_cast<size_t>(sd.nsel) * sd.nsel, st_));
@@ -997,7 +1003,8 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
             h2d(b, emrow.data(), ne, st_);
             h2d(b + ne, emkey.data(), ne, st_);
             h2d(rows_.seed, emseed.data(), ne, st_);
-            launch_emit(logits_, V, b, rows_.seed, b + ne, ne, a.temperature, emitted_, err_, st_);
+            launch_emit(logits_, V, b, rows_.seed, b + ne, ne, a.temperature, emitted_, err_, rsc_, st_);
+            count(emit_launches(a.temperature) - 1);
             h2d(b + 2 * ne, emseq.data(), ne, st_);
             h2d(b + 3 * ne, emq.data(), ne, st_);
             h2d(lm_idx_, emcap.data(), ne, st_);
@@ -1126,7 +1133,7 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
                 if (hs[i].k) dft_len[hs[i].seq] = hs[i].p;
             // root logits -> level 1
             lm_head(a2_, act_a2_, n_spec, logits_);
-            launch_topk_lsm(logits_, V, n_spec, kstep, topk_tok_, topk_lp_, st_);
+            launch_topk_lsm(logits_, V, n_spec, kstep, topk_tok_, topk_lp_, rsc_, st_);
             launch_tree_root(B, steps_, ss_, tr_, topk_tok_, topk_lp_, kstep, st_);
             count(2);
             // levels 2..L: one batched draft forward per level
@@ -1168,7 +1175,7 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
                     res.draft_forwards++;
                     stat.draft_rows += R;
                     launch_copy_rows_f32(y_, nullptr, rows_.out_off, R, d, dfeat_, st_);
-                    launch_topk_lsm(logits_, V, R, kstep, topk_tok_, topk_lp_, st_);
+                    launch_topk_lsm(logits_, V, R, kstep, topk_tok_, topk_lp_, rsc_, st_);
                     launch_tree_expand(B, level, steps_, dro, tr_, topk_tok_, topk_lp_, st_);
                     count(3);
                 }
@@ -1197,7 +1204,8 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
         res.target_forwards++;
         // ---- acceptance, walk, commit (scheduler.cpp:219-231)
         pe0 = pbeg();
-        launch_emit(logits_, V, nullptr, rows_.seed, rows_.key_pos, vrows, a.temperature, emitted_, err_, st_);
+        launch_emit(logits_, V, nullptr, rows_.seed, rows_.key_pos, vrows, a.temperature, emitted_, err_, rsc_, st_);
+        count(emit_launches(a.temperature) - 1);
         pend(kClsSample, pe0, 4.0 * vrows * V, 0);
         pe0 = pbeg();
         launch_walk_commit(B, steps_, ss_, tr_, rows_, emitted_, acc_rows_, result_, st_);

@@ -43,9 +43,20 @@ void launch_attention(const float* q, const __nv_bfloat16* K, const __nv_bfloat1
                       cudaStream_t st);
 
 // ---- sample.cu
+// Per-(row, chunk) records + per-row tickets of the multi-CTA row reductions.
+struct RowScratch {
+    void* buf;
+    size_t bytes;
+    int* ctr;       // [rows], zero between launches
+    float* rowmax;  // [rows]
+    int rows;
+};
+size_t row_scratch_bytes(int rows, int V);
 void launch_emit(const float* logits, int V, const int* row_idx, const unsigned long long* seeds, const int* key_pos,
-                 int R, double temperature, int* out, int* err, cudaStream_t st);
-void launch_topk_lsm(const float* logits, int V, int R, int k, int* out_tok, double* out_lp, cudaStream_t st);
+                 int R, double temperature, int* out, int* err, const RowScratch& sc, cudaStream_t st);
+int emit_launches(double temperature);
+void launch_topk_lsm(const float* logits, int V, int R, int k, int* out_tok, double* out_lp, const RowScratch& sc,
+                     cudaStream_t st);
 
 // ---- tree.cu
 // Per-step descriptor of the live sequences (index i = live order), uploaded once a step.

@@ -1,5 +1,9 @@
 """Low-concurrency regime at the c2 shape: per-step device time of AR vs speculative steps
-for B sequences (diagnostic for the concurrency-sweep tail)."""
+for B sequences (diagnostic for the concurrency-sweep tail). Timing runs are unprofiled; a
+second, profiled run gives the per-class split (events around every launch inflate it).
+
+    python scripts/bench_lowb.py [B ...] [--ncu]   (--ncu: one short run per mode, for ncu)
+"""
 import json
 import sys
 
@@ -7,22 +11,28 @@ sys.path.insert(0, '.')
 from bench import WORKLOADS, make_prompts, model_cfg  # noqa: E402
 from paper_2509_21792_b200 import capi  # noqa: E402
 
+args = [a for a in sys.argv[1:] if not a.startswith("--")]
+ncu = "--ncu" in sys.argv
 w = dict(WORKLOADS["c2"])
 cfg = model_cfg(w)
-eng = capi.Engine(cfg, 1, 0, 64, 2048, 10, 6)
+eng = capi.Engine(cfg, 1, 0, 128, 2048, 10, 6)
 eng.init_random(1234)
 prompts = make_prompts(w, 0)
-for B in [int(x) for x in (sys.argv[1:] or ["1", "4", "16", "64"])]:
+for B in [int(x) for x in (args or ["1", "4", "16", "64"])]:
     pr = prompts[:B]
     for mode in ("vanilla", "adaptive_spec"):
-        kw = dict(c_peak=211, temperature=0.0, seed=7, max_new_tokens=48, want_features=False)
+        kw = dict(c_peak=211, temperature=0.0, seed=7, max_new_tokens=8 if ncu else 48, want_features=False)
         eng.generate(pr, 1, mode=mode, **kw)  # warm
-        eng.profile(True)
+        if ncu:
+            continue
         r = eng.generate(pr, 1, mode=mode, **kw)
+        eng.profile(True)
+        rp = eng.generate(pr, 1, mode=mode, **kw)
         eng.profile(False)
         prof = eng.read_profile(reset=True)
         n = len(r.steps)
-        print(json.dumps(dict(B=B, mode=mode, steps=n, ms_per_step=round(1e3 * r.seconds / n, 3), tau=round(r.tau(), 3),
+        print(json.dumps(dict(B=B, mode=mode, steps=n, ms_per_step=round(1e3 * r.seconds / n, 3),
+                              profiled_ms_per_step=round(1e3 * rp.seconds / n, 3), tau=round(r.tau(), 3),
                               tok_s=round(r.generated() / r.seconds, 1), nkl=r.steps[-1][1:4],
                               launches_per_step=round(r.kernel_launches / n, 1),
-                              cls_ms_per_step={k: round(v["ms"] / n, 3) for k, v in prof.items()})))
+                              cls_ms_per_step={k: round(v["ms"] / n, 3) for k, v in prof.items()})), flush=True)

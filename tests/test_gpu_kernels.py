@@ -196,3 +196,37 @@ def test_device_tree_matches_oracle(k, l, nv):
     sel, mask = O.rerank_candidates(ref, nv)
     assert dev["sel"].tolist() == sel
     assert np.array_equal(dev["mask"], mask)
+
+
+LARGE_V = O.ModelConfig(vocab_size=70001, d_model=64, n_layers=1, n_heads=1, d_ff=128, max_seq_len=32, seed=2)
+
+
+def test_multichunk_topk_and_sampling_match_oracle():
+    """Rows longer than one 8192-logit chunk: the per-(row, chunk) CTAs and the last-arriver
+    merge give the oracle's top-k / log-probs and sample_token results."""
+    e, _, _ = make_engine(LARGE_V, max_seqs=2, max_rows=64, seed_models=False)
+    V = LARGE_V.vocab_size
+    rng = np.random.default_rng(13)
+    lg = (3 * rng.standard_normal((24, V))).astype(np.float32)
+    lg[0, [5, 8192 + 7, 65536 + 3]] = lg[0].max() + 1  # exact ties in three chunks
+    lg[1, :] = 0.0                                       # all equal
+    lg[2, :] = -np.inf
+    lg[2, [9000, 70000]] = 1.0                           # mostly -inf, winners in two chunks
+    lg[3, 8192:] = lg[3].max() + 2                       # mass concentrated after chunk 0
+    for k in (1, 10, 16):
+        tok, lp = e.topk_logsoftmax(lg, k)
+        for r in range(24):
+            lps = O.log_softmax_row(lg[r])
+            want = O.topk_tokens(lps, k)
+            assert tok[r].tolist() == want, (k, r)
+            np.testing.assert_allclose(lp[r], lps[want], rtol=0, atol=1e-12)
+    seeds = rng.integers(0, 2**63, size=24, dtype=np.uint64)
+    kp = rng.integers(1, 90, size=24).astype(np.int32)
+    for temp in (0.0, 0.7, 1.0):
+        got = e.sample_rows(lg, temp, seeds, kp)
+        want = [O.sample_token(lg[i], temp, O.mix_key(int(seeds[i]), int(kp[i]))) for i in range(24)]
+        assert got.tolist() == want, temp
+    bad = lg[4:6].copy()
+    bad[1, 60000] = np.nan
+    with pytest.raises(ArithmeticError):
+        e.sample_rows(bad, 1.0, seeds[:2], kp[:2])
