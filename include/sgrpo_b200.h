@@ -170,6 +170,14 @@ int sgb_adamw_reset(sgb_engine* e);
 /* GEMM microbenchmark (device-resident operands): average device ms per launch. */
 int sgb_bench_gemm(int M, int N, int K, int splits, int iters, double* ms_out);
 
+/* Decode-attention microbenchmark: B rows x (ctx + 1) keys, H heads of dh. */
+int sgb_bench_attention(int B, int ctx, int H, int dh, int iters, double* ms_out);
+/* Attention self-test: row r attends to n_keys[r] keys (rows concatenated in k/v
+ * [sum n_keys][H*dh] fp32, converted to bf16); the last key of each row goes through the
+ * tree-path slot list. out [B][H*dh] (bf16 values). */
+int sgb_debug_attention(int B, const int* n_keys, int H, int dh, const float* q, const float* k, const float* v,
+                        float* out);
+
 /* tcgen05 GEMM self-test: out[M][N] = bf16(x)[M][K] . bf16(w)[N][K]^T (K-major). */
 int sgb_debug_gemm(const float* w, const float* x, int M, int N, int K, float* out, int* splits_out);
 

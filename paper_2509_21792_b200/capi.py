@@ -59,7 +59,8 @@ EXPORTED = ["sgb_last_error", "sgb_version", "sgb_device_count", "sgb_engine_cre
             "sgb_param_counts", "sgb_upload_target", "sgb_upload_draft", "sgb_download_draft", "sgb_init_random",
             "sgb_cache_reset", "sgb_cache_len", "sgb_cache_read", "sgb_cache_gather_tail", "sgb_forward_target",
             "sgb_forward_draft_rows", "sgb_sample_rows", "sgb_topk_logsoftmax", "sgb_build_tree", "sgb_rollout",
-            "sgb_debug_gemm", "sgb_profile_enable", "sgb_profile_read"]
+            "sgb_debug_gemm", "sgb_profile_enable", "sgb_profile_read", "sgb_bench_gemm", "sgb_bench_attention",
+            "sgb_debug_attention"]
 
 KERNEL_CLASSES = ["gemm_tcgen05", "attention", "rowops", "lm_head", "sample", "tree", "kv_commit"]
 
@@ -83,6 +84,20 @@ def device_count() -> int:
     n = C.c_int()
     _check(_lib.sgb_device_count(C.byref(n)))
     return n.value
+
+
+def debug_attention(q: np.ndarray, k_rows, v_rows, n_heads: int) -> np.ndarray:
+    """Tree/paged attention self-test: q [B][d]; k_rows/v_rows: per row an [n_keys][d]
+    array (the last key goes through the tree-path slot list). Returns [B][d] (bf16 values)."""
+    q = np.ascontiguousarray(q, np.float32)
+    B, d = q.shape
+    nk = np.array([len(k) for k in k_rows], np.int32)
+    k = np.ascontiguousarray(np.concatenate(k_rows), np.float32)
+    v = np.ascontiguousarray(np.concatenate(v_rows), np.float32)
+    out = np.zeros((B, d), np.float32)
+    _check(_lib.sgb_debug_attention(B, _p(nk, C.c_int), n_heads, d // n_heads, _p(q, C.c_float), _p(k, C.c_float),
+                                    _p(v, C.c_float), _p(out, C.c_float)))
+    return out
 
 
 def debug_gemm(w: np.ndarray, x: np.ndarray, splits: int = 0):

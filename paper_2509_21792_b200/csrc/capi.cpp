@@ -368,6 +368,10 @@ int sgb_adamw_reset(sgb_engine* e) {
 int sgb_bench_gemm(int M, int N, int K, int splits, int iters, double* ms_out) {
     return guarded([&] {
         const int cap = ((M + 255) / 256) * 256;
+        // Weights rotate over enough copies to exceed the 126 MB L2, so every launch streams
+        // its weights from HBM as in the rollout (28 layers x 74 MB at the c2 shape).
+        const size_t wbytes = static_cast<size_t>(N) * K * 2;
+        const int ncopy = static_cast<int>(std::max<size_t>(1, (320u << 20) / wbytes + 1));
         std::vector<__nv_bfloat16> hw(static_cast<size_t>(N) * K), hx(static_cast<size_t>(cap) * K);
         uint64_t st = 12345;
         auto rnd = [&]() {
@@ -378,12 +382,14 @@ int sgb_bench_gemm(int M, int N, int K, int splits, int iters, double* ms_out) {
         for (auto& v : hx) v = __float2bfloat16(rnd());
         __nv_bfloat16 *dw = nullptr, *dx = nullptr;
         float* dp = nullptr;
-        SGB_CUDA(cudaMalloc(&dw, hw.size() * 2));
+        SGB_CUDA(cudaMalloc(&dw, wbytes * ncopy));
         SGB_CUDA(cudaMalloc(&dx, hx.size() * 2));
-        SGB_CUDA(cudaMemcpy(dw, hw.data(), hw.size() * 2, cudaMemcpyHostToDevice));
+        for (int c = 0; c < ncopy; ++c)
+            SGB_CUDA(cudaMemcpy(reinterpret_cast<char*>(dw) + c * wbytes, hw.data(), wbytes, cudaMemcpyHostToDevice));
         SGB_CUDA(cudaMemcpy(dx, hx.data(), hx.size() * 2, cudaMemcpyHostToDevice));
-        sgb::GemmWeight gw;
-        gw.init(dw, N, K);
+        std::vector<sgb::GemmWeight> gw(ncopy);
+        for (int c = 0; c < ncopy; ++c)
+            gw[c].init(reinterpret_cast<const __nv_bfloat16*>(reinterpret_cast<const char*>(dw) + c * wbytes), N, K);
         sgb::GemmAct ga;
         ga.init(dx, cap, K);
         sgb::GemmWorkspace ws;
@@ -400,9 +406,9 @@ int sgb_bench_gemm(int M, int N, int K, int splits, int iters, double* ms_out) {
         cudaEvent_t a, b;
         SGB_CUDA(cudaEventCreate(&a));
         SGB_CUDA(cudaEventCreate(&b));
-        for (int i = 0; i < 3; ++i) sgb::gemm_run(gw, ga, M, epi, ws, 0, splits);
+        for (int i = 0; i < 3; ++i) sgb::gemm_run(gw[i % ncopy], ga, M, epi, ws, 0, splits);
         SGB_CUDA(cudaEventRecord(a, 0));
-        for (int i = 0; i < iters; ++i) sgb::gemm_run(gw, ga, M, epi, ws, 0, splits);
+        for (int i = 0; i < iters; ++i) sgb::gemm_run(gw[(i + 3) % ncopy], ga, M, epi, ws, 0, splits);
         SGB_CUDA(cudaEventRecord(b, 0));
         SGB_CUDA(cudaEventSynchronize(b));
         SGB_KCHECK();
@@ -416,6 +422,69 @@ int sgb_bench_gemm(int M, int N, int K, int splits, int iters, double* ms_out) {
         cudaFree(dp);
         cudaFree(ws.buf);
         cudaFree(ws.ctr);
+    });
+}
+
+// Attention self-test: row r attends to n_keys[r] keys stored consecutively (rows
+// concatenated) in K/V [sum n_keys][H*dh]; the LAST key of every row is addressed through
+// the tree-path (chain) slot list, the rest as the contiguous cached prefix. out [B][H*dh].
+int sgb_debug_attention(int B, const int* n_keys, int H, int dh, const float* q, const float* k, const float* v,
+                        float* out) {
+    return guarded([&] {
+        if (B <= 0 || H <= 0 || dh <= 0) throw std::invalid_argument("debug_attention: bad shape");
+        const int d = H * dh;
+        std::vector<long long> base(B), chain(static_cast<size_t>(B) * sgb::kMaxChain, 0);
+        std::vector<int> cl(B), chl(B, 1);
+        long long tot = 0;
+        int maxk = 1;
+        double keys = 0;
+        for (int b = 0; b < B; ++b) {
+            if (n_keys[b] < 1) throw std::invalid_argument("debug_attention: rows need >= 1 key");
+            base[b] = tot;
+            cl[b] = n_keys[b] - 1;
+            chain[static_cast<size_t>(b) * sgb::kMaxChain] = tot + n_keys[b] - 1;
+            tot += n_keys[b];
+            maxk = std::max(maxk, n_keys[b]);
+            keys += n_keys[b];
+        }
+        std::vector<__nv_bfloat16> hk(tot * d), hv(tot * d);
+        for (size_t i = 0; i < hk.size(); ++i) {
+            hk[i] = __float2bfloat16(k[i]);
+            hv[i] = __float2bfloat16(v[i]);
+        }
+        __nv_bfloat16 *K = nullptr, *V = nullptr, *o = nullptr;
+        float *dq = nullptr, *pacc = nullptr, *pml = nullptr;
+        long long *dbase = nullptr, *dchain = nullptr;
+        int *dcl = nullptr, *dchl = nullptr;
+        const int ns = sgb::attn_splits_for(maxk);
+        SGB_CUDA(cudaMalloc(&K, hk.size() * 2));
+        SGB_CUDA(cudaMalloc(&V, hv.size() * 2));
+        SGB_CUDA(cudaMalloc(&o, static_cast<size_t>(B) * d * 2));
+        SGB_CUDA(cudaMalloc(&dq, static_cast<size_t>(B) * d * 4));
+        SGB_CUDA(cudaMalloc(&pacc, static_cast<size_t>(B) * d * ns * 4));
+        SGB_CUDA(cudaMalloc(&pml, static_cast<size_t>(B) * H * ns * 2 * 4));
+        SGB_CUDA(cudaMalloc(&dbase, B * 8));
+        SGB_CUDA(cudaMalloc(&dchain, chain.size() * 8));
+        SGB_CUDA(cudaMalloc(&dcl, B * 4));
+        SGB_CUDA(cudaMalloc(&dchl, B * 4));
+        SGB_CUDA(cudaMemcpy(K, hk.data(), hk.size() * 2, cudaMemcpyHostToDevice));
+        SGB_CUDA(cudaMemcpy(V, hv.data(), hv.size() * 2, cudaMemcpyHostToDevice));
+        SGB_CUDA(cudaMemcpy(dq, q, static_cast<size_t>(B) * d * 4, cudaMemcpyHostToDevice));
+        SGB_CUDA(cudaMemcpy(dbase, base.data(), B * 8, cudaMemcpyHostToDevice));
+        SGB_CUDA(cudaMemcpy(dchain, chain.data(), chain.size() * 8, cudaMemcpyHostToDevice));
+        SGB_CUDA(cudaMemcpy(dcl, cl.data(), B * 4, cudaMemcpyHostToDevice));
+        SGB_CUDA(cudaMemcpy(dchl, chl.data(), B * 4, cudaMemcpyHostToDevice));
+        sgb::AttnRowsDev ar{dbase, dcl, dchl, dchain};
+        sgb::AttnScratch sc{pacc, pml, nullptr, static_cast<long long>(B) * H};
+        SGB_CUDA(cudaMalloc(&sc.row_ctr, sc.ctr_cap * 4));
+        SGB_CUDA(cudaMemset(sc.row_ctr, 0, sc.ctr_cap * 4));
+        sgb::launch_attention(dq, K, V, ar, B, H, d, maxk, keys, sc, o, 0);
+        SGB_CUDA(cudaDeviceSynchronize());
+        std::vector<__nv_bfloat16> ho(static_cast<size_t>(B) * d);
+        SGB_CUDA(cudaMemcpy(ho.data(), o, ho.size() * 2, cudaMemcpyDeviceToHost));
+        for (size_t i = 0; i < ho.size(); ++i) out[i] = __bfloat162float(ho[i]);
+        void* ptrs[] = {K, V, o, dq, pacc, pml, dbase, dchain, dcl, dchl, sc.row_ctr};
+        for (void* p : ptrs) cudaFree(p);
     });
 }
 
@@ -454,18 +523,22 @@ int sgb_bench_attention(int B, int ctx, int H, int dh, int iters, double* ms_out
         SGB_CUDA(cudaMemcpy(dcl, cl.data(), B * 4, cudaMemcpyHostToDevice));
         SGB_CUDA(cudaMemcpy(dchl, chl.data(), B * 4, cudaMemcpyHostToDevice));
         sgb::AttnRowsDev ar{dbase, dcl, dchl, dchain};
+        sgb::AttnScratch sc{pacc, pml, nullptr, static_cast<long long>(B) * H};
+        SGB_CUDA(cudaMalloc(&sc.row_ctr, sc.ctr_cap * 4));
+        SGB_CUDA(cudaMemset(sc.row_ctr, 0, sc.ctr_cap * 4));
+        const double keys = static_cast<double>(B) * (ctx + 1);
         cudaEvent_t a, b;
         SGB_CUDA(cudaEventCreate(&a));
         SGB_CUDA(cudaEventCreate(&b));
-        for (int i = 0; i < 2; ++i) sgb::launch_attention(q, K, V, ar, B, H, d, ctx + 1, pacc, pml, out, 0);
+        for (int i = 0; i < 2; ++i) sgb::launch_attention(q, K, V, ar, B, H, d, ctx + 1, keys, sc, out, 0);
         SGB_CUDA(cudaEventRecord(a, 0));
-        for (int i = 0; i < iters; ++i) sgb::launch_attention(q, K, V, ar, B, H, d, ctx + 1, pacc, pml, out, 0);
+        for (int i = 0; i < iters; ++i) sgb::launch_attention(q, K, V, ar, B, H, d, ctx + 1, keys, sc, out, 0);
         SGB_CUDA(cudaEventRecord(b, 0));
         SGB_CUDA(cudaEventSynchronize(b));
         float ms = 0.f;
         SGB_CUDA(cudaEventElapsedTime(&ms, a, b));
         *ms_out = ms / iters;
-        void* ptrs[] = {K, V, out, q, pacc, pml, dbase, dchain, dcl, dchl};
+        void* ptrs[] = {K, V, out, q, pacc, pml, dbase, dchain, dcl, dchl, sc.row_ctr};
         for (void* p : ptrs) cudaFree(p);
         cudaEventDestroy(a);
         cudaEventDestroy(b);

@@ -246,6 +246,11 @@ Engine::Engine(const ModelDims& dims, int draft_layers, int device, int max_seqs
     const int ns = attn_splits_for(max_vlen_cap_);
     pacc_ = dalloc<float>(R * d * ns);
     pml_ = dalloc<float>(R * dims.heads * ns * 2);
+    asc_.part_acc = pacc_;
+    asc_.part_ml = pml_;
+    asc_.ctr_cap = static_cast<long long>(R) * dims.heads;
+    asc_.row_ctr = dalloc<int>(asc_.ctr_cap);
+    SGB_CUDA(cudaMemset(asc_.row_ctr, 0, sizeof(int) * asc_.ctr_cap));
     alloc_rows();
     SGB_CUDA(cudaMallocHost(&h_result_, sizeof(int) * (2 * S + 4)));
     SGB_CUDA(cudaMemset(err_, 0, sizeof(int)));
@@ -289,7 +294,7 @@ Engine::~Engine() {
                     a2_, h_, fuse_, ws_.buf, ws_.ctr, logits_, pacc_, pml_, rows_.tok, rows_.pos, rows_.kv_dst,
                     rows_.ctx_base, rows_.ctx_len, rows_.chain_len, rows_.chain, rows_.feat_off, rows_.out_off,
                     rows_.key_pos, rows_.seed, rows_.par_row, lm_idx_, topk_tok_, topk_lp_, emitted_, acc_rows_,
-                    result_, err_, steps_, drow_, misc_i_, misc_l_, mask_dbg_, rsc_.buf, rsc_.ctr, rsc_.rowmax};
+                    result_, err_, steps_, drow_, misc_i_, misc_l_, mask_dbg_, rsc_.buf, rsc_.ctr, rsc_.rowmax, asc_.row_ctr};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (h_result_) cudaFreeHost(h_result_);
@@ -524,7 +529,7 @@ void Engine::forward(const Fwd& f) {
         eq.d = d;
         gemm(W.qkv, act_a_, M, eq, kClsGemm, 8.0 / 3.0);
         e0 = pbeg();
-        launch_attention(q_, eq.K, eq.V, ar, M, H, d, f.max_vlen, pacc_, pml_, att_, st_);
+        launch_attention(q_, eq.K, eq.V, ar, M, H, d, f.max_vlen, f.attn_row_keys, asc_, att_, st_);
         pend(kClsAttn, e0, attn_bytes, attn_flops);
         count();
         GemmEpi er;

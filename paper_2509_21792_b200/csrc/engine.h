@@ -231,6 +231,7 @@ class Engine {
     float *x_ = nullptr, *q_ = nullptr, *y_ = nullptr, *logits_ = nullptr, *featin_ = nullptr;
     RowScratch rsc_{};  // multi-CTA sampling / top-k records
     float *pacc_ = nullptr, *pml_ = nullptr;
+    AttnScratch asc_{};
     __nv_bfloat16 *a_ = nullptr, *att_ = nullptr, *h_ = nullptr, *fuse_ = nullptr, *a2_ = nullptr;
     GemmAct act_a_, act_att_, act_h_, act_fuse_, act_a2_;
     GemmWorkspace ws_;

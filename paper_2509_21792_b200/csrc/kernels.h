@@ -37,9 +37,17 @@ void launch_init_normal(float* out, size_t n, unsigned long long seed, float std
 void launch_fill(float* out, size_t n, float v, cudaStream_t st);
 
 // ---- attention.cu
+// Block partials + per-(row, head group) tickets of the persistent attention kernel.
+struct AttnScratch {
+    float* part_acc;  // [rows][nb_max][H][dh]
+    float* part_ml;   // [rows][nb_max][H][2]
+    int* row_ctr;     // [ctr_cap], zero between launches
+    long long ctr_cap;
+};
 int attn_splits_for(int max_virtual_len);
+// total_keys: sum over rows of keys attended (host estimate; only sizes the launch)
 void launch_attention(const float* q, const __nv_bfloat16* K, const __nv_bfloat16* V, const AttnRowsDev& rows, int M,
-                      int H, int d, int max_virtual_len, float* part_acc, float* part_ml, __nv_bfloat16* out,
+                      int H, int d, int max_virtual_len, double total_keys, const AttnScratch& sc, __nv_bfloat16* out,
                       cudaStream_t st);
 
 // ---- sample.cu

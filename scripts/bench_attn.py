@@ -1,14 +1,23 @@
-"""Decode-attention microbenchmark: achieved HBM GB/s on K/V reads."""
-import ctypes as C, sys, json
+"""Decode-attention microbenchmark: achieved HBM GB/s on K/V reads.
+
+    python scripts/bench_attn.py [B:ctx ...]
+"""
+import ctypes as C
+import json
+import sys
+
 sys.path.insert(0, '.')
-from paper_2509_21792_b200 import capi
+from paper_2509_21792_b200 import capi  # noqa: E402
+
 lib = capi.lib()
-cases = [(512, 128), (512, 640), (512, 1151), (64, 1151), (8, 1151), (1, 1151)]
+cases = [tuple(int(x) for x in a.split(':')) for a in sys.argv[1:]] or \
+    [(512, 128), (512, 640), (512, 1151), (211, 150), (64, 1151), (16, 150), (8, 1151), (1, 150), (1, 1151)]
 for B, ctx in cases:
     ms = C.c_double()
     rc = lib.sgb_bench_attention(B, ctx, 12, 128, 20, C.byref(ms))
     if rc:
-        print("error", lib.sgb_last_error()); continue
+        print("error", lib.sgb_last_error())
+        continue
     t = ms.value * 1e-3
     by = B * (ctx + 1) * 1536 * 2 * 2
-    print(json.dumps(dict(B=B, ctx=ctx, us=round(ms.value * 1e3, 1), GBps=round(by / t / 1e9, 1))))
+    print(json.dumps(dict(B=B, ctx=ctx, us=round(ms.value * 1e3, 1), GBps=round(by / t / 1e9, 1))), flush=True)

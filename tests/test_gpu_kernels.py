@@ -230,3 +230,46 @@ def test_multichunk_topk_and_sampling_match_oracle():
     bad[1, 60000] = np.nan
     with pytest.raises(ArithmeticError):
         e.sample_rows(bad, 1.0, seeds[:2], kp[:2])
+
+
+def _attn_ref(q, k, v, H):
+    """fp64 softmax(q.k^T/sqrt(dh)).v per head (tinylm.hpp:335-395) on bf16-rounded K/V."""
+    d = q.shape[0]
+    dh = d // H
+    bf = lambda a: (np.asarray(a, np.float32).view(np.uint32) + 0x7FFF + ((np.asarray(a, np.float32).view(np.uint32) >> 16) & 1)  # noqa: E731
+                    & 0xFFFF0000).view(np.float32).astype(np.float64)
+    kk, vv = bf(k), bf(v)
+    out = np.zeros(d)
+    for h in range(H):
+        s = kk[:, h * dh:(h + 1) * dh] @ q[h * dh:(h + 1) * dh].astype(np.float64) / np.sqrt(dh)
+        p = np.exp(s - s.max())
+        out[h * dh:(h + 1) * dh] = (p / p.sum()) @ vv[:, h * dh:(h + 1) * dh]
+    return out
+
+
+@pytest.mark.parametrize("H,dh", [(12, 128), (2, 64), (28, 128)])
+def test_attention_long_context_and_launch_shape_invariance(H, dh):
+    """The persistent attention kernel vs an fp64 reference at long contexts (rows spread over
+    many CTAs, tickets, in-kernel merge), and bitwise invariance of a row's output to the
+    batch it is launched with (head grouping and block-to-CTA mapping change with it)."""
+    c = pytest.importorskip("paper_2509_21792_b200.capi")
+    d = H * dh
+    rng = np.random.default_rng(H * 7 + dh)
+    lens = [1, 63, 64, 65, 700, 2100, 129, 5]
+    qs = rng.standard_normal((len(lens), d)).astype(np.float32)
+    ks = [rng.standard_normal((n, d)).astype(np.float32) for n in lens]
+    vs = [rng.standard_normal((n, d)).astype(np.float32) for n in lens]
+    out = c.debug_attention(qs, ks, vs, H)
+    for i, n in enumerate(lens):
+        ref = _attn_ref(qs[i], ks[i], vs[i], H)
+        err = np.abs(out[i] - ref).max()
+        assert err < 2e-2 * max(1.0, np.abs(ref).max()), (n, err)
+    # the same rows alone and inside a bigger batch: identical bits
+    for i in (0, 4, 5):
+        solo = c.debug_attention(qs[i:i + 1], ks[i:i + 1], vs[i:i + 1], H)
+        assert np.array_equal(solo[0], out[i]), i
+    big_q = np.concatenate([qs, rng.standard_normal((40, d)).astype(np.float32)])
+    big_k = ks + [rng.standard_normal((300, d)).astype(np.float32) for _ in range(40)]
+    big_v = vs + [rng.standard_normal((300, d)).astype(np.float32) for _ in range(40)]
+    big = c.debug_attention(big_q, big_k, big_v, H)
+    assert np.array_equal(big[:len(lens)], out)
