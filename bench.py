@@ -112,6 +112,22 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+def ncu_traffic(name):
+    """dram read+write bytes of one attention launch from the committed ncu --set full summary
+    (profiles/), with that launch's algorithmic bytes: traffic/algorithmic ~1 means no re-reads."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", name)
+    t = a = None
+    try:
+        for line in open(path):
+            if line.strip().startswith("traffic (dram read+write, bytes)"):
+                t = float(line.split()[-1])
+            elif line.strip().startswith("algorithmic bytes"):
+                a = float(line.split()[-1])
+    except OSError:
+        return None, None, None
+    return t, a, (f"profiles/{name}: ncu --set full of the c2-shaped launch (512 rows x 641 keys)" if t else None)
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -288,9 +304,11 @@ def main():
     att = prof["attention"]
     ach = att["bytes"] / (att["ms"] * 1e-3) / 1e9 if att["ms"] else 0.0
     total_ms = sum(v["ms"] for v in prof.values())
-    roofline = {"bound": "hbm", "kernel": "attn_split_kernel+attn_combine_kernel (tree/paged KV attention)",
+    traffic, traffic_alg, traffic_src = ncu_traffic("r01_attn_c2_b512_ctx640.txt")
+    roofline = {"bound": "hbm", "kernel": "attn_kernel (persistent tree/paged KV attention, in-kernel block merge)",
                 "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s", "frac": round(ach / hbm, 4),
-                "traffic": None, "peak_source": src,
+                "traffic": traffic, "traffic_algorithmic": traffic_alg, "traffic_source": traffic_src,
+                "peak_source": src,
                 "share_of_step": round(att["ms"] / total_ms, 4) if total_ms else None,
                 "measured": "per-launch CUDA events on the engine stream, one profiled rollout after the timed steps",
                 "classes": {k: {"ms_per_step": round(v["ms"], 2),

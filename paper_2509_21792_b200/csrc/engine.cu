@@ -236,6 +236,13 @@ Engine::Engine(const ModelDims& dims, int draft_layers, int device, int max_seqs
     ws_.ctr = dalloc<int>(ws_.ctr_cap);
     SGB_CUDA(cudaMemset(ws_.ctr, 0, sizeof(int) * ws_.ctr_cap));
     logits_ = dalloc<float>(R * V);
+    {
+        int ncmax = std::max(gemm_chunks(static_cast<int>(d), static_cast<int>(d)),
+                             gemm_chunks(static_cast<int>(d), static_cast<int>(F)));
+        ncmax = std::max(ncmax, gemm_chunks(static_cast<int>(d), static_cast<int>(2 * d)));
+        gpart_cap_ = static_cast<size_t>(ncmax) * R * d;
+        gpart_ = dalloc<float>(gpart_cap_);
+    }
     rsc_.rows = static_cast<int>(R);
     rsc_.bytes = row_scratch_bytes(static_cast<int>(R), static_cast<int>(V));
     rsc_.buf = dalloc<unsigned char>(rsc_.bytes);
@@ -294,7 +301,7 @@ Engine::~Engine() {
                     a2_, h_, fuse_, ws_.buf, ws_.ctr, logits_, pacc_, pml_, rows_.tok, rows_.pos, rows_.kv_dst,
                     rows_.ctx_base, rows_.ctx_len, rows_.chain_len, rows_.chain, rows_.feat_off, rows_.out_off,
                     rows_.key_pos, rows_.seed, rows_.par_row, lm_idx_, topk_tok_, topk_lp_, emitted_, acc_rows_,
-                    result_, err_, steps_, drow_, misc_i_, misc_l_, mask_dbg_, rsc_.buf, rsc_.ctr, rsc_.rowmax, asc_.row_ctr};
+                    result_, err_, steps_, drow_, misc_i_, misc_l_, mask_dbg_, rsc_.buf, rsc_.ctr, rsc_.rowmax, asc_.row_ctr, gpart_};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (h_result_) cudaFreeHost(h_result_);
@@ -486,6 +493,36 @@ void Engine::ln(int M, const float* g, const float* b, float* y) {
     count();
 }
 
+void Engine::gemm_resid_ln(const GemmWeight& w, const GemmAct& a, int M, bool accumulate, bool add_pos,
+                           const float* g, const float* b, float* y) {
+    const int d = dims_.d;
+    const int nc = gemm_chunks(w.N, w.K);
+    if (gemm_bn_for(M) >= 64 && nc > 1 && static_cast<size_t>(nc) * M * d <= gpart_cap_) {
+        GemmEpi e;
+        e.kind = kEpiPartials;
+        e.f32 = gpart_;
+        e.ld = d;
+        gemm(w, a, M, e, kClsGemm, 4.0 * nc);
+        const int e0 = pbeg();
+        launch_reduce_residual_ln(gpart_, nc, M, d, x_, accumulate, add_pos ? pos_emb_ : nullptr,
+                                  add_pos ? rows_.pos : nullptr, g, b, a_, y, st_);
+        pend(kClsRow, e0, static_cast<double>(M) * d * (4.0 * nc + 8 + 2 + (y ? 4 : 0)), 0);
+        count();
+        return;
+    }
+    GemmEpi e;
+    e.kind = add_pos ? kEpiFusePos : kEpiResid;
+    e.f32 = x_;
+    e.ld = d;
+    if (add_pos) {
+        e.pos_emb = pos_emb_;
+        e.pos = rows_.pos;
+    }
+    if (!accumulate && !add_pos) throw std::logic_error("gemm_resid_ln: plain store unsupported");
+    gemm(w, a, M, e, kClsGemm, 8.0);
+    ln(M, g, b, y);
+}
+
 void Engine::forward(const Fwd& f) {
     const int M = f.M, d = dims_.d, F = dims_.dff, H = dims_.heads;
     if (M <= 0) return;
@@ -505,14 +542,7 @@ void Engine::forward(const Fwd& f) {
         launch_gather_fuse(rows_.tok, rows_.feat_off, f.feat_base, tok_emb_, M, d, fuse_, st_);
         pend(kClsRow, e0, 3 * row_bytes, 0);
         count();
-        GemmEpi e;
-        e.kind = kEpiFusePos;
-        e.f32 = x_;
-        e.pos_emb = pos_emb_;
-        e.pos = rows_.pos;
-        e.ld = d;
-        gemm(w_fuse_, act_fuse_, M, e, kClsGemm, 8.0);
-        ln(M, L[0].ln1_g, L[0].ln1_b, nullptr);
+        gemm_resid_ln(w_fuse_, act_fuse_, M, false, true, L[0].ln1_g, L[0].ln1_b, nullptr);
     }
     const size_t lstride = static_cast<size_t>(kv.n_slots) * d;
     const double attn_bytes = f.attn_kv_unique * d * 4.0 + row_bytes * 1.5;
@@ -532,22 +562,16 @@ void Engine::forward(const Fwd& f) {
         launch_attention(q_, eq.K, eq.V, ar, M, H, d, f.max_vlen, f.attn_row_keys, asc_, att_, st_);
         pend(kClsAttn, e0, attn_bytes, attn_flops);
         count();
-        GemmEpi er;
-        er.kind = kEpiResid;
-        er.f32 = x_;
-        er.ld = d;
-        gemm(W.wo, act_att_, M, er, kClsGemm, 8.0);
-        ln(M, W.ln2_g, W.ln2_b, nullptr);
+        gemm_resid_ln(W.wo, act_att_, M, true, false, W.ln2_g, W.ln2_b, nullptr);
         GemmEpi eg;
         eg.kind = kEpiGeluBF16;
         eg.b16 = h_;
         eg.ld = F;
         gemm(W.w1, act_a_, M, eg, kClsGemm, 2.0);
-        gemm(W.w2, act_h_, M, er, kClsGemm, 8.0);
         const bool last = l + 1 == L.size();
         const float* g = last ? (f.draft ? dlnf_g_ : lnf_g_) : L[l + 1].ln1_g;
         const float* b = last ? (f.draft ? dlnf_b_ : lnf_b_) : L[l + 1].ln1_b;
-        ln(M, g, b, last ? f.y_out : nullptr);
+        gemm_resid_ln(W.w2, act_h_, M, true, false, g, b, last ? f.y_out : nullptr);
     }
     if (f.logits) {
         if (f.lm_idx) {

@@ -191,6 +191,12 @@ class Engine {
     void count(int n = 1) { launches_ += n; }
     void gemm(const GemmWeight& w, const GemmAct& a, int M, const GemmEpi& epi, int cls, double out_bytes);
     void ln(int M, const float* g, const float* b, float* y);
+    // x (+)= a.W^T [+ pos_emb], then LayerNorm(x) -> a_ (and y): the residual GEMMs (wo, w2)
+    // and the draft fuse. Token tiles >= 64 run the GEMM in kEpiPartials mode (one unit per
+    // (tile, chunk)) and add the chunks in order inside the LayerNorm kernel; smaller ones
+    // use the GEMM's own split-K finisher. Both give the same bits.
+    void gemm_resid_ln(const GemmWeight& w, const GemmAct& a, int M, bool accumulate, bool add_pos, const float* g,
+                       const float* b, float* y);
     int pbeg();
     void pend(int cls, int e0, double bytes, double flops);
     void pflush();
@@ -230,6 +236,8 @@ class Engine {
     // activations
     float *x_ = nullptr, *q_ = nullptr, *y_ = nullptr, *logits_ = nullptr, *featin_ = nullptr;
     RowScratch rsc_{};  // multi-CTA sampling / top-k records
+    float* gpart_ = nullptr;  // kEpiPartials chunk sums [chunks][max_rows][d]
+    size_t gpart_cap_ = 0;
     float *pacc_ = nullptr, *pml_ = nullptr;
     AttnScratch asc_{};
     __nv_bfloat16 *a_ = nullptr, *att_ = nullptr, *h_ = nullptr, *fuse_ = nullptr, *a2_ = nullptr;

@@ -18,13 +18,21 @@
 // warps 2-9 = epilogue (TMEM lane quarter = warp % 4 -> one output feature per thread;
 // two warps per quarter split the token columns).
 //
-// Batch invariance (SURVEY.md §7 hard part 1). K is cut into fixed 1024-wide chunks.
-// Every chunk is accumulated separately in TMEM, read out, and the chunk sums are added
-// in fp32 registers strictly in chunk order: ((c0 + c1) + c2) + ... A K split only decides
-// WHICH CTA computes which chunks: split 0 keeps the running prefix, later splits publish
-// their raw chunk sums, and the last-arriving CTA continues the same sequential sum. The
-// bits of an output element are therefore independent of M, of the token tile BN and of
-// the split count, which makes the speculative and the AR rollouts bit-identical.
+// Batch invariance (SURVEY.md §7 hard part 1). K is cut into fixed chunks whose width is
+// a property of the WEIGHT (chosen once from N and K so that a one-token GEMM still spans
+// the 148 SMs, never from the token count). Every chunk is accumulated separately in TMEM,
+// read out, and the chunk sums are added in fp32 registers strictly in chunk order:
+// ((c0 + c1) + c2) + ... A K split only decides WHICH CTA computes which chunks: split 0
+// keeps the running prefix, later splits publish their raw chunk sums, and the last-
+// arriving CTA continues the same sequential sum. The bits of an output element are
+// therefore independent of M, of the token tile BN and of the split count, which makes the
+// speculative and the AR rollouts bit-identical.
+//
+// Streaming: a pipeline stage carries kSub 64-wide k-boxes (up to 64 KB of weight) on one
+// mbarrier -- measured on B200, per-SM TMA throughput grows with the bytes per stage, not
+// with the stage count (scripts/probes/probe_bw.cu). With PDL the producer issues the
+// weight boxes of its first stages BEFORE griddepcontrol.wait (weights never depend on the
+// previous kernel), so the first HBM round trip overlaps the predecessor's tail.
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -39,9 +47,20 @@ namespace sgb {
 
 namespace {
 
+#ifndef SGB_KSUB32
+#define SGB_KSUB32 4
+#endif
+#ifndef SGB_KSUB64
+#define SGB_KSUB64 2
+#endif
+#ifndef SGB_KSUB128
+#define SGB_KSUB128 2
+#endif
+#ifndef SGB_CHUNK_MIN
+#define SGB_CHUNK_MIN 4
+#endif
 constexpr int kBK = 64;       // 64 bf16 = 128 B = one swizzle row
 constexpr int kBM = 128;      // output features per tile (UMMA M)
-constexpr int kChunkKB = 16;  // k-blocks per accumulation chunk (K = 1024); fixes the fp32 association
 constexpr int kABytes = kBM * kBK * 2;
 constexpr int kThreads = 320;  // TMA warp, MMA warp, 8 epilogue warps (2 per TMEM lane quarter)
 constexpr int kEpiThreads = 256;
@@ -49,9 +68,10 @@ constexpr int kNumSMs = 148;
 
 template <int BN>
 struct GemmCfg {
+    static constexpr int kSub = BN <= 32 ? SGB_KSUB32 : (BN == 64 ? SGB_KSUB64 : SGB_KSUB128);  // 64-wide k-boxes per stage
     static constexpr int kBBytes = BN * kBK * 2;
-    static constexpr int kStage = kABytes + kBBytes;
-    static constexpr int kStages = (196 * 1024) / kStage > 8 ? 8 : (196 * 1024) / kStage;
+    static constexpr int kStage = kSub * (kABytes + kBBytes);
+    static constexpr int kStages = (200 * 1024) / kStage > 8 ? 8 : (200 * 1024) / kStage;
     static constexpr int kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;
     static constexpr int kSmem = kStages * kStage + 1024 /*align*/ + 256 /*barriers*/;
 };
@@ -131,24 +151,52 @@ struct Unit {
     int m0, n0, split, tile;
 };
 
-__device__ __forceinline__ Unit decode_unit(int u, int m_tiles, int n_tiles, int BN) {
+// Units are tile-major (the K splits of a tile are adjacent), so the splits of a tile run
+// concurrently and the finisher work is spread over the launch instead of its last wave.
+__device__ __forceinline__ Unit decode_unit(int u, int m_tiles, int S, int BN) {
     Unit r;
-    const int mt = u % m_tiles;
-    const int rest = u / m_tiles;
-    const int nt = rest % n_tiles;
-    r.split = rest / n_tiles;
+    r.tile = u / S;
+    r.split = u - r.tile * S;
+    const int mt = r.tile % m_tiles;
+    const int nt = r.tile / m_tiles;
     r.m0 = mt * BN;
     r.n0 = nt * kBM;
-    r.tile = nt * m_tiles + mt;
     return r;
 }
+
+// The stage sequence of a CTA: units u = blockIdx.x + k*gridDim.x, each unit's chunks in
+// order, each chunk in stages of up to kSub k-blocks (a stage never straddles a chunk).
+struct StageSeq {
+    int u, c, c_end, kb, hi;
+    int n_units, stride, S, cps, nc, ckb, kbt, m_tiles, BN;
+    __device__ void start_unit() {
+        const Unit un = decode_unit(u, m_tiles, S, BN);
+        c = un.split * cps;
+        c_end = min(nc, c + cps);
+        kb = c * ckb;
+        hi = min(kbt, kb + ckb);
+    }
+    __device__ bool valid() const { return u < n_units; }
+    __device__ void next(int ksub) {
+        kb += ksub;
+        if (kb < hi) return;
+        if (++c < c_end) {
+            kb = c * ckb;
+            hi = min(kbt, kb + ckb);
+            return;
+        }
+        u += stride;
+        if (u < n_units) start_unit();
+    }
+};
 
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap mapW, const __grid_constant__ CUtensorMap mapX, int M,
-                        int N, int kb_total, int n_chunks, int cps, int S, int m_tiles, int n_tiles, GemmEpi epi,
+                        int N, int kb_total, int n_chunks, int ckb, int cps, int S, int m_tiles, int n_tiles, GemmEpi epi,
                         float* __restrict__ ws, int* __restrict__ ctr) {
     using Cfg = GemmCfg<BN>;
+    constexpr int SUB = Cfg::kSub;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::kStages * Cfg::kStage);
@@ -179,56 +227,102 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    // PDL: the prologue above overlapped the previous kernel; from here on we touch its outputs
-    pdl_wait();
-    pdl_trigger();
+    StageSeq seq0;
+    seq0.u = blockIdx.x;
+    seq0.n_units = n_units;
+    seq0.stride = gridDim.x;
+    seq0.S = S;
+    seq0.cps = cps;
+    seq0.nc = n_chunks;
+    seq0.ckb = ckb;
+    seq0.kbt = kb_total;
+    seq0.m_tiles = m_tiles;
+    seq0.BN = BN;
+    if (seq0.valid()) seq0.start_unit();
 
     if (warp == 0) {
         if (lane == 0) {
             const uint64_t pol_w = policy_evict_first();
-            int i = 0;
-            for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-                const Unit un = decode_unit(u, m_tiles, n_tiles, BN);
-                const int kb_begin = un.split * cps * kChunkKB;
-                const int kb_end = min(kb_total, (un.split + 1) * cps * kChunkKB);
-                for (int kb = kb_begin; kb < kb_end; ++kb, ++i) {
-                    const int s = i % Cfg::kStages;
-                    if (i >= Cfg::kStages) mbar_wait(&empty[s], ((i / Cfg::kStages) & 1) ^ 1);
-                    uint8_t* a = smem + s * Cfg::kStage;
-                    mbar_arrive_expect_tx(&full[s], Cfg::kStage);
-                    tma_load_2d_hint(a, &mapW, &full[s], kb * kBK, un.n0, pol_w);
-                    tma_load_2d(a + kABytes, &mapX, &full[s], kb * kBK, un.m0);
+            // (1) weight boxes of the first stages: independent of the previous kernel
+            StageSeq sq = seq0;
+            int npre = 0;
+            int pre_kb[Cfg::kStages], pre_ns[Cfg::kStages], pre_m0[Cfg::kStages];
+            for (; npre < Cfg::kStages && sq.valid(); ++npre) {
+                const int ns = min(SUB, sq.hi - sq.kb);
+                const Unit un = decode_unit(sq.u, m_tiles, S, BN);
+                uint8_t* a = smem + npre * Cfg::kStage;
+                mbar_arrive_expect_tx(&full[npre], ns * (kABytes + Cfg::kBBytes));
+                for (int j = 0; j < ns; ++j)
+                    tma_load_2d_hint(a + j * kABytes, &mapW, &full[npre], (sq.kb + j) * kBK, un.n0, pol_w);
+                pre_kb[npre] = sq.kb;
+                pre_ns[npre] = ns;
+                pre_m0[npre] = un.m0;
+                sq.next(SUB);
+            }
+            // (2) activations are produced by the previous kernel
+            pdl_wait();
+            pdl_trigger();
+            for (int s = 0; s < npre; ++s) {
+                uint8_t* b = smem + s * Cfg::kStage + SUB * kABytes;
+                for (int j = 0; j < pre_ns[s]; ++j)
+                    tma_load_2d(b + j * Cfg::kBBytes, &mapX, &full[s], (pre_kb[s] + j) * kBK, pre_m0[s]);
+            }
+            // (3) steady state
+            for (int i = npre; sq.valid(); ++i, sq.next(SUB)) {
+                const int s = i % Cfg::kStages;
+                mbar_wait(&empty[s], ((i / Cfg::kStages) & 1) ^ 1);
+                const int ns = min(SUB, sq.hi - sq.kb);
+                const Unit un = decode_unit(sq.u, m_tiles, S, BN);
+                uint8_t* a = smem + s * Cfg::kStage;
+                mbar_arrive_expect_tx(&full[s], ns * (kABytes + Cfg::kBBytes));
+                for (int j = 0; j < ns; ++j) {
+                    tma_load_2d_hint(a + j * kABytes, &mapW, &full[s], (sq.kb + j) * kBK, un.n0, pol_w);
+                    tma_load_2d(a + SUB * kABytes + j * Cfg::kBBytes, &mapX, &full[s], (sq.kb + j) * kBK, un.m0);
                 }
             }
+        } else {
+            pdl_wait();
+            pdl_trigger();
         }
     } else if (warp == 1) {
+        pdl_wait();
+        pdl_trigger();
         if (lane == 0) {
             constexpr uint32_t idesc = idesc_bf16_m128(BN);
-            int i = 0, it = 0;
-            for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-                const Unit un = decode_unit(u, m_tiles, n_tiles, BN);
-                const int c_begin = un.split * cps, c_end = min(n_chunks, c_begin + cps);
-                for (int c = c_begin; c < c_end; ++c, ++it) {
-                    const int buf = it & 1;
-                    if (it >= 2) mbar_wait(&tempty[buf], ((it >> 1) - 1) & 1);
+            StageSeq sq = seq0;
+            int i = 0, it = -1, cur_c = -1, cur_u = -1;
+            for (; sq.valid(); ++i) {
+                const bool chunk_start = (sq.u != cur_u || sq.c != cur_c);
+                if (chunk_start) {
+                    cur_u = sq.u;
+                    cur_c = sq.c;
+                    ++it;
+                    if (it >= 2) mbar_wait(&tempty[it & 1], ((it >> 1) - 1) & 1);
                     tc_fence_after();
-                    const int lo = c * kChunkKB, hi = min(kb_total, lo + kChunkKB);
-                    for (int kb = lo; kb < hi; ++kb, ++i) {
-                        const int s = i % Cfg::kStages;
-                        mbar_wait(&full[s], (i / Cfg::kStages) & 1);
-                        tc_fence_after();
-                        const uint32_t a = smem_u32(smem + s * Cfg::kStage);
-                        const uint64_t adesc = sw128_desc(a), bdesc = sw128_desc(a + kABytes);
-#pragma unroll
-                        for (int k = 0; k < kBK / 16; ++k)
-                            umma_bf16(tmem + buf * BN, adesc + 2 * k, bdesc + 2 * k, idesc, (kb != lo || k != 0));
-                        umma_commit(&empty[s]);
-                    }
-                    umma_commit(&tfull[buf]);
                 }
+                const int buf = it & 1;
+                const int ns = min(SUB, sq.hi - sq.kb);
+                const bool first = sq.kb == sq.c * ckb;
+                const bool chunk_end = sq.kb + ns >= sq.hi;
+                const int s = i % Cfg::kStages;
+                mbar_wait(&full[s], (i / Cfg::kStages) & 1);
+                tc_fence_after();
+                const uint32_t a = smem_u32(smem + s * Cfg::kStage);
+                const uint32_t b = a + SUB * kABytes;
+                for (int j = 0; j < ns; ++j) {
+                    const uint64_t adesc = sw128_desc(a + j * kABytes), bdesc = sw128_desc(b + j * Cfg::kBBytes);
+#pragma unroll
+                    for (int k = 0; k < kBK / 16; ++k)
+                        umma_bf16(tmem + buf * BN, adesc + 2 * k, bdesc + 2 * k, idesc, (!first || j != 0 || k != 0));
+                }
+                umma_commit(&empty[s]);
+                if (chunk_end) umma_commit(&tfull[buf]);
+                sq.next(SUB);
             }
         }
     } else {
+        pdl_wait();
+        pdl_trigger();
         // ---------------- epilogue warps: TMEM lane quarter q (output feature o), column half h
         constexpr int HB = BN / 2;
         const int q = warp & 3;
@@ -237,7 +331,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int j0 = h * HB;
         int it = 0;
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-            const Unit un = decode_unit(u, m_tiles, n_tiles, BN);
+            const Unit un = decode_unit(u, m_tiles, S, BN);
             const int o = un.n0 + r;
             const int ncols = min(BN, M - un.m0);
             const int nmine = max(0, min(HB, ncols - j0));
@@ -254,7 +348,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int p0 = 0; p0 < HB; p0 += PC) {
                     float v[PC];
                     tmem_ld<PC>(tmem + (static_cast<uint32_t>(32 * q) << 16) + buf * BN + j0 + p0, v);
-                    if (un.split == 0) {
+                    if (epi.kind == kEpiPartials) {
+                        float* dst = epi.f32 + (static_cast<size_t>(c) * M + un.m0 + j0 + p0) * epi.ld + o;
+#pragma unroll
+                        for (int j = 0; j < PC; ++j)
+                            if (p0 + j < nmine && o < N) dst[static_cast<size_t>(j) * epi.ld] = v[j];
+                    } else if (un.split == 0) {
                         if (c == c_begin) {
 #pragma unroll
                             for (int j = 0; j < PC; ++j) run[p0 + j] = v[j];
@@ -272,7 +371,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&tempty[buf]);
             }
-            if (S == 1) {
+            if (epi.kind == kEpiPartials) {
+                // raw chunk sums already stored; the consumer kernel reduces them in order
+            } else if (S == 1) {
                 if (o < N) epi_store_run<HB>(epi, un.m0 + j0, nmine, o, run);
             } else {
                 if (un.split == 0)
@@ -291,26 +392,32 @@ __global__ void __launch_bounds__(kThreads, 1)
                     __threadfence();
                     if (o < N) {
                         // The finisher continues the sequential chunk sum. Columns are
-                        // independent, so 8 of them are processed together (8 loads in
-                        // flight per chunk) while each column keeps its strict chunk order.
+                        // independent: 8 columns x FB chunks of loads are in flight at once,
+                        // then added strictly in chunk order per column.
+                        constexpr int FB = HB <= 8 ? 8 : 4;
                         for (int jb = j0; jb < j0 + nmine; jb += 8) {
                             float v[8];
 #pragma unroll
-                            for (int u = 0; u < 8; ++u)
-                                v[u] = (jb + u < j0 + nmine) ? __ldcg(&wst[static_cast<size_t>(jb + u) * kBM + r]) : 0.f;
-                            for (int c = cps; c < n_chunks; ++c) {
-                                float a[8];
+                            for (int t = 0; t < 8; ++t)
+                                v[t] = (jb + t < j0 + nmine) ? __ldcg(&wst[static_cast<size_t>(jb + t) * kBM + r]) : 0.f;
+                            for (int c0 = cps; c0 < n_chunks; c0 += FB) {
+                                float a[FB][8];
 #pragma unroll
-                                for (int u = 0; u < 8; ++u)
-                                    a[u] = (jb + u < j0 + nmine)
-                                               ? __ldcg(&wst[(static_cast<size_t>(c) * BN + jb + u) * kBM + r])
-                                               : 0.f;
+                                for (int cc = 0; cc < FB; ++cc)
 #pragma unroll
-                                for (int u = 0; u < 8; ++u) v[u] += a[u];
+                                    for (int t = 0; t < 8; ++t)
+                                        a[cc][t] = (c0 + cc < n_chunks && jb + t < j0 + nmine)
+                                                       ? __ldcg(&wst[(static_cast<size_t>(c0 + cc) * BN + jb + t) * kBM + r])
+                                                       : 0.f;
+#pragma unroll
+                                for (int cc = 0; cc < FB; ++cc)
+                                    if (c0 + cc < n_chunks)
+#pragma unroll
+                                        for (int t = 0; t < 8; ++t) v[t] += a[cc][t];
                             }
 #pragma unroll
-                            for (int u = 0; u < 8; ++u)
-                                if (jb + u < j0 + nmine) epi_store(epi, un.m0 + jb + u, o, v[u]);
+                            for (int t = 0; t < 8; ++t)
+                                if (jb + t < j0 + nmine) epi_store(epi, un.m0 + jb + t, o, v[t]);
                         }
                     }
                     if (threadIdx.x == 64) ctr[un.tile] = 0;
@@ -337,7 +444,7 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 template <int BN>
-void launch_bn(const CUtensorMap& w, const CUtensorMap& x, int M, int N, int kbt, int n_chunks, int S, int cps,
+void launch_bn(const CUtensorMap& w, const CUtensorMap& x, int M, int N, int kbt, int n_chunks, int ckb, int S, int cps,
                const GemmEpi& epi, float* ws, int* ctr, cudaStream_t st) {
     using Cfg = GemmCfg<BN>;
     static bool attr = false;
@@ -348,13 +455,37 @@ void launch_bn(const CUtensorMap& w, const CUtensorMap& x, int M, int N, int kbt
     const int m_tiles = (M + BN - 1) / BN, n_tiles = (N + kBM - 1) / kBM;
     const int units = m_tiles * n_tiles * S;
     const int grid = std::min(units, kNumSMs);
-    launch_pdl(gemm_bf16_tn_kernel<BN>, dim3(grid), dim3(kThreads), Cfg::kSmem, st, w, x, M, N, kbt, n_chunks, cps, S,
-               m_tiles, n_tiles, epi, ws, ctr);
+    launch_pdl(gemm_bf16_tn_kernel<BN>, dim3(grid), dim3(kThreads), Cfg::kSmem, st, w, x, M, N, kbt, n_chunks, ckb, cps,
+               S, m_tiles, n_tiles, epi, ws, ctr);
 }
 
-int chunks_of(int K) { return ((K + kBK - 1) / kBK + kChunkKB - 1) / kChunkKB; }
-
 }  // namespace
+
+// Chunk width (in 64-wide k-blocks) of a weight [N][K]: enough chunks that a one-token
+// GEMM has ~one unit per SM, at least 4 k-blocks (one full stage) per chunk. A function
+// of the weight shape only -- never of the token count -- so the fp32 association of
+// every output is fixed per weight.
+int gemm_chunk_kb(int N, int K) {
+    const int kbt = (K + kBK - 1) / kBK;
+    const int n_tiles = (N + kBM - 1) / kBM;
+    const int want = std::max(1, (kNumSMs + n_tiles - 1) / n_tiles);
+    int ckb = (kbt + want - 1) / want;
+    ckb = ((ckb + 3) / 4) * 4;
+    ckb = std::max(ckb, SGB_CHUNK_MIN);
+    return std::min(ckb, ((kbt + 3) / 4) * 4);
+}
+
+int gemm_chunks(int N, int K) {
+    const int kbt = (K + kBK - 1) / kBK;
+    const int ckb = gemm_chunk_kb(N, K);
+    return (kbt + ckb - 1) / ckb;
+}
+
+static int chunks_of(int N, int K) {
+    const int kbt = (K + kBK - 1) / kBK;
+    const int ckb = gemm_chunk_kb(N, K);
+    return (kbt + ckb - 1) / ckb;
+}
 
 CUtensorMap make_kmajor_map(const void* ptr, int rows, int K, int box_rows) {
     if (K % 8) throw std::invalid_argument("GEMM K must be a multiple of 8");
@@ -377,17 +508,22 @@ int gemm_bn_for(int M) {
     return 128;  // BN=256 (kernel instantiated) spills the epilogue's running sums at 320 threads
 }
 
-// K split: enough work units for one wave on 148 SMs. Any choice gives identical bits.
+// K split: which CTA computes which chunks. Any choice gives identical bits.
 int gemm_splits_for(int M, int N, int K) {
     const int bn = gemm_bn_for(M);
     const int tiles = ((M + bn - 1) / bn) * ((N + kBM - 1) / kBM);
-    const int nc = chunks_of(K);
-    // Split only in the HBM-bound decode regime (<= 32 token rows) where the finisher's
-    // serial tail is a handful of columns; larger M has enough tiles or is MMA-bound.
-    if (tiles >= 96 || (bn > 32 && (tiles >= 74 || nc < 4))) return 1;
-    int S = (kNumSMs + tiles - 1) / tiles;
-    if (S > nc) S = nc;
-    if (S < 1) S = 1;
+    const int nc = chunks_of(N, K);
+    if (nc <= 1) return 1;
+    int S = 1;
+    if (bn <= 32) {
+        // HBM-bound decode regime: up to one unit per SM; with more than ~64 weight tiles a
+        // split only adds finisher latency (measured, scripts/gemm_sweep.py)
+        if (tiles <= 64) S = std::min(nc, kNumSMs / tiles);
+    }
+    // token tiles of 64-128: the in-kernel finisher would read (nc - cps) raw chunk partials
+    // of BN x 128 fp32 each; those GEMMs run unsplit, or in kEpiPartials mode when a row
+    // kernel follows (wo, w2, draft fuse)
+    S = std::max(1, S);
     const int cps = (nc + S - 1) / S;
     return (nc + cps - 1) / cps;
 }
@@ -395,7 +531,7 @@ int gemm_splits_for(int M, int N, int K) {
 size_t gemm_ws_floats(int M, int N, int K) {
     const int bn = gemm_bn_for(M);
     const size_t tiles = static_cast<size_t>((M + bn - 1) / bn) * ((N + kBM - 1) / kBM);
-    return tiles * chunks_of(K) * bn * kBM;
+    return tiles * chunks_of(N, K) * bn * kBM;
 }
 
 void gemm_run(const GemmWeight& w, const GemmAct& x, int M, const GemmEpi& epi, const GemmWorkspace& ws,
@@ -403,20 +539,22 @@ void gemm_run(const GemmWeight& w, const GemmAct& x, int M, const GemmEpi& epi, 
     if (M <= 0) return;
     if (M > x.cap_rows) throw std::invalid_argument("gemm: rows exceed activation capacity");
     const int kbt = (w.K + kBK - 1) / kBK;
-    const int nc = chunks_of(w.K);
+    const int ckb = w.chunk_kb;
+    const int nc = (kbt + ckb - 1) / ckb;
     int S = force_splits > 0 ? std::min(force_splits, nc) : gemm_splits_for(M, w.N, w.K);
     const int bn = gemm_bn_for(M);
     const int tiles = ((M + bn - 1) / bn) * ((w.N + kBM - 1) / kBM);
-    if (S > 1 && (ws.buf == nullptr || gemm_ws_floats(M, w.N, w.K) > ws.cap_floats || tiles > ws.ctr_cap)) S = 1;
+    if (epi.kind == kEpiPartials) S = nc;  // one unit per (tile, chunk), no in-kernel finisher
+    else if (S > 1 && (ws.buf == nullptr || gemm_ws_floats(M, w.N, w.K) > ws.cap_floats || tiles > ws.ctr_cap)) S = 1;
     const int cps = (nc + S - 1) / S;
     S = (nc + cps - 1) / cps;
     const CUtensorMap& xm = x.map_for_bn(bn);
     switch (bn) {
-        case 16: launch_bn<16>(w.map, xm, M, w.N, kbt, nc, S, cps, epi, ws.buf, ws.ctr, st); break;
-        case 32: launch_bn<32>(w.map, xm, M, w.N, kbt, nc, S, cps, epi, ws.buf, ws.ctr, st); break;
-        case 64: launch_bn<64>(w.map, xm, M, w.N, kbt, nc, S, cps, epi, ws.buf, ws.ctr, st); break;
-        case 128: launch_bn<128>(w.map, xm, M, w.N, kbt, nc, S, cps, epi, ws.buf, ws.ctr, st); break;
-        default: launch_bn<256>(w.map, xm, M, w.N, kbt, nc, S, cps, epi, ws.buf, ws.ctr, st); break;
+        case 16: launch_bn<16>(w.map, xm, M, w.N, kbt, nc, ckb, S, cps, epi, ws.buf, ws.ctr, st); break;
+        case 32: launch_bn<32>(w.map, xm, M, w.N, kbt, nc, ckb, S, cps, epi, ws.buf, ws.ctr, st); break;
+        case 64: launch_bn<64>(w.map, xm, M, w.N, kbt, nc, ckb, S, cps, epi, ws.buf, ws.ctr, st); break;
+        case 128: launch_bn<128>(w.map, xm, M, w.N, kbt, nc, ckb, S, cps, epi, ws.buf, ws.ctr, st); break;
+        default: launch_bn<256>(w.map, xm, M, w.N, kbt, nc, ckb, S, cps, epi, ws.buf, ws.ctr, st); break;
     }
 }
 
@@ -424,6 +562,7 @@ void GemmWeight::init(const __nv_bfloat16* p, int n, int k) {
     ptr = p;
     N = n;
     K = k;
+    chunk_kb = gemm_chunk_kb(n, k);
     map = make_kmajor_map(p, n, k, kBM);
 }
 

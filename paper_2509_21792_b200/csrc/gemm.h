@@ -11,6 +11,7 @@ namespace sgb {
 struct GemmWeight {
     const __nv_bfloat16* ptr = nullptr;
     int N = 0, K = 0;
+    int chunk_kb = 16;  // accumulation chunk in 64-wide k-blocks (gemm_chunk_kb: fixed per weight shape)
     CUtensorMap map;
     void init(const __nv_bfloat16* p, int n, int k);
 };
@@ -32,6 +33,8 @@ enum GemmEpiKind : int {
     kEpiResid = 3,    // x[t*ld + o] += v   (residual stream, fp32)           (tinylm.hpp:396-403)
     kEpiQKV = 4,      // o<d: q[t*d+o]=v; K/V[kv_dst[t]*d + o-d|o-2d] = bf16(v) (tinylm.hpp:325-327,405-408)
     kEpiFusePos = 5,  // x[t*ld + o] = v + pos_emb[pos[t]*ld + o]            (tinylm.hpp:528-533)
+    kEpiPartials = 6, // f32[(c*M + t)*ld + o] = raw chunk sum c (one unit per chunk); the row
+                      // kernel that follows adds the chunks in order (launch_reduce_residual_ln)
 };
 
 struct GemmEpi {
@@ -57,6 +60,8 @@ struct GemmWorkspace {
 
 CUtensorMap make_kmajor_map(const void* ptr, int rows, int K, int box_rows);
 int gemm_bn_for(int M);
+int gemm_chunk_kb(int N, int K);
+int gemm_chunks(int N, int K);  // chunk count of a weight (rows of a kEpiPartials output)
 int gemm_splits_for(int M, int N, int K);
 size_t gemm_ws_floats(int M, int N, int K);
 void gemm_run(const GemmWeight& w, const GemmAct& x, int M, const GemmEpi& epi, const GemmWorkspace& ws,

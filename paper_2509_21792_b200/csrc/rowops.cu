@@ -104,23 +104,56 @@ __global__ void __launch_bounds__(kRowThreads)
     const int r = blockIdx.x;
     float xs[PER];
     const float* pe = pos_emb ? pos_emb + static_cast<size_t>(positions[r]) * d : nullptr;
+    const size_t row = static_cast<size_t>(r) * d;
+    if (P) {
+        // chunk partials, strictly in chunk order per element; the loads of two chunks for
+        // all of this thread's elements are in flight together
+        const size_t st = static_cast<size_t>(M) * d;
+        float acc[PER];
 #pragma unroll
-    for (int i = 0; i < PER; ++i) {
-        const int e = threadIdx.x + i * kRowThreads;
-        if (e < d) {
-            const size_t idx = static_cast<size_t>(r) * d + e;
-            if (P) {
-                float acc = P[idx];
-                for (int s = 1; s < S; ++s) acc += P[static_cast<size_t>(s) * M * d + idx];
-                float v = accumulate ? x[idx] + acc : acc;
+        for (int i = 0; i < PER; ++i) {
+            const int e = threadIdx.x + i * kRowThreads;
+            acc[i] = e < d ? P[row + e] : 0.f;
+        }
+        int s = 1;
+        for (; s + 2 <= S; s += 2) {
+            float p1[PER], p2[PER];
+#pragma unroll
+            for (int i = 0; i < PER; ++i) {
+                const int e = threadIdx.x + i * kRowThreads;
+                p1[i] = e < d ? P[s * st + row + e] : 0.f;
+                p2[i] = e < d ? P[(s + 1) * st + row + e] : 0.f;
+            }
+#pragma unroll
+            for (int i = 0; i < PER; ++i) {
+                acc[i] += p1[i];
+                acc[i] += p2[i];
+            }
+        }
+        if (s < S) {
+#pragma unroll
+            for (int i = 0; i < PER; ++i) {
+                const int e = threadIdx.x + i * kRowThreads;
+                acc[i] += e < d ? P[s * st + row + e] : 0.f;
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int e = threadIdx.x + i * kRowThreads;
+            if (e < d) {
+                float v = accumulate ? x[row + e] + acc[i] : acc[i];
                 if (pe) v += pe[e];
-                x[idx] = v;
+                x[row + e] = v;
                 xs[i] = v;
             } else {
-                xs[i] = x[idx];  // plain LayerNorm of the residual stream
+                xs[i] = 0.f;
             }
-        } else {
-            xs[i] = 0.f;
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int e = threadIdx.x + i * kRowThreads;
+            xs[i] = e < d ? x[row + e] : 0.f;  // plain LayerNorm of the residual stream
         }
     }
     if (g)
