@@ -167,6 +167,17 @@ int sgb_draft_update_last(sgb_engine* e, const sgb_adamw* opt, float* grad_out, 
 /* Reset the AdamW moments and step counter (a fresh AdamW object). */
 int sgb_adamw_reset(sgb_engine* e);
 
+/* ---- hardware profile: C_peak calibration (Alg. 2, src/roofline.cpp:39-108) ------------- */
+/* detect_knee (roofline.cpp:39-76): farthest point from the chord of the unit-normalised
+ * curve; confidence in [0, 1]. n >= 4 (else SGB_EINVAL). */
+int sgb_detect_knee(const int* b, const double* s, int n, int* index, double* confidence);
+/* measure_c_peak (roofline.cpp:78-108) with the reference CLI's latency_fn
+ * (tools/sgrpo.cpp:38-49): a batched b-row target forward (EOS token, position 0, self-only
+ * mask) on the engine's device, median of `reps` CUDA-event timings for b = 1..b_max.
+ * curve_s (optional) receives the b_max median latencies in seconds. */
+int sgb_measure_c_peak(sgb_engine* e, int b_max, int warmup, int reps, int* c_peak, double* confidence,
+                       int* low_confidence, double* curve_s);
+
 /* GEMM microbenchmark (device-resident operands): average device ms per launch. */
 int sgb_bench_gemm(int M, int N, int K, int splits, int iters, double* ms_out);
 

@@ -1109,3 +1109,53 @@ def load_checkpoint(path: str):
     if hdr["kind"] == "draft":
         return "draft", draft_from_flat(cfg, flat, int(hdr["draft_layers"]))
     return "target", model_from_flat(cfg, flat)
+
+
+# ----------------------------------------------------------------------------------
+# Hardware profile: C_peak calibration -- src/roofline.cpp:39-108 (Alg. 2)
+# ----------------------------------------------------------------------------------
+def detect_knee(curve):
+    """roofline.cpp:39-76: normalise both axes to the unit box; the knee is the point
+    farthest from the chord first->last; confidence = distance / (sqrt(2)/2), clamped."""
+    n = len(curve)
+    if n < 4:
+        raise ValueError("detect_knee: need at least 4 points")
+    xs = [float(b) for b, _ in curve]
+    ys = [float(s) for _, s in curve]
+    xmin, xmax, ymin, ymax = min(xs), max(xs), min(ys), max(ys)
+    xspan = xmax - xmin if xmax > xmin else 1.0
+    yspan = ymax - ymin if ymax > ymin else 1.0
+    nx = [(x - xmin) / xspan for x in xs]
+    ny = [(y - ymin) / yspan for y in ys]
+    x0, y0, x1, y1 = nx[0], ny[0], nx[-1], ny[-1]
+    cx, cy = x1 - x0, y1 - y0
+    clen = math.sqrt(cx * cx + cy * cy)
+    best, idx = -1.0, 0
+    for i in range(n):
+        if clen == 0:
+            dist = math.sqrt((nx[i] - x0) ** 2 + (ny[i] - y0) ** 2)
+        else:
+            dist = abs(cx * (ny[i] - y0) - cy * (nx[i] - x0)) / clen
+        if dist > best:
+            best, idx = dist, i
+    return idx, min(max(best / 0.7071067811865476, 0.0), 1.0)
+
+
+def measure_c_peak(latency_fn, b_max: int, warmup: int = 1, reps: int = 3):
+    """roofline.cpp:78-108: median of `reps` latencies per b = 1..b_max; a >2% drop marks
+    low confidence; confidence < 0.05 falls back to c_peak = b_max."""
+    if b_max < 4:
+        raise ValueError("measure_c_peak: b_max must be >= 4")
+    if reps < 1:
+        raise ValueError("measure_c_peak: reps must be >= 1")
+    curve = []
+    for b in range(1, b_max + 1):
+        for _ in range(warmup):
+            latency_fn(b)
+        samples = sorted(latency_fn(b) for _ in range(reps))
+        curve.append((b, samples[reps // 2]))
+    low = any(curve[i][1] < curve[i - 1][1] * (1.0 - 0.02) for i in range(1, len(curve)))
+    idx, conf = detect_knee(curve)
+    if conf < 0.05:
+        return dict(c_peak=b_max, confidence=conf, low_confidence=True, curve=curve)
+    return dict(c_peak=curve[idx][0], confidence=conf, low_confidence=low, curve=curve)

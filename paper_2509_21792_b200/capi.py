@@ -60,7 +60,7 @@ EXPORTED = ["sgb_last_error", "sgb_version", "sgb_device_count", "sgb_engine_cre
             "sgb_cache_reset", "sgb_cache_len", "sgb_cache_read", "sgb_cache_gather_tail", "sgb_forward_target",
             "sgb_forward_draft_rows", "sgb_sample_rows", "sgb_topk_logsoftmax", "sgb_build_tree", "sgb_rollout",
             "sgb_debug_gemm", "sgb_profile_enable", "sgb_profile_read", "sgb_bench_gemm", "sgb_bench_attention",
-            "sgb_debug_attention"]
+            "sgb_debug_attention", "sgb_detect_knee", "sgb_measure_c_peak"]
 
 KERNEL_CLASSES = ["gemm_tcgen05", "attention", "rowops", "lm_head", "sample", "tree", "kv_commit"]
 
@@ -399,3 +399,26 @@ Engine.nccl_init = _nccl_init
 Engine.allreduce_f64 = _allreduce_f64
 Engine.allreduce_i64 = _allreduce_i64
 EXPORTED += ["sgb_nccl_unique_id", "sgb_nccl_init", "sgb_allreduce_sum_f64", "sgb_allreduce_sum_i64"]
+
+
+def detect_knee(curve):
+    """detect_knee (roofline.cpp:39-76) on [(b, seconds), ...] -> (index, confidence)."""
+    b = np.ascontiguousarray([int(x) for x, _ in curve], np.int32)
+    sec = np.ascontiguousarray([float(y) for _, y in curve], np.float64)
+    idx, conf = C.c_int(), C.c_double()
+    _check(_lib.sgb_detect_knee(_p(b, C.c_int), _p(sec, C.c_double), len(b), C.byref(idx), C.byref(conf)))
+    return idx.value, conf.value
+
+
+def _measure_c_peak(self, b_max: int, warmup: int = 1, reps: int = 3):
+    """measure_c_peak (roofline.cpp:78-108) on this engine's device. Returns a dict in the
+    reference's HardwareProfile JSON vocabulary (roofline.cpp:188-201)."""
+    cp, conf, low = C.c_int(), C.c_double(), C.c_int()
+    curve = np.zeros(b_max, np.float64)
+    _check(_lib.sgb_measure_c_peak(self.h, b_max, warmup, reps, C.byref(cp), C.byref(conf), C.byref(low),
+                                   _p(curve, C.c_double)))
+    return dict(c_peak=cp.value, confidence=conf.value, low_confidence=bool(low.value),
+                latency_curve=[[b + 1, float(curve[b])] for b in range(b_max)])
+
+
+Engine.measure_c_peak = _measure_c_peak

@@ -5,6 +5,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -356,6 +357,81 @@ int sgb_draft_update_last(sgb_engine* e, const sgb_adamw* opt, float* grad_out, 
         }
         a.use_last_rollout = true;
         fill_terms(E(e).draft_update(a), terms);
+    });
+}
+
+// ---- C_peak calibration (roofline.cpp:39-108) -------------------------------------------
+namespace {
+// detect_knee: normalise both axes to the unit box, take the point farthest from the chord
+// joining the first and last points; confidence = distance / (sqrt(2)/2).
+void knee_of(const int* b, const double* s, int n, int* index, double* confidence) {
+    if (n < 4) throw std::invalid_argument("detect_knee: need at least 4 points");
+    double xmin = b[0], xmax = b[0], ymin = s[0], ymax = s[0];
+    for (int i = 0; i < n; ++i) {
+        xmin = std::min(xmin, static_cast<double>(b[i]));
+        xmax = std::max(xmax, static_cast<double>(b[i]));
+        ymin = std::min(ymin, s[i]);
+        ymax = std::max(ymax, s[i]);
+    }
+    const double xspan = xmax > xmin ? xmax - xmin : 1.0;
+    const double yspan = ymax > ymin ? ymax - ymin : 1.0;
+    auto nx = [&](int i) { return (b[i] - xmin) / xspan; };
+    auto ny = [&](int i) { return (s[i] - ymin) / yspan; };
+    const double x0 = nx(0), y0 = ny(0), x1 = nx(n - 1), y1 = ny(n - 1);
+    const double cx = x1 - x0, cy = y1 - y0;
+    const double clen = std::sqrt(cx * cx + cy * cy);
+    double best = -1;
+    int bi = 0;
+    for (int i = 0; i < n; ++i) {
+        double dist;
+        if (clen == 0) {
+            const double dx = nx(i) - x0, dy = ny(i) - y0;
+            dist = std::sqrt(dx * dx + dy * dy);
+        } else {
+            dist = std::abs(cx * (ny(i) - y0) - cy * (nx(i) - x0)) / clen;
+        }
+        if (dist > best) {
+            best = dist;
+            bi = i;
+        }
+    }
+    *index = bi;
+    *confidence = std::clamp(best / 0.7071067811865476, 0.0, 1.0);
+}
+}  // namespace
+
+int sgb_detect_knee(const int* b, const double* s, int n, int* index, double* confidence) {
+    return guarded([&] { knee_of(b, s, n, index, confidence); });
+}
+
+int sgb_measure_c_peak(sgb_engine* e, int b_max, int warmup, int reps, int* c_peak, double* confidence,
+                       int* low_confidence, double* curve_s) {
+    return guarded([&] {
+        if (b_max < 4) throw std::invalid_argument("measure_c_peak: b_max must be >= 4");
+        if (reps < 1) throw std::invalid_argument("measure_c_peak: reps must be >= 1");
+        std::vector<int> bs(b_max);
+        std::vector<double> ss(b_max);
+        for (int b = 1; b <= b_max; ++b) {
+            bs[b - 1] = b;
+            ss[b - 1] = E(e).latency_probe(b, warmup, reps);
+        }
+        // non-monotone noise beyond 2% lowers confidence in the knee
+        bool low = false;
+        for (int i = 1; i < b_max; ++i)
+            if (ss[i] < ss[i - 1] * (1.0 - 0.02)) low = true;
+        int idx = 0;
+        double conf = 0;
+        knee_of(bs.data(), ss.data(), b_max, &idx, &conf);
+        *confidence = conf;
+        if (conf < 0.05) {  // no detectable knee: fall back to b_max
+            *c_peak = b_max;
+            low = true;
+        } else {
+            *c_peak = bs[idx];
+        }
+        *low_confidence = low ? 1 : 0;
+        if (curve_s)
+            for (int i = 0; i < b_max; ++i) curve_s[i] = ss[i];
     });
 }
 

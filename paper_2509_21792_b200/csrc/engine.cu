@@ -647,6 +647,43 @@ void Engine::upload_rows_host(int M, const std::vector<int>& tok, const std::vec
     if (feat_off) h2d(rows_.feat_off, feat_off->data(), M, st_);
 }
 
+// ------------------------------------------------------------------ C_peak calibration
+double Engine::latency_probe(int b, int warmup, int reps) {
+    if (b < 1 || b > max_rows_) throw std::invalid_argument("latency_probe: batch outside [1, max_rows]");
+    if (b > tkv_.n_slots) throw std::invalid_argument("latency_probe: batch exceeds KV slots");
+    if (!target_ready_) throw std::runtime_error("weights not uploaded");
+    // rows of the reference latency_fn: token kEosToken at position 0, self-only mask ->
+    // each row's only key is its own (written to a distinct KV slot)
+    std::vector<int> tok(b, 1), pos(b, 0), cl(b, 0), chl(b, 1);
+    std::vector<long long> kvd(b), cb(b, 0), ch(static_cast<size_t>(b) * kMaxChain, 0);
+    for (int i = 0; i < b; ++i) {
+        kvd[i] = i;
+        ch[static_cast<size_t>(i) * kMaxChain] = i;
+    }
+    upload_rows_host(b, tok, pos, kvd, cb, cl, chl, ch, nullptr);
+    Fwd f;
+    f.M = b;
+    f.y_out = y_;
+    f.logits = true;
+    f.logits_out = logits_;
+    f.max_vlen = 1;
+    f.attn_kv_unique = b;
+    f.attn_row_keys = b;
+    std::vector<double> t(reps);
+    for (int w = 0; w < warmup; ++w) forward(f);
+    for (int r = 0; r < reps; ++r) {
+        SGB_CUDA(cudaEventRecord(ev0_, st_));
+        forward(f);
+        SGB_CUDA(cudaEventRecord(ev1_, st_));
+        SGB_CUDA(cudaEventSynchronize(ev1_));
+        float ms = 0.f;
+        SGB_CUDA(cudaEventElapsedTime(&ms, ev0_, ev1_));
+        t[r] = ms * 1e-3;
+    }
+    std::nth_element(t.begin(), t.begin() + reps / 2, t.end());
+    return t[reps / 2];
+}
+
 // ------------------------------------------------------------------ per-op parity entry points
 void Engine::cache_reset(int slot, bool draft) {
     if (slot < 0 || slot >= max_seqs_) throw std::invalid_argument("cache slot out of range");

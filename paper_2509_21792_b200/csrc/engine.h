@@ -153,6 +153,10 @@ class Engine {
     };
     DraftLossTerms draft_update(const DraftUpdateArgs& a);
     void adamw_reset();
+    // measure_c_peak's latency_fn on the device (roofline.cpp:78-108 / tools/sgrpo.cpp:38-49):
+    // one batched target forward of b rows (EOS token, position 0, self-only attention),
+    // median device seconds over `reps` after `warmup` untimed launches.
+    double latency_probe(int b, int warmup, int reps);
 
     // debug tree driver (tests): expands one tree on device with host-supplied logits
     struct DebugTree {

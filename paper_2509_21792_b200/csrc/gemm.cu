@@ -503,7 +503,8 @@ CUtensorMap make_kmajor_map(const void* ptr, int rows, int K, int box_rows) {
 
 int gemm_bn_for(int M) {
     if (M <= 16) return 16;
-    if (M <= 32) return 32;
+    // BN=32 measured slower than BN=64 for 17..32 tokens at the c2 shapes
+    // (profiles/hw_profile_c2.json latency curve); BN=32 stays instantiated for tests
     if (M <= 64) return 64;
     return 128;  // BN=256 (kernel instantiated) spills the epilogue's running sums at 320 threads
 }
