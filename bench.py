@@ -34,11 +34,21 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 WORKLOADS = {
-    # name: (V, d, L, H, dff, P, G, queries, max_new)
-    "c2": dict(V=151936, d=1536, L=28, H=12, dff=8960, P=128, G=8, Q=64, new=1024,
+    # V, d, L, H, dff; P prompt tokens, G group, Q queries per GPU, new max new tokens
+    "c2": dict(V=151936, d=1536, L=28, H=12, dff=8960, P=128, G=8, Q=64, new=1024, stops=False, online=False, warm=0,
                desc="Qwen2.5-1.5B-shaped target + 1-layer draft, 64 queries x group 8, 128-token prompts, "
                     "1024 new tokens, greedy, adaptive spec (c_peak 211)"),
-    "c1": dict(V=512, d=256, L=2, H=4, dff=1024, P=32, G=4, Q=8, new=128,
+    # c3 per-GPU shard (BASELINE configs[2] is 128 queries x 8 over the box: 16 x 8 per GPU)
+    "c3": dict(V=152064, d=3584, L=28, H=28, dff=18944, P=128, G=8, Q=16, new=1024, stops=True, online=False, warm=24,
+               desc="Qwen2.5-7B-shaped target + 1-layer draft, 16 queries x group 8 per GPU (c3's 128 x 8 over 8 "
+                    "GPUs), 128-token prompts, variable-length stops 256..1024 new tokens (concurrency sweep "
+                    "128 -> 1 per GPU), greedy, adaptive spec, draft warmed online"),
+    # c4: the c3 shard + the online draft-learning step (NCCL gradient all-reduce) in every step
+    "c4": dict(V=152064, d=3584, L=28, H=28, dff=18944, P=128, G=8, Q=16, new=1024, stops=True, online=True, warm=24,
+               desc="Qwen2.5-7B-shaped GRPO rollout, data-parallel by query group, 16 queries x group 8 per GPU, "
+                    "variable-length stops 256..1024, adaptive spec + one online draft-learning AdamW step with "
+                    "NCCL gradient all-reduce per step"),
+    "c1": dict(V=512, d=256, L=2, H=4, dff=1024, P=32, G=4, Q=8, new=128, stops=False, online=False, warm=0,
                desc="2-layer d=256 target + 1-layer draft, 8 queries x group 4, 32-token prompts, 128 new tokens"),
 }
 C_PEAK = 211  # analytic crossover s*F/(2*BW) at the measured sustained peaks
@@ -67,6 +77,34 @@ def make_prompts(w, rank):
     toks = (z % np.uint64(w["V"] - 2) + np.uint64(2)).astype(np.int64)
     toks = toks[rank * w["Q"] * w["P"]:].reshape(w["Q"], w["P"])
     return [row.tolist() for row in toks]
+
+
+def _splitmix_stream(seed, n):
+    with np.errstate(over="ignore"):
+        st = np.uint64(seed) + np.uint64(0x9E3779B97F4A7C15) * np.arange(2, n + 2, dtype=np.uint64)
+        z = (st ^ (st >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        return z ^ (z >> np.uint64(31))
+
+
+def stream_prompts(key, n, P, V):
+    """Training prompts for online draft learning, disjoint from the benchmark prompts:
+    Rng(mix_key(0, key)) (key = 0x7a11 + iteration)."""
+    from oracle.oracle import mix_key  # integer key derivation only
+    z = _splitmix_stream(mix_key(0, key), n * P)
+    return (z % np.uint64(V - 2) + np.uint64(2)).astype(np.int64).reshape(n, P).tolist()
+
+
+def stop_caps(w, sid0, n):
+    """c3 variable-length stops: per-sequence max_new from Rng(mix_key(0, 0x5709 + sid)),
+    uniform in [new/4, new] (max/min = 4x), keyed by GLOBAL sequence id."""
+    from oracle.oracle import mix_key
+    lo, hi = w["new"] // 4, w["new"]
+    caps = []
+    for sid in range(sid0, sid0 + n):
+        z = _splitmix_stream(mix_key(0, 0x5709 + sid), 1)[0]
+        caps.append(int(lo + int(z % np.uint64(hi - lo + 1))))
+    return caps
 
 
 class ClockSampler:
@@ -226,10 +264,14 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ar", action="store_true", help="skip the AR (vanilla) comparison rollout")
     ap.add_argument("--max-new", type=int, default=0, help="override new tokens (profiling runs)")
+    ap.add_argument("--warm-iters", type=int, default=-1, help="online draft-warming iterations (default per config)")
+    ap.add_argument("--c-peak", type=int, default=C_PEAK)
     args = ap.parse_args()
     w = dict(WORKLOADS[args.config])
     if args.max_new:
         w["new"] = args.max_new
+    if args.warm_iters >= 0:
+        w["warm"] = args.warm_iters
     if args.impl == "reference":
         return reference_arm(args, w)
 
@@ -238,35 +280,75 @@ def main():
     if world > 1:
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("gloo", rank=rank, world_size=world)
+        dist.init_process_group("gloo", rank=rank, world_size=world)  # host plumbing only
     from paper_2509_21792_b200 import capi
     cfg = model_cfg(w)
     n_seq = w["Q"] * w["G"]
-    eng = capi.Engine(cfg, 1, local, n_seq, max(2048, n_seq), 10, 6)
+    eng = capi.Engine(cfg, 1, local, max(n_seq, 64), 2048, 10, 6)
     eng.init_random(1234)
+    # NCCL data-parallel group over NVLink (C1 gradient all-reduce, C2 statistics)
+    uid = [capi.nccl_unique_id() if rank == 0 else None]
+    if dist:
+        dist.broadcast_object_list(uid, src=0)
+    eng.nccl_init(rank, world, uid[0])
     prompts = make_prompts(w, rank)
-    gen = dict(c_peak=C_PEAK, alpha=2.0, k_max=10, l_max=6, temperature=0.0, seed=7, max_new_tokens=w["new"],
-               sid_offset=rank * n_seq)
+    caps = stop_caps(w, rank * n_seq, n_seq) if w["stops"] else None
+    gen = dict(c_peak=args.c_peak, alpha=2.0, k_max=10, l_max=6, temperature=0.0, seed=7, max_new_tokens=w["new"],
+               sid_offset=rank * n_seq, seq_max_new=caps)
 
-    def rollout(mode, prof=False):
+    def rollout(mode):
         t0 = time.perf_counter()
         r = eng.generate(prompts, w["G"], mode=mode, want_features=True, **gen)
-        wall = time.perf_counter() - t0
-        return r, wall
+        return r, time.perf_counter() - t0
+
+    def draft_step(r):
+        """one online draft-learning step on this rollout (grpo.cpp:329-345): global row
+        count first (int64 all-reduce), local gradient with the global normaliser, NCCL
+        all-reduce (sum) of the fp32 gradient, identical AdamW step on every replica."""
+        rows = sum(max(0, len(t) - 2) for t in r.tokens)
+        rows_total = int(eng.allreduce_i64([rows])[0])  # noqa: F841 (used below)
+        t0 = time.perf_counter()
+        (fl, tl, _, n, secs), _ = eng.draft_update(None, lr=1e-3, rows_total=rows_total, allreduce_grad=True)
+        return secs, time.perf_counter() - t0, fl, tl, rows_total
+
+    # ---- draft warming (untimed): online learning on a disjoint prompt stream
+    warm = None
+    if w["warm"] > 0:
+        t0 = time.perf_counter()
+        fl = tl = None
+        for it in range(1, w["warm"] + 1):
+            tp = stream_prompts(0x7A11 + it + 1000 * rank, 32, w["P"], w["V"])
+            rw = eng.generate(tp, 2, c_peak=args.c_peak, mode="vanilla", temperature=0.0, seed=it,
+                              max_new_tokens=128, want_features=True)
+            for _ in range(4):
+                _, _, fl, tl, _ = draft_step(rw)
+        warm = {"iterations": w["warm"], "adamw_steps": 4 * w["warm"], "train_seqs_per_iter": 64,
+                "feature_loss": round(fl, 5), "token_loss": round(tl, 4), "seconds": round(time.perf_counter() - t0, 1)}
 
     for _ in range(args.warmup):
-        rollout(args.mode)
+        r, _ = rollout(args.mode)
+        if w["online"]:
+            draft_step(r)
     eng.read_profile(reset=True)
     if dist:
         dist.barrier()
     clocks = ClockSampler(local)
     clocks.start()
     dev_s, wall_s, toks, launches, acc, slots, h2d, d2h = 0.0, 0.0, 0, 0, 0, 0, 0, 0
-    spec_steps = 0
+    spec_steps, upd_s, upd_wall, upd_rows = 0, 0.0, 0.0, 0
+    terms = None
     for _ in range(args.steps):
         r, wall = rollout(args.mode)
         dev_s += r.seconds
         wall_s += wall
+        if w["online"]:
+            us, uw, fl, tl, nrows = draft_step(r)
+            dev_s += us
+            wall_s += uw
+            upd_s += us
+            upd_wall += uw
+            upd_rows += nrows
+            terms = (fl, tl)
         toks += r.generated()
         launches += r.kernel_launches
         acc += r.total_accepted
@@ -275,23 +357,28 @@ def main():
         d2h += r.d2h_bytes
         spec_steps += sum(1 for s in r.steps if s[1] > 1)
     clk = clocks.stop()
-    t_max, w_max, tok_all = dev_s, wall_s, toks
-    if dist:
+    # C2: statistics over the data-parallel group (NCCL); times take the max over ranks
+    t_max, w_max = dev_s, wall_s
+    tok_all, acc_all, slots_all = toks, acc, slots
+    if world > 1:
         import torch
         t = torch.tensor([dev_s, wall_s], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        n = torch.tensor([toks], dtype=torch.float64)
-        dist.all_reduce(n, op=dist.ReduceOp.SUM)
-        t_max, w_max, tok_all = float(t[0]), float(t[1]), int(n[0])
+        t_max, w_max = float(t[0]), float(t[1])
+        tok_all, acc_all, slots_all = (int(x) for x in eng.allreduce_i64([toks, acc, slots]))
     ar = None
     if not args.no_ar and args.mode != "vanilla":
         if spec_steps == 0:
             ar = {"value": tok_all / t_max, "unit": "tokens/s", "speedup": 1.0,
                   "note": "every step had B_cur > C_peak, so Eqs. 1-3 planned N_verify=1 (AR) throughout"}
         else:
-            r, _ = rollout("vanilla")
-            ar = {"value": r.generated() / r.seconds, "unit": "tokens/s"}
-            ar["speedup"] = (toks / dev_s) / ar["value"]
+            rs, _ = rollout(args.mode)
+            ra, _ = rollout("vanilla")
+            same = all(list(a) == list(b) for a, b in zip(rs.tokens, ra.tokens))
+            ar = {"value": ra.generated() / ra.seconds, "unit": "tokens/s",
+                  "spec_value": rs.generated() / rs.seconds,
+                  "speedup": (rs.generated() / rs.seconds) / (ra.generated() / ra.seconds),
+                  "tokens_identical": same, "note": "rollout only (no draft step), this rank"}
     # kernel-class breakdown: one more rollout of the same workload with a CUDA-event pair
     # around every launch (kept out of the timed steps: events between launches defeat PDL)
     eng.profile(True)
@@ -299,6 +386,9 @@ def main():
     eng.profile(False)
     prof = eng.read_profile(reset=True)
     if rank != 0:
+        eng.close()
+        if dist:
+            dist.destroy_process_group()
         return 0
     hbm, tf, src = measured_peaks()
     att = prof["attention"]
@@ -318,20 +408,30 @@ def main():
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(w, max(1, min(os.cpu_count() or 1, 64)))
+    config = {"workload": f"{args.config}: {w['desc']}", "mode": args.mode, "c_peak": args.c_peak,
+              "sequences_per_gpu": n_seq, "new_tokens": w["new"], "prompt_len": w["P"],
+              "l2": "inputs larger than L2 (KV cache of the shard >> 126 MB L2)",
+              "parallelism": f"dp{world} (query groups)", "weights": "random init on device"}
+    if caps:
+        config["stops"] = {"min_new": min(caps), "max_new": max(caps), "mean_new": round(sum(caps) / len(caps), 1)}
     line = {
         "metric": "rollout tokens/s", "value": round(tok_all / t_max, 1), "unit": "tokens/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * t_max / args.steps, 1),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": f"{args.config}: {w['desc']}", "mode": args.mode, "c_peak": C_PEAK,
-                   "sequences_per_gpu": n_seq, "new_tokens": w["new"], "prompt_len": w["P"],
-                   "l2": "inputs larger than L2 (KV cache ~100 GB per GPU at c2)",
-                   "parallelism": f"dp{world} (query groups)", "weights": "random init on device"},
-        "tau": round(acc / slots, 4) if slots else None, "spec_steps": spec_steps,
-        "speedup_vs_ar": ar["speedup"] if ar else None, "ar": ar,
+        "config": config,
+        "tau": round(acc_all / slots_all, 4) if slots_all else None, "spec_steps": spec_steps,
+        "speedup_vs_ar": ar["speedup"] if ar else None, "ar": ar, "draft_warm": warm,
         "e2e": {"value": round(tok_all / w_max, 1), "unit": "tokens/s", "h2d_bytes_per_step": h2d // args.steps,
                 "d2h_bytes_per_step": d2h // args.steps},
         "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk,
     }
+    if w["online"]:
+        line["online_draft_step"] = {"device_ms_per_step": round(1e3 * upd_s / args.steps, 2),
+                                     "wall_ms_per_step": round(1e3 * upd_wall / args.steps, 2),
+                                     "global_rows_per_step": upd_rows // args.steps,
+                                     "share_of_step": round(upd_s / dev_s, 4),
+                                     "feature_loss": round(terms[0], 5), "token_loss": round(terms[1], 4),
+                                     "collective": f"ncclAllReduce(sum) fp32 gradient over {world} rank(s)"}
     print(json.dumps(line))
     eng.close()
     if dist:
