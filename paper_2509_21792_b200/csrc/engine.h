@@ -270,7 +270,7 @@ class Engine {
         float *lse, *Drow, *mu1, *rs1, *mu2, *rs2, *muf, *rsf, *logits, *sc, *grad, *m, *v, *feat_in;
         __nv_bfloat16 *fuse, *a1, *a2, *ctx_b, *fhat_b, *dx_b, *dxmid_b, *hg, *dfch_b, *dqkv_b, *dlog, *tA, *tB;
         __nv_bfloat16 *dflat_b, *wqkv_ref, *lm_ref;
-        int *tok, *pos, *next, *seq_first, *seq_last;
+        int *tok, *pos, *next, *seq_first, *seq_last, *tiles;
         long long *prev_off, *tgt_off;
         double* loss_row;
         long long adam_t = 0;

@@ -97,6 +97,7 @@ void Engine::train_alloc() {
     t.next = talloc<int>(R);
     t.seq_first = talloc<int>(R);
     t.seq_last = talloc<int>(R);
+    t.tiles = talloc<int>(R);
     t.prev_off = talloc<long long>(R);
     t.tgt_off = talloc<long long>(R);
     t.loss_row = talloc<double>(2 * R);
@@ -227,7 +228,7 @@ Engine::DraftLossTerms Engine::draft_update(const DraftUpdateArgs& A) {
     size_t s_begin = 0;
     std::vector<double> hloss;
     while (s_begin < lens.size()) {
-        std::vector<int> tok, pos, next, sfirst, slast;
+        std::vector<int> tok, pos, next, sfirst, slast, tiles;
         std::vector<long long> poff, toff;
         size_t s = s_begin;
         for (; s < lens.size(); ++s) {
@@ -235,6 +236,7 @@ Engine::DraftLossTerms Engine::draft_update(const DraftUpdateArgs& A) {
             if (!tok.empty() && static_cast<int>(tok.size()) + rows > t.rmax) break;
             if (rows > t.rmax) throw std::invalid_argument("draft_update: sequence longer than the training chunk");
             const int first = static_cast<int>(tok.size());
+            for (int m = 0; m < rows; m += 64) tiles.push_back(first + m);  // attention tiles per sequence
             for (int j = 1; j <= rows; ++j) {  // pair (t_j, f_{j-1}) -> targets (f_j, t_{j+1})
                 tok.push_back(htok[tok_off[s] + j]);
                 pos.push_back(j);
@@ -254,6 +256,8 @@ Engine::DraftLossTerms Engine::draft_update(const DraftUpdateArgs& A) {
         SGB_CUDA(cudaMemcpyAsync(t.next, next.data(), R * 4, cudaMemcpyHostToDevice, st_));
         SGB_CUDA(cudaMemcpyAsync(t.seq_first, sfirst.data(), R * 4, cudaMemcpyHostToDevice, st_));
         SGB_CUDA(cudaMemcpyAsync(t.seq_last, slast.data(), R * 4, cudaMemcpyHostToDevice, st_));
+        const int n_tiles = static_cast<int>(tiles.size());
+        SGB_CUDA(cudaMemcpyAsync(t.tiles, tiles.data(), n_tiles * 4, cudaMemcpyHostToDevice, st_));
         SGB_CUDA(cudaMemcpyAsync(t.prev_off, poff.data(), R * 8, cudaMemcpyHostToDevice, st_));
         SGB_CUDA(cudaMemcpyAsync(t.tgt_off, toff.data(), R * 8, cudaMemcpyHostToDevice, st_));
 
@@ -272,7 +276,7 @@ Engine::DraftLossTerms Engine::draft_update(const DraftUpdateArgs& A) {
         e.f32 = t.qkv;
         e.ld = 3 * d;
         gemm(W.qkv, t.act_a1, R, e, kClsGemm, 4.0);
-        launch_train_attn_fwd(t.qkv, t.seq_first, R, d, H, t.ctx, t.ctx_b, t.lse, t.sc, t.smax, st_);
+        launch_train_attn_fwd(t.qkv, t.seq_first, t.seq_last, t.tiles, n_tiles, d, H, t.ctx, t.ctx_b, t.lse, st_);
         SGB_CUDA(cudaMemcpyAsync(t.xmid, t.x0, static_cast<size_t>(R) * d * 4, cudaMemcpyDeviceToDevice, st_));
         e = GemmEpi{};
         e.kind = kEpiResid;
@@ -355,7 +359,8 @@ Engine::DraftLossTerms Engine::draft_update(const DraftUpdateArgs& A) {
         e.f32 = t.dctx;
         e.ld = d;
         gemm(t.wo_ref, t.act_dxmid, R, e, kClsGemm, 4.0);
-        launch_train_attn_bwd(t.qkv, t.dctx, t.lse, t.seq_first, t.seq_last, R, d, H, t.Drow, t.dqkv, t.sc, t.smax, st_);
+        launch_train_attn_bwd(t.qkv, t.ctx, t.dctx, t.lse, t.seq_first, t.seq_last, t.tiles, n_tiles, R, d, H, t.Drow,
+                              t.dqkv, st_);
         launch_transpose_bf16(t.a1, R, d, d, t.tB, Rp, st_);
         const size_t qkv_off[3] = {lo.wq, lo.wk, lo.wv};
         for (int k = 0; k < 3; ++k) {

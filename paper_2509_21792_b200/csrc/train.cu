@@ -137,139 +137,6 @@ __global__ void gelu_bwd_kernel(const float* __restrict__ x, const float* __rest
 }
 
 // Causal attention over each sequence's own rows (tinylm.hpp:673-700), fp32, one CTA per
-// (row, head); saves log-sum-exp for the backward. q/k/v packed [rows][3d].
-__global__ void __launch_bounds__(128) train_attn_fwd_kernel(const float* __restrict__ qkv, const int* __restrict__ seq_first,
-                                                             int d, int H, float scale, float* __restrict__ ctx,
-                                                             __nv_bfloat16* __restrict__ ctx_b, float* __restrict__ lse,
-                                                             float* __restrict__ sc_buf, int sc_stride) {
-    __shared__ float red[4];
-    const int i = blockIdx.x, h = blockIdx.y;
-    const int dh = d / H;
-    const int j0 = seq_first[i];
-    const int n = i - j0 + 1;
-    const float* qi = qkv + static_cast<size_t>(i) * 3 * d + h * dh;
-    extern __shared__ float dyn_sc[];
-    float* sc = dyn_sc;  // per-(row, head) score scratch in shared memory
-    float mx = -INFINITY;
-    for (int j = threadIdx.x; j < n; j += blockDim.x) {
-        const float* kj = qkv + static_cast<size_t>(j0 + j) * 3 * d + d + h * dh;
-        float s = 0.f;
-        for (int e = 0; e < dh; ++e) s += qi[e] * kj[e];
-        s *= scale;
-        sc[j] = s;
-        mx = fmaxf(mx, s);
-    }
-    mx = warp_max(mx);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
-    __syncthreads();
-    mx = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
-    __syncthreads();
-    float sum = 0.f;
-    for (int j = threadIdx.x; j < n; j += blockDim.x) {
-        const float p = expf(sc[j] - mx);
-        sc[j] = p;
-        sum += p;
-    }
-    sum = warp_sum(sum);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sum;
-    __syncthreads();
-    sum = red[0] + red[1] + red[2] + red[3];
-    for (int e = threadIdx.x; e < dh; e += blockDim.x) {
-        float o = 0.f;
-        for (int j = 0; j < n; ++j) o += sc[j] * qkv[static_cast<size_t>(j0 + j) * 3 * d + 2 * d + h * dh + e];
-        o /= sum;
-        ctx[static_cast<size_t>(i) * d + h * dh + e] = o;
-        ctx_b[static_cast<size_t>(i) * d + h * dh + e] = __float2bfloat16(o);
-    }
-    if (threadIdx.x == 0) lse[static_cast<size_t>(i) * H + h] = mx + logf(sum);
-}
-
-// Attention backward, pass 1 (per query row i): Drow_i = sum_j P_ij dP_ij and
-// dq_i = scale * sum_j P_ij (dP_ij - Drow_i) k_j   (tinylm.hpp:755-785).
-__global__ void __launch_bounds__(128) train_attn_bwd_q_kernel(const float* __restrict__ qkv, const float* __restrict__ dctx,
-                                                               const float* __restrict__ lse, const int* __restrict__ seq_first,
-                                                               int d, int H, float scale, float* __restrict__ Drow,
-                                                               float* __restrict__ dqkv, float* __restrict__ sc_buf,
-                                                               int sc_stride) {
-    __shared__ float red[4];
-    const int i = blockIdx.x, h = blockIdx.y;
-    const int dh = d / H;
-    const int j0 = seq_first[i];
-    const int n = i - j0 + 1;
-    const float* qi = qkv + static_cast<size_t>(i) * 3 * d + h * dh;
-    const float* di = dctx + static_cast<size_t>(i) * d + h * dh;
-    const float L = lse[static_cast<size_t>(i) * H + h];
-    extern __shared__ float dyn_sc[];
-    float* P = dyn_sc;
-    float* dP = P + sc_stride;
-    float dsum = 0.f;
-    for (int j = threadIdx.x; j < n; j += blockDim.x) {
-        const float* kj = qkv + static_cast<size_t>(j0 + j) * 3 * d + d + h * dh;
-        const float* vj = qkv + static_cast<size_t>(j0 + j) * 3 * d + 2 * d + h * dh;
-        float s = 0.f, dp = 0.f;
-        for (int e = 0; e < dh; ++e) {
-            s += qi[e] * kj[e];
-            dp += di[e] * vj[e];
-        }
-        const float p = expf(s * scale - L);
-        P[j] = p;
-        dP[j] = dp;
-        dsum += p * dp;
-    }
-    dsum = warp_sum(dsum);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = dsum;
-    __syncthreads();
-    dsum = red[0] + red[1] + red[2] + red[3];
-    for (int e = threadIdx.x; e < dh; e += blockDim.x) {
-        float o = 0.f;
-        for (int j = 0; j < n; ++j)
-            o += P[j] * (dP[j] - dsum) * qkv[static_cast<size_t>(j0 + j) * 3 * d + d + h * dh + e];
-        dqkv[static_cast<size_t>(i) * 3 * d + h * dh + e] = o * scale;
-    }
-    if (threadIdx.x == 0) Drow[static_cast<size_t>(i) * H + h] = dsum;
-}
-
-// Attention backward, pass 2 (per key row j): dk_j = scale * sum_{i>=j} dS_ij q_i,
-// dv_j = sum_{i>=j} P_ij dctx_i (deterministic: no atomics).
-__global__ void __launch_bounds__(128) train_attn_bwd_kv_kernel(const float* __restrict__ qkv, const float* __restrict__ dctx,
-                                                                const float* __restrict__ lse, const float* __restrict__ Drow,
-                                                                const int* __restrict__ seq_first, const int* __restrict__ seq_last,
-                                                                int d, int H, float scale, float* __restrict__ dqkv,
-                                                                float* __restrict__ sc_buf, int sc_stride) {
-    const int j = blockIdx.x, h = blockIdx.y;
-    const int dh = d / H;
-    const int i1 = seq_last[j];
-    const int n = i1 - j + 1;
-    const float* kj = qkv + static_cast<size_t>(j) * 3 * d + d + h * dh;
-    const float* vj = qkv + static_cast<size_t>(j) * 3 * d + 2 * d + h * dh;
-    extern __shared__ float dyn_sc[];
-    float* P = dyn_sc;
-    float* dS = P + sc_stride;
-    for (int t = threadIdx.x; t < n; t += blockDim.x) {
-        const int i = j + t;
-        const float* qi = qkv + static_cast<size_t>(i) * 3 * d + h * dh;
-        const float* di = dctx + static_cast<size_t>(i) * d + h * dh;
-        float s = 0.f, dp = 0.f;
-        for (int e = 0; e < dh; ++e) {
-            s += qi[e] * kj[e];
-            dp += di[e] * vj[e];
-        }
-        const float p = expf(s * scale - lse[static_cast<size_t>(i) * H + h]);
-        P[t] = p;
-        dS[t] = p * (dp - Drow[static_cast<size_t>(i) * H + h]) * scale;
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < dh; e += blockDim.x) {
-        float dk = 0.f, dv = 0.f;
-        for (int t = 0; t < n; ++t) {
-            const int i = j + t;
-            dk += dS[t] * qkv[static_cast<size_t>(i) * 3 * d + h * dh + e];
-            dv += P[t] * dctx[static_cast<size_t>(i) * d + h * dh + e];
-        }
-        dqkv[static_cast<size_t>(j) * 3 * d + d + h * dh + e] = dk;
-        dqkv[static_cast<size_t>(j) * 3 * d + 2 * d + h * dh + e] = dv;
-    }
-}
 
 // SmoothL1(beta=1) vs the target feature (grpo.hpp:311-322): dfeat and the per-row loss.
 __global__ void __launch_bounds__(kT) smoothl1_kernel(const float* __restrict__ fhat, const float* __restrict__ feat_base,
@@ -400,25 +267,6 @@ void launch_gelu_fwd(const float* x, size_t n, __nv_bfloat16* y, cudaStream_t st
 }
 void launch_gelu_bwd(const float* x, const float* dy, size_t n, __nv_bfloat16* dx, cudaStream_t st) {
     gelu_bwd_kernel<<<grid_n(n), 256, 0, st>>>(x, dy, n, dx);
-    SGB_KCHECK();
-}
-void launch_train_attn_fwd(const float* qkv, const int* seq_first, int R, int d, int H, float* ctx,
-                           __nv_bfloat16* ctx_b, float* lse, float* sc_buf, int sc_stride, cudaStream_t st) {
-    if (R <= 0) return;
-    const float scale = 1.0f / sqrtf(static_cast<float>(d / H));
-    train_attn_fwd_kernel<<<dim3(R, H), 128, sc_stride * 4, st>>>(qkv, seq_first, d, H, scale, ctx, ctx_b, lse, sc_buf, sc_stride);
-    SGB_KCHECK();
-}
-void launch_train_attn_bwd(const float* qkv, const float* dctx, const float* lse, const int* seq_first,
-                           const int* seq_last, int R, int d, int H, float* Drow, float* dqkv, float* sc_buf,
-                           int sc_stride, cudaStream_t st) {
-    if (R <= 0) return;
-    const float scale = 1.0f / sqrtf(static_cast<float>(d / H));
-    train_attn_bwd_q_kernel<<<dim3(R, H), 128, 2 * sc_stride * 4, st>>>(qkv, dctx, lse, seq_first, d, H, scale, Drow, dqkv, sc_buf,
-                                                        sc_stride);
-    SGB_KCHECK();
-    train_attn_bwd_kv_kernel<<<dim3(R, H), 128, 2 * sc_stride * 4, st>>>(qkv, dctx, lse, Drow, seq_first, seq_last, d, H, scale, dqkv,
-                                                         sc_buf, sc_stride);
     SGB_KCHECK();
 }
 void launch_smoothl1(const float* fhat, const float* feat_base, const long long* tgt_off, int R, int d, double scale,

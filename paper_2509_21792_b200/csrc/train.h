@@ -15,11 +15,15 @@ void launch_ln_bwd(const float* x, const float* g, const float* mu, const float*
 void launch_colsum_add(const float* m, int rows, int cols, float* out, cudaStream_t st);
 void launch_gelu_fwd(const float* x, size_t n, __nv_bfloat16* y, cudaStream_t st);
 void launch_gelu_bwd(const float* x, const float* dy, size_t n, __nv_bfloat16* dx, cudaStream_t st);
-void launch_train_attn_fwd(const float* qkv, const int* seq_first, int R, int d, int H, float* ctx,
-                           __nv_bfloat16* ctx_b, float* lse, float* sc_buf, int sc_stride, cudaStream_t st);
-void launch_train_attn_bwd(const float* qkv, const float* dctx, const float* lse, const int* seq_first,
-                           const int* seq_last, int R, int d, int H, float* Drow, float* dqkv, float* sc_buf,
-                           int sc_stride, cudaStream_t st);
+// Causal training attention on tensor cores (train_attn.cu): row i attends keys
+// seq_first[i] .. i. Forward writes ctx (fp32 + bf16) and lse [R][H]; backward writes
+// dq/dk/dv into dqkv [R][3d] and uses Drow [R][H] as scratch.
+// tiles[n_tiles]: first row of every 64-row tile, tiles starting at seq_first + 64m.
+void launch_train_attn_fwd(const float* qkv, const int* seq_first, const int* seq_last, const int* tiles, int n_tiles,
+                           int d, int H, float* ctx, __nv_bfloat16* ctx_b, float* lse, cudaStream_t st);
+void launch_train_attn_bwd(const float* qkv, const float* ctx, const float* dctx, const float* lse,
+                           const int* seq_first, const int* seq_last, const int* tiles, int n_tiles, int R, int d,
+                           int H, float* Drow, float* dqkv, cudaStream_t st);
 void launch_smoothl1(const float* fhat, const float* feat_base, const long long* tgt_off, int R, int d, double scale,
                      float* dfeat, double* loss_row, cudaStream_t st);
 void launch_ce(const float* logits, int R, int V, const int* tgt, double scale, __nv_bfloat16* dlog, double* loss_row,
