@@ -34,6 +34,7 @@
 //
 // Roofline: HBM-bound on K/V reads, 4*d bytes per key per layer.
 #include <algorithm>
+#include <cstdlib>
 #include <cfloat>
 
 #include "common.cuh"
@@ -452,6 +453,11 @@ void launch_attention(const float* q, const __nv_bfloat16* K, const __nv_bfloat1
         while (H % g2) ++g2;
         G = g2;
     }
+    static const int g_force = [] {
+        const char* v = getenv("SGB_ATTN_G");  // tuning experiments only
+        return v ? atoi(v) : 0;
+    }();
+    if (g_force > 0 && H % g_force == 0) G = g_force;
     const int HG = H / G;
     const bool two = HG > 12;  // one head per warp up to 12 heads (two CTAs per SM fit)
     const long long est = blocks * G;
