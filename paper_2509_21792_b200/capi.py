@@ -379,9 +379,6 @@ def nccl_unique_id() -> bytes:
 
 
 def _nccl_init(self, rank: int, world: int, uid: bytes):
-    # NCCL prints its version banner to stdout at communicator init unless told otherwise;
-    # bench.py's stdout must stay one JSON line
-    os.environ.setdefault("NCCL_DEBUG", "WARN")
     buf = (C.c_ubyte * 128).from_buffer_copy(uid)
     _check(_lib.sgb_nccl_init(self.h, rank, world, buf))
 

@@ -6,7 +6,9 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
+#include <unistd.h>
 #include <memory>
 #include <string>
 #include <unordered_map>
@@ -70,6 +72,25 @@ std::unordered_map<const sgb_engine*, DpGroup>& groups() {
 void nccl_check(ncclResult_t r, const char* what) {
     if (r != ncclSuccess) throw std::runtime_error(std::string(what) + ": " + ncclGetErrorString(r));
 }
+// NCCL prints a version banner on stdout at its first call (also at NCCL_DEBUG=WARN); callers
+// (bench.py) keep stdout for their own output, so NCCL's setup calls run with fd 1 pointed at
+// stderr.
+struct StdoutToStderr {
+    int saved = -1;
+    StdoutToStderr() {
+        fflush(stdout);
+        saved = dup(1);
+        if (saved >= 0) dup2(2, 1);
+    }
+    ~StdoutToStderr() {
+        fflush(stdout);
+        if (saved >= 0) {
+            dup2(saved, 1);
+            close(saved);
+        }
+    }
+};
+
 DpGroup& group_of(sgb_engine* e) {
     auto it = groups().find(e);
     if (it == groups().end() || !it->second.comm) throw std::invalid_argument("engine has no NCCL group (sgb_nccl_init)");
@@ -279,7 +300,10 @@ int sgb_rollout(sgb_engine* e, const int* prompts, const int* prompt_lens, int n
 int sgb_nccl_unique_id(unsigned char* id128) {
     return guarded([&] {
         ncclUniqueId id;
-        nccl_check(ncclGetUniqueId(&id), "ncclGetUniqueId");
+        {
+            StdoutToStderr guard;
+            nccl_check(ncclGetUniqueId(&id), "ncclGetUniqueId");
+        }
         static_assert(sizeof(id) == 128, "NCCL unique id size");
         std::memcpy(id128, &id, 128);
     });
@@ -293,7 +317,10 @@ int sgb_nccl_init(sgb_engine* e, int rank, int world, const unsigned char* id128
         DpGroup g;
         g.rank = rank;
         g.world = world;
-        nccl_check(ncclCommInitRank(&g.comm, world, id, rank), "ncclCommInitRank");
+        {
+            StdoutToStderr guard;
+            nccl_check(ncclCommInitRank(&g.comm, world, id, rank), "ncclCommInitRank");
+        }
         SGB_CUDA(cudaMalloc(&g.dbuf, 4096 * sizeof(double)));
         groups()[e] = g;
     });

@@ -199,7 +199,11 @@ struct EmitRec {
     double s;   // T>0: chunk sum of exp((l - max)/T)
 };
 
-__global__ void __launch_bounds__(kT) emit_max_kernel(const float* __restrict__ logits, int V, int P,
+// Max / argmax is order-free, so a CTA takes kCPC chunks (32 K logits, float4 loads) and
+// the row's last CTA merges ceil(P / kCPC) records.
+constexpr int kCPC = 4;
+
+__global__ void __launch_bounds__(kT) emit_max_kernel(const float* __restrict__ logits, int V, int Pc,
                                                       const int* __restrict__ row_idx, double temperature,
                                                       EmitRec* __restrict__ rec, int* __restrict__ ctr,
                                                       float* __restrict__ rowmax, int* __restrict__ out,
@@ -208,38 +212,47 @@ __global__ void __launch_bounds__(kT) emit_max_kernel(const float* __restrict__ 
     pdl_trigger();
     __shared__ VI shv[kT / 32];
     __shared__ int flag;
-    const int p = blockIdx.x, r = blockIdx.y;
-    const int base = p * kCH;
+    const int q = blockIdx.x, r = blockIdx.y;
+    const int lo = q * kCPC * kCH, hi = min(V, lo + kCPC * kCH);
     const float* L = logits + static_cast<size_t>(row_idx ? row_idx[r] : r) * V;
     VI best{-INFINITY, 0x7fffffff};
     bool nan = false, nonfinite = false;
-#pragma unroll 8
-    for (int j = 0; j < kPer; ++j) {
-        const int i = base + j * kT + static_cast<int>(threadIdx.x);
-        if (i < V) {
-            const float x = __ldcs(L + i);
-            if (x != x) nan = true;
-            if (!isfinite(x)) nonfinite = true;
-            const VI c{x, i};
-            if (better(c, best)) best = c;
+    auto see = [&](float x, int i) {
+        if (x != x) nan = true;
+        if (!isfinite(x)) nonfinite = true;
+        const VI c{x, i};
+        if (better(c, best)) best = c;
+    };
+    if ((V & 3) == 0) {
+        const float4* L4 = reinterpret_cast<const float4*>(L);
+#pragma unroll 4
+        for (int i4 = lo / 4 + static_cast<int>(threadIdx.x); i4 < hi / 4; i4 += kT) {
+            const float4 x = __ldcs(L4 + i4);
+            see(x.x, 4 * i4);
+            see(x.y, 4 * i4 + 1);
+            see(x.z, 4 * i4 + 2);
+            see(x.w, 4 * i4 + 3);
         }
+    } else {
+#pragma unroll 8
+        for (int i = lo + static_cast<int>(threadIdx.x); i < hi; i += kT) see(__ldcs(L + i), i);
     }
     const int any_nonfinite = __syncthreads_or(nonfinite);
     const int any_nan = __syncthreads_or(nan);
     best = block_best(best, shv);
     if (threadIdx.x == 0) {
-        EmitRec* my = rec + static_cast<size_t>(r) * P + p;
+        EmitRec* my = rec + static_cast<size_t>(r) * (Pc * kCPC) + q;
         my->best = best;
         my->flags = (any_nonfinite ? 1 : 0) | (any_nan ? 2 : 0);
     }
-    if (!last_of_row(ctr, r, P, &flag)) return;
+    if (!last_of_row(ctr, r, Pc, &flag)) return;
     if (threadIdx.x != 0) return;
-    const EmitRec* rr = rec + static_cast<size_t>(r) * P;
+    const EmitRec* rr = rec + static_cast<size_t>(r) * (Pc * kCPC);
     VI b{-INFINITY, 0x7fffffff};
     int fl = 0;
-    for (int q = 0; q < P; ++q) {
-        const VI c{__ldcg(&rr[q].best.v), __ldcg(&rr[q].best.i)};
-        fl |= __ldcg(&rr[q].flags);
+    for (int k = 0; k < Pc; ++k) {
+        const VI c{__ldcg(&rr[k].best.v), __ldcg(&rr[k].best.i)};
+        fl |= __ldcg(&rr[k].flags);
         if (better(c, b)) b = c;
     }
     if (fl) atomicOr(err, (fl & 2) ? 3 : 1);
@@ -286,10 +299,10 @@ __global__ void __launch_bounds__(kT) emit_sample_kernel(const float* __restrict
     if (threadIdx.x == 0) {
         double acc = 0.0;
         for (int t = 0; t < kT; ++t) acc += ts[t];
-        rec[static_cast<size_t>(r) * P + p].s = acc;
+        rec[static_cast<size_t>(r) * (((P + kCPC - 1) / kCPC) * kCPC) + p].s = acc;
     }
     if (!last_of_row(ctr, r, P, &flag)) return;
-    const EmitRec* rr = rec + static_cast<size_t>(r) * P;
+    const EmitRec* rr = rec + static_cast<size_t>(r) * (((P + kCPC - 1) / kCPC) * kCPC);
     if (threadIdx.x == 0) {
         // chunk prefixes in order; the winner chunk is the last non-empty one whose
         // exclusive prefix is <= u
@@ -364,10 +377,11 @@ void launch_emit(const float* logits, int V, const int* row_idx, const unsigned 
                  int R, double temperature, int* out, int* err, const RowScratch& sc, cudaStream_t st) {
     if (R <= 0) return;
     const int P = chunks_for(V);
-    if (R > sc.rows || static_cast<size_t>(R) * P * sizeof(EmitRec) > sc.bytes)
+    if (R > sc.rows || static_cast<size_t>(R) * (((P + kCPC - 1) / kCPC) * kCPC) * sizeof(EmitRec) > sc.bytes)
         throw std::invalid_argument("emit: rows exceed the sampling scratch");
     EmitRec* rec = reinterpret_cast<EmitRec*>(sc.buf);
-    launch_pdl(emit_max_kernel, dim3(P, R), dim3(kT), 0, st, logits, V, P, row_idx, temperature, rec, sc.ctr,
+    const int Pc = (P + kCPC - 1) / kCPC;
+    launch_pdl(emit_max_kernel, dim3(Pc, R), dim3(kT), 0, st, logits, V, Pc, row_idx, temperature, rec, sc.ctr,
                sc.rowmax, out, err);
     SGB_KCHECK();
     if (temperature != 0.0) {
