@@ -175,6 +175,8 @@ __global__ void __launch_bounds__(HPW == 1 ? 416 : 544, HPW == 1 ? 2 : 1)  // co
             const int Lv = ctx_len + rows.chain_len[x.r];
             const long long ctx_base = rows.ctx_base[x.r];
             const long long* chain = rows.chain_slots + static_cast<size_t>(x.r) * kMaxChain;
+            const int pre_len = rows.pre_len ? rows.pre_len[x.r] : 0;
+            const long long pre_base = rows.pre_len ? rows.pre_base[x.r] : 0;
             const int kb = x.b * kBlock, ke = min(Lv, kb + kBlock);
             const size_t col = static_cast<size_t>(x.g) * wd;
             for (int v0 = kb; v0 < ke; v0 += KPC, ++i) {
@@ -189,9 +191,18 @@ __global__ void __launch_bounds__(HPW == 1 ? 416 : 544, HPW == 1 ? 2 : 1)  // co
                 __nv_bfloat16* vd = Vs + static_cast<size_t>(s) * KPC * wd;
                 if (G == 1) {
                     if (lane == 0 && nctx > 0) {
-                        const size_t src = static_cast<size_t>(ctx_base + v0) * d;
-                        bulk_g2s(kd, K + src, row_bytes * nctx, &full[s]);
-                        bulk_g2s(vd, V + src, row_bytes * nctx, &full[s]);
+                        // prompt keys from the group's shared copy, the rest from the row's region
+                        const int npre = max(0, min(nctx, pre_len - v0));
+                        if (npre > 0) {
+                            const size_t src = static_cast<size_t>(pre_base + v0) * d;
+                            bulk_g2s(kd, K + src, row_bytes * npre, &full[s]);
+                            bulk_g2s(vd, V + src, row_bytes * npre, &full[s]);
+                        }
+                        if (nctx > npre) {
+                            const size_t src = static_cast<size_t>(ctx_base + v0 + npre) * d;
+                            bulk_g2s(kd + static_cast<size_t>(npre) * wd, K + src, row_bytes * (nctx - npre), &full[s]);
+                            bulk_g2s(vd + static_cast<size_t>(npre) * wd, V + src, row_bytes * (nctx - npre), &full[s]);
+                        }
                     }
                     if (lane >= nctx && lane < nk) {
                         const size_t src = static_cast<size_t>(chain[v0 + lane - ctx_len]) * d;
@@ -199,7 +210,8 @@ __global__ void __launch_bounds__(HPW == 1 ? 416 : 544, HPW == 1 ? 2 : 1)  // co
                         bulk_g2s(vd + static_cast<size_t>(lane) * wd, V + src, row_bytes, &full[s]);
                     }
                 } else if (lane < nk) {
-                    const long long slot = lane < nctx ? ctx_base + v0 + lane : chain[v0 + lane - ctx_len];
+                    const long long slot = lane < nctx ? (v0 + lane < pre_len ? pre_base : ctx_base) + v0 + lane
+                                                       : chain[v0 + lane - ctx_len];
                     const size_t src = static_cast<size_t>(slot) * d + col;
                     bulk_g2s(kd + static_cast<size_t>(lane) * wd, K + src, row_bytes, &full[s]);
                     bulk_g2s(vd + static_cast<size_t>(lane) * wd, V + src, row_bytes, &full[s]);

@@ -278,6 +278,8 @@ void Engine::alloc_rows() {
     rows_.key_pos = dalloc<int>(R);
     rows_.seed = dalloc<unsigned long long>(R);
     rows_.par_row = dalloc<int>(R);
+    rows_.pre_base = dalloc<long long>(R);
+    rows_.pre_len = dalloc<int>(R);
     lm_idx_ = dalloc<int>(R);
     topk_tok_ = dalloc<int>(R * 16);
     topk_lp_ = dalloc<double>(R * 16);
@@ -300,7 +302,7 @@ Engine::~Engine() {
                     tr_.sel, tr_.n_nodes, tr_.lvl_start, tr_.lvl_cnt, tr_.frontier, x_, q_, y_, featin_, a_, att_,
                     a2_, h_, fuse_, ws_.buf, ws_.ctr, logits_, pacc_, pml_, rows_.tok, rows_.pos, rows_.kv_dst,
                     rows_.ctx_base, rows_.ctx_len, rows_.chain_len, rows_.chain, rows_.feat_off, rows_.out_off,
-                    rows_.key_pos, rows_.seed, rows_.par_row, lm_idx_, topk_tok_, topk_lp_, emitted_, acc_rows_,
+                    rows_.key_pos, rows_.seed, rows_.par_row, rows_.pre_base, rows_.pre_len, lm_idx_, topk_tok_, topk_lp_, emitted_, acc_rows_,
                     result_, err_, steps_, drow_, misc_i_, misc_l_, mask_dbg_, rsc_.buf, rsc_.ctr, rsc_.rowmax, asc_.row_ctr, gpart_};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -531,7 +533,11 @@ void Engine::forward(const Fwd& f) {
     if (!target_ready_ || (f.draft && !draft_ready_)) throw std::runtime_error("weights not uploaded");
     const std::vector<LayerDev>& L = f.draft ? dL_ : tL_;
     KvStore& kv = f.draft ? dkv_ : tkv_;
-    const AttnRowsDev ar{rows_.ctx_base, rows_.ctx_len, rows_.chain_len, rows_.chain};
+    AttnRowsDev ar{rows_.ctx_base, rows_.ctx_len, rows_.chain_len, rows_.chain};
+    if (f.prefix_share) {
+        ar.pre_base = rows_.pre_base;
+        ar.pre_len = rows_.pre_len;
+    }
     const double row_bytes = static_cast<double>(M) * d * 4;
     int e0 = pbeg();
     if (!f.draft) {
@@ -1123,6 +1129,8 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
             e.vrow_off = vrows;
             e.root_row = k_eff ? n_spec++ : -1;
             e.len_cap = len_cap[s];
+            e.pre_len = plen[s];
+            e.pre_base = static_cast<long long>(s - s % a.g) * tkv_.seq_stride;  // group leader's prompt K/V
             vrows += e.nsel;
             max_l = std::max(max_l, l_eff);
             max_p = std::max(max_p, p);
@@ -1258,6 +1266,7 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
         count();
         Fwd f;
         f.M = vrows;
+        f.prefix_share = a.g > 1;
         f.y_out = y_;
         f.logits = true;
         f.logits_out = logits_;

@@ -182,6 +182,7 @@ class Engine {
         int max_vlen = 0;
         double attn_kv_unique = 0;  // distinct KV tokens read per layer (roofline bytes)
         double attn_row_keys = 0;   // sum over rows of keys attended (roofline flops)
+        bool prefix_share = false;  // verify rows read their prompt K/V from the group leader
     };
     void forward(const Fwd& f);
     void convert_target(const float* staging);

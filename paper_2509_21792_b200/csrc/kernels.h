@@ -16,6 +16,10 @@ struct AttnRowsDev {
     const int* ctx_len;            // [M] contiguous prefix length
     const int* chain_len;          // [M] number of chain (tree-path) slots
     const long long* chain_slots;  // [M][kMaxChain] global KV slots, root-first
+    // optional shared prompt: virtual index v < pre_len[r] reads slot pre_base[r] + v instead
+    // of ctx_base[r] + v (the G members of a group read their prompt's K/V from one copy)
+    const long long* pre_base = nullptr;
+    const int* pre_len = nullptr;
 };
 
 // ---- rowops.cu
@@ -76,6 +80,8 @@ struct StepSeqDev {
     int vrow_off;   // first verify row
     int root_row;   // row of this sequence's root logits in the draft top-k output (-1: no draft)
     int len_cap;
+    int pre_len;         // prompt length (prefix shared by the group's members)
+    long long pre_base;  // KV slot of the group leader's position 0
 };
 
 struct TreeDev {
@@ -117,6 +123,8 @@ struct RowsDev {
     int* key_pos;          // [M] verify: sampling key position
     unsigned long long* seed;  // [M] verify: sequence seed
     int* par_row;          // [M] verify: parent row within the sequence (-1 root)
+    long long* pre_base;   // [M] verify: shared prompt K/V base (group leader)
+    int* pre_len;          // [M] verify: shared prompt length
 };
 
 void launch_tree_root(int B, const StepSeqDev* steps, const SeqStateDev& ss, const TreeDev& tr, const int* topk_tok,

@@ -200,6 +200,8 @@ __global__ void __launch_bounds__(kSelT)
         rows.kv_dst[row] = tscratch_base + row;
         rows.ctx_base[row] = static_cast<long long>(s) * tcache_stride;
         rows.ctx_len[row] = st.p;
+        rows.pre_base[row] = st.pre_base;
+        rows.pre_len[row] = min(st.pre_len, st.p);
         long long* ch = rows.chain + static_cast<size_t>(row) * kMaxChain;
         for (int a = v; a >= 0; a = spar[a]) {
             const int pa = spos[a];
