@@ -46,6 +46,8 @@ typedef struct sgb_gen_options {
     const int* seq_max_new;    /* optional per-sequence caps (c3 extension) or NULL */
     int want_features;         /* copy SeqResult.features back                   */
     int sid_offset;            /* global sid of this shard's first sequence (data-parallel ranks) */
+    double* step_seconds;      /* optional [step_cap]: measured device seconds of every step (GenStats
+                                  StepRecord.sim_latency_s, scheduler.cpp:356-368), or NULL */
 } sgb_gen_options;
 
 /* GenStats summary (scheduler.hpp:68-89) plus device measurements. */
@@ -78,6 +80,14 @@ int sgb_upload_draft(sgb_engine* e, const float* flat, size_t n);
 int sgb_download_draft(sgb_engine* e, float* flat, size_t n);
 /* Benchmark weights drawn on the device with init_flat's distributions (not bit-identical). */
 int sgb_init_random(sgb_engine* e, unsigned long long seed);
+
+/* SGRPOCK1 checkpoints (src/tinylm.cpp:14-105): header query (host only, no GPU), load into
+ * the engine (target or draft, config must match; payload mmapped and converted on the
+ * device), and save the engine's fp32 draft master in the reference's byte layout. */
+int sgb_checkpoint_info(const char* path, int* kind /* 0 target, 1 draft */, sgb_model_config* cfg,
+                        int* draft_layers, size_t* param_count);
+int sgb_load_checkpoint(sgb_engine* e, const char* path, int* kind);
+int sgb_save_draft_checkpoint(sgb_engine* e, const char* path);
 
 /* ---- per-op parity entry points -------------------------------------------------- */
 /* KvCacheT reset / len / gather_tail (tinylm.hpp:232-269). slot = engine sequence slot. */

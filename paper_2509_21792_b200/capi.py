@@ -11,6 +11,7 @@ There is no CPU fallback: if the shared library is missing this module raises at
 from __future__ import annotations
 
 import ctypes as C
+import json
 import os
 from dataclasses import dataclass
 from typing import List, Optional, Sequence
@@ -37,7 +38,7 @@ class GenOptionsC(C.Structure):
                 ("mode", C.c_int), ("early_term", C.c_int), ("temperature", C.c_double), ("seed", C.c_ulonglong),
                 ("max_new_tokens", C.c_int), ("fixed_n_verify", C.c_int), ("fixed_k_draft", C.c_int),
                 ("fixed_l_draft", C.c_int), ("seq_max_new", C.POINTER(C.c_int)), ("want_features", C.c_int),
-                ("sid_offset", C.c_int)]
+                ("sid_offset", C.c_int), ("step_seconds", C.POINTER(C.c_double))]
 
 
 class RolloutStatsC(C.Structure):
@@ -132,6 +133,7 @@ class Rollout:
     seconds: float
     h2d_bytes: int = 0
     d2h_bytes: int = 0
+    step_seconds: Optional[List[float]] = None  # measured device seconds per decode step
 
     def tau(self) -> float:
         if self.total_verify_slots == 0:
@@ -291,9 +293,10 @@ class Engine:
         flat = np.ascontiguousarray(np.concatenate([np.asarray(p, np.int32) for p in prompts])
                                     if n_p else np.zeros(0, np.int32), np.int32)
         smn = None if seq_max_new is None else np.ascontiguousarray(seq_max_new, np.int32)
+        step_s = np.zeros(max_steps_record, np.float64)
         opt = GenOptionsC(alpha, k_max, l_max, c_peak, MODES[mode], int(early_term), temperature, seed,
                           max_new_tokens, fixed[0], fixed[1], fixed[2], _p(smn, C.c_int), int(want_features),
-                          sid_offset)
+                          sid_offset, _p(step_s, C.c_double))
         toks = np.zeros((max(ns, 1), T), np.int32)
         lens = np.zeros(max(ns, 1), np.int32)
         pl = np.zeros(max(ns, 1), np.int32)
@@ -313,7 +316,7 @@ class Engine:
             total_accepted=st.total_accepted, total_verify_slots=st.total_verify_slots,
             target_forwards=st.target_forwards, draft_forwards=st.draft_forwards,
             kernel_launches=st.kernel_launches, seconds=st.seconds, h2d_bytes=st.h2d_bytes,
-            d2h_bytes=st.d2h_bytes)
+            d2h_bytes=st.d2h_bytes, step_seconds=step_s[:nst].tolist())
 
     # ---- kernel-class profiler
     def profile(self, on: bool = True):
@@ -422,3 +425,39 @@ def _measure_c_peak(self, b_max: int, warmup: int = 1, reps: int = 3):
 
 
 Engine.measure_c_peak = _measure_c_peak
+
+
+def checkpoint_info(path: str) -> dict:
+    """SGRPOCK1 header (src/tinylm.cpp:14-105) parsed by the library (host only)."""
+    kind, dl, n = C.c_int(), C.c_int(), C.c_size_t()
+    cfg = ModelConfigC()
+    _check(_lib.sgb_checkpoint_info(path.encode(), C.byref(kind), C.byref(cfg), C.byref(dl), C.byref(n)))
+    return dict(kind="target" if kind.value == 0 else "draft", vocab_size=cfg.vocab_size, d_model=cfg.d_model,
+                n_layers=cfg.n_layers, n_heads=cfg.n_heads, d_ff=cfg.d_ff, max_seq_len=cfg.max_seq_len,
+                seed=cfg.seed, draft_layers=dl.value, param_count=n.value)
+
+
+def _load_checkpoint(self, path: str) -> str:
+    kind = C.c_int()
+    _check(_lib.sgb_load_checkpoint(self.h, path.encode(), C.byref(kind)))
+    return "target" if kind.value == 0 else "draft"
+
+
+def _save_draft_checkpoint(self, path: str):
+    _check(_lib.sgb_save_draft_checkpoint(self.h, path.encode()))
+
+
+Engine.load_checkpoint = _load_checkpoint
+Engine.save_draft_checkpoint = _save_draft_checkpoint
+EXPORTED += ["sgb_checkpoint_info", "sgb_load_checkpoint", "sgb_save_draft_checkpoint"]
+
+
+def gen_stats_jsonl(r: "Rollout") -> str:
+    """gen_stats_to_jsonl (scheduler.cpp:356-368) with MEASURED step seconds in sim_latency_s:
+    one JSON object per decode step; accepted_total = tokens appended that step."""
+    out = []
+    for i, (b, n, k, l, acc) in enumerate(r.steps):
+        sec = r.step_seconds[i] if r.step_seconds else 0.0
+        out.append(json.dumps({"step": i, "b_cur": b, "spec_config": {"n_verify": n, "k_draft": k, "l_draft": l},
+                               "accepted_total": acc, "sim_latency_s": sec}, separators=(",", ":")))
+    return "".join(x + "\n" for x in out)

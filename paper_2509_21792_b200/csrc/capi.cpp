@@ -9,6 +9,10 @@
 #include <cstdlib>
 #include <cstring>
 #include <unistd.h>
+#include <cstdio>
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <sys/mman.h>
 #include <memory>
 #include <string>
 #include <unordered_map>
@@ -24,6 +28,8 @@
 
 struct sgb_engine {
     std::unique_ptr<sgb::Engine> eng;
+    sgb_model_config cfg{};  // as created (checkpoint headers carry it)
+    int draft_layers = 1;
 };
 
 namespace {
@@ -138,6 +144,8 @@ int sgb_engine_create(const sgb_model_config* c, int draft_layers, int device, i
         auto* h = new sgb_engine;
         try {
             h->eng = std::make_unique<sgb::Engine>(d, draft_layers, device, max_seqs, max_rows, k_max, l_max);
+            h->cfg = *c;
+            h->draft_layers = draft_layers;
         } catch (...) {
             delete h;
             throw;
@@ -280,6 +288,7 @@ int sgb_rollout(sgb_engine* e, const int* prompts, const int* prompt_lens, int n
                 step_rec[5 * i + 2] = r.steps[i].k_draft;
                 step_rec[5 * i + 3] = r.steps[i].l_draft;
                 step_rec[5 * i + 4] = r.steps[i].accepted;
+                if (opt->step_seconds) opt->step_seconds[i] = r.step_seconds[i];
             }
         }
         if (stats) {
@@ -459,6 +468,132 @@ int sgb_measure_c_peak(sgb_engine* e, int b_max, int warmup, int reps, int* c_pe
         *low_confidence = low ? 1 : 0;
         if (curve_s)
             for (int i = 0; i < b_max; ++i) curve_s[i] = ss[i];
+    });
+}
+
+// ---- SGRPOCK1 checkpoints (src/tinylm.cpp:14-105) ------------------------------------------
+// Layout: "SGRPOCK1" | u32 header length | JSON header | param_count little-endian fp32.
+// The header is the reference's nlohmann::json dump (keys sorted):
+//   {"config":{"d_ff":..,"d_model":..,"max_seq_len":..,"n_heads":..,"n_layers":..,"seed":..,
+//    "vocab_size":..},["draft_layers":..,]"kind":"target"|"draft","param_count":..}
+namespace {
+struct CkptHeader {
+    int kind = -1;  // 0 target, 1 draft
+    sgb_model_config cfg{};
+    int draft_layers = 0;
+    size_t param_count = 0;
+    size_t data_off = 0;
+};
+
+long long json_int(const std::string& h, const char* key) {
+    const std::string k = std::string("\"") + key + "\":";
+    const size_t p = h.find(k);
+    if (p == std::string::npos) throw std::runtime_error(std::string("checkpoint header lacks ") + key);
+    return std::stoll(h.substr(p + k.size()));
+}
+
+CkptHeader read_header(const std::string& path) {
+    FILE* f = std::fopen(path.c_str(), "rb");
+    if (!f) throw std::runtime_error("cannot open checkpoint: " + path);
+    char magic[8];
+    uint32_t hl = 0;
+    const bool ok = std::fread(magic, 1, 8, f) == 8 && std::memcmp(magic, "SGRPOCK1", 8) == 0 &&
+                    std::fread(&hl, 4, 1, f) == 1;
+    std::string h(hl, '\0');
+    const bool ok2 = ok && std::fread(&h[0], 1, hl, f) == hl;
+    std::fclose(f);
+    if (!ok) throw std::runtime_error("bad checkpoint magic: " + path);
+    if (!ok2) throw std::runtime_error("truncated checkpoint: " + path);
+    CkptHeader c;
+    const size_t kp = h.find("\"kind\":\"");
+    if (kp == std::string::npos) throw std::runtime_error("checkpoint header lacks kind");
+    const std::string kind = h.substr(kp + 8, h.find('"', kp + 8) - (kp + 8));
+    if (kind == "target") c.kind = 0;
+    else if (kind == "draft") c.kind = 1;
+    else throw std::runtime_error("unknown checkpoint kind: " + kind);
+    c.cfg.vocab_size = static_cast<int>(json_int(h, "vocab_size"));
+    c.cfg.d_model = static_cast<int>(json_int(h, "d_model"));
+    c.cfg.n_layers = static_cast<int>(json_int(h, "n_layers"));
+    c.cfg.n_heads = static_cast<int>(json_int(h, "n_heads"));
+    c.cfg.d_ff = static_cast<int>(json_int(h, "d_ff"));
+    c.cfg.max_seq_len = static_cast<int>(json_int(h, "max_seq_len"));
+    c.cfg.seed = static_cast<unsigned long long>(json_int(h, "seed"));
+    c.draft_layers = c.kind == 1 ? static_cast<int>(json_int(h, "draft_layers")) : 0;
+    c.param_count = static_cast<size_t>(json_int(h, "param_count"));
+    c.data_off = 12 + hl;
+    return c;
+}
+
+bool same_shape(const sgb_model_config& a, const sgb_model_config& b) {
+    return a.vocab_size == b.vocab_size && a.d_model == b.d_model && a.n_layers == b.n_layers &&
+           a.n_heads == b.n_heads && a.d_ff == b.d_ff && a.max_seq_len == b.max_seq_len;
+}
+}  // namespace
+
+int sgb_checkpoint_info(const char* path, int* kind, sgb_model_config* cfg, int* draft_layers, size_t* param_count) {
+    return guarded([&] {
+        const CkptHeader c = read_header(path);
+        if (kind) *kind = c.kind;
+        if (cfg) *cfg = c.cfg;
+        if (draft_layers) *draft_layers = c.draft_layers;
+        if (param_count) *param_count = c.param_count;
+    });
+}
+
+int sgb_load_checkpoint(sgb_engine* e, const char* path, int* kind_out) {
+    return guarded([&] {
+        E(e);
+        const CkptHeader c = read_header(path);
+        if (!same_shape(c.cfg, e->cfg)) throw std::invalid_argument("checkpoint config does not match the engine");
+        if (c.kind == 1 && c.draft_layers != e->draft_layers)
+            throw std::invalid_argument("checkpoint draft_layers does not match the engine");
+        const size_t nt = E(e).target_param_count(), nd = E(e).draft_param_count();
+        if (c.param_count != (c.kind == 0 ? nt : nd)) throw std::runtime_error("checkpoint param count mismatch");
+        // the payload is mapped, not copied: upload reads it straight from the page cache
+        const int fd = open(path, O_RDONLY);
+        if (fd < 0) throw std::runtime_error(std::string("cannot open checkpoint: ") + path);
+        const size_t bytes = c.data_off + c.param_count * sizeof(float);
+        struct stat stt;
+        if (fstat(fd, &stt) != 0 || static_cast<size_t>(stt.st_size) < bytes) {
+            close(fd);
+            throw std::runtime_error(std::string("truncated checkpoint: ") + path);
+        }
+        void* m = mmap(nullptr, bytes, PROT_READ, MAP_PRIVATE, fd, 0);
+        close(fd);
+        if (m == MAP_FAILED) throw std::runtime_error("mmap failed for checkpoint");
+        const float* flat = reinterpret_cast<const float*>(static_cast<const char*>(m) + c.data_off);
+        try {
+            if (c.kind == 0) E(e).upload_target(flat, c.param_count);
+            else E(e).upload_draft(flat, c.param_count);
+        } catch (...) {
+            munmap(m, bytes);
+            throw;
+        }
+        munmap(m, bytes);
+        if (kind_out) *kind_out = c.kind;
+    });
+}
+
+int sgb_save_draft_checkpoint(sgb_engine* e, const char* path) {
+    return guarded([&] {
+        const size_t nd = E(e).draft_param_count();
+        std::vector<float> flat(nd);
+        E(e).download_draft(flat.data(), nd);
+        const sgb_model_config& c = e->cfg;
+        const std::string h = "{\"config\":{\"d_ff\":" + std::to_string(c.d_ff) + ",\"d_model\":" +
+                              std::to_string(c.d_model) + ",\"max_seq_len\":" + std::to_string(c.max_seq_len) +
+                              ",\"n_heads\":" + std::to_string(c.n_heads) + ",\"n_layers\":" +
+                              std::to_string(c.n_layers) + ",\"seed\":" + std::to_string(c.seed) +
+                              ",\"vocab_size\":" + std::to_string(c.vocab_size) + "},\"draft_layers\":" +
+                              std::to_string(e->draft_layers) + ",\"kind\":\"draft\",\"param_count\":" +
+                              std::to_string(nd) + "}";
+        FILE* f = std::fopen(path, "wb");
+        if (!f) throw std::runtime_error(std::string("cannot open checkpoint for writing: ") + path);
+        const uint32_t hl = static_cast<uint32_t>(h.size());
+        bool ok = std::fwrite("SGRPOCK1", 1, 8, f) == 8 && std::fwrite(&hl, 4, 1, f) == 1 &&
+                  std::fwrite(h.data(), 1, hl, f) == hl && std::fwrite(flat.data(), 4, nd, f) == nd;
+        ok = (std::fclose(f) == 0) && ok;
+        if (!ok) throw std::runtime_error(std::string("checkpoint write failed: ") + path);
     });
 }
 

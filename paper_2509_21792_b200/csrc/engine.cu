@@ -165,6 +165,8 @@ Engine::Engine(const ModelDims& dims, int draft_layers, int device, int max_seqs
     SGB_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
     SGB_CUDA(cudaEventCreate(&ev0_));
     SGB_CUDA(cudaEventCreate(&ev1_));
+    SGB_CUDA(cudaEventCreate(&evs_a_));
+    SGB_CUDA(cudaEventCreate(&evs_b_));
     tlay_ = FlatLayout::target(dims);
     dlay_ = FlatLayout::draft(dims, draft_layers);
 
@@ -309,6 +311,8 @@ Engine::~Engine() {
     if (h_result_) cudaFreeHost(h_result_);
     if (ev0_) cudaEventDestroy(ev0_);
     if (ev1_) cudaEventDestroy(ev1_);
+    if (evs_a_) cudaEventDestroy(evs_a_);
+    if (evs_b_) cudaEventDestroy(evs_b_);
     if (st_) cudaStreamDestroy(st_);
 }
 
@@ -1096,6 +1100,13 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
     }
 
     // ---------------- step loop (scheduler.cpp:299-341)
+    SGB_CUDA(cudaEventRecord(evs_a_, st_));  // prefill done; each step's end is timed against the last
+    {
+        float ms = 0.f;
+        SGB_CUDA(cudaEventSynchronize(evs_a_));
+        SGB_CUDA(cudaEventElapsedTime(&ms, ev0_, evs_a_));
+        res.prefill_seconds = ms * 1e-3;
+    }
     std::vector<StepSeqDev> hs;
     std::vector<int> drow, live;
     for (int step = 0;; ++step) {
@@ -1292,7 +1303,14 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
         count(3);
         d2h(h_result_, result_, 2 * B, st_);
         d2h(h_result_ + 2 * B, err_, 1, st_);
+        SGB_CUDA(cudaEventRecord(evs_b_, st_));
         SGB_CUDA(cudaStreamSynchronize(st_));
+        {
+            float ms = 0.f;
+            SGB_CUDA(cudaEventElapsedTime(&ms, evs_a_, evs_b_));
+            res.step_seconds.push_back(ms * 1e-3);
+            std::swap(evs_a_, evs_b_);
+        }
         const int err = h_result_[2 * B];
         if (err & 1) throw std::runtime_error("forward_target: non-finite logits");
         if (err & 8) throw std::invalid_argument("build_tree_mask: closure violation");

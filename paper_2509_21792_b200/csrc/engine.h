@@ -84,6 +84,8 @@ struct RolloutResult {
     long long total_accepted = 0, total_verify_slots = 0;
     long long target_forwards = 0, draft_forwards = 0, kernel_launches = 0;
     double seconds = 0;  // device time of the step loop incl. prefill (CUDA events)
+    double prefill_seconds = 0;
+    std::vector<double> step_seconds;  // device time of every decode step (CUDA events)
     long long h2d_bytes = 0, d2h_bytes = 0;
 };
 
@@ -283,7 +285,7 @@ class Engine {
     void train_alloc();
     void train_refresh_ref_weights();
     void wgrad(const __nv_bfloat16* dyT, int N, const __nv_bfloat16* xT, int Kfeat, int Rp, float* grad_dst, int ld);
-    cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
+    cudaEvent_t ev0_ = nullptr, ev1_ = nullptr, evs_a_ = nullptr, evs_b_ = nullptr;  // rollout / per-step
 };
 
 }  // namespace sgb

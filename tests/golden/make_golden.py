@@ -240,6 +240,21 @@ def c1_fixture():
         json.dump({"config": cfgd(cfg), "prompts": prompts, "g": 2, "runs": runs}, f)
 
 
+CKPT = ModelConfig(64, 64, 1, 1, 128, 32, 5)  # head dim 64: loadable by the GPU engine too
+
+
+def checkpoint_fixture():
+    """SGRPOCK1 files written by the reference itself (tinylm.cpp:73-105): a target and a
+    1-layer draft with the reference init weights (a perturbed draft, so it is not the init)."""
+    m = R.RefModel(CKPT)
+    d0 = R.init_draft(CKPT, 1)
+    d = R.RefDraft(CKPT, 1, d0 + np.float32(0.001) * np.arange(d0.size, dtype=np.float32) % np.float32(0.01))
+    R.check(R.lib().sgref_save_checkpoint(C.c_void_p(m.h), os.path.join(OUT, "ckpt_target.bin").encode()))
+    R.check(R.lib().sgref_save_draft_checkpoint(C.c_void_p(d.h), os.path.join(OUT, "ckpt_draft.bin").encode()))
+    with open(os.path.join(OUT, "ckpt.json"), "w") as f:
+        json.dump({"config": cfgd(CKPT), "draft_layers": 1}, f)
+
+
 if __name__ == "__main__":
     if not R.available():
         sys.exit("build oracle/_ref first: make -C oracle")
@@ -250,4 +265,5 @@ if __name__ == "__main__":
     plan_fixture()
     generate_fixture()
     c1_fixture()
+    checkpoint_fixture()
     print("golden fixtures written to", OUT)

@@ -125,3 +125,22 @@ def test_rollout_errors():
         e.generate([[2, 3]], 1, c_peak=0)
     with pytest.raises(ValueError):  # k_draft > n_verify - 1
         e.generate([[2, 3]], 1, c_peak=4, mode="fixed_spec", fixed=(2, 3, 1))
+
+
+def test_gen_stats_jsonl_with_measured_step_seconds():
+    """gen_stats_to_jsonl (scheduler.cpp:356-368): one record per step; the B200 build writes
+    measured device seconds where the reference writes simulated ones."""
+    import json as _json
+    from paper_2509_21792_b200 import capi as _c
+    e, _, _ = make_engine(SMALL)
+    rng = np.random.default_rng(8)
+    prompts = [rng.integers(2, SMALL.vocab_size, size=7).tolist() for _ in range(3)]
+    r = e.generate(prompts, 2, c_peak=16, mode="adaptive_spec", seed=4, max_new_tokens=20)
+    lines = _c.gen_stats_jsonl(r).splitlines()
+    assert len(lines) == len(r.steps) == len(r.step_seconds)
+    for i, (ln, st) in enumerate(zip(lines, r.steps)):
+        j = _json.loads(ln)
+        assert j["step"] == i and j["b_cur"] == st[0]
+        assert (j["spec_config"]["n_verify"], j["spec_config"]["k_draft"], j["spec_config"]["l_draft"]) == st[1:4]
+        assert j["accepted_total"] == st[4] and j["sim_latency_s"] > 0
+    assert sum(r.step_seconds) <= r.seconds * 1.0001
