@@ -636,11 +636,14 @@ int sgb_bench_gemm(int M, int N, int K, int splits, int iters, double* ms_out) {
         SGB_CUDA(cudaMalloc(&ws.buf, ws.cap_floats * 4));
         SGB_CUDA(cudaMalloc(&ws.ctr, ws.ctr_cap * sizeof(int)));
         SGB_CUDA(cudaMemset(ws.ctr, 0, ws.ctr_cap * sizeof(int)));
-        SGB_CUDA(cudaMalloc(&dp, static_cast<size_t>(M) * N * 4));
+        // splits < 0: kEpiPartials (raw chunk sums, one unit per (tile, chunk))
+        const size_t out_floats = static_cast<size_t>(M) * N * (splits < 0 ? sgb::gemm_chunks(N, K) : 1);
+        SGB_CUDA(cudaMalloc(&dp, out_floats * 4));
         sgb::GemmEpi epi;
-        epi.kind = sgb::kEpiF32;
+        epi.kind = splits < 0 ? sgb::kEpiPartials : sgb::kEpiF32;
         epi.f32 = dp;
         epi.ld = N;
+        if (splits < 0) splits = 0;
         cudaEvent_t a, b;
         SGB_CUDA(cudaEventCreate(&a));
         SGB_CUDA(cudaEventCreate(&b));

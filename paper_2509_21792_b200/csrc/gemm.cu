@@ -36,6 +36,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 #include <stdexcept>
 #include <string>
@@ -68,7 +69,7 @@ constexpr int kNumSMs = 148;
 
 template <int BN>
 struct GemmCfg {
-    static constexpr int kSub = BN <= 32 ? SGB_KSUB32 : (BN == 64 ? SGB_KSUB64 : SGB_KSUB128);  // 64-wide k-boxes per stage
+    static constexpr int kSub = BN <= 32 ? SGB_KSUB32 : (BN == 64 ? SGB_KSUB64 : (BN == 128 ? SGB_KSUB128 : 1));
     static constexpr int kBBytes = BN * kBK * 2;
     static constexpr int kStage = kSub * (kABytes + kBBytes);
     static constexpr int kStages = (200 * 1024) / kStage > 8 ? 8 : (200 * 1024) / kStage;
@@ -190,7 +191,7 @@ struct StageSeq {
     }
 };
 
-template <int BN>
+template <int BN, bool PART>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap mapW, const __grid_constant__ CUtensorMap mapX, int M,
                         int N, int kb_total, int n_chunks, int ckb, int cps, int S, int m_tiles, int n_tiles, GemmEpi epi,
@@ -337,7 +338,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int nmine = max(0, min(HB, ncols - j0));
             const int c_begin = un.split * cps, c_end = min(n_chunks, c_begin + cps);
             float* wst = ws ? ws + static_cast<size_t>(un.tile) * n_chunks * BN * kBM : nullptr;
-            float run[HB];
+            float run[PART ? 1 : HB];  // the chunk-ordered running sum (not needed for raw partials)
             for (int c = c_begin; c < c_end; ++c, ++it) {
                 const int buf = it & 1;
                 mbar_wait(&tfull[buf], (it >> 1) & 1);
@@ -348,7 +349,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int p0 = 0; p0 < HB; p0 += PC) {
                     float v[PC];
                     tmem_ld<PC>(tmem + (static_cast<uint32_t>(32 * q) << 16) + buf * BN + j0 + p0, v);
-                    if (epi.kind == kEpiPartials) {
+                    if constexpr (PART) {
                         float* dst = epi.f32 + (static_cast<size_t>(c) * M + un.m0 + j0 + p0) * epi.ld + o;
 #pragma unroll
                         for (int j = 0; j < PC; ++j)
@@ -371,7 +372,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&tempty[buf]);
             }
-            if (epi.kind == kEpiPartials) {
+            if constexpr (PART) {
                 // raw chunk sums already stored; the consumer kernel reduces them in order
             } else if (S == 1) {
                 if (o < N) epi_store_run<HB>(epi, un.m0 + j0, nmine, o, run);
@@ -443,20 +444,20 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     return fn;
 }
 
-template <int BN>
+template <int BN, bool PART>
 void launch_bn(const CUtensorMap& w, const CUtensorMap& x, int M, int N, int kbt, int n_chunks, int ckb, int S, int cps,
                const GemmEpi& epi, float* ws, int* ctr, cudaStream_t st) {
     using Cfg = GemmCfg<BN>;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(gemm_bf16_tn_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
+        cudaFuncSetAttribute(gemm_bf16_tn_kernel<BN, PART>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
         attr = true;
     }
     const int m_tiles = (M + BN - 1) / BN, n_tiles = (N + kBM - 1) / kBM;
     const int units = m_tiles * n_tiles * S;
     const int grid = std::min(units, kNumSMs);
-    launch_pdl(gemm_bf16_tn_kernel<BN>, dim3(grid), dim3(kThreads), Cfg::kSmem, st, w, x, M, N, kbt, n_chunks, ckb, cps,
-               S, m_tiles, n_tiles, epi, ws, ctr);
+    launch_pdl(gemm_bf16_tn_kernel<BN, PART>, dim3(grid), dim3(kThreads), Cfg::kSmem, st, w, x, M, N, kbt, n_chunks, ckb,
+               cps, S, m_tiles, n_tiles, epi, ws, ctr);
 }
 
 }  // namespace
@@ -545,17 +546,29 @@ void gemm_run(const GemmWeight& w, const GemmAct& x, int M, const GemmEpi& epi, 
     int S = force_splits > 0 ? std::min(force_splits, nc) : gemm_splits_for(M, w.N, w.K);
     const int bn = gemm_bn_for(M);
     const int tiles = ((M + bn - 1) / bn) * ((w.N + kBM - 1) / kBM);
-    if (epi.kind == kEpiPartials) S = nc;  // one unit per (tile, chunk), no in-kernel finisher
-    else if (S > 1 && (ws.buf == nullptr || gemm_ws_floats(M, w.N, w.K) > ws.cap_floats || tiles > ws.ctr_cap)) S = 1;
+    if (epi.kind == kEpiPartials) {
+        // one unit per (tile, chunk), no in-kernel finisher. Token tile: 128 up to 384 rows
+        // (more units), 256 above (each weight tile read once per 256 tokens); measured with
+        // scripts/gemm_part.py at the c2/c3 residual shapes
+        static const int part_bn = [] {
+            const char* v = getenv("SGB_PART_BN");  // tuning experiments only
+            return v ? atoi(v) : 0;
+        }();
+        const int pbn = part_bn > 0 && M > 128 ? part_bn : (M > 384 ? 256 : std::max(64, bn));
+        const CUtensorMap& xm = x.map_for_bn(pbn);
+        if (pbn == 256) launch_bn<256, true>(w.map, xm, M, w.N, kbt, nc, ckb, nc, 1, epi, nullptr, nullptr, st);
+        else if (pbn == 128) launch_bn<128, true>(w.map, xm, M, w.N, kbt, nc, ckb, nc, 1, epi, nullptr, nullptr, st);
+        else launch_bn<64, true>(w.map, xm, M, w.N, kbt, nc, ckb, nc, 1, epi, nullptr, nullptr, st);
+        return;
+    }
+    if (S > 1 && (ws.buf == nullptr || gemm_ws_floats(M, w.N, w.K) > ws.cap_floats || tiles > ws.ctr_cap)) S = 1;
     const int cps = (nc + S - 1) / S;
     S = (nc + cps - 1) / cps;
     const CUtensorMap& xm = x.map_for_bn(bn);
     switch (bn) {
-        case 16: launch_bn<16>(w.map, xm, M, w.N, kbt, nc, ckb, S, cps, epi, ws.buf, ws.ctr, st); break;
-        case 32: launch_bn<32>(w.map, xm, M, w.N, kbt, nc, ckb, S, cps, epi, ws.buf, ws.ctr, st); break;
-        case 64: launch_bn<64>(w.map, xm, M, w.N, kbt, nc, ckb, S, cps, epi, ws.buf, ws.ctr, st); break;
-        case 128: launch_bn<128>(w.map, xm, M, w.N, kbt, nc, ckb, S, cps, epi, ws.buf, ws.ctr, st); break;
-        default: launch_bn<256>(w.map, xm, M, w.N, kbt, nc, ckb, S, cps, epi, ws.buf, ws.ctr, st); break;
+        case 16: launch_bn<16, false>(w.map, xm, M, w.N, kbt, nc, ckb, S, cps, epi, ws.buf, ws.ctr, st); break;
+        case 64: launch_bn<64, false>(w.map, xm, M, w.N, kbt, nc, ckb, S, cps, epi, ws.buf, ws.ctr, st); break;
+        default: launch_bn<128, false>(w.map, xm, M, w.N, kbt, nc, ckb, S, cps, epi, ws.buf, ws.ctr, st); break;
     }
 }
 
