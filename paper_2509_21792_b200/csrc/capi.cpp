@@ -268,17 +268,15 @@ int sgb_rollout(sgb_engine* e, const int* prompts, const int* prompt_lens, int n
         if (opt->seq_max_new) a.seq_max_new.assign(opt->seq_max_new, opt->seq_max_new + n_prompts * g);
         a.want_features = features != nullptr && opt->want_features;
         a.sid_offset = opt->sid_offset;
+        if (a.want_features) a.features_out = features;
         sgb::RolloutResult r = en.rollout(a);
-        const int T = en.dims().max_seq, d = en.dims().d;
+        const int T = en.dims().max_seq;
         const int ns = static_cast<int>(r.tokens.size());
         for (int s = 0; s < ns; ++s) {
             if (tokens) std::copy(r.tokens[s].begin(), r.tokens[s].end(), tokens + static_cast<size_t>(s) * T);
             if (lens) lens[s] = static_cast<int>(r.tokens[s].size());
             if (prompt_len) prompt_len[s] = r.prompt_len[s];
             if (hit_eos) hit_eos[s] = r.hit_eos[s];
-            if (features && a.want_features)
-                std::copy(r.features[s].begin(), r.features[s].end(),
-                          features + static_cast<size_t>(s) * (T - 1) * d);
         }
         if (step_rec) {
             const int n = std::min(step_cap, static_cast<int>(r.steps.size()));

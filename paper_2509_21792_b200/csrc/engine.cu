@@ -8,6 +8,8 @@
 // scheduler.cpp:14-54 -- pure integer work that needs the live count B_cur) and reads back
 // one small per-sequence result vector per step.
 #include <algorithm>
+#include <cstring>
+#include <thread>
 #include <cmath>
 #include <cstring>
 #include <numeric>
@@ -309,6 +311,7 @@ Engine::~Engine() {
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (h_result_) cudaFreeHost(h_result_);
+    if (feats_host_) cudaFreeHost(feats_host_);
     if (ev0_) cudaEventDestroy(ev0_);
     if (ev1_) cudaEventDestroy(ev1_);
     if (evs_a_) cudaEventDestroy(evs_a_);
@@ -1340,7 +1343,17 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
         res.tokens[s].resize(len[s]);
         d2h(res.tokens[s].data(), ss_.tokens + static_cast<size_t>(s) * T, len[s], st_);
     }
-    if (a.want_features) {
+    if (a.want_features && a.features_out) {
+        // one DMA of the whole feature store into pinned staging at full link rate ...
+        const size_t n = static_cast<size_t>(n_seqs) * T * d;
+        if (feats_host_cap_ < n) {
+            if (feats_host_) cudaFreeHost(feats_host_);
+            feats_host_ = nullptr;
+            SGB_CUDA(cudaMallocHost(&feats_host_, n * sizeof(float)));
+            feats_host_cap_ = n;
+        }
+        SGB_CUDA(cudaMemcpyAsync(feats_host_, feats_, n * sizeof(float), cudaMemcpyDeviceToHost, st_));
+    } else if (a.want_features) {
         res.features.resize(n_seqs);
         for (int s = 0; s < n_seqs; ++s) {
             res.features[s].resize(static_cast<size_t>(len[s] - 1) * d);
@@ -1348,6 +1361,19 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
         }
     }
     SGB_CUDA(cudaStreamSynchronize(st_));
+    if (a.want_features && a.features_out) {
+        // ... then the per-sequence scatter into the caller's layout on several host threads
+        const int nth = std::max(1, std::min(16, static_cast<int>(std::thread::hardware_concurrency())));
+        std::vector<std::thread> pool;
+        for (int w = 0; w < nth; ++w)
+            pool.emplace_back([&, w] {
+                for (int s = w; s < n_seqs; s += nth)
+                    std::memcpy(a.features_out + static_cast<size_t>(s) * (T - 1) * d,
+                                feats_host_ + static_cast<size_t>(s) * T * d,
+                                static_cast<size_t>(len[s] - 1) * d * sizeof(float));
+            });
+        for (auto& t : pool) t.join();
+    }
     res.hit_eos = h_eos;
     last_lens_ = len;  // the draft update can consume this rollout straight from HBM
     for (int s = 0; s < n_seqs; ++s) {

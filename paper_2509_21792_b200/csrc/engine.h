@@ -62,6 +62,9 @@ struct RolloutArgs {
     std::vector<int> seq_max_new;  // optional per-sequence caps (c3 extension)
     bool want_features = true;
     int sid_offset = 0;  // global sid of local sequence 0 (seed parity under sharding)
+    // optional caller buffer [n_seqs][max_seq-1][d] for the features (skips RolloutResult.features):
+    // one pinned-staging DMA of the feature store, then a multi-threaded host scatter
+    float* features_out = nullptr;
 };
 
 struct StepStat {
@@ -244,6 +247,8 @@ class Engine {
     float *x_ = nullptr, *q_ = nullptr, *y_ = nullptr, *logits_ = nullptr, *featin_ = nullptr;
     RowScratch rsc_{};  // multi-CTA sampling / top-k records
     float* gpart_ = nullptr;  // kEpiPartials chunk sums [chunks][max_rows][d]
+    float* feats_host_ = nullptr;  // pinned staging of the feature store (lazy)
+    size_t feats_host_cap_ = 0;
     size_t gpart_cap_ = 0;
     float *pacc_ = nullptr, *pml_ = nullptr;
     AttnScratch asc_{};
