@@ -33,6 +33,7 @@ T* talloc(size_t n) {
     return p;
 }
 int pad8(int x) { return (x + 7) & ~7; }
+constexpr int kWholeK = 1 << 20;  // one accumulation chunk: training GEMMs have tiles to spare
 }  // namespace
 
 void Engine::train_alloc() {
@@ -116,7 +117,7 @@ void Engine::train_alloc() {
     // frozen target LM head in the reference layout [d][V] (K-major operand of its dgrad)
     launch_transpose_bf16(lm_head_.ptr, static_cast<int>(V), static_cast<int>(d), static_cast<int>(d), t.lm_ref,
                           static_cast<int>(V), st_);
-    t.lm_ref_w.init(t.lm_ref, d, V);
+    t.lm_ref_w.init(t.lm_ref, d, V, kWholeK);
     t.ready = true;
     train_refresh_ref_weights();
 }
@@ -140,17 +141,17 @@ void Engine::train_refresh_ref_weights() {
         SGB_CUDA(cudaMemcpy2DAsync(t.wqkv_ref + k * d, 3 * d * 2, t.dflat_b + off, d * 2, d * 2, d,
                                    cudaMemcpyDeviceToDevice, st_));
     }
-    t.wqkv_ref_w.init(t.wqkv_ref, d, 3 * d);
-    t.wo_ref.init(t.dflat_b + o.wo, d, d);
-    t.w1_ref.init(t.dflat_b + o.w1, d, F);
-    t.w2_ref.init(t.dflat_b + o.w2, F, d);
+    t.wqkv_ref_w.init(t.wqkv_ref, d, 3 * d, kWholeK);
+    t.wo_ref.init(t.dflat_b + o.wo, d, d, kWholeK);
+    t.w1_ref.init(t.dflat_b + o.w1, d, F, kWholeK);
+    t.w2_ref.init(t.dflat_b + o.w2, F, d, kWholeK);
 }
 
 // grad[k][n] (+)= sum_r X[r][k] dY[r][n], from transposed operands dyT [N][Rp], xT [Kfeat][Rp].
 void Engine::wgrad(const __nv_bfloat16* dyT, int N, const __nv_bfloat16* xT, int Kfeat, int Rp, float* grad_dst,
                    int ld) {
     GemmWeight w;
-    w.init(dyT, N, Rp);
+    w.init(dyT, N, Rp, kWholeK);
     GemmAct a;
     a.init(xT, Kfeat, Rp);
     GemmEpi e;

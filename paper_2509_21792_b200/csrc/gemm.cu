@@ -572,11 +572,11 @@ void gemm_run(const GemmWeight& w, const GemmAct& x, int M, const GemmEpi& epi, 
     }
 }
 
-void GemmWeight::init(const __nv_bfloat16* p, int n, int k) {
+void GemmWeight::init(const __nv_bfloat16* p, int n, int k, int chunk_kb_override) {
     ptr = p;
     N = n;
     K = k;
-    chunk_kb = gemm_chunk_kb(n, k);
+    chunk_kb = chunk_kb_override > 0 ? chunk_kb_override : gemm_chunk_kb(n, k);
     map = make_kmajor_map(p, n, k, kBM);
 }
 

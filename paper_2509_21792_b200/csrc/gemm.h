@@ -13,7 +13,9 @@ struct GemmWeight {
     int N = 0, K = 0;
     int chunk_kb = 16;  // accumulation chunk in 64-wide k-blocks (gemm_chunk_kb: fixed per weight shape)
     CUtensorMap map;
-    void init(const __nv_bfloat16* p, int n, int k);
+    // chunk_kb > 0 overrides the per-shape chunk width (training operands: one chunk, no
+    // intermediate TMEM readouts; their numerics need determinism, not batch invariance)
+    void init(const __nv_bfloat16* p, int n, int k, int chunk_kb_override = 0);
 };
 
 // A bf16 activation buffer [cap_rows][K] with one TMA map per supported token tile.

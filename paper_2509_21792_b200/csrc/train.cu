@@ -167,28 +167,73 @@ __global__ void __launch_bounds__(kT) smoothl1_kernel(const float* __restrict__ 
 // loss row and dlogits = scale * (softmax - onehot) in bf16.
 __global__ void __launch_bounds__(kT) ce_kernel(const float* __restrict__ logits, int V, const int* __restrict__ tgt,
                                                 double scale, __nv_bfloat16* __restrict__ dlog, double* __restrict__ loss_row) {
+    // Two passes over the 608 KB row: (1) online max + sum of exp with per-thread rescaling
+    // (fp32 exps, fp64 sums), (2) the bf16 gradient scale * (softmax - onehot). The gradient
+    // is stored in bf16, so its exps are fp32; the loss keeps an fp64 log-sum-exp.
     __shared__ double redd[kT / 32];
     __shared__ float redf[kT / 32];
     const int r = blockIdx.x;
     const float* L = logits + static_cast<size_t>(r) * V;
-    float mx = -INFINITY;
-    for (int c = threadIdx.x; c < V; c += kT) mx = fmaxf(mx, L[c]);
-    mx = warp_max(mx);
+    float mt = -INFINITY;
+    double st = 0.0;
+    const bool vec = (V & 3) == 0;
+    auto see = [&](float x) {
+        if (x > mt) {
+            st = st * static_cast<double>(expf(mt - x)) + 1.0;
+            mt = x;
+        } else {
+            st += static_cast<double>(expf(x - mt));
+        }
+    };
+    if (vec) {
+        const float4* L4 = reinterpret_cast<const float4*>(L);
+        for (int c = threadIdx.x; c < V / 4; c += kT) {
+            const float4 x = L4[c];
+            see(x.x);
+            see(x.y);
+            see(x.z);
+            see(x.w);
+        }
+    } else {
+        for (int c = threadIdx.x; c < V; c += kT) see(L[c]);
+    }
+    // block max, then rescale every thread's sum to it
+    float mx = warp_max(mt);
     if ((threadIdx.x & 31) == 0) redf[threadIdx.x >> 5] = mx;
     __syncthreads();
     float m2 = redf[0];
     for (int i = 1; i < kT / 32; ++i) m2 = fmaxf(m2, redf[i]);
-    const double m = m2;
-    double s = 0.0;
-    for (int c = threadIdx.x; c < V; c += kT) s += exp(static_cast<double>(L[c]) - m);
-    s = block_sum_dd(s, redd);
+    const double s = block_sum_dd(mt == -INFINITY ? 0.0 : st * static_cast<double>(expf(mt - m2)), redd);
+    const double lse = static_cast<double>(m2) + log(s);
+    const float lse_f = static_cast<float>(lse);
+    const float sc = static_cast<float>(scale);
     const int t = tgt[r];
-    for (int c = threadIdx.x; c < V; c += kT) {
-        double g = scale * exp(static_cast<double>(L[c]) - m) / s;
-        if (c == t) g -= scale;
-        dlog[static_cast<size_t>(r) * V + c] = __float2bfloat16(static_cast<float>(g));
+    __nv_bfloat16* D = dlog + static_cast<size_t>(r) * V;
+    if (vec) {
+        const float4* L4 = reinterpret_cast<const float4*>(L);
+        for (int c = threadIdx.x; c < V / 4; c += kT) {
+            const float4 x = L4[c];
+            float g0 = sc * expf(x.x - lse_f), g1 = sc * expf(x.y - lse_f), g2 = sc * expf(x.z - lse_f),
+                  g3 = sc * expf(x.w - lse_f);
+            const int c0 = 4 * c;
+            if (t == c0) g0 -= sc;
+            if (t == c0 + 1) g1 -= sc;
+            if (t == c0 + 2) g2 -= sc;
+            if (t == c0 + 3) g3 -= sc;
+            __nv_bfloat162 a = __floats2bfloat162_rn(g0, g1), b = __floats2bfloat162_rn(g2, g3);
+            uint2 u;
+            u.x = *reinterpret_cast<uint32_t*>(&a);
+            u.y = *reinterpret_cast<uint32_t*>(&b);
+            *reinterpret_cast<uint2*>(D + c0) = u;
+        }
+    } else {
+        for (int c = threadIdx.x; c < V; c += kT) {
+            float g = sc * expf(L[c] - lse_f);
+            if (c == t) g -= sc;
+            D[c] = __float2bfloat16(g);
+        }
     }
-    if (threadIdx.x == 0) loss_row[r] = -scale * (static_cast<double>(L[t]) - m - log(s));
+    if (threadIdx.x == 0) loss_row[r] = -scale * (static_cast<double>(L[t]) - lse);
 }
 
 // [rows][cols] (fp32 or bf16) -> [cols][ld] bf16 transposed (zero-padded columns).
