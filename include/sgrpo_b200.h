@@ -199,6 +199,21 @@ int sgb_bench_attention(int B, int ctx, int H, int dh, int iters, double* ms_out
 int sgb_debug_attention(int B, const int* n_keys, int H, int dh, const float* q, const float* k, const float* v,
                         float* out);
 
+/* Prefix-shared tree attention self-test. n_groups sequences; group g has ctx_len[g]
+ * committed keys (kctx/vctx rows, concatenated over groups) and n_rows[g] tree rows in
+ * level order with parent[r] (index within the group, -1 = root); row r attends to the
+ * group's committed keys then its ancestors-or-self node keys (knode/vnode, one per row),
+ * exactly the verify rows of a speculative step (build_tree_mask, drafttree.cpp:145-168;
+ * decode_blocks, tinylm.hpp:335-395). The rows run through BOTH the per-row kernel
+ * (out_row) and the prefix-shared group kernel (out_group); [rows][H*dh], bf16 values. */
+int sgb_debug_tree_attention(int n_groups, const int* ctx_len, const int* n_rows, const int* parent, int H, int dh,
+                             const float* q, const float* kctx, const float* vctx, const float* knode,
+                             const float* vnode, float* out_row, float* out_group);
+
+/* Tree-verify attention microbenchmark: B sequences x (ctx committed keys + an EAGLE-shaped
+ * tree of N rows); ms per launch of the per-row and of the prefix-shared group kernel. */
+int sgb_bench_tree_attention(int B, int N, int ctx, int H, int dh, int iters, double* ms_row, double* ms_group);
+
 /* tcgen05 GEMM self-test: out[M][N] = bf16(x)[M][K] . bf16(w)[N][K]^T (K-major). */
 int sgb_debug_gemm(const float* w, const float* x, int M, int N, int K, float* out, int* splits_out);
 

@@ -61,7 +61,7 @@ EXPORTED = ["sgb_last_error", "sgb_version", "sgb_device_count", "sgb_engine_cre
             "sgb_cache_reset", "sgb_cache_len", "sgb_cache_read", "sgb_cache_gather_tail", "sgb_forward_target",
             "sgb_forward_draft_rows", "sgb_sample_rows", "sgb_topk_logsoftmax", "sgb_build_tree", "sgb_rollout",
             "sgb_debug_gemm", "sgb_profile_enable", "sgb_profile_read", "sgb_bench_gemm", "sgb_bench_attention",
-            "sgb_debug_attention", "sgb_detect_knee", "sgb_measure_c_peak"]
+            "sgb_debug_attention", "sgb_debug_tree_attention", "sgb_bench_tree_attention", "sgb_detect_knee", "sgb_measure_c_peak"]
 
 KERNEL_CLASSES = ["gemm_tcgen05", "attention", "rowops", "lm_head", "sample", "tree", "kv_commit"]
 
@@ -99,6 +99,24 @@ def debug_attention(q: np.ndarray, k_rows, v_rows, n_heads: int) -> np.ndarray:
     _check(_lib.sgb_debug_attention(B, _p(nk, C.c_int), n_heads, d // n_heads, _p(q, C.c_float), _p(k, C.c_float),
                                     _p(v, C.c_float), _p(out, C.c_float)))
     return out
+
+
+def debug_tree_attention(ctx_len, parents, q, kctx, vctx, knode, vnode, n_heads: int):
+    """Prefix-shared tree attention self-test (sgb_debug_tree_attention): per group g,
+    ctx_len[g] committed keys and a tree of rows (parents[g], level order, -1 = root).
+    Returns (per-row kernel output, group kernel output), each [rows][d] (bf16 values)."""
+    q = np.ascontiguousarray(q, np.float32)
+    M, d = q.shape
+    cl = np.ascontiguousarray(ctx_len, np.int32)
+    nr = np.array([len(p) for p in parents], np.int32)
+    par = np.ascontiguousarray(np.concatenate([np.asarray(p, np.int32) for p in parents]), np.int32)
+    f = [np.ascontiguousarray(a, np.float32) for a in (kctx, vctx, knode, vnode)]
+    o1 = np.zeros((M, d), np.float32)
+    o2 = np.zeros((M, d), np.float32)
+    _check(_lib.sgb_debug_tree_attention(len(cl), _p(cl, C.c_int), _p(nr, C.c_int), _p(par, C.c_int), n_heads,
+                                         d // n_heads, _p(q, C.c_float), *[_p(a, C.c_float) for a in f],
+                                         _p(o1, C.c_float), _p(o2, C.c_float)))
+    return o1, o2
 
 
 def debug_gemm(w: np.ndarray, x: np.ndarray, splits: int = 0):

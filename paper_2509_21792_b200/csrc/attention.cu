@@ -37,6 +37,7 @@
 #include <cstdlib>
 #include <cfloat>
 
+#include "attn_numerics.cuh"
 #include "common.cuh"
 #include "kernels.h"
 #include "util.h"
@@ -45,7 +46,7 @@ namespace sgb {
 
 namespace {
 
-constexpr int kBlock = 64;  // keys per softmax partial (fixed: part of the numerics)
+constexpr int kBlock = kAttnBlock;
 
 SGB_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -295,15 +296,15 @@ __global__ void __launch_bounds__(HPW == 1 ? 416 : 544, HPW == 1 ? 2 : 1)  // co
 #pragma unroll
                     for (int o = LPR / 2; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
                     const float dr = __shfl_sync(0xffffffffu, dot, (lane % RPI) * LPR);
-                    if (lane / RPI == t && lane < nvalid) sc = dr * scale;
+                    if (lane / RPI == t && lane < nvalid) sc = attn_scale(dr, scale);
                 }
                 const float cm = warp_max(sc);
                 const float nm = fmaxf(m[hh], cm);
-                const float alpha = (m[hh] == -INFINITY) ? 0.f : expf(m[hh] - nm);
-                const float p = (lane < nvalid) ? expf(sc - nm) : 0.f;
-                l[hh] = l[hh] * alpha + warp_sum(p);
+                const float alpha = attn_alpha(m[hh], nm);
+                const float p = (lane < nvalid) ? attn_p(sc, nm) : 0.f;
+                l[hh] = attn_l(l[hh], alpha, warp_sum(p));
 #pragma unroll
-                for (int e = 0; e < PL; ++e) acc[hh][e] *= alpha;
+                for (int e = 0; e < PL; ++e) acc[hh][e] = __fmul_rn(acc[hh][e], alpha);
                 m[hh] = nm;
 #pragma unroll
                 for (int j = 0; j < KPC; ++j) {
@@ -394,20 +395,13 @@ __global__ void __launch_bounds__(HPW == 1 ? 416 : 544, HPW == 1 ? 2 : 1)  // co
                 }
 #pragma unroll
                 for (int u = 0; u < kMB; ++u) {
-                    if (b0 + u < done.nb) {
-                        const float Mn = fmaxf(Mx, mb[u]);
-                        const float ca = Mx == -INFINITY ? 0.f : expf(Mx - Mn), cb = expf(mb[u] - Mn);
-                        Lx = Lx * ca + lb[u] * cb;
-#pragma unroll
-                        for (int e0 = 0; e0 < PL; ++e0) A[e0] = A[e0] * ca + ab[u][e0] * cb;
-                        Mx = Mn;
-                    }
+                    if (b0 + u < done.nb) attn_merge<PL>(Mx, Lx, A, mb[u], lb[u], ab[u]);
                 }
             }
 #pragma unroll
             for (int e0 = 0; e0 < PL; ++e0) {
                 const int e = lane * PL + e0;
-                out[static_cast<size_t>(done.r) * d + h * DH + e] = __float2bfloat16(A[e0] / Lx);
+                out[static_cast<size_t>(done.r) * d + h * DH + e] = __float2bfloat16(__fdiv_rn(A[e0], Lx));
             }
         }
     }

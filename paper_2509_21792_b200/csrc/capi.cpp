@@ -727,6 +727,173 @@ int sgb_debug_attention(int B, const int* n_keys, int H, int dh, const float* q,
     });
 }
 
+namespace {
+// Device state of a tree-attention case: n_groups sequences, each with ctx_len committed keys
+// and a tree of rows (level order, parent within the group) -- the verify rows of one step.
+struct TreeAttnCase {
+    int M = 0, H = 0, d = 0, max_vlen = 1, n_tiles = 0, items = 0;
+    double keys = 0;
+    std::vector<void*> ptrs;
+    __nv_bfloat16 *K = nullptr, *V = nullptr, *o1 = nullptr, *o2 = nullptr;
+    float* q = nullptr;
+    sgb::AttnRowsDev ar{};
+    sgb::AttnScratch sc{};
+    sgb::AttnTileDev* tiles = nullptr;
+
+    void* dev(size_t bytes) {
+        void* p = nullptr;
+        SGB_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 16)));
+        ptrs.push_back(p);
+        return p;
+    }
+    TreeAttnCase(int n_groups, const int* ctx_len, const int* n_rows, const int* parent, int H_, int dh,
+                 const float* hq, const float* kctx, const float* vctx, const float* knode, const float* vnode)
+        : H(H_), d(H_ * dh) {
+        if (n_groups <= 0 || H <= 0 || dh <= 0) throw std::invalid_argument("tree_attention: bad shape");
+        long long n_ctx = 0;
+        for (int g = 0; g < n_groups; ++g) {
+            if (ctx_len[g] < 0 || n_rows[g] < 1) throw std::invalid_argument("tree_attention: bad group");
+            n_ctx += ctx_len[g];
+            M += n_rows[g];
+        }
+        // KV store: committed keys of every group, then one node slot per row
+        const long long slots = n_ctx + M;
+        std::vector<long long> base(M), chain(static_cast<size_t>(M) * sgb::kMaxChain, 0);
+        std::vector<int> cl(M), chl(M);
+        std::vector<sgb::AttnTileDev> ht;
+        long long cbase = 0;
+        int row = 0;
+        for (int g = 0; g < n_groups; ++g) {
+            const int r0 = row;
+            std::vector<int> depth(n_rows[g]);
+            int gmax = 1;
+            for (int i = 0; i < n_rows[g]; ++i, ++row) {
+                const int p = parent[row];
+                if (i == 0 ? p != -1 : (p < 0 || p >= i)) throw std::invalid_argument("tree_attention: bad parent");
+                depth[i] = i == 0 ? 0 : depth[p] + 1;
+                if (depth[i] + 1 > sgb::kMaxChain) throw std::invalid_argument("tree_attention: tree too deep");
+                base[row] = cbase;
+                cl[row] = ctx_len[g];
+                chl[row] = depth[i] + 1;
+                for (int a = i; a >= 0; a = a == 0 ? -1 : parent[r0 + a])
+                    chain[static_cast<size_t>(row) * sgb::kMaxChain + depth[a]] = n_ctx + r0 + a;
+                gmax = std::max(gmax, ctx_len[g] + depth[i] + 1);
+                keys += ctx_len[g] + depth[i] + 1;
+            }
+            max_vlen = std::max(max_vlen, gmax);
+            const int nb = sgb::attn_splits_for(gmax);
+            for (int o = 0; o < n_rows[g]; o += sgb::kAttnTileRows) {
+                ht.push_back({r0 + o, std::min(sgb::kAttnTileRows, n_rows[g] - o), nb, items});
+                items += nb * H;
+            }
+            cbase += ctx_len[g];
+        }
+        n_tiles = static_cast<int>(ht.size());
+        const int ns = sgb::attn_splits_for(max_vlen);
+        K = static_cast<__nv_bfloat16*>(dev(static_cast<size_t>(slots) * d * 2));
+        V = static_cast<__nv_bfloat16*>(dev(static_cast<size_t>(slots) * d * 2));
+        o1 = static_cast<__nv_bfloat16*>(dev(static_cast<size_t>(M) * d * 2));
+        o2 = static_cast<__nv_bfloat16*>(dev(static_cast<size_t>(M) * d * 2));
+        q = static_cast<float*>(dev(static_cast<size_t>(M) * d * 4));
+        if (hq) {
+            std::vector<__nv_bfloat16> hk(static_cast<size_t>(slots) * d), hv(hk.size());
+            for (size_t i = 0; i < static_cast<size_t>(n_ctx) * d; ++i) {
+                hk[i] = __float2bfloat16(kctx[i]);
+                hv[i] = __float2bfloat16(vctx[i]);
+            }
+            for (size_t i = 0; i < static_cast<size_t>(M) * d; ++i) {
+                hk[n_ctx * d + i] = __float2bfloat16(knode[i]);
+                hv[n_ctx * d + i] = __float2bfloat16(vnode[i]);
+            }
+            SGB_CUDA(cudaMemcpy(K, hk.data(), hk.size() * 2, cudaMemcpyHostToDevice));
+            SGB_CUDA(cudaMemcpy(V, hv.data(), hv.size() * 2, cudaMemcpyHostToDevice));
+            SGB_CUDA(cudaMemcpy(q, hq, static_cast<size_t>(M) * d * 4, cudaMemcpyHostToDevice));
+        } else {  // timing only: constant data
+            SGB_CUDA(cudaMemset(K, 0x3c, static_cast<size_t>(slots) * d * 2));
+            SGB_CUDA(cudaMemset(V, 0x3c, static_cast<size_t>(slots) * d * 2));
+            SGB_CUDA(cudaMemset(q, 0, static_cast<size_t>(M) * d * 4));
+        }
+        auto* pacc = static_cast<float*>(dev(static_cast<size_t>(M) * d * ns * 4));
+        auto* pml = static_cast<float*>(dev(static_cast<size_t>(M) * H * ns * 2 * 4));
+        auto* dbase = static_cast<long long*>(dev(M * 8));
+        auto* dchain = static_cast<long long*>(dev(chain.size() * 8));
+        auto* dcl = static_cast<int*>(dev(M * 4));
+        auto* dchl = static_cast<int*>(dev(M * 4));
+        tiles = static_cast<sgb::AttnTileDev*>(dev(ht.size() * sizeof(sgb::AttnTileDev)));
+        sc = sgb::AttnScratch{pacc, pml, nullptr, static_cast<long long>(M) * H};
+        sc.row_ctr = static_cast<int*>(dev(sc.ctr_cap * 4));
+        SGB_CUDA(cudaMemset(sc.row_ctr, 0, sc.ctr_cap * 4));
+        SGB_CUDA(cudaMemcpy(dbase, base.data(), M * 8, cudaMemcpyHostToDevice));
+        SGB_CUDA(cudaMemcpy(dchain, chain.data(), chain.size() * 8, cudaMemcpyHostToDevice));
+        SGB_CUDA(cudaMemcpy(dcl, cl.data(), M * 4, cudaMemcpyHostToDevice));
+        SGB_CUDA(cudaMemcpy(dchl, chl.data(), M * 4, cudaMemcpyHostToDevice));
+        SGB_CUDA(cudaMemcpy(tiles, ht.data(), ht.size() * sizeof(sgb::AttnTileDev), cudaMemcpyHostToDevice));
+        ar = sgb::AttnRowsDev{dbase, dcl, dchl, dchain};
+    }
+    ~TreeAttnCase() {
+        for (void* p : ptrs) cudaFree(p);
+    }
+    void run_row() { sgb::launch_attention(q, K, V, ar, M, H, d, max_vlen, keys, sc, o1, 0); }
+    void run_group() { sgb::launch_attention_group(q, K, V, ar, tiles, n_tiles, items, H, d, max_vlen, sc, o2, 0); }
+    void read(const __nv_bfloat16* o, float* out) const {
+        std::vector<__nv_bfloat16> ho(static_cast<size_t>(M) * d);
+        SGB_CUDA(cudaMemcpy(ho.data(), o, ho.size() * 2, cudaMemcpyDeviceToHost));
+        for (size_t i = 0; i < ho.size(); ++i) out[i] = __bfloat162float(ho[i]);
+    }
+};
+}  // namespace
+
+int sgb_debug_tree_attention(int n_groups, const int* ctx_len, const int* n_rows, const int* parent, int H, int dh,
+                             const float* q, const float* kctx, const float* vctx, const float* knode,
+                             const float* vnode, float* out_row, float* out_group) {
+    return guarded([&] {
+        if (!q) throw std::invalid_argument("debug_tree_attention: null inputs");
+        TreeAttnCase c(n_groups, ctx_len, n_rows, parent, H, dh, q, kctx, vctx, knode, vnode);
+        c.run_row();
+        c.run_group();
+        SGB_CUDA(cudaDeviceSynchronize());
+        c.read(c.o1, out_row);
+        c.read(c.o2, out_group);
+    });
+}
+
+// Tree-verify attention microbenchmark: B sequences with ctx committed keys each, an EAGLE-
+// shaped tree of N rows per sequence (node i's parent (i-1)/k, depth <= kMaxChain-1); times
+// the per-row kernel and the prefix-shared group kernel (CUDA events, default stream).
+int sgb_bench_tree_attention(int B, int N, int ctx, int H, int dh, int iters, double* ms_row, double* ms_group) {
+    return guarded([&] {
+        if (B <= 0 || N <= 0 || iters <= 0) throw std::invalid_argument("bench_tree_attention: bad shape");
+        std::vector<int> cl(B, ctx), nr(B, N), par;
+        for (int b = 0; b < B; ++b) {
+            std::vector<int> dep(N, 0);
+            for (int i = 0; i < N; ++i) {
+                int p = i == 0 ? -1 : (i - 1) / 10;
+                if (i) {
+                    while (dep[p] + 1 >= sgb::kMaxChain) p = (p - 1) / 10;
+                    dep[i] = dep[p] + 1;
+                }
+                par.push_back(p);
+            }
+        }
+        TreeAttnCase c(B, cl.data(), nr.data(), par.data(), H, dh, nullptr, nullptr, nullptr, nullptr, nullptr);
+        cudaEvent_t a, b;
+        SGB_CUDA(cudaEventCreate(&a));
+        SGB_CUDA(cudaEventCreate(&b));
+        float ms = 0.f;
+        for (int pass = 0; pass < 2; ++pass) {
+            for (int i = 0; i < 2; ++i) pass ? c.run_group() : c.run_row();
+            SGB_CUDA(cudaEventRecord(a, 0));
+            for (int i = 0; i < iters; ++i) pass ? c.run_group() : c.run_row();
+            SGB_CUDA(cudaEventRecord(b, 0));
+            SGB_CUDA(cudaEventSynchronize(b));
+            SGB_CUDA(cudaEventElapsedTime(&ms, a, b));
+            (pass ? *ms_group : *ms_row) = ms / iters;
+        }
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+    });
+}
+
 // Decode-attention microbenchmark: B sequences x H heads, each one query row attending to
 // ctx cached keys + itself (AR decode shape), KV in a [B*(ctx+1)][d] bf16 store.
 int sgb_bench_attention(int B, int ctx, int H, int dh, int iters, double* ms_out) {

@@ -8,6 +8,7 @@
 // scheduler.cpp:14-54 -- pure integer work that needs the live count B_cur) and reads back
 // one small per-sequence result vector per step.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <thread>
 #include <cmath>
@@ -292,6 +293,7 @@ void Engine::alloc_rows() {
     result_ = dalloc<int>(2 * S);
     err_ = dalloc<int>(1);
     steps_ = dalloc<StepSeqDev>(S);
+    tiles_ = dalloc<AttnTileDev>(R);
     drow_ = dalloc<int>(S * std::max(1, l_max_));
     misc_i_ = dalloc<int>(4 * R + 4 * S);
     misc_l_ = dalloc<long long>(2 * R + 2 * S);
@@ -532,6 +534,19 @@ void Engine::gemm_resid_ln(const GemmWeight& w, const GemmAct& a, int M, bool ac
     ln(M, g, b, y);
 }
 
+// Group (prefix-shared) attention pays once several rows share each prefix; SGB_ATTN_GROUP=0
+// disables it, =1 forces it for every grouped forward (tests of the bit-identity).
+static bool group_attn_enabled(int n_groups, int M) {
+    static const int mode = [] {
+        const char* v = getenv("SGB_ATTN_GROUP");
+        return v ? atoi(v) : -1;
+    }();
+    if (mode == 0 || n_groups <= 0) return false;
+    if (mode == 1) return true;
+    // measured (scripts/bench_tree_attn.py): faster from ~24 rows per prefix at 12-28 heads
+    return M >= 24 * n_groups;
+}
+
 void Engine::forward(const Fwd& f) {
     const int M = f.M, d = dims_.d, F = dims_.dff, H = dims_.heads;
     if (M <= 0) return;
@@ -557,6 +572,20 @@ void Engine::forward(const Fwd& f) {
         count();
         gemm_resid_ln(w_fuse_, act_fuse_, M, false, true, L[0].ln1_g, L[0].ln1_b, nullptr);
     }
+    // prefix-shared attention when the rows come in groups of >= kGroupMin sharing a prefix
+    int n_tiles = 0, n_items = 0;
+    if (f.groups && group_attn_enabled(static_cast<int>(f.groups->size()), M)) {
+        htiles_.clear();
+        for (const auto& g : *f.groups) {
+            const int nb = attn_splits_for(g[2]);
+            for (int o = 0; o < g[1]; o += kAttnTileRows) {
+                htiles_.push_back(AttnTileDev{g[0] + o, std::min(kAttnTileRows, g[1] - o), nb, n_items});
+                n_items += nb * H;
+            }
+        }
+        n_tiles = static_cast<int>(htiles_.size());
+        h2d(tiles_, htiles_.data(), htiles_.size(), st_);
+    }
     const size_t lstride = static_cast<size_t>(kv.n_slots) * d;
     const double attn_bytes = f.attn_kv_unique * d * 4.0 + row_bytes * 1.5;
     const double attn_flops = 4.0 * f.attn_row_keys * d;
@@ -572,7 +601,10 @@ void Engine::forward(const Fwd& f) {
         eq.d = d;
         gemm(W.qkv, act_a_, M, eq, kClsGemm, 8.0 / 3.0);
         e0 = pbeg();
-        launch_attention(q_, eq.K, eq.V, ar, M, H, d, f.max_vlen, f.attn_row_keys, asc_, att_, st_);
+        if (n_tiles)
+            launch_attention_group(q_, eq.K, eq.V, ar, tiles_, n_tiles, n_items, H, d, f.max_vlen, asc_, att_, st_);
+        else
+            launch_attention(q_, eq.K, eq.V, ar, M, H, d, f.max_vlen, f.attn_row_keys, asc_, att_, st_);
         pend(kClsAttn, e0, attn_bytes, attn_flops);
         count();
         gemm_resid_ln(W.wo, act_att_, M, true, false, W.ln2_g, W.ln2_b, nullptr);
@@ -1254,11 +1286,14 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
                     f.logits = true;
                     f.logits_out = logits_;
                     f.max_vlen = max_p + level;
+                    groups_.clear();
                     for (int i = 0; i < B; ++i)
                         if (hs[i].k && hs[i].l >= level) {
                             f.attn_kv_unique += hs[i].p + level - 1;
                             f.attn_row_keys += static_cast<double>(hs[i].k) * (hs[i].p + level - 1);
+                            groups_.push_back({drow[static_cast<size_t>(level - 2) * B + i], hs[i].k, hs[i].p + level});
                         }
+                    f.groups = &groups_;
                     forward(f);
                     res.draft_forwards++;
                     stat.draft_rows += R;
@@ -1285,10 +1320,13 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
         f.logits = true;
         f.logits_out = logits_;
         f.max_vlen = max_p + max_l + 1;
+        groups_.clear();
         for (int i = 0; i < B; ++i) {
             f.attn_kv_unique += hs[i].p + hs[i].nsel;
             f.attn_row_keys += static_cast<double>(hs[i].nsel) * (hs[i].p + 1);
+            groups_.push_back({hs[i].vrow_off, hs[i].nsel, hs[i].p + 1 + std::min(hs[i].l, hs[i].nsel - 1)});
         }
+        f.groups = &groups_;
         forward(f);
         res.target_forwards++;
         // ---- acceptance, walk, commit (scheduler.cpp:219-231)

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <array>
 #include <vector>
 
 #include "gemm.h"
@@ -188,6 +189,9 @@ class Engine {
         double attn_kv_unique = 0;  // distinct KV tokens read per layer (roofline bytes)
         double attn_row_keys = 0;   // sum over rows of keys attended (roofline flops)
         bool prefix_share = false;  // verify rows read their prompt K/V from the group leader
+        // rows sharing one committed prefix: (row0, nrows, max virtual length); when set and
+        // the groups are large enough, attention runs prefix-shared (attention_group.cu)
+        const std::vector<std::array<int, 3>>* groups = nullptr;
     };
     void forward(const Fwd& f);
     void convert_target(const float* staging);
@@ -263,6 +267,9 @@ class Engine {
     int *topk_tok_ = nullptr, *emitted_ = nullptr, *acc_rows_ = nullptr, *result_ = nullptr, *err_ = nullptr;
     double* topk_lp_ = nullptr;
     StepSeqDev* steps_ = nullptr;
+    AttnTileDev* tiles_ = nullptr;  // [max_rows] group-attention tiles of the current forward
+    std::vector<AttnTileDev> htiles_;
+    std::vector<std::array<int, 3>> groups_;
     int* drow_ = nullptr;
     int* misc_i_ = nullptr;
     long long* misc_l_ = nullptr;

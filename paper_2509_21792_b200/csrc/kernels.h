@@ -49,6 +49,15 @@ struct AttnScratch {
     long long ctr_cap;
 };
 int attn_splits_for(int max_virtual_len);
+// Prefix-shared group attention (attention_group.cu): rows [row0, row0+nrows) share one
+// (ctx_base, ctx_len, shared prompt); items [item0, item0 + nb*H) are its (block, head) work.
+constexpr int kAttnTileRows = 64;
+struct AttnTileDev {
+    int row0, nrows, nb, item0;
+};
+void launch_attention_group(const float* q, const __nv_bfloat16* K, const __nv_bfloat16* V, const AttnRowsDev& rows,
+                            const AttnTileDev* tiles, int n_tiles, int n_items, int H, int d, int max_virtual_len,
+                            const AttnScratch& sc, __nv_bfloat16* out, cudaStream_t st);
 // total_keys: sum over rows of keys attended (host estimate; only sizes the launch)
 void launch_attention(const float* q, const __nv_bfloat16* K, const __nv_bfloat16* V, const AttnRowsDev& rows, int M,
                       int H, int d, int max_virtual_len, double total_keys, const AttnScratch& sc, __nv_bfloat16* out,
