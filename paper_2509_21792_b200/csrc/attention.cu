@@ -1,38 +1,48 @@
-// Tree-masked paged-KV attention (decode / tree verify / draft expansion / prefill).
+// Tree-masked paged-KV attention on tensor cores (decode / tree verify / draft expansion /
+// prefill), one kernel for every attention row of the engine.
 //
 // Replaces the per-row, per-head scalar loop of the reference decode block
 // (include/sgrpo/tinylm.hpp:335-395): scores over [cache | ancestor pool | masked new
 // rows], softmax (nn.hpp:157-169), then P.V.
 //
-// Device formulation. Every query row carries a *virtual key sequence*: virtual index
-// v < ctx_len maps to the contiguous cache slots ctx_base+v (the committed prefix), and
-// ctx_len <= v < ctx_len+chain_len maps to chain_slots[v-ctx_len] (the row's own tree
-// path: ancestors root-first, then itself). The virtual index equals the absolute
-// position (target) or position-1 (draft cache), so a tree row and the AR row for the
-// same token see the *same* key sequence in the same order -- the tree mask of
-// build_tree_mask (drafttree.cpp:145-168) is exactly "keys = ancestors-or-self".
+// Rows. Every query row carries a *virtual key sequence*: virtual index v < ctx_len maps to
+// the contiguous cache slots ctx_base+v (the committed prefix; v < pre_len reads the group
+// leader's shared prompt copy), and ctx_len <= v < ctx_len+chain_len maps to
+// chain_slots[v-ctx_len] (the row's own tree path: ancestors root-first, then itself). The
+// virtual index equals the absolute position (target) or position-1 (draft cache), so a
+// tree row and the AR row of the same token see the same keys in the same order -- the tree
+// mask of build_tree_mask (drafttree.cpp:145-168) is exactly "keys = ancestors-or-self".
+//
+// Tiles. A tile is up to 8 query rows and a range of 64-key blocks. Rows of one tile share
+// every key of those blocks: either one row (the AR / prefill / boundary case) or up to 8
+// verify rows of one sequence over the blocks that lie entirely inside its committed prefix
+// (build_attn_tiles). So the tree rows of a sequence stream its prefix once per 8 rows
+// instead of once per row, and the blocks that reach into the tree path run per row.
 //
 // Kernel (B200): persistent and flat. The work of a launch is the list of items
-// (row, head group, 64-key block), rows in order; CTA c takes the contiguous slice
-// [c*T/G, (c+1)*T/G) of it, so every CTA streams the same number of blocks (+-1) whatever
-// the mix of context lengths, and its shared-memory ring never drains between rows. The K
-// and V rows of a KPC-key chunk are contiguous in the store ([slot][d], heads interleaved
-// as in the reference): with all heads in one item a chunk is ONE bulk DMA
-// (cp.async.bulk, mbarrier completion); at small batch the heads are split into groups so
-// the launch still covers the SMs, and each key row of the group is its own bulk copy.
-// Tree-path keys come from the scratch slots with one bulk copy per key. One consumer warp
-// per head (two heads per warp above 12 heads) computes dot products from smem, an online
-// softmax per chunk, and P.V with each lane owning DH/32 dims. The CTA that completes the
-// last block of a (row, head group) -- an atomic ticket per row -- merges the row's block
-// partials in block order and writes the bf16 output: no separate combine launch.
+// (tile, head group, 64-key block), tiles in order; CTA c takes the contiguous slice
+// [c*T/G, (c+1)*T/G), so every CTA streams the same number of blocks whatever the context
+// mix, and its shared-memory ring never drains between tiles. A producer warp stages each
+// 16-key chunk (K and V rows of the head group, one cp.async.bulk per key row into padded
+// rows: conflict-free ldmatrix). One consumer warp per head runs the chunk on the tensor
+// cores with mma.sync.m16n8k16 (bf16 in, fp32 accumulate):
+//   S^T[16 keys][8 queries] = K[16][dh] . Q^T[dh][8]          (dh/16 mma, keys in M)
+//   online softmax per query column (running max / sum over the chunk, quad shuffles)
+//   P^T -> bf16, transposed in registers with movmatrix into the B fragment
+//   O^T[dh][8] += V^T[dh][16] . P^T[16][8]                      (dh/16 mma, ldmatrix.trans)
+// Each 64-key block yields its own partial (m, l, O) from a fresh state; the warp that
+// completes a (row, head group) -- an atomic ticket per row -- merges the row's block
+// partials in block order and writes the bf16 output (no combine launch).
 //
-// Determinism / batch invariance (SURVEY.md §7 hard part 1): every 64-key block yields
-// its own partial (m, l, acc) from a fresh state, with chunk boundaries fixed in virtual
-// index; the merge runs strictly in block order. How the blocks are spread over CTAs and
-// heads over groups (launch-shape choices) never changes the bits, so the AR and the tree
-// rows of the same token produce identical outputs.
+// Determinism / batch invariance (SURVEY.md §7 hard part 1). Key slot j of a chunk is
+// virtual index 16c+j in every tile; an mma output element depends only on its own row of
+// A and column of B (scripts/probes/probe_mma.cu: bit-identical under any permutation of
+// the other rows / columns), so a query's scores, probabilities and P.V sums are the same
+// bits whichever tile column it occupies and whatever the other queries are. Block
+// partials merge strictly in block order. Hence a tree row, the AR row of the same token,
+// and a row run alone or in any batch produce identical outputs (spec == AR rollouts).
 //
-// Roofline: HBM-bound on K/V reads, 4*d bytes per key per layer.
+// Roofline: HBM-bound on K/V reads, 4*d bytes per key per layer per tile.
 #include <algorithm>
 #include <cstdlib>
 #include <cfloat>
@@ -46,7 +56,13 @@ namespace sgb {
 
 namespace {
 
-constexpr int kBlock = kAttnBlock;
+constexpr int kBlock = kAttnBlock;  // 64 keys per softmax partial
+constexpr int kChunk = 16;          // keys per stage = one mma k-step of P.V
+constexpr int kQT = kAttnTileRows;  // 8 queries per tile = mma N
+constexpr int kSmemBudget = 227 * 1024;
+constexpr int kMaxScanTiles = 1 << 20;
+constexpr int kMaxCons = 16;                // consumer warps per CTA
+constexpr int kMaxTileRows = kQT * kMaxCons;  // rows of one shared tile
 
 SGB_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -54,45 +70,80 @@ SGB_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar)
                  "l"(src), "r"(bytes), "r"(smem_u32(bar))
                  : "memory");
 }
-
-constexpr int kMaxScanRows = 1 << 20;
-constexpr int kSmemBudget = 227 * 1024;
-
-struct ItemIt {
-    int r, g, b, nb;
-};
-
-__device__ __forceinline__ int row_blocks(const AttnRowsDev& rows, int r) {
-    return (rows.ctx_len[r] + rows.chain_len[r] + kBlock - 1) / kBlock;
+SGB_DEV void ldsm_x4(uint32_t addr, uint32_t* r) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(addr));
+}
+SGB_DEV void ldsm_x4_t(uint32_t addr, uint32_t* r) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(addr));
+}
+SGB_DEV uint32_t movm_t(uint32_t x) {
+    uint32_t y;
+    asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
+    return y;
+}
+SGB_DEV void mma16816(float* d, const uint32_t* a, uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+SGB_DEV uint32_t pack_bf16(float lo, float hi) {
+    const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<const uint32_t*>(&v);
 }
 
-// KPC keys per chunk (fixed per d), HPW heads per consumer warp.
-template <int DH, int KPC, int HPW>
-__global__ void __launch_bounds__(HPW == 1 ? 416 : 544, HPW == 1 ? 2 : 1)  // consumers + producer
+// one tile of the launch: explicit (host-built) or implicit (tile i = row i, all its blocks)
+struct TileView {
+    const AttnTileDev* tiles;
+    const int* ctx_len;
+    const int* chain_len;
+    __device__ int row_blocks(int r) const { return (ctx_len[r] + chain_len[r] + kBlock - 1) / kBlock; }
+    __device__ AttnTileDev get(int t) const {
+        if (tiles) return tiles[t];
+        return AttnTileDev{t, 1, 0, row_blocks(t)};
+    }
+};
+
+struct ItemIt {
+    int t, g, b;
+    AttnTileDev tl;
+    int lv;  // virtual length of the tile's first row (1-row tiles: the row's key count)
+};
+
+template <int DH>
+__global__ void __launch_bounds__(32 * (kMaxCons + 1), 1)
     attn_kernel(const float* __restrict__ q, const __nv_bfloat16* __restrict__ K, const __nv_bfloat16* __restrict__ V,
-                AttnRowsDev rows, int M, int H, int d, int G, int nst, int nb_max, float scale,
-                float* __restrict__ part_acc, float* __restrict__ part_ml, int* __restrict__ row_ctr,
-                __nv_bfloat16* __restrict__ out) {
-    constexpr int PL = DH / 32;      // P.V dims per lane
-    constexpr int LPR = DH / 16;     // lanes per key row in the score pass (16 dims = 32 B each)
-    constexpr int RPI = 32 / LPR;    // key rows per score instruction
-    constexpr int NIT = KPC / RPI;   // score instructions per chunk
+                AttnRowsDev rows, const AttnTileDev* __restrict__ tiles, int n_tiles, int H, int d, int G, int QW,
+                int nst, int nb_max, float scale, float* __restrict__ part_acc, float* __restrict__ part_ml,
+                int* __restrict__ row_ctr, __nv_bfloat16* __restrict__ out) {
+    constexpr int NK = DH / 16;   // mma k-steps of S (dims) = m-tiles of O (dims)
+    constexpr int DPL = DH / 32;  // merge: dims per lane
     extern __shared__ __align__(128) uint8_t smem[];
-    const int HG = H / G;            // heads per item
-    const int wd = HG * DH;          // item width (elements)
-    const size_t kv_bytes = static_cast<size_t>(KPC) * wd * 2;  // one of K or V per stage
-    __nv_bfloat16* Ks = reinterpret_cast<__nv_bfloat16*>(smem);
-    __nv_bfloat16* Vs = reinterpret_cast<__nv_bfloat16*>(smem + nst * kv_bytes);
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + 2 * nst * kv_bytes);
+    const int HG = H / G;                                            // heads per item
+    // consumer warp w: head w % HG, query tile w / HG (8 queries each, QW per item)
+    const int rowb = HG * DH * 2 + 16;                               // padded staged key row (bytes)
+    const size_t stage_bytes = static_cast<size_t>(kChunk) * rowb;  // one of K or V per stage
+    uint8_t* Ks = smem;
+    uint8_t* Vs = smem + nst * stage_bytes;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + 2 * nst * stage_bytes);
     uint64_t* empty = full + nst;
-    int* flag = reinterpret_cast<int*>(empty + nst);
-    int* tsum = flag + 4;                 // [blockDim.x + 1]
-    int* loc = tsum + blockDim.x + 1;     // [2] start row, start block offset
+    int* flag = reinterpret_cast<int*>(empty + nst);  // [kMaxTileRows]
+    int* tsum = flag + kMaxTileRows;                   // [blockDim.x + 1]
+    int* loc = tsum + blockDim.x + 1;                  // [2] start tile, start item offset
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int n_cons = (HG + HPW - 1) / HPW;
+    const int n_cons = HG * QW;
     const int nthr = blockDim.x;
 
+    // stale smem may hold any bit pattern; key rows past a chunk's end meet p = 0 in the
+    // P.V mma, so they must be finite: zero the ring once (later chunks leave real K/V)
+    for (size_t o = threadIdx.x * 16; o < 2 * nst * stage_bytes; o += nthr * 16)
+        *reinterpret_cast<uint4*>(smem + o) = make_uint4(0, 0, 0, 0);
     if (threadIdx.x == 0) {
         for (int s = 0; s < nst; ++s) {
             mbar_init(&full[s], 1);
@@ -100,14 +151,19 @@ __global__ void __launch_bounds__(HPW == 1 ? 416 : 544, HPW == 1 ? 2 : 1)  // co
         }
         fence_barrier_init();
     }
-    // PDL: barrier setup overlapped the previous kernel; row metadata is produced by it
+    fence_proxy_async();
+    // PDL: setup overlapped the previous kernel; row metadata and q are produced by it
     pdl_wait();
     pdl_trigger();
-    // ---- block counts per thread slice of rows [t*per, (t+1)*per), exclusive scan over slices
-    const int per = (M + nthr - 1) / nthr;
-    const int r0 = min(M, static_cast<int>(threadIdx.x) * per), r1 = min(M, r0 + per);
+    const TileView tv{tiles, rows.ctx_len, rows.chain_len};
+    // ---- item counts per thread slice of tiles, exclusive scan over slices
+    const int per = (n_tiles + nthr - 1) / nthr;
+    const int t0 = min(n_tiles, static_cast<int>(threadIdx.x) * per), t1 = min(n_tiles, t0 + per);
     int own = 0;
-    for (int r = r0; r < r1; ++r) own += row_blocks(rows, r);
+    for (int t = t0; t < t1; ++t) {
+        const AttnTileDev tl = tv.get(t);
+        own += tl.bhi - tl.blo;
+    }
     tsum[threadIdx.x] = own;
     __syncthreads();
     if (warp == 0) {
@@ -133,14 +189,14 @@ __global__ void __launch_bounds__(HPW == 1 ? 416 : 544, HPW == 1 ? 2 : 1)  // co
     const long long i0 = T * blockIdx.x / gridDim.x, i1 = T * (blockIdx.x + 1) / gridDim.x;
     if (i0 >= i1) return;
     {
-        // the slice holding item i0 walks its rows to find it
         const long long s0 = static_cast<long long>(G) * tsum[threadIdx.x];
         if (own > 0 && s0 <= i0 && i0 < s0 + static_cast<long long>(G) * own) {
             long long c = s0;
-            for (int r = r0; r < r1; ++r) {
-                const long long n = static_cast<long long>(G) * row_blocks(rows, r);
+            for (int t = t0; t < t1; ++t) {
+                const AttnTileDev tl = tv.get(t);
+                const long long n = static_cast<long long>(G) * (tl.bhi - tl.blo);
                 if (i0 < c + n) {
-                    loc[0] = r;
+                    loc[0] = t;
                     loc[1] = static_cast<int>(i0 - c);
                     break;
                 }
@@ -150,72 +206,69 @@ __global__ void __launch_bounds__(HPW == 1 ? 416 : 544, HPW == 1 ? 2 : 1)  // co
     }
     __syncthreads();
     ItemIt it0;
-    it0.r = loc[0];
-    it0.nb = row_blocks(rows, it0.r);
-    it0.g = loc[1] / it0.nb;
-    it0.b = loc[1] % it0.nb;
+    it0.t = loc[0];
+    it0.tl = tv.get(it0.t);
+    it0.lv = rows.ctx_len[it0.tl.row0] + rows.chain_len[it0.tl.row0];
+    {
+        const int nbt = it0.tl.bhi - it0.tl.blo;
+        it0.g = loc[1] / nbt;
+        it0.b = it0.tl.blo + loc[1] % nbt;
+    }
     const int n_items = static_cast<int>(i1 - i0);
     auto advance = [&](ItemIt& x) {
-        if (++x.b == x.nb) {
-            x.b = 0;
+        if (++x.b == x.tl.bhi) {
             if (++x.g == G) {
                 x.g = 0;
-                ++x.r;
-                if (x.r < M) x.nb = row_blocks(rows, x.r);
+                ++x.t;
+                if (x.t < n_tiles) {
+                    x.tl = tv.get(x.t);
+                    x.lv = rows.ctx_len[x.tl.row0] + rows.chain_len[x.tl.row0];
+                }
             }
+            x.b = x.tl.blo;
         }
+    };
+    // the keys of item x: virtual [64b, v_end); v_end <= 64b when the row has no such block
+    auto item_end = [&](const ItemIt& x) -> int {
+        const int kb = x.b * kBlock;
+        if (x.tl.nrows > 1) return kb + kBlock;  // shared blocks lie inside the committed prefix
+        return min(kb + kBlock, x.lv);
     };
 
     if (warp == n_cons) {
-        // ---------------- producer warp: bulk DMA of K/V chunks into the smem ring
+        // ---------------- producer warp: one bulk DMA per staged K / V key row
         ItemIt x = it0;
         int i = 0;
-        const uint32_t row_bytes = static_cast<uint32_t>(wd) * 2;
+        const uint32_t row_bytes = static_cast<uint32_t>(HG) * DH * 2;
+        int cur_r = -1, ctx_len = 0, pre_len = 0;
+        long long ctx_base = 0, pre_base = 0;
+        const long long* chain = nullptr;
         for (int n = 0; n < n_items; ++n, advance(x)) {
-            const int ctx_len = rows.ctx_len[x.r];
-            const int Lv = ctx_len + rows.chain_len[x.r];
-            const long long ctx_base = rows.ctx_base[x.r];
-            const long long* chain = rows.chain_slots + static_cast<size_t>(x.r) * kMaxChain;
-            const int pre_len = rows.pre_len ? rows.pre_len[x.r] : 0;
-            const long long pre_base = rows.pre_len ? rows.pre_base[x.r] : 0;
-            const int kb = x.b * kBlock, ke = min(Lv, kb + kBlock);
-            const size_t col = static_cast<size_t>(x.g) * wd;
-            for (int v0 = kb; v0 < ke; v0 += KPC, ++i) {
+            const int r = x.tl.row0;
+            const int ve = item_end(x);
+            if (r != cur_r) {
+                cur_r = r;
+                ctx_len = rows.ctx_len[r];
+                ctx_base = rows.ctx_base[r];
+                chain = rows.chain_slots + static_cast<size_t>(r) * kMaxChain;
+                pre_len = rows.pre_len ? rows.pre_len[r] : 0;
+                pre_base = rows.pre_len ? rows.pre_base[r] : 0;
+            }
+            const size_t col = static_cast<size_t>(x.g) * HG * DH;
+            for (int v0 = x.b * kBlock; v0 < ve; v0 += kChunk, ++i) {
                 const int s = i % nst;
                 if (i >= nst) mbar_wait(&empty[s], ((i / nst) & 1) ^ 1);
-                const int v1 = min(ke, v0 + KPC);
-                const int nk = v1 - v0;
-                const int nctx = max(0, min(v1, ctx_len) - v0);
+                const int nk = min(kChunk, ve - v0);
                 if (lane == 0) mbar_arrive_expect_tx(&full[s], 2u * row_bytes * nk);
                 __syncwarp();
-                __nv_bfloat16* kd = Ks + static_cast<size_t>(s) * KPC * wd;
-                __nv_bfloat16* vd = Vs + static_cast<size_t>(s) * KPC * wd;
-                if (G == 1) {
-                    if (lane == 0 && nctx > 0) {
-                        // prompt keys from the group's shared copy, the rest from the row's region
-                        const int npre = max(0, min(nctx, pre_len - v0));
-                        if (npre > 0) {
-                            const size_t src = static_cast<size_t>(pre_base + v0) * d;
-                            bulk_g2s(kd, K + src, row_bytes * npre, &full[s]);
-                            bulk_g2s(vd, V + src, row_bytes * npre, &full[s]);
-                        }
-                        if (nctx > npre) {
-                            const size_t src = static_cast<size_t>(ctx_base + v0 + npre) * d;
-                            bulk_g2s(kd + static_cast<size_t>(npre) * wd, K + src, row_bytes * (nctx - npre), &full[s]);
-                            bulk_g2s(vd + static_cast<size_t>(npre) * wd, V + src, row_bytes * (nctx - npre), &full[s]);
-                        }
-                    }
-                    if (lane >= nctx && lane < nk) {
-                        const size_t src = static_cast<size_t>(chain[v0 + lane - ctx_len]) * d;
-                        bulk_g2s(kd + static_cast<size_t>(lane) * wd, K + src, row_bytes, &full[s]);
-                        bulk_g2s(vd + static_cast<size_t>(lane) * wd, V + src, row_bytes, &full[s]);
-                    }
-                } else if (lane < nk) {
-                    const long long slot = lane < nctx ? (v0 + lane < pre_len ? pre_base : ctx_base) + v0 + lane
-                                                       : chain[v0 + lane - ctx_len];
+                if (lane < nk) {
+                    const int v = v0 + lane;
+                    const long long slot = v < ctx_len ? (v < pre_len ? pre_base : ctx_base) + v : chain[v - ctx_len];
                     const size_t src = static_cast<size_t>(slot) * d + col;
-                    bulk_g2s(kd + static_cast<size_t>(lane) * wd, K + src, row_bytes, &full[s]);
-                    bulk_g2s(vd + static_cast<size_t>(lane) * wd, V + src, row_bytes, &full[s]);
+                    bulk_g2s(Ks + static_cast<size_t>(s) * stage_bytes + static_cast<size_t>(lane) * rowb, K + src,
+                             row_bytes, &full[s]);
+                    bulk_g2s(Vs + static_cast<size_t>(s) * stage_bytes + static_cast<size_t>(lane) * rowb, V + src,
+                             row_bytes, &full[s]);
                 }
             }
         }
@@ -223,258 +276,313 @@ __global__ void __launch_bounds__(HPW == 1 ? 416 : 544, HPW == 1 ? 2 : 1)  // co
     }
     if (warp > n_cons) return;
 
-    // ---------------- consumer warps: warp w owns local heads w*HPW .. +HPW-1 of the group
-    const int piece = lane % LPR, sub = lane / LPR;
-    float qreg[HPW][16];
-    float m[HPW], l[HPW], acc[HPW][PL];
+    // ---------------- consumer warps: head hl, query tile qt (rows 8qt .. 8qt+7 of the tile)
+    const int hl = warp % HG, qt = warp / HG;
+    const int g8 = lane >> 2, t4 = lane & 3;
+    // ldmatrix lane addresses (bytes within a stage): K as A of S^T (key = lane%8 + 8*(i&1),
+    // dim 8*(i>>1)), V as A of O^T via .trans (key = lane%8 + 8*(i>>1), dim 8*(i&1))
+    const int li = lane >> 3, lr = lane & 7;
+    const uint32_t k_lane = static_cast<uint32_t>((lr + 8 * (li & 1)) * rowb + (hl * DH + 8 * (li >> 1)) * 2);
+    const uint32_t v_lane = static_cast<uint32_t>((lr + 8 * (li >> 1)) * rowb + (hl * DH + 8 * (li & 1)) * 2);
+    const uint32_t ks_base = smem_u32(Ks), vs_base = smem_u32(Vs);
+    uint32_t qf[NK][2];
     ItemIt x = it0;
-    int i = 0, seg_blocks = 0;
-    int cur_r = -1, cur_g = -1;
+    int i = 0;
+    int cur_t = -1, cur_g = -1;
     for (int n = 0; n < n_items; ++n) {
-        const int ctx_len = rows.ctx_len[x.r];
-        const int Lv = ctx_len + rows.chain_len[x.r];
-        const int kb = x.b * kBlock, ke = min(Lv, kb + kBlock);
-        if (x.r != cur_r || x.g != cur_g) {
-            cur_r = x.r;
+        const int ve = item_end(x);
+        const int kb = x.b * kBlock;
+        const int h = x.g * HG + hl;
+        const int qrow0 = x.tl.row0 + kQT * qt;                      // this warp's first query row
+        const int nrows = max(0, min(kQT, x.tl.nrows - kQT * qt));  // its real query columns
+        if (x.t != cur_t || x.g != cur_g) {
+            cur_t = x.t;
             cur_g = x.g;
-            seg_blocks = 0;
+            // Q^T as the B operand: query column g8 (tile row, clamped), dims 16ks + {2t, 2t+1, 2t+8, 2t+9}
+            const int qrow = nrows > 0 ? qrow0 + min(g8, nrows - 1) : x.tl.row0;
+            const float* qr = q + static_cast<size_t>(qrow) * d + h * DH + 2 * t4;
 #pragma unroll
-            for (int hh = 0; hh < HPW; ++hh) {
-                const int hl = min(warp * HPW + hh, HG - 1);
-                const float* qrow = q + static_cast<size_t>(x.r) * d + x.g * wd + hl * DH;
-#pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                    const float4 a = *reinterpret_cast<const float4*>(qrow + piece * 16 + 4 * t);
-                    qreg[hh][4 * t] = a.x;
-                    qreg[hh][4 * t + 1] = a.y;
-                    qreg[hh][4 * t + 2] = a.z;
-                    qreg[hh][4 * t + 3] = a.w;
-                }
+            for (int ks = 0; ks < NK; ++ks) {
+                const float2 a = __ldg(reinterpret_cast<const float2*>(qr + 16 * ks));
+                const float2 b = __ldg(reinterpret_cast<const float2*>(qr + 16 * ks + 8));
+                qf[ks][0] = pack_bf16(a.x, a.y);
+                qf[ks][1] = pack_bf16(b.x, b.y);
             }
         }
+        if (ve > kb) {
+            float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;  // query columns 2t4, 2t4+1
+            float o[NK][4];
 #pragma unroll
-        for (int hh = 0; hh < HPW; ++hh) {
-            m[hh] = -INFINITY;
-            l[hh] = 0.f;
+            for (int mt = 0; mt < NK; ++mt) o[mt][0] = o[mt][1] = o[mt][2] = o[mt][3] = 0.f;
+            for (int v0 = kb; v0 < ve; v0 += kChunk, ++i) {
+                const int s = i % nst;
+                mbar_wait(&full[s], (i / nst) & 1);
+                const uint32_t kst = ks_base + static_cast<uint32_t>(s * stage_bytes);
+                const uint32_t vst = vs_base + static_cast<uint32_t>(s * stage_bytes);
+                // S^T = K . Q^T
+                float sc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-            for (int e = 0; e < PL; ++e) acc[hh][e] = 0.f;
-        }
-        for (int v0 = kb; v0 < ke; v0 += KPC, ++i) {
-            const int s = i % nst;
-            const int nvalid = min(KPC, ke - v0);
-            mbar_wait(&full[s], (i / nst) & 1);
-            const __nv_bfloat16* kc = Ks + static_cast<size_t>(s) * KPC * wd;
-            const __nv_bfloat16* vc = Vs + static_cast<size_t>(s) * KPC * wd;
-#pragma unroll
-            for (int hh = 0; hh < HPW; ++hh) {
-                const int hl = warp * HPW + hh;
-                if (hl >= HG) break;
-                // scores: RPI key rows per iteration, each lane a 16-dim slice (two LDS.128),
-                // LPR-lane butterfly, one shuffle hands key j's score to lane j
-                float sc = -INFINITY;
-#pragma unroll
-                for (int t = 0; t < NIT; ++t) {
-                    const int key = t * RPI + sub;
-                    const __nv_bfloat16* kr = kc + static_cast<size_t>(key) * wd + hl * DH + piece * 16;
-                    const uint4 u0 = *reinterpret_cast<const uint4*>(kr);
-                    const uint4 u1 = *reinterpret_cast<const uint4*>(kr + 8);
-                    const __nv_bfloat162* b0 = reinterpret_cast<const __nv_bfloat162*>(&u0);
-                    const __nv_bfloat162* b1 = reinterpret_cast<const __nv_bfloat162*>(&u1);
-                    float dot = 0.f;
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const float2 f = __bfloat1622float2(b0[e]);
-                        dot = fmaf(qreg[hh][2 * e], f.x, dot);
-                        dot = fmaf(qreg[hh][2 * e + 1], f.y, dot);
-                    }
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const float2 f = __bfloat1622float2(b1[e]);
-                        dot = fmaf(qreg[hh][8 + 2 * e], f.x, dot);
-                        dot = fmaf(qreg[hh][8 + 2 * e + 1], f.y, dot);
-                    }
-#pragma unroll
-                    for (int o = LPR / 2; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-                    const float dr = __shfl_sync(0xffffffffu, dot, (lane % RPI) * LPR);
-                    if (lane / RPI == t && lane < nvalid) sc = attn_scale(dr, scale);
+                for (int ks = 0; ks < NK; ++ks) {
+                    uint32_t a[4];
+                    ldsm_x4(kst + k_lane + ks * 32, a);
+                    mma16816(sc, a, qf[ks][0], qf[ks][1]);
                 }
-                const float cm = warp_max(sc);
-                const float nm = fmaxf(m[hh], cm);
-                const float alpha = attn_alpha(m[hh], nm);
-                const float p = (lane < nvalid) ? attn_p(sc, nm) : 0.f;
-                l[hh] = attn_l(l[hh], alpha, warp_sum(p));
+                const bool va = v0 + g8 < ve, vb = v0 + g8 + 8 < ve;
+                const float s0 = va ? attn_scale(sc[0], scale) : -INFINITY;  // key g8,   query 2t
+                const float s1 = va ? attn_scale(sc[1], scale) : -INFINITY;  // key g8,   query 2t+1
+                const float s2 = vb ? attn_scale(sc[2], scale) : -INFINITY;  // key g8+8, query 2t
+                const float s3 = vb ? attn_scale(sc[3], scale) : -INFINITY;  // key g8+8, query 2t+1
+                float c0 = fmaxf(s0, s2), c1 = fmaxf(s1, s3);
 #pragma unroll
-                for (int e = 0; e < PL; ++e) acc[hh][e] = __fmul_rn(acc[hh][e], alpha);
-                m[hh] = nm;
+                for (int o2 = 4; o2 < 32; o2 <<= 1) {
+                    c0 = fmaxf(c0, __shfl_xor_sync(0xffffffffu, c0, o2));
+                    c1 = fmaxf(c1, __shfl_xor_sync(0xffffffffu, c1, o2));
+                }
+                const float n0 = fmaxf(m0, c0), n1 = fmaxf(m1, c1);
+                const float a0 = attn_alpha(m0, n0), a1 = attn_alpha(m1, n1);
+                const float p0 = va ? attn_p(s0, n0) : 0.f, p1 = va ? attn_p(s1, n1) : 0.f;
+                const float p2 = vb ? attn_p(s2, n0) : 0.f, p3 = vb ? attn_p(s3, n1) : 0.f;
+                float ps0 = __fadd_rn(p0, p2), ps1 = __fadd_rn(p1, p3);
 #pragma unroll
-                for (int j = 0; j < KPC; ++j) {
-                    const float pj = __shfl_sync(0xffffffffu, p, j);
-                    if (j < nvalid) {
-                        const __nv_bfloat16* vr = vc + static_cast<size_t>(j) * wd + hl * DH + lane * PL;
-                        if constexpr (PL == 4) {
-                            const uint2 u = *reinterpret_cast<const uint2*>(vr);
-                            const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
-                            const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
-                            acc[hh][0] = fmaf(pj, a.x, acc[hh][0]);
-                            acc[hh][1] = fmaf(pj, a.y, acc[hh][1]);
-                            acc[hh][2] = fmaf(pj, b.x, acc[hh][2]);
-                            acc[hh][3] = fmaf(pj, b.y, acc[hh][3]);
-                        } else {
+                for (int o2 = 4; o2 < 32; o2 <<= 1) {
+                    ps0 = __fadd_rn(ps0, __shfl_xor_sync(0xffffffffu, ps0, o2));
+                    ps1 = __fadd_rn(ps1, __shfl_xor_sync(0xffffffffu, ps1, o2));
+                }
+                l0 = attn_l(l0, a0, ps0);
+                l1 = attn_l(l1, a1, ps1);
+                m0 = n0;
+                m1 = n1;
+                // V fragments first: the stage is released before the P.V math
+                uint32_t va4[NK][4];
 #pragma unroll
-                            for (int e = 0; e < PL; e += 2) {
-                                const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(vr + e));
-                                acc[hh][e] = fmaf(pj, a.x, acc[hh][e]);
-                                acc[hh][e + 1] = fmaf(pj, a.y, acc[hh][e + 1]);
-                            }
-                        }
+                for (int mt = 0; mt < NK; ++mt) ldsm_x4_t(vst + v_lane + mt * 32, va4[mt]);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[s]);
+                // P^T as the B operand: [key][query] fragments transposed to [query][key]
+                const uint32_t b0 = movm_t(pack_bf16(p0, p1)), b1 = movm_t(pack_bf16(p2, p3));
+#pragma unroll
+                for (int mt = 0; mt < NK; ++mt) {
+                    o[mt][0] = __fmul_rn(o[mt][0], a0);
+                    o[mt][1] = __fmul_rn(o[mt][1], a1);
+                    o[mt][2] = __fmul_rn(o[mt][2], a0);
+                    o[mt][3] = __fmul_rn(o[mt][3], a1);
+                    mma16816(o[mt], va4[mt], b0, b1);
+                }
+            }
+            // publish the block partial of every real query column
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const int qc = 2 * t4 + c;
+                if (qc < nrows) {
+                    const int r = qrow0 + qc;
+                    const size_t pidx = (static_cast<size_t>(r) * nb_max + x.b) * H + h;
+                    float* pa = part_acc + pidx * DH;
+#pragma unroll
+                    for (int mt = 0; mt < NK; ++mt) {
+                        pa[16 * mt + g8] = o[mt][c];
+                        pa[16 * mt + g8 + 8] = o[mt][2 + c];
+                    }
+                    if (g8 == 0) {
+                        part_ml[2 * pidx] = c ? m1 : m0;
+                        part_ml[2 * pidx + 1] = c ? l1 : l0;
                     }
                 }
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[s]);
         }
-        // end of the 64-key block: publish its partial
-#pragma unroll
-        for (int hh = 0; hh < HPW; ++hh) {
-            const int hl = warp * HPW + hh;
-            if (hl >= HG) break;
-            const size_t pidx = (static_cast<size_t>(x.r) * nb_max + x.b) * H + x.g * HG + hl;
-            float* pa = part_acc + pidx * DH + lane * PL;
-#pragma unroll
-            for (int e = 0; e < PL; ++e) pa[e] = acc[hh][e];
-            if (lane == 0) {
-                part_ml[2 * pidx] = m[hh];
-                part_ml[2 * pidx + 1] = l[hh];
-            }
-        }
-        ++seg_blocks;
         const ItemIt done = x;
         advance(x);
-        const bool seg_end = (n + 1 == n_items) || x.r != done.r || x.g != done.g;
-        if (!seg_end) continue;
-        // ---- segment end: ticket on (row, group); the completing CTA merges the row
-        __threadfence();
+        if (ve <= kb) continue;  // no keys for this (row, block): nothing published, no ticket
+        // ---- ticket per (row, head group); the CTA that completes a row merges it. The
+        // ticket thread's gpu-scope fence after the CTA barrier orders every warp's partial
+        // stores before its ticket (cumulative release, as in a grid barrier).
         asm volatile("bar.sync 1, %0;" ::"r"(n_cons * 32) : "memory");
-        if (threadIdx.x == 0) {
-            int* c = row_ctr + static_cast<size_t>(done.r) * G + done.g;
-            const int old = atomicAdd(c, seg_blocks);
-            const int last = (old + seg_blocks == done.nb);
-            if (last) *c = 0;  // re-armed for the next launch
-            *flag = last;
+        if (threadIdx.x < done.tl.nrows) {
+            __threadfence();
+            const int r = done.tl.row0 + threadIdx.x;
+            int* c = row_ctr + static_cast<size_t>(r) * G + done.g;
+            const int old = atomicAdd(c, 1);
+            const int last = (old + 1 == tv.row_blocks(r));
+            if (last) {
+                *c = 0;  // re-armed for the next launch
+                __threadfence();  // acquire side: the other CTAs' partials are read after the barrier
+            }
+            flag[threadIdx.x] = last;
         }
         asm volatile("bar.sync 1, %0;" ::"r"(n_cons * 32) : "memory");
-        if (!*flag) continue;
-        __threadfence();
-#pragma unroll
-        for (int hh = 0; hh < HPW; ++hh) {
-            const int hl = warp * HPW + hh;
-            if (hl >= HG) break;
+        int any = 0;
+        for (int j = 0; j < done.tl.nrows; ++j) any |= flag[j];
+        if (any) {
             const int h = done.g * HG + hl;
-            // merge from the identity (-inf, 0, 0): the first merge reproduces partial 0
-            // exactly, so this equals "start from block 0"; loads are batched 8 blocks at
-            // a time so the serial tail is the arithmetic, not 8 L2 round trips
-            float Mx = -INFINITY, Lx = 0.f, A[PL];
+            for (int j = qt; j < done.tl.nrows; j += QW) {
+                if (!flag[j]) continue;
+                const int r = done.tl.row0 + j;
+                const int nbr = tv.row_blocks(r);
+                // merge from the identity (-inf, 0, 0): the first merge reproduces partial 0
+                float Mx = -INFINITY, Lx = 0.f, A[DPL];
 #pragma unroll
-            for (int e0 = 0; e0 < PL; ++e0) A[e0] = 0.f;
-            constexpr int kMB = 4;
-            for (int b0 = 0; b0 < done.nb; b0 += kMB) {
-                float mb[kMB], lb[kMB], ab[kMB][PL];
+                for (int e = 0; e < DPL; ++e) A[e] = 0.f;
+                constexpr int kMB = 4;
+                for (int b0 = 0; b0 < nbr; b0 += kMB) {
+                    float mb[kMB], lb[kMB], ab[kMB][DPL];
 #pragma unroll
-                for (int u = 0; u < kMB; ++u) {
-                    const int b = min(b0 + u, done.nb - 1);
-                    const size_t pidx = (static_cast<size_t>(done.r) * nb_max + b) * H + h;
-                    mb[u] = __ldcg(part_ml + 2 * pidx);
-                    lb[u] = __ldcg(part_ml + 2 * pidx + 1);
-                    if constexpr (PL == 4) {
-                        const float4 t = __ldcg(reinterpret_cast<const float4*>(part_acc + pidx * DH + lane * PL));
-                        ab[u][0] = t.x; ab[u][1] = t.y; ab[u][2] = t.z; ab[u][3] = t.w;
-                    } else {
+                    for (int u = 0; u < kMB; ++u) {
+                        const int b = min(b0 + u, nbr - 1);
+                        const size_t pidx = (static_cast<size_t>(r) * nb_max + b) * H + h;
+                        mb[u] = __ldcg(part_ml + 2 * pidx);
+                        lb[u] = __ldcg(part_ml + 2 * pidx + 1);
 #pragma unroll
-                        for (int e0 = 0; e0 < PL; ++e0) ab[u][e0] = __ldcg(part_acc + pidx * DH + lane * PL + e0);
+                        for (int e = 0; e < DPL; ++e) ab[u][e] = __ldcg(part_acc + pidx * DH + lane * DPL + e);
                     }
+#pragma unroll
+                    for (int u = 0; u < kMB; ++u)
+                        if (b0 + u < nbr) attn_merge<DPL>(Mx, Lx, A, mb[u], lb[u], ab[u]);
                 }
 #pragma unroll
-                for (int u = 0; u < kMB; ++u) {
-                    if (b0 + u < done.nb) attn_merge<PL>(Mx, Lx, A, mb[u], lb[u], ab[u]);
-                }
-            }
-#pragma unroll
-            for (int e0 = 0; e0 < PL; ++e0) {
-                const int e = lane * PL + e0;
-                out[static_cast<size_t>(done.r) * d + h * DH + e] = __float2bfloat16(__fdiv_rn(A[e0], Lx));
+                for (int e = 0; e < DPL; ++e)
+                    out[static_cast<size_t>(r) * d + h * DH + lane * DPL + e] = __float2bfloat16(__fdiv_rn(A[e], Lx));
             }
         }
+        // flags are rewritten by the next item's ticket
+        asm volatile("bar.sync 1, %0;" ::"r"(n_cons * 32) : "memory");
     }
 }
 
-template <int DH, int KPC, int HPW>
-void launch_impl(const float* q, const __nv_bfloat16* K, const __nv_bfloat16* V, const AttnRowsDev& rows, int M,
-                 int H, int d, int G, int nb_max, long long est_items, const AttnScratch& sc, __nv_bfloat16* out,
-                 cudaStream_t st) {
-    const int HG = H / G;
-    const int wd = HG * DH;
-    const int n_cons = (HG + HPW - 1) / HPW;
-    const int threads = 32 * (n_cons + 1);
-    const size_t fixed = static_cast<size_t>(8 * 4 + 16 + 4 * (threads + 3)) + 128;
-    const size_t stage = 2 * static_cast<size_t>(KPC) * wd * 2;
-    // two CTAs per SM when two 2-stage rings fit (more warps to hide the consumers'
-    // shuffle / shared-memory latency), else one CTA with up to 4 stages
-    const int per_sm = (2 * (2 * stage + fixed) <= static_cast<size_t>(kSmemBudget)) ? 2 : 1;
-    const int nst = static_cast<int>(std::min<size_t>(4, (kSmemBudget / per_sm - fixed) / stage));
-    if (nst < 2) throw std::invalid_argument("attention: shared memory too small for the model width");
+template <int DH>
+void launch_impl(const float* q, const __nv_bfloat16* K, const __nv_bfloat16* V, const AttnRowsDev& rows, int n_rows,
+                 const AttnTileDev* tiles, int n_tiles, int QW, int H, int d, int nb_max, long long est_items,
+                 const AttnScratch& sc, __nv_bfloat16* out, cudaStream_t st) {
+    auto stage_of = [&](int G) { return 2 * static_cast<size_t>(kChunk) * ((H / G) * DH * 2 + 16); };
+    auto fixed_of = [&](int G) {
+        return static_cast<size_t>(8 * 8 + 4 * kMaxTileRows + 4 * (32 * (QW * H / G + 1) + 3)) + 128;
+    };
+    auto next_div = [&](int g) {
+        int g2 = g + 1;
+        while (H % g2) ++g2;
+        return g2;
+    };
+    static const int regs = [] {
+        cudaFuncAttributes fa{};
+        return cudaFuncGetAttributes(&fa, attn_kernel<DH>) == cudaSuccess && fa.numRegs > 0 ? fa.numRegs : 128;
+    }();
+    static const int env_sm = [] {
+        const char* v = getenv("SGB_ATTN_PERSM");  // tuning experiments only
+        return v ? atoi(v) : 0;
+    }();
+    static const int g_force = [] {
+        const char* v = getenv("SGB_ATTN_G");  // tuning experiments only
+        return v ? atoi(v) : 0;
+    }();
+    // CTAs per SM for a head grouping: shared memory for >= 2 stages each, and registers
+    auto ctas_per_sm = [&](int G) {
+        const int threads = 32 * (QW * (H / G) + 1);
+        const int by_regs = std::max(1, 65536 / (threads * ((regs + 7) / 8 * 8)));
+        int n = 0;
+        while (n < std::min(by_regs, 4) && (n + 1) * (2 * stage_of(G) + fixed_of(G)) <= static_cast<size_t>(kSmemBudget))
+            ++n;
+        return n;
+    };
+    // head groups: the grouping with the most consumer warps resident per SM (measured:
+    // decode throughput follows it, scripts/bench_attn.py), ties to fewer groups; more
+    // groups only when the launch has too few items to cover the SMs
+    int G = 0, best = -1;
+    for (int g = 1; g <= H; g = next_div(g)) {
+        if (QW * (H / g) > kMaxCons) continue;
+        const int n = ctas_per_sm(g);
+        if (n == 0) continue;
+        const int w = n * QW * (H / g);
+        if (w > best) {
+            best = w;
+            G = g;
+        }
+        if (g == H) break;
+    }
+    if (G == 0) throw std::invalid_argument("attention: shared memory too small for the model width");
+    while (G < H && est_items * G < 2 * 148 && ctas_per_sm(next_div(G)) > 0) G = next_div(G);
+    if (g_force > 0 && H % g_force == 0 && QW * (H / g_force) <= kMaxCons && ctas_per_sm(g_force) > 0) G = g_force;
+    const size_t stage = stage_of(G), fixed = fixed_of(G);
+    const int threads = 32 * (QW * (H / G) + 1);
+    int per_sm = ctas_per_sm(G);
+    if (env_sm > 0 && env_sm <= per_sm) per_sm = env_sm;
+    const int nst = static_cast<int>(std::min<size_t>(8, (kSmemBudget / per_sm - fixed) / stage));
     const size_t smem = nst * stage + fixed;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(attn_kernel<DH, KPC, HPW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(kSmemBudget));
+        cudaFuncSetAttribute(attn_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget);
         attr = true;
     }
-    const int fit = std::max(1, std::min(8, static_cast<int>(kSmemBudget / smem)));
-    const long long grid = std::max(1LL, std::min<long long>(est_items, 148LL * fit));
-    launch_pdl(attn_kernel<DH, KPC, HPW>, dim3(static_cast<unsigned>(grid)), dim3(threads), smem, st, q, K, V, rows, M,
-               H, d, G, nst, nb_max, 1.0f / sqrtf(static_cast<float>(DH)), sc.part_acc, sc.part_ml, sc.row_ctr, out);
+    if (static_cast<long long>(n_rows) * G > sc.ctr_cap) throw std::invalid_argument("attention: row tickets too small");
+    const long long grid = std::max(1LL, std::min<long long>(est_items * G, 148LL * per_sm));
+    launch_pdl(attn_kernel<DH>, dim3(static_cast<unsigned>(grid)), dim3(threads), smem, st, q, K, V, rows, tiles,
+               n_tiles, H, d, G, QW, nst, nb_max, 1.0f / sqrtf(static_cast<float>(DH)), sc.part_acc, sc.part_ml,
+               sc.row_ctr, out);
+}
+
+void launch_any(const float* q, const __nv_bfloat16* K, const __nv_bfloat16* V, const AttnRowsDev& rows, int n_rows,
+                const AttnTileDev* tiles, int n_tiles, int QW, int H, int d, int max_virtual_len, long long est_items,
+                const AttnScratch& sc, __nv_bfloat16* out, cudaStream_t st) {
+    if (n_tiles <= 0) return;
+    if (n_tiles > kMaxScanTiles) throw std::invalid_argument("attention: too many tiles in one launch");
+    if (H > 64) throw std::invalid_argument("attention: at most 64 heads");
+    const int dh = d / H;
+    const int nb = attn_splits_for(max_virtual_len);
+    if (dh == 128) launch_impl<128>(q, K, V, rows, n_rows, tiles, n_tiles, QW, H, d, nb, est_items, sc, out, st);
+    else if (dh == 64) launch_impl<64>(q, K, V, rows, n_rows, tiles, n_tiles, QW, H, d, nb, est_items, sc, out, st);
+    else throw std::invalid_argument("attention: head dim must be 64 or 128");
+    SGB_KCHECK();
 }
 
 }  // namespace
 
 int attn_splits_for(int max_virtual_len) { return (max_virtual_len + kBlock - 1) / kBlock; }
 
-void launch_attention(const float* q, const __nv_bfloat16* K, const __nv_bfloat16* V, const AttnRowsDev& rows, int M,
-                      int H, int d, int max_virtual_len, double total_keys, const AttnScratch& sc, __nv_bfloat16* out,
-                      cudaStream_t st) {
-    if (M <= 0) return;
-    if (M > kMaxScanRows) throw std::invalid_argument("attention: too many rows in one launch");
-    const int dh = d / H;
-    const int nb = attn_splits_for(max_virtual_len);
-    if (H > 32) throw std::invalid_argument("attention: at most 32 heads");
-    if (static_cast<long long>(M) * H > sc.ctr_cap) throw std::invalid_argument("attention: row tickets too small");
-    // chunk size KPC is fixed per model width; it is part of the numerics, never a
-    // function of the batch
-    const int kpc = d <= 3328 ? 8 : 4;
-    // head groups: split the heads only when the launch has too few blocks to cover the SMs
-    const long long blocks = static_cast<long long>(total_keys / kBlock) + M;
-    int G = 1;
-    while (G < H && blocks * G < 2 * 148) {
-        int g2 = G + 1;
-        while (H % g2) ++g2;
-        G = g2;
-    }
-    static const int g_force = [] {
-        const char* v = getenv("SGB_ATTN_G");  // tuning experiments only
-        return v ? atoi(v) : 0;
+int attn_tile_qw(const std::vector<std::array<int, 4>>& groups) {
+    int mx = 1;
+    for (const auto& g : groups) mx = std::max(mx, g[1]);
+    static const int cap = [] {
+        const char* v = getenv("SGB_ATTN_QW");  // tuning experiments only
+        return v ? std::max(1, std::min(kMaxCons / 2, atoi(v))) : 2;
     }();
-    if (g_force > 0 && H % g_force == 0) G = g_force;
-    const int HG = H / G;
-    const bool two = HG > 12;  // one head per warp up to 12 heads (two CTAs per SM fit)
-    const long long est = blocks * G;
-#define SGB_ATT(DH_, KPC_, HPW_) \
-    launch_impl<DH_, KPC_, HPW_>(q, K, V, rows, M, H, d, G, nb, est, sc, out, st)
-    if (dh == 128 && kpc == 8) { if (two) SGB_ATT(128, 8, 2); else SGB_ATT(128, 8, 1); }
-    else if (dh == 128 && kpc == 4) { if (two) SGB_ATT(128, 4, 2); else SGB_ATT(128, 4, 1); }
-    else if (dh == 64 && kpc == 8) { if (two) SGB_ATT(64, 8, 2); else SGB_ATT(64, 8, 1); }
-#undef SGB_ATT
-    else throw std::invalid_argument("attention: head dim must be 64 or 128");
-    SGB_KCHECK();
+    return std::min(cap, (mx + kQT - 1) / kQT);
+}
+
+long long build_attn_tiles(const std::vector<std::array<int, 4>>& groups, std::vector<AttnTileDev>& out, int qw) {
+    out.clear();
+    long long n = 0;
+    const int rows_per_tile = kQT * qw;
+    for (const auto& g : groups) {
+        const int row0 = g[0], nr = g[1], ctx_len = g[2], vmax = g[3];
+        const int nb = attn_splits_for(vmax);
+        // blocks entirely inside the committed prefix are shared by the tile's rows
+        const int nsb = nr > 1 ? std::min(nb, ctx_len / kBlock) : 0;
+        if (nsb > 0)
+            for (int o = 0; o < nr; o += rows_per_tile) {
+                out.push_back(AttnTileDev{row0 + o, std::min(rows_per_tile, nr - o), 0, nsb});
+                n += nsb;
+            }
+        // the blocks that reach into each row's own tree path run per row
+        if (nb > nsb)
+            for (int r = 0; r < nr; ++r) {
+                out.push_back(AttnTileDev{row0 + r, 1, nsb, nb});
+                n += nb - nsb;
+            }
+    }
+    return n;
+}
+
+void launch_attention(const float* q, const __nv_bfloat16* K, const __nv_bfloat16* V, long long /*kv_slots*/,
+                      const AttnRowsDev& rows, int M, int H, int d, int max_virtual_len, double total_keys,
+                      const AttnScratch& sc, __nv_bfloat16* out, cudaStream_t st) {
+    if (M <= 0) return;
+    const long long est = static_cast<long long>(total_keys / kBlock) + M;
+    launch_any(q, K, V, rows, M, nullptr, M, 1, H, d, max_virtual_len, est, sc, out, st);
+}
+
+void launch_attention_tiles(const float* q, const __nv_bfloat16* K, const __nv_bfloat16* V, long long /*kv_slots*/,
+                            const AttnRowsDev& rows, int M, const AttnTileDev* tiles, int n_tiles, long long n_items,
+                            int qw, int H, int d, int max_virtual_len, const AttnScratch& sc, __nv_bfloat16* out,
+                            cudaStream_t st) {
+    if (M <= 0) return;
+    launch_any(q, K, V, rows, M, tiles, n_tiles, qw, H, d, max_virtual_len, n_items, sc, out, st);
 }
 
 }  // namespace sgb

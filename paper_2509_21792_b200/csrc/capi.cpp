@@ -5,6 +5,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -717,7 +718,7 @@ int sgb_debug_attention(int B, const int* n_keys, int H, int dh, const float* q,
         sgb::AttnScratch sc{pacc, pml, nullptr, static_cast<long long>(B) * H};
         SGB_CUDA(cudaMalloc(&sc.row_ctr, sc.ctr_cap * 4));
         SGB_CUDA(cudaMemset(sc.row_ctr, 0, sc.ctr_cap * 4));
-        sgb::launch_attention(dq, K, V, ar, B, H, d, maxk, keys, sc, o, 0);
+        sgb::launch_attention(dq, K, V, tot, ar, B, H, d, maxk, keys, sc, o, 0);
         SGB_CUDA(cudaDeviceSynchronize());
         std::vector<__nv_bfloat16> ho(static_cast<size_t>(B) * d);
         SGB_CUDA(cudaMemcpy(ho.data(), o, ho.size() * 2, cudaMemcpyDeviceToHost));
@@ -731,7 +732,8 @@ namespace {
 // Device state of a tree-attention case: n_groups sequences, each with ctx_len committed keys
 // and a tree of rows (level order, parent within the group) -- the verify rows of one step.
 struct TreeAttnCase {
-    int M = 0, H = 0, d = 0, max_vlen = 1, n_tiles = 0, items = 0;
+    int M = 0, H = 0, d = 0, max_vlen = 1, n_tiles = 0, qw = 1;
+    long long items = 0, n_slots = 0;
     double keys = 0;
     std::vector<void*> ptrs;
     __nv_bfloat16 *K = nullptr, *V = nullptr, *o1 = nullptr, *o2 = nullptr;
@@ -758,9 +760,11 @@ struct TreeAttnCase {
         }
         // KV store: committed keys of every group, then one node slot per row
         const long long slots = n_ctx + M;
+        n_slots = slots;
         std::vector<long long> base(M), chain(static_cast<size_t>(M) * sgb::kMaxChain, 0);
         std::vector<int> cl(M), chl(M);
         std::vector<sgb::AttnTileDev> ht;
+        std::vector<std::array<int, 4>> groups;
         long long cbase = 0;
         int row = 0;
         for (int g = 0; g < n_groups; ++g) {
@@ -781,13 +785,11 @@ struct TreeAttnCase {
                 keys += ctx_len[g] + depth[i] + 1;
             }
             max_vlen = std::max(max_vlen, gmax);
-            const int nb = sgb::attn_splits_for(gmax);
-            for (int o = 0; o < n_rows[g]; o += sgb::kAttnTileRows) {
-                ht.push_back({r0 + o, std::min(sgb::kAttnTileRows, n_rows[g] - o), nb, items});
-                items += nb * H;
-            }
+            groups.push_back({r0, n_rows[g], ctx_len[g], gmax});
             cbase += ctx_len[g];
         }
+        qw = sgb::attn_tile_qw(groups);
+        items = sgb::build_attn_tiles(groups, ht, qw);
         n_tiles = static_cast<int>(ht.size());
         const int ns = sgb::attn_splits_for(max_vlen);
         K = static_cast<__nv_bfloat16*>(dev(static_cast<size_t>(slots) * d * 2));
@@ -820,7 +822,7 @@ struct TreeAttnCase {
         auto* dcl = static_cast<int*>(dev(M * 4));
         auto* dchl = static_cast<int*>(dev(M * 4));
         tiles = static_cast<sgb::AttnTileDev*>(dev(ht.size() * sizeof(sgb::AttnTileDev)));
-        sc = sgb::AttnScratch{pacc, pml, nullptr, static_cast<long long>(M) * H};
+        sc = sgb::AttnScratch{pacc, pml, nullptr, static_cast<long long>(M) * H};  // >= rows x head groups
         sc.row_ctr = static_cast<int*>(dev(sc.ctr_cap * 4));
         SGB_CUDA(cudaMemset(sc.row_ctr, 0, sc.ctr_cap * 4));
         SGB_CUDA(cudaMemcpy(dbase, base.data(), M * 8, cudaMemcpyHostToDevice));
@@ -833,8 +835,9 @@ struct TreeAttnCase {
     ~TreeAttnCase() {
         for (void* p : ptrs) cudaFree(p);
     }
-    void run_row() { sgb::launch_attention(q, K, V, ar, M, H, d, max_vlen, keys, sc, o1, 0); }
-    void run_group() { sgb::launch_attention_group(q, K, V, ar, tiles, n_tiles, items, H, d, max_vlen, sc, o2, 0); }
+    void run_row() { sgb::launch_attention(q, K, V, n_slots, ar, M, H, d, max_vlen, keys, sc, o1, 0); }
+    void run_group() { sgb::launch_attention_tiles(q, K, V, n_slots, ar, M, tiles, n_tiles, items, qw, H, d, max_vlen, sc, o2,
+                                                    0); }
     void read(const __nv_bfloat16* o, float* out) const {
         std::vector<__nv_bfloat16> ho(static_cast<size_t>(M) * d);
         SGB_CUDA(cudaMemcpy(ho.data(), o, ho.size() * 2, cudaMemcpyDeviceToHost));
@@ -936,9 +939,9 @@ int sgb_bench_attention(int B, int ctx, int H, int dh, int iters, double* ms_out
         cudaEvent_t a, b;
         SGB_CUDA(cudaEventCreate(&a));
         SGB_CUDA(cudaEventCreate(&b));
-        for (int i = 0; i < 2; ++i) sgb::launch_attention(q, K, V, ar, B, H, d, ctx + 1, keys, sc, out, 0);
+        for (int i = 0; i < 2; ++i) sgb::launch_attention(q, K, V, slots, ar, B, H, d, ctx + 1, keys, sc, out, 0);
         SGB_CUDA(cudaEventRecord(a, 0));
-        for (int i = 0; i < iters; ++i) sgb::launch_attention(q, K, V, ar, B, H, d, ctx + 1, keys, sc, out, 0);
+        for (int i = 0; i < iters; ++i) sgb::launch_attention(q, K, V, slots, ar, B, H, d, ctx + 1, keys, sc, out, 0);
         SGB_CUDA(cudaEventRecord(b, 0));
         SGB_CUDA(cudaEventSynchronize(b));
         float ms = 0.f;

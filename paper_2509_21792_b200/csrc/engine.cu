@@ -293,7 +293,7 @@ void Engine::alloc_rows() {
     result_ = dalloc<int>(2 * S);
     err_ = dalloc<int>(1);
     steps_ = dalloc<StepSeqDev>(S);
-    tiles_ = dalloc<AttnTileDev>(R);
+    tiles_ = dalloc<AttnTileDev>(2 * R);
     drow_ = dalloc<int>(S * std::max(1, l_max_));
     misc_i_ = dalloc<int>(4 * R + 4 * S);
     misc_l_ = dalloc<long long>(2 * R + 2 * S);
@@ -534,8 +534,8 @@ void Engine::gemm_resid_ln(const GemmWeight& w, const GemmAct& a, int M, bool ac
     ln(M, g, b, y);
 }
 
-// Group (prefix-shared) attention pays once several rows share each prefix; SGB_ATTN_GROUP=0
-// disables it, =1 forces it for every grouped forward (tests of the bit-identity).
+// Shared-prefix tiles for grouped rows; SGB_ATTN_GROUP=0 runs every row alone (bit-identical,
+// for A/B timing), =1 forces tiles for every grouped forward.
 static bool group_attn_enabled(int n_groups, int M) {
     static const int mode = [] {
         const char* v = getenv("SGB_ATTN_GROUP");
@@ -543,8 +543,7 @@ static bool group_attn_enabled(int n_groups, int M) {
     }();
     if (mode == 0 || n_groups <= 0) return false;
     if (mode == 1) return true;
-    // measured (scripts/bench_tree_attn.py): faster from ~24 rows per prefix at 12-28 heads
-    return M >= 24 * n_groups;
+    return M >= 2 * n_groups;
 }
 
 void Engine::forward(const Fwd& f) {
@@ -572,18 +571,14 @@ void Engine::forward(const Fwd& f) {
         count();
         gemm_resid_ln(w_fuse_, act_fuse_, M, false, true, L[0].ln1_g, L[0].ln1_b, nullptr);
     }
-    // prefix-shared attention when the rows come in groups of >= kGroupMin sharing a prefix
-    int n_tiles = 0, n_items = 0;
+    // rows sharing a committed prefix (tree verify, draft levels): shared tiles of <= 8 rows
+    int n_tiles = 0, qw = 1;
+    long long n_items = 0;
     if (f.groups && group_attn_enabled(static_cast<int>(f.groups->size()), M)) {
-        htiles_.clear();
-        for (const auto& g : *f.groups) {
-            const int nb = attn_splits_for(g[2]);
-            for (int o = 0; o < g[1]; o += kAttnTileRows) {
-                htiles_.push_back(AttnTileDev{g[0] + o, std::min(kAttnTileRows, g[1] - o), nb, n_items});
-                n_items += nb * H;
-            }
-        }
+        qw = attn_tile_qw(*f.groups);
+        n_items = build_attn_tiles(*f.groups, htiles_, qw);
         n_tiles = static_cast<int>(htiles_.size());
+        if (n_tiles > 2 * max_rows_) throw std::logic_error("forward: attention tiles exceed capacity");
         h2d(tiles_, htiles_.data(), htiles_.size(), st_);
     }
     const size_t lstride = static_cast<size_t>(kv.n_slots) * d;
@@ -602,9 +597,10 @@ void Engine::forward(const Fwd& f) {
         gemm(W.qkv, act_a_, M, eq, kClsGemm, 8.0 / 3.0);
         e0 = pbeg();
         if (n_tiles)
-            launch_attention_group(q_, eq.K, eq.V, ar, tiles_, n_tiles, n_items, H, d, f.max_vlen, asc_, att_, st_);
+            launch_attention_tiles(q_, eq.K, eq.V, kv.n_slots, ar, M, tiles_, n_tiles, n_items, qw, H, d, f.max_vlen,
+                                   asc_, att_, st_);
         else
-            launch_attention(q_, eq.K, eq.V, ar, M, H, d, f.max_vlen, f.attn_row_keys, asc_, att_, st_);
+            launch_attention(q_, eq.K, eq.V, kv.n_slots, ar, M, H, d, f.max_vlen, f.attn_row_keys, asc_, att_, st_);
         pend(kClsAttn, e0, attn_bytes, attn_flops);
         count();
         gemm_resid_ln(W.wo, act_att_, M, true, false, W.ln2_g, W.ln2_b, nullptr);
@@ -1291,7 +1287,8 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
                         if (hs[i].k && hs[i].l >= level) {
                             f.attn_kv_unique += hs[i].p + level - 1;
                             f.attn_row_keys += static_cast<double>(hs[i].k) * (hs[i].p + level - 1);
-                            groups_.push_back({drow[static_cast<size_t>(level - 2) * B + i], hs[i].k, hs[i].p + level});
+                            groups_.push_back(
+                                {drow[static_cast<size_t>(level - 2) * B + i], hs[i].k, hs[i].p, hs[i].p + level});
                         }
                     f.groups = &groups_;
                     forward(f);
@@ -1324,7 +1321,8 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
         for (int i = 0; i < B; ++i) {
             f.attn_kv_unique += hs[i].p + hs[i].nsel;
             f.attn_row_keys += static_cast<double>(hs[i].nsel) * (hs[i].p + 1);
-            groups_.push_back({hs[i].vrow_off, hs[i].nsel, hs[i].p + 1 + std::min(hs[i].l, hs[i].nsel - 1)});
+            groups_.push_back(
+                {hs[i].vrow_off, hs[i].nsel, hs[i].p, hs[i].p + 1 + std::min(hs[i].l, hs[i].nsel - 1)});
         }
         f.groups = &groups_;
         forward(f);

@@ -189,9 +189,9 @@ class Engine {
         double attn_kv_unique = 0;  // distinct KV tokens read per layer (roofline bytes)
         double attn_row_keys = 0;   // sum over rows of keys attended (roofline flops)
         bool prefix_share = false;  // verify rows read their prompt K/V from the group leader
-        // rows sharing one committed prefix: (row0, nrows, max virtual length); when set and
-        // the groups are large enough, attention runs prefix-shared (attention_group.cu)
-        const std::vector<std::array<int, 3>>* groups = nullptr;
+        // rows sharing one committed prefix: (row0, nrows, ctx_len, max virtual length); the
+        // prefix blocks then run as shared tiles of up to 8 rows (attention.cu)
+        const std::vector<std::array<int, 4>>* groups = nullptr;
     };
     void forward(const Fwd& f);
     void convert_target(const float* staging);
@@ -267,9 +267,9 @@ class Engine {
     int *topk_tok_ = nullptr, *emitted_ = nullptr, *acc_rows_ = nullptr, *result_ = nullptr, *err_ = nullptr;
     double* topk_lp_ = nullptr;
     StepSeqDev* steps_ = nullptr;
-    AttnTileDev* tiles_ = nullptr;  // [max_rows] group-attention tiles of the current forward
+    AttnTileDev* tiles_ = nullptr;  // [2 * max_rows] attention tiles of the current forward
     std::vector<AttnTileDev> htiles_;
-    std::vector<std::array<int, 3>> groups_;
+    std::vector<std::array<int, 4>> groups_;
     int* drow_ = nullptr;
     int* misc_i_ = nullptr;
     long long* misc_l_ = nullptr;

@@ -4,7 +4,9 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <array>
 #include <cstddef>
+#include <vector>
 
 namespace sgb {
 
@@ -49,19 +51,27 @@ struct AttnScratch {
     long long ctr_cap;
 };
 int attn_splits_for(int max_virtual_len);
-// Prefix-shared group attention (attention_group.cu): rows [row0, row0+nrows) share one
-// (ctx_base, ctx_len, shared prompt); items [item0, item0 + nb*H) are its (block, head) work.
-constexpr int kAttnTileRows = 64;
+// Tiles of rows sharing keys (attention.cu): rows [row0, row0+nrows) read the same keys in
+// 64-key blocks [blo, bhi) -- one row, or up to 8*qw verify rows of one sequence over the
+// blocks inside its committed prefix (kAttnTileRows queries per mma tile).
+constexpr int kAttnTileRows = 8;
 struct AttnTileDev {
-    int row0, nrows, nb, item0;
+    int row0, nrows, blo, bhi;
 };
-void launch_attention_group(const float* q, const __nv_bfloat16* K, const __nv_bfloat16* V, const AttnRowsDev& rows,
-                            const AttnTileDev* tiles, int n_tiles, int n_items, int H, int d, int max_virtual_len,
-                            const AttnScratch& sc, __nv_bfloat16* out, cudaStream_t st);
+// groups: (row0, nrows, ctx_len, max virtual length) of rows sharing one committed prefix.
+// attn_tile_qw: 8-query tiles per CTA item for these groups; build_attn_tiles returns the
+// number of (tile, block) items of tiles of up to 8*qw rows
+int attn_tile_qw(const std::vector<std::array<int, 4>>& groups);
+long long build_attn_tiles(const std::vector<std::array<int, 4>>& groups, std::vector<AttnTileDev>& out, int qw);
+void launch_attention_tiles(const float* q, const __nv_bfloat16* K, const __nv_bfloat16* V, long long kv_slots,
+                            const AttnRowsDev& rows, int M, const AttnTileDev* tiles, int n_tiles, long long n_items,
+                            int qw, int H, int d, int max_virtual_len, const AttnScratch& sc, __nv_bfloat16* out,
+                            cudaStream_t st);
 // total_keys: sum over rows of keys attended (host estimate; only sizes the launch)
-void launch_attention(const float* q, const __nv_bfloat16* K, const __nv_bfloat16* V, const AttnRowsDev& rows, int M,
-                      int H, int d, int max_virtual_len, double total_keys, const AttnScratch& sc, __nv_bfloat16* out,
-                      cudaStream_t st);
+// K/V: one layer of a [kv_slots][d] bf16 store
+void launch_attention(const float* q, const __nv_bfloat16* K, const __nv_bfloat16* V, long long kv_slots,
+                      const AttnRowsDev& rows, int M, int H, int d, int max_virtual_len, double total_keys,
+                      const AttnScratch& sc, __nv_bfloat16* out, cudaStream_t st);
 
 // ---- sample.cu
 // Per-(row, chunk) records + per-row tickets of the multi-CTA row reductions.

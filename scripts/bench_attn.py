@@ -12,7 +12,8 @@ from paper_2509_21792_b200 import capi  # noqa: E402
 lib = capi.lib()
 # B:ctx[:H] (H heads of 128; default 12 = the c2 width, 28 = c3/c4)
 cases = [tuple(int(x) for x in a.split(':')) for a in sys.argv[1:]] or \
-    [(512, 128), (512, 640), (512, 1151), (211, 150), (64, 1151), (16, 150), (8, 1151), (1, 150), (1, 1151)]
+    [(512, 128), (512, 640), (512, 1151), (211, 150), (64, 1151), (16, 150), (8, 1151), (1, 150), (1, 1151),
+     (128, 640, 28), (128, 1151, 28), (16, 1151, 28), (1, 1151, 28)]
 for case in cases:
     B, ctx = case[0], case[1]
     H = case[2] if len(case) > 2 else 12
