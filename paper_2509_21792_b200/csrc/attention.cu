@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(32 * (kMaxCons + 1), 1)
     uint32_t qf[NK][2];
     ItemIt x = it0;
     int i = 0;
-    int cur_t = -1, cur_g = -1;
+    int cur_t = -1, cur_g = -1, seg = 0;
     for (int n = 0; n < n_items; ++n) {
         const int ve = item_end(x);
         const int kb = x.b * kBlock;
@@ -389,25 +389,29 @@ __global__ void __launch_bounds__(32 * (kMaxCons + 1), 1)
                 }
             }
         }
+        if (ve > kb) ++seg;
         const ItemIt done = x;
         advance(x);
-        if (ve <= kb) continue;  // no keys for this (row, block): nothing published, no ticket
-        // ---- ticket per (row, head group); the CTA that completes a row merges it. The
-        // ticket thread's gpu-scope fence after the CTA barrier orders every warp's partial
-        // stores before its ticket (cumulative release, as in a grid barrier).
+        // ---- ticket per (row, head group) at the end of this CTA's run of the tile's blocks
+        // (counts every block published in the run); the CTA that completes a row merges it.
+        // The ticket thread's gpu-scope fence after the CTA barrier orders every warp's
+        // partial stores before its ticket (cumulative release, as in a grid barrier).
+        const bool seg_end = (n + 1 == n_items) || x.t != done.t || x.g != done.g;
+        if (!seg_end || seg == 0) continue;
         asm volatile("bar.sync 1, %0;" ::"r"(n_cons * 32) : "memory");
         if (threadIdx.x < done.tl.nrows) {
             __threadfence();
             const int r = done.tl.row0 + threadIdx.x;
             int* c = row_ctr + static_cast<size_t>(r) * G + done.g;
-            const int old = atomicAdd(c, 1);
-            const int last = (old + 1 == tv.row_blocks(r));
+            const int old = atomicAdd(c, seg);
+            const int last = (old + seg == tv.row_blocks(r));
             if (last) {
                 *c = 0;  // re-armed for the next launch
                 __threadfence();  // acquire side: the other CTAs' partials are read after the barrier
             }
             flag[threadIdx.x] = last;
         }
+        seg = 0;
         asm volatile("bar.sync 1, %0;" ::"r"(n_cons * 32) : "memory");
         int any = 0;
         for (int j = 0; j < done.tl.nrows; ++j) any |= flag[j];

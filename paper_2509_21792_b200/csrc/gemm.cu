@@ -63,8 +63,10 @@ namespace {
 constexpr int kBK = 64;       // 64 bf16 = 128 B = one swizzle row
 constexpr int kBM = 128;      // output features per tile (UMMA M)
 constexpr int kABytes = kBM * kBK * 2;
-constexpr int kThreads = 320;  // TMA warp, MMA warp, 8 epilogue warps (2 per TMEM lane quarter)
-constexpr int kEpiThreads = 256;
+// TMA warp, MMA warp, then 4*CQ epilogue warps: CQ column parts per TMEM lane quarter, so
+// every epilogue thread owns one output feature and BN/CQ <= 64 token columns
+constexpr int cq_for(int BN) { return BN >= 256 ? 4 : 2; }
+constexpr int threads_for(int BN) { return 64 + 128 * cq_for(BN); }
 constexpr int kNumSMs = 148;
 
 template <int BN>
@@ -75,6 +77,9 @@ struct GemmCfg {
     static constexpr int kStages = (200 * 1024) / kStage > 8 ? 8 : (200 * 1024) / kStage;
     static constexpr int kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;
     static constexpr int kSmem = kStages * kStage + 1024 /*align*/ + 256 /*barriers*/;
+    static constexpr int kCQ = cq_for(BN);
+    static constexpr int kEpiThreads = 128 * kCQ;
+    static constexpr int kThreads = threads_for(BN);
 };
 
 __device__ __forceinline__ float gelu_tanh(float x) {
@@ -146,7 +151,8 @@ __device__ __forceinline__ void epi_store_run(const GemmEpi& e, int t0, int n, i
     }
 }
 
-__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+template <int NT>
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory"); }
 
 struct Unit {
     int m0, n0, split, tile;
@@ -192,7 +198,7 @@ struct StageSeq {
 };
 
 template <int BN, bool PART>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(threads_for(BN), 1)
     gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap mapW, const __grid_constant__ CUtensorMap mapX, int M,
                         int N, int kb_total, int n_chunks, int ckb, int cps, int S, int m_tiles, int n_tiles, GemmEpi epi,
                         float* __restrict__ ws, int* __restrict__ ctr) {
@@ -219,7 +225,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], kEpiThreads / 32);
+            mbar_init(&tempty[b], Cfg::kEpiThreads / 32);
         }
         fence_barrier_init();
     }
@@ -324,8 +330,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else {
         pdl_wait();
         pdl_trigger();
-        // ---------------- epilogue warps: TMEM lane quarter q (output feature o), column half h
-        constexpr int HB = BN / 2;
+        // ---------------- epilogue warps: TMEM lane quarter q (output feature o), column part h
+        constexpr int HB = BN / Cfg::kCQ;
         const int q = warp & 3;
         const int h = (warp - 2) >> 2;
         const int r = 32 * q + lane;
@@ -338,7 +344,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int nmine = max(0, min(HB, ncols - j0));
             const int c_begin = un.split * cps, c_end = min(n_chunks, c_begin + cps);
             float* wst = ws ? ws + static_cast<size_t>(un.tile) * n_chunks * BN * kBM : nullptr;
-            float run[PART ? 1 : HB];  // the chunk-ordered running sum (not needed for raw partials)
+            // 256-token tiles run only single-chunk weights (gemm_run), so their pieces are final
+            constexpr bool kOneChunk = (BN == 256);
+            float run[(PART || kOneChunk) ? 1 : HB];  // the chunk-ordered running sum
             for (int c = c_begin; c < c_end; ++c, ++it) {
                 const int buf = it & 1;
                 mbar_wait(&tfull[buf], (it >> 1) & 1);
@@ -354,6 +362,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                         for (int j = 0; j < PC; ++j)
                             if (p0 + j < nmine && o < N) dst[static_cast<size_t>(j) * epi.ld] = v[j];
+                    } else if constexpr (kOneChunk) {
+                        if (o < N && p0 < nmine) epi_store_run<PC>(epi, un.m0 + j0 + p0, nmine - p0, o, v);
                     } else if (un.split == 0) {
                         if (c == c_begin) {
 #pragma unroll
@@ -372,8 +382,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&tempty[buf]);
             }
-            if constexpr (PART) {
-                // raw chunk sums already stored; the consumer kernel reduces them in order
+            if constexpr (PART || kOneChunk) {
+                // raw chunk sums / single-chunk results already stored
             } else if (S == 1) {
                 if (o < N) epi_store_run<HB>(epi, un.m0 + j0, nmine, o, run);
             } else {
@@ -382,12 +392,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int j = 0; j < HB; ++j)
                         if (j < nmine) wst[static_cast<size_t>(j0 + j) * kBM + r] = run[j];
                 __threadfence();
-                epi_bar();
+                epi_bar<Cfg::kEpiThreads>();
                 if (threadIdx.x == 64) {
                     const int old = atomicAdd(&ctr[un.tile], 1);
                     *last_flag = (old == S - 1);
                 }
-                epi_bar();
+                epi_bar<Cfg::kEpiThreads>();
                 const int last = *last_flag;
                 if (last) {
                     __threadfence();
@@ -423,7 +433,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     if (threadIdx.x == 64) ctr[un.tile] = 0;
                 }
-                epi_bar();  // last_flag is reused by the next unit
+                epi_bar<Cfg::kEpiThreads>();  // last_flag is reused by the next unit
             }
         }
     }
@@ -456,7 +466,7 @@ void launch_bn(const CUtensorMap& w, const CUtensorMap& x, int M, int N, int kbt
     const int m_tiles = (M + BN - 1) / BN, n_tiles = (N + kBM - 1) / kBM;
     const int units = m_tiles * n_tiles * S;
     const int grid = std::min(units, kNumSMs);
-    launch_pdl(gemm_bf16_tn_kernel<BN, PART>, dim3(grid), dim3(kThreads), Cfg::kSmem, st, w, x, M, N, kbt, n_chunks, ckb,
+    launch_pdl(gemm_bf16_tn_kernel<BN, PART>, dim3(grid), dim3(Cfg::kThreads), Cfg::kSmem, st, w, x, M, N, kbt, n_chunks, ckb,
                cps, S, m_tiles, n_tiles, epi, ws, ctr);
 }
 
@@ -507,7 +517,14 @@ int gemm_bn_for(int M) {
     // BN=32 measured slower than BN=64 for 17..32 tokens at the c2 shapes
     // (profiles/hw_profile_c2.json latency curve); BN=32 stays instantiated for tests
     if (M <= 64) return 64;
-    return 128;  // BN=256 (kernel instantiated) spills the epilogue's running sums at 320 threads
+    if (M <= 128) return 128;
+    // 256-token tiles (16 epilogue warps, 64 columns each): every weight tile is streamed
+    // once per 256 rows -- the 129..256-row verify forwards read the weights once, not twice
+    static const int max_bn = [] {
+        const char* v = getenv("SGB_GEMM_MAXBN");  // tuning experiments only
+        return v ? atoi(v) : 256;
+    }();
+    return max_bn >= 256 ? 256 : 128;
 }
 
 // K split: which CTA computes which chunks. Any choice gives identical bits.
@@ -564,11 +581,13 @@ void gemm_run(const GemmWeight& w, const GemmAct& x, int M, const GemmEpi& epi, 
     if (S > 1 && (ws.buf == nullptr || gemm_ws_floats(M, w.N, w.K) > ws.cap_floats || tiles > ws.ctr_cap)) S = 1;
     const int cps = (nc + S - 1) / S;
     S = (nc + cps - 1) / cps;
-    const CUtensorMap& xm = x.map_for_bn(bn);
-    switch (bn) {
+    const int bn_run = (bn == 256 && (nc > 1 || S > 1)) ? 128 : bn;  // 256-token tiles: single-chunk weights
+    const CUtensorMap& xm = x.map_for_bn(bn_run);
+    switch (bn_run) {
         case 16: launch_bn<16, false>(w.map, xm, M, w.N, kbt, nc, ckb, S, cps, epi, ws.buf, ws.ctr, st); break;
         case 64: launch_bn<64, false>(w.map, xm, M, w.N, kbt, nc, ckb, S, cps, epi, ws.buf, ws.ctr, st); break;
-        default: launch_bn<128, false>(w.map, xm, M, w.N, kbt, nc, ckb, S, cps, epi, ws.buf, ws.ctr, st); break;
+        case 128: launch_bn<128, false>(w.map, xm, M, w.N, kbt, nc, ckb, S, cps, epi, ws.buf, ws.ctr, st); break;
+        default: launch_bn<256, false>(w.map, xm, M, w.N, kbt, nc, ckb, S, cps, epi, ws.buf, ws.ctr, st); break;
     }
 }
 
