@@ -394,8 +394,8 @@ def main():
     att = prof["attention"]
     ach = att["bytes"] / (att["ms"] * 1e-3) / 1e9 if att["ms"] else 0.0
     total_ms = sum(v["ms"] for v in prof.values())
-    traffic, traffic_alg, traffic_src = ncu_traffic("r01_attn_c2_b512_ctx640.txt")
-    roofline = {"bound": "hbm", "kernel": "attn_kernel (persistent tree/paged KV attention, in-kernel block merge)",
+    traffic, traffic_alg, traffic_src = ncu_traffic("r01_attn_mma_c2_b512_ctx640.txt")
+    roofline = {"bound": "hbm", "kernel": "attn_kernel (mma.sync tree/paged KV attention: shared-prefix tiles, bulk-DMA ring, in-kernel block merge)",
                 "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s", "frac": round(ach / hbm, 4),
                 "traffic": traffic, "traffic_algorithmic": traffic_alg, "traffic_source": traffic_src,
                 "peak_source": src,

@@ -558,17 +558,20 @@ long long build_attn_tiles(const std::vector<std::array<int, 4>>& groups, std::v
         const int nb = attn_splits_for(vmax);
         // blocks entirely inside the committed prefix are shared by the tile's rows
         const int nsb = nr > 1 ? std::min(nb, ctx_len / kBlock) : 0;
-        if (nsb > 0)
-            for (int o = 0; o < nr; o += rows_per_tile) {
-                out.push_back(AttnTileDev{row0 + o, std::min(rows_per_tile, nr - o), 0, nsb});
+        // ... and the blocks that reach into each row's own tree path run per row, listed
+        // right after the row's shared tile so every CTA's slice mixes heavy and light items
+        for (int o = 0; o < nr; o += rows_per_tile) {
+            const int nt = std::min(rows_per_tile, nr - o);
+            if (nsb > 0) {
+                out.push_back(AttnTileDev{row0 + o, nt, 0, nsb});
                 n += nsb;
             }
-        // the blocks that reach into each row's own tree path run per row
-        if (nb > nsb)
-            for (int r = 0; r < nr; ++r) {
-                out.push_back(AttnTileDev{row0 + r, 1, nsb, nb});
-                n += nb - nsb;
-            }
+            if (nb > nsb)
+                for (int r = o; r < o + nt; ++r) {
+                    out.push_back(AttnTileDev{row0 + r, 1, nsb, nb});
+                    n += nb - nsb;
+                }
+        }
     }
     return n;
 }
