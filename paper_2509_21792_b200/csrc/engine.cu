@@ -1318,11 +1318,28 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
         f.logits_out = logits_;
         f.max_vlen = max_p + max_l + 1;
         groups_.clear();
+        bool all_ar = true;
         for (int i = 0; i < B; ++i) {
             f.attn_kv_unique += hs[i].p + hs[i].nsel;
             f.attn_row_keys += static_cast<double>(hs[i].nsel) * (hs[i].p + 1);
             groups_.push_back(
                 {hs[i].vrow_off, hs[i].nsel, hs[i].p, hs[i].p + 1 + std::min(hs[i].l, hs[i].nsel - 1)});
+            all_ar = all_ar && hs[i].nsel == 1;
+        }
+        if (all_ar && a.g > 1) {
+            // AR step: the live members of a query group (consecutive rows) read their prompt's
+            // K/V from the leader's copy, so they share the prompt blocks as one tile
+            groups_.clear();
+            for (int i = 0; i < B;) {
+                int j = i + 1, shared = std::min(hs[i].pre_len, hs[i].p), vmax = hs[i].p + 1;
+                while (j < B && hs[j].pre_base == hs[i].pre_base) {
+                    shared = std::min(shared, std::min(hs[j].pre_len, hs[j].p));
+                    vmax = std::max(vmax, hs[j].p + 1);
+                    ++j;
+                }
+                groups_.push_back({hs[i].vrow_off, j - i, shared, vmax});
+                i = j;
+            }
         }
         f.groups = &groups_;
         forward(f);
