@@ -115,7 +115,22 @@ __global__ void __launch_bounds__(kRowThreads)
             const int e = threadIdx.x + i * kRowThreads;
             acc[i] = e < d ? P[row + e] : 0.f;
         }
+        // four chunks per round of loads (w2 at the c2 shape has 12 chunks: 3 round trips)
         int s = 1;
+        for (; s + 4 <= S; s += 4) {
+            float pp[4][PER];
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+#pragma unroll
+                for (int i = 0; i < PER; ++i) {
+                    const int e = threadIdx.x + i * kRowThreads;
+                    pp[c][i] = e < d ? P[(s + c) * st + row + e] : 0.f;
+                }
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+#pragma unroll
+                for (int i = 0; i < PER; ++i) acc[i] += pp[c][i];
+        }
         for (; s + 2 <= S; s += 2) {
             float p1[PER], p2[PER];
 #pragma unroll
