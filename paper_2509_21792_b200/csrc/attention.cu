@@ -476,12 +476,17 @@ void launch_impl(const float* q, const __nv_bfloat16* K, const __nv_bfloat16* V,
         const char* v = getenv("SGB_ATTN_G");  // tuning experiments only
         return v ? atoi(v) : 0;
     }();
+    static const int max_sm = [] {
+        const char* v = getenv("SGB_ATTN_MAXSM");  // tuning experiments only
+        return v ? std::max(1, std::min(16, atoi(v))) : 4;
+    }();
     // CTAs per SM for a head grouping: shared memory for >= 2 stages each, and registers
     auto ctas_per_sm = [&](int G) {
         const int threads = 32 * (QW * (H / G) + 1);
         const int by_regs = std::max(1, 65536 / (threads * ((regs + 7) / 8 * 8)));
         int n = 0;
-        while (n < std::min(by_regs, 4) && (n + 1) * (2 * stage_of(G) + fixed_of(G)) <= static_cast<size_t>(kSmemBudget))
+        while (n < std::min(by_regs, max_sm) && (n + 1) * (2 * stage_of(G) + fixed_of(G)) <= static_cast<size_t>(kSmemBudget) &&
+               (n + 1) * threads <= 2048)
             ++n;
         return n;
     };

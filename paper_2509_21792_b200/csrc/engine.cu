@@ -1326,7 +1326,14 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
                 {hs[i].vrow_off, hs[i].nsel, hs[i].p, hs[i].p + 1 + std::min(hs[i].l, hs[i].nsel - 1)});
             all_ar = all_ar && hs[i].nsel == 1;
         }
-        if (all_ar && a.g > 1) {
+        // measured A/B (SGB_PROMPT_TILES, bench.py vanilla): +5 % at 12 heads (c2), -13 % at
+        // 28 heads (c3, where the per-row kernel already hits the prompt pages in L2)
+        static const int prompt_tiles = [] {
+            const char* v = getenv("SGB_PROMPT_TILES");  // A/B switch
+            return v ? atoi(v) : -1;
+        }();
+        const bool use_prompt_tiles = prompt_tiles < 0 ? dims_.heads <= 16 : prompt_tiles != 0;
+        if (all_ar && a.g > 1 && use_prompt_tiles) {
             // AR step: the live members of a query group (consecutive rows) read their prompt's
             // K/V from the leader's copy, so they share the prompt blocks as one tile
             groups_.clear();

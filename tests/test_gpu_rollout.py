@@ -111,6 +111,24 @@ def test_rollout_equals_teacher_forced_greedy(mode):
         assert lg.argmax(1)[31:].tolist() == toks[32:], s
 
 
+def test_group_members_share_prompt_blocks_losslessly():
+    """AR steps tile the live members of a query group over their shared prompt blocks
+    (prompt >= 2 full 64-key blocks here); the rollout must still equal the teacher-forced
+    argmax of each sequence alone, and the speculative rollout must equal it bit for bit."""
+    e, m, d = make_engine(C1, max_seqs=8)
+    pr = prompts_for(C1, 2, 130, 131, seed=9)
+    kw = dict(temperature=0.0, seed=7, max_new_tokens=20)
+    van = e.generate(pr, 4, c_peak=4, mode="vanilla", **kw)
+    ada = e.generate(pr, 4, c_peak=64, mode="adaptive_spec", **kw)
+    assert ada.tokens == van.tokens
+    assert max(s[1] for s in ada.steps) > 1
+    for s in (0, 5):
+        toks = van.tokens[s]
+        e.cache_reset(7)
+        lg, _ = e.forward_target(7, toks[:-1], list(range(len(toks) - 1)))
+        assert lg.argmax(1)[129:].tolist() == toks[130:], s
+
+
 def test_rollout_errors():
     e, m, d = make_engine(SMALL, max_seqs=4)
     with pytest.raises(ValueError):
