@@ -48,6 +48,14 @@ WORKLOADS = {
                desc="Qwen2.5-7B-shaped GRPO rollout, data-parallel by query group, 16 queries x group 8 per GPU, "
                     "variable-length stops 256..1024, adaptive spec + one online draft-learning AdamW step with "
                     "NCCL gradient all-reduce per step"),
+    # c5 (BASELINE configs[4]): Llama-3-8B shape, T=1.0 keyed sampling (the reference's strict-match
+    # verify at T>0, the parity mode), group 16, 4096 new tokens. The full per-GPU
+    # shard (32 queries x 16 = 512 sequences x 4224 positions) needs ~1.1 TB of KV at 524 KB per
+    # token, beyond one GPU's 180 GB: this shard runs 2 queries x 16 = 32 sequences (71 GB of KV)
+    "c5": dict(V=128256, d=4096, L=32, H=32, dff=14336, P=128, G=16, Q=2, new=4096, stops=False, online=False,
+               warm=0, temp=1.0,
+               desc="Llama-3-8B-shaped target + 1-layer draft, T=1.0 keyed sampling, 2 queries x group 16 per GPU "
+                    "(memory-bounded shard of 256 x 16 over 8 GPUs), 128-token prompts, 4096 new tokens, adaptive spec"),
     "c1": dict(V=512, d=256, L=2, H=4, dff=1024, P=32, G=4, Q=8, new=128, stops=False, online=False, warm=0,
                desc="2-layer d=256 target + 1-layer draft, 8 queries x group 4, 32-token prompts, 128 new tokens"),
 }
@@ -284,7 +292,7 @@ def main():
     from paper_2509_21792_b200 import capi
     cfg = model_cfg(w)
     n_seq = w["Q"] * w["G"]
-    eng = capi.Engine(cfg, 1, local, max(n_seq, 64), 2048, 10, 6)
+    eng = capi.Engine(cfg, 1, local, max(n_seq, 64 if w["warm"] > 0 else 1), 2048, 10, 6)
     eng.init_random(1234)
     # NCCL data-parallel group over NVLink (C1 gradient all-reduce, C2 statistics)
     uid = [capi.nccl_unique_id() if rank == 0 else None]
@@ -293,7 +301,8 @@ def main():
     eng.nccl_init(rank, world, uid[0])
     prompts = make_prompts(w, rank)
     caps = stop_caps(w, rank * n_seq, n_seq) if w["stops"] else None
-    gen = dict(c_peak=args.c_peak, alpha=2.0, k_max=10, l_max=6, temperature=0.0, seed=7, max_new_tokens=w["new"],
+    gen = dict(c_peak=args.c_peak, alpha=2.0, k_max=10, l_max=6, temperature=w.get("temp", 0.0), seed=7,
+               max_new_tokens=w["new"],
                sid_offset=rank * n_seq, seq_max_new=caps)
 
     def rollout(mode):
