@@ -310,10 +310,26 @@ def main():
         r = eng.generate(prompts, w["G"], mode=mode, want_features=True, **gen)
         return r, time.perf_counter() - t0
 
-    def draft_step(r):
+    adv_stats = {"ms": 0.0, "calls": 0, "groups": 0, "filtered": 0, "reward_mean": 0.0}
+
+    def group_rewards(r, g):
+        """group rewards + standardized advantages of this rollout on the device (grpo.cpp:
+        99-136, 352-380) and the data-parallel gather of every rank's rewards (NCCL
+        all-gather). Synthetic prompts carry no addition task: the answer key is 0."""
+        t0 = time.perf_counter()
+        rw, _, valid = eng.group_advantages([0] * (len(r.tokens) // g), g)
+        allr = eng.allgather_f64(rw, world)
+        adv_stats["ms"] += 1e3 * (time.perf_counter() - t0)
+        adv_stats["calls"] += 1
+        adv_stats["groups"] += len(valid) * world
+        adv_stats["filtered"] += int(len(valid) - int(np.sum(valid)))
+        adv_stats["reward_mean"] = float(np.mean(allr))
+
+    def draft_step(r, g):
         """one online draft-learning step on this rollout (grpo.cpp:329-345): global row
         count first (int64 all-reduce), local gradient with the global normaliser, NCCL
         all-reduce (sum) of the fp32 gradient, identical AdamW step on every replica."""
+        group_rewards(r, g)
         rows = sum(max(0, len(t) - 2) for t in r.tokens)
         rows_total = int(eng.allreduce_i64([rows])[0])  # noqa: F841 (used below)
         t0 = time.perf_counter()
@@ -330,14 +346,14 @@ def main():
             rw = eng.generate(tp, 2, c_peak=args.c_peak, mode="vanilla", temperature=0.0, seed=it,
                               max_new_tokens=128, want_features=True)
             for _ in range(4):
-                _, _, fl, tl, _ = draft_step(rw)
+                _, _, fl, tl, _ = draft_step(rw, 2)
         warm = {"iterations": w["warm"], "adamw_steps": 4 * w["warm"], "train_seqs_per_iter": 64,
                 "feature_loss": round(fl, 5), "token_loss": round(tl, 4), "seconds": round(time.perf_counter() - t0, 1)}
 
     for _ in range(args.warmup):
         r, _ = rollout(args.mode)
         if w["online"]:
-            draft_step(r)
+            draft_step(r, w["G"])
     eng.read_profile(reset=True)
     if dist:
         dist.barrier()
@@ -351,7 +367,7 @@ def main():
         dev_s += r.seconds
         wall_s += wall
         if w["online"]:
-            us, uw, fl, tl, nrows = draft_step(r)
+            us, uw, fl, tl, nrows = draft_step(r, w["G"])
             dev_s += us
             wall_s += uw
             upd_s += us
@@ -440,7 +456,11 @@ def main():
                                      "global_rows_per_step": upd_rows // args.steps,
                                      "share_of_step": round(upd_s / dev_s, 4),
                                      "feature_loss": round(terms[0], 5), "token_loss": round(terms[1], 4),
-                                     "collective": f"ncclAllReduce(sum) fp32 gradient over {world} rank(s)"}
+                                     "collective": f"ncclAllReduce(sum) fp32 gradient over {world} rank(s)",
+                                     "group_advantages": {
+                                         "wall_ms_per_step": round(adv_stats["ms"] / max(1, adv_stats["calls"]), 3),
+                                         "groups_per_step": w["Q"] * world, "reward_mean": adv_stats["reward_mean"],
+                                         "collective": f"ncclAllGather fp64 rewards over {world} rank(s)"}}
     print(json.dumps(line))
     eng.close()
     if dist:

@@ -199,6 +199,24 @@ int sgb_bench_attention(int B, int ctx, int H, int dh, int iters, double* ms_out
 int sgb_debug_attention(int B, const int* n_keys, int H, int dh, const float* q, const float* k, const float* v,
                         float* out);
 
+/* GRPO rewards and advantages of the LAST rollout's groups, from its token table in HBM:
+ * rewards[s] = compute_reward (src/grpo.cpp:99-116) of sequence s's response (tokens after
+ * its prompt, scored against answers[s / g] = a + b of query s / g, call site grpo.cpp:352-363);
+ * advantages = standardize_advantages (grpo.cpp:121-136) per group, valid[b] = 0 where the
+ * reference returns nullopt (sd < eps_var; advantages 0). n_groups * g must equal the last
+ * rollout's sequence count. */
+int sgb_group_advantages(sgb_engine* e, const long long* answers, int n_groups, int g, double eps_var,
+                         double* rewards, double* advantages, int* valid);
+
+/* The same on host token tables ([n_groups*g][stride], lens / prompt_lens per sequence). */
+int sgb_debug_group_advantages(const int* tokens, const int* lens, const int* prompt_lens, int n_groups, int g,
+                               int stride, const long long* answers, double eps_var, double* rewards,
+                               double* advantages, int* valid);
+
+/* Data-parallel group-reward/advantage gather (north star: NCCL where the path shards):
+ * recv[r * n + i] = rank r's send[i] (ncclAllGather over the engine's communicator). */
+int sgb_allgather_f64(sgb_engine* e, const double* send, int n, double* recv);
+
 /* Prefix-shared tree attention self-test. n_groups sequences; group g has ctx_len[g]
  * committed keys (kctx/vctx rows, concatenated over groups) and n_rows[g] tree rows in
  * level order with parent[r] (index within the group, -1 = root); row r attends to the

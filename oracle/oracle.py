@@ -1159,3 +1159,62 @@ def measure_c_peak(latency_fn, b_max: int, warmup: int = 1, reps: int = 3):
     if conf < 0.05:
         return dict(c_peak=b_max, confidence=conf, low_confidence=True, curve=curve)
     return dict(c_peak=curve[idx][0], confidence=conf, low_confidence=low, curve=curve)
+
+
+# ----------------------------------------------------------------------------- GRPO rewards
+# Task token ids (include/sgrpo/grpo.hpp:19-21) and EOS (tinylm.hpp:41).
+K_DIGIT_BASE, K_PLUS, K_EQ, K_EOS = 2, 12, 13, 1
+
+
+def compute_reward(a: int, b: int, response: Sequence[int]) -> float:
+    """compute_reward (src/grpo.cpp:99-116): 1.0 iff the digits after the LAST '=' spell a+b
+    (an EOS is allowed only as the very last token), 0.0 for anything malformed."""
+    last_eq = -1
+    for i, t in enumerate(response):
+        if t == K_EQ:
+            last_eq = i
+    if last_eq < 0:
+        return 0.0
+    value, digits = 0, 0
+    for i in range(last_eq + 1, len(response)):
+        t = response[i]
+        if t == K_EOS and i + 1 == len(response):
+            break
+        if t < K_DIGIT_BASE or t >= K_DIGIT_BASE + 10:
+            return 0.0
+        value = value * 10 + (t - K_DIGIT_BASE)
+        digits += 1
+        if digits > 15:
+            return 0.0
+    if digits == 0:
+        return 0.0
+    return 1.0 if value == a + b else 0.0
+
+
+def _fma(a: float, b: float, c: float) -> float:
+    from fractions import Fraction
+    return float(Fraction(a) * Fraction(b) + Fraction(c))  # one rounding
+
+
+def standardize_advantages(rewards: Sequence[float], eps_var: float):
+    """standardize_advantages (src/grpo.cpp:121-136): population-standardized rewards, or None
+    (the group is filtered) when sd < eps_var. Sequential fp64 sums as in the reference -- as
+    COMPILED (oracle/Makefile, g++ -O3 -march=x86-64-v3): the deviation loop is vectorised
+    two/four wide with exact products added in order, and the odd tail element is fused into
+    one vfmadd231sd (objdump of grpo.o); pinned bit for bit by tests/golden/rewards.json."""
+    g = len(rewards)
+    if g < 2:
+        raise ValueError("standardize_advantages: need G >= 2")
+    mean = 0.0
+    for r in rewards:
+        mean += float(r)
+    mean /= float(g)
+    var = 0.0
+    for i, r in enumerate(rewards):
+        dv = float(r) - mean
+        var = _fma(dv, dv, var) if (g % 2 == 1 and i == g - 1) else var + dv * dv
+    var /= float(g)
+    sd = math.sqrt(var)
+    if sd < eps_var:
+        return None
+    return [(float(r) - mean) / sd for r in rewards]

@@ -300,6 +300,21 @@ int sgref_verify(int n, const int* tok, const int* par, const int* depth, const 
 }
 
 // ---- scheduler.cpp:14-54 ------------------------------------------------------------
+// GRPO rewards / advantages (src/grpo.cpp:99-136)
+double sgref_compute_reward(long long a, long long b, const int* resp, int n) {
+    TaskExample ex;
+    ex.a = a;
+    ex.b = b;
+    return compute_reward(ex, std::span<const int>(resp, static_cast<size_t>(n)));
+}
+int sgref_standardize_advantages(const double* rewards, int g, double eps_var, double* out) {
+    std::vector<double> r(rewards, rewards + g);
+    auto adv = standardize_advantages(r, eps_var);
+    if (!adv) return 0;
+    for (int i = 0; i < g; ++i) out[i] = (*adv)[i];
+    return 1;
+}
+
 int sgref_plan_step(int c_peak, int b, double alpha, int kmax, int lmax, int* out3) {
     return guarded([&] {
         SpecConfig c = plan_step(c_peak, b, alpha, kmax, lmax);

@@ -61,7 +61,8 @@ EXPORTED = ["sgb_last_error", "sgb_version", "sgb_device_count", "sgb_engine_cre
             "sgb_cache_reset", "sgb_cache_len", "sgb_cache_read", "sgb_cache_gather_tail", "sgb_forward_target",
             "sgb_forward_draft_rows", "sgb_sample_rows", "sgb_topk_logsoftmax", "sgb_build_tree", "sgb_rollout",
             "sgb_debug_gemm", "sgb_profile_enable", "sgb_profile_read", "sgb_bench_gemm", "sgb_bench_attention",
-            "sgb_debug_attention", "sgb_debug_tree_attention", "sgb_bench_tree_attention", "sgb_detect_knee", "sgb_measure_c_peak"]
+            "sgb_debug_attention", "sgb_debug_tree_attention", "sgb_bench_tree_attention", "sgb_group_advantages",
+            "sgb_debug_group_advantages", "sgb_allgather_f64", "sgb_detect_knee", "sgb_measure_c_peak"]
 
 KERNEL_CLASSES = ["gemm_tcgen05", "attention", "rowops", "lm_head", "sample", "tree", "kv_commit"]
 
@@ -117,6 +118,27 @@ def debug_tree_attention(ctx_len, parents, q, kctx, vctx, knode, vnode, n_heads:
                                          d // n_heads, _p(q, C.c_float), *[_p(a, C.c_float) for a in f],
                                          _p(o1, C.c_float), _p(o2, C.c_float)))
     return o1, o2
+
+
+def debug_group_advantages(tokens, prompt_lens, answers, g: int, eps_var: float = 1e-8):
+    """Device rewards + standardized advantages on host token lists (sgb_debug_group_advantages).
+    tokens: n_groups*g full sequences; answers: per group a+b. Returns (rewards, adv, valid)."""
+    n = len(tokens)
+    ng = n // g
+    stride = max(1, max(len(t) for t in tokens))
+    tab = np.zeros((n, stride), np.int32)
+    for i, t in enumerate(tokens):
+        tab[i, :len(t)] = t
+    lens = np.array([len(t) for t in tokens], np.int32)
+    pl = np.ascontiguousarray(prompt_lens, np.int32)
+    ans = np.ascontiguousarray(answers, np.int64)
+    r = np.zeros(n, np.float64)
+    a = np.zeros(n, np.float64)
+    v = np.zeros(ng, np.int32)
+    _check(_lib.sgb_debug_group_advantages(_p(tab, C.c_int), _p(lens, C.c_int), _p(pl, C.c_int), ng, g, stride,
+                                           _p(ans, C.c_longlong), C.c_double(eps_var), _p(r, C.c_double),
+                                           _p(a, C.c_double), _p(v, C.c_int)))
+    return r, a, v
 
 
 def debug_gemm(w: np.ndarray, x: np.ndarray, splits: int = 0):
@@ -404,6 +426,25 @@ def _nccl_init(self, rank: int, world: int, uid: bytes):
     _check(_lib.sgb_nccl_init(self.h, rank, world, buf))
 
 
+def _group_advantages(self, answers, g: int, eps_var: float = 1e-8):
+    """rewards / advantages / valid of the last rollout's groups (sgb_group_advantages)."""
+    ans = np.ascontiguousarray(answers, np.int64)
+    ng = ans.size
+    r = np.zeros(ng * g, np.float64)
+    a = np.zeros(ng * g, np.float64)
+    v = np.zeros(ng, np.int32)
+    _check(_lib.sgb_group_advantages(self.h, _p(ans, C.c_longlong), ng, g, C.c_double(eps_var), _p(r, C.c_double),
+                                     _p(a, C.c_double), _p(v, C.c_int)))
+    return r, a, v
+
+
+def _allgather_f64(self, vals, world: int):
+    s = np.ascontiguousarray(vals, np.float64)
+    out = np.zeros(s.size * world, np.float64)
+    _check(_lib.sgb_allgather_f64(self.h, _p(s, C.c_double), s.size, _p(out, C.c_double)))
+    return out
+
+
 def _allreduce_f64(self, vals):
     a = np.ascontiguousarray(vals, np.float64).copy()
     _check(_lib.sgb_allreduce_sum_f64(self.h, _p(a, C.c_double), a.size))
@@ -419,6 +460,8 @@ def _allreduce_i64(self, vals):
 Engine.nccl_init = _nccl_init
 Engine.allreduce_f64 = _allreduce_f64
 Engine.allreduce_i64 = _allreduce_i64
+Engine.group_advantages = _group_advantages
+Engine.allgather_f64 = _allgather_f64
 EXPORTED += ["sgb_nccl_unique_id", "sgb_nccl_init", "sgb_allreduce_sum_f64", "sgb_allreduce_sum_i64"]
 
 

@@ -335,6 +335,62 @@ int sgb_nccl_init(sgb_engine* e, int rank, int world, const unsigned char* id128
 }
 
 
+int sgb_group_advantages(sgb_engine* e, const long long* answers, int n_groups, int g, double eps_var,
+                         double* rewards, double* advantages, int* valid) {
+    return guarded([&] {
+        if (!answers || !rewards || !advantages || !valid) throw std::invalid_argument("group_advantages: null output");
+        E(e).group_advantages(answers, n_groups, g, eps_var, rewards, advantages, valid);
+    });
+}
+
+int sgb_debug_group_advantages(const int* tokens, const int* lens, const int* prompt_lens, int n_groups, int g,
+                               int stride, const long long* answers, double eps_var, double* rewards,
+                               double* advantages, int* valid) {
+    return guarded([&] {
+        if (n_groups <= 0 || g < 2) throw std::invalid_argument("standardize_advantages: need G >= 2");
+        const int n = n_groups * g;
+        for (int s = 0; s < n; ++s)
+            if (lens[s] < prompt_lens[s] || lens[s] > stride || prompt_lens[s] < 0)
+                throw std::invalid_argument("group_advantages: bad sequence lengths");
+        int *dt = nullptr, *dl = nullptr, *dp = nullptr, *dv = nullptr;
+        long long* da = nullptr;
+        double* db = nullptr;
+        SGB_CUDA(cudaMalloc(&dt, sizeof(int) * static_cast<size_t>(n) * stride));
+        SGB_CUDA(cudaMalloc(&dl, sizeof(int) * n));
+        SGB_CUDA(cudaMalloc(&dp, sizeof(int) * n));
+        SGB_CUDA(cudaMalloc(&dv, sizeof(int) * n_groups));
+        SGB_CUDA(cudaMalloc(&da, sizeof(long long) * n_groups));
+        SGB_CUDA(cudaMalloc(&db, sizeof(double) * 2 * n));
+        SGB_CUDA(cudaMemcpy(dt, tokens, sizeof(int) * static_cast<size_t>(n) * stride, cudaMemcpyHostToDevice));
+        SGB_CUDA(cudaMemcpy(dl, lens, sizeof(int) * n, cudaMemcpyHostToDevice));
+        SGB_CUDA(cudaMemcpy(dp, prompt_lens, sizeof(int) * n, cudaMemcpyHostToDevice));
+        SGB_CUDA(cudaMemcpy(da, answers, sizeof(long long) * n_groups, cudaMemcpyHostToDevice));
+        sgb::launch_group_advantages(n_groups, g, dt, stride, dl, dp, da, eps_var, db, db + n, dv, 0);
+        SGB_CUDA(cudaDeviceSynchronize());
+        SGB_CUDA(cudaMemcpy(rewards, db, sizeof(double) * n, cudaMemcpyDeviceToHost));
+        SGB_CUDA(cudaMemcpy(advantages, db + n, sizeof(double) * n, cudaMemcpyDeviceToHost));
+        SGB_CUDA(cudaMemcpy(valid, dv, sizeof(int) * n_groups, cudaMemcpyDeviceToHost));
+        void* ptrs[] = {dt, dl, dp, dv, da, db};
+        for (void* p : ptrs) cudaFree(p);
+    });
+}
+
+int sgb_allgather_f64(sgb_engine* e, const double* send, int n, double* recv) {
+    return guarded([&] {
+        DpGroup& g = group_of(e);
+        if (n < 0 || !send || !recv) throw std::invalid_argument("allgather: bad arguments");
+        cudaStream_t st = E(e).stream();
+        const size_t need = static_cast<size_t>(n) * (g.world + 1);
+        double* d = g.dbuf;  // the group's 4096-double staging buffer when it fits
+        if (need > 4096) SGB_CUDA(cudaMalloc(&d, sizeof(double) * need));
+        SGB_CUDA(cudaMemcpyAsync(d, send, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+        nccl_check(ncclAllGather(d, d + n, n, ncclFloat64, g.comm, st), "ncclAllGather");
+        SGB_CUDA(cudaMemcpyAsync(recv, d + n, sizeof(double) * static_cast<size_t>(n) * g.world, cudaMemcpyDeviceToHost, st));
+        SGB_CUDA(cudaStreamSynchronize(st));
+        if (d != g.dbuf) SGB_CUDA(cudaFree(d));
+    });
+}
+
 int sgb_allreduce_sum_f64(sgb_engine* e, double* vals, int n) {
     return guarded([&] { allreduce_host(e, vals, n, ncclFloat64); });
 }

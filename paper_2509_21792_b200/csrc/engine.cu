@@ -303,6 +303,7 @@ void Engine::alloc_rows() {
 Engine::~Engine() {
     cudaSetDevice(device_);
     cudaStreamSynchronize(st_);
+    if (adv_buf_) cudaFree(adv_buf_);
     void* ptrs[] = {tw_, dw_, tsmall_, dmaster_, tkv_.K, tkv_.V, dkv_.K, dkv_.V, ss_.tokens, ss_.len, ss_.finished,
                     ss_.hit_eos, ss_.seed, feats_, dfeat_, tr_.tok, tr_.par, tr_.dep, tr_.lp, tr_.conf, tr_.fslot,
                     tr_.sel, tr_.n_nodes, tr_.lvl_start, tr_.lvl_cnt, tr_.frontier, x_, q_, y_, featin_, a_, att_,
@@ -532,6 +533,30 @@ void Engine::gemm_resid_ln(const GemmWeight& w, const GemmAct& a, int M, bool ac
     if (!accumulate && !add_pos) throw std::logic_error("gemm_resid_ln: plain store unsupported");
     gemm(w, a, M, e, kClsGemm, 8.0);
     ln(M, g, b, y);
+}
+
+// ------------------------------------------------------------------ GRPO rewards / advantages
+void Engine::group_advantages(const long long* answers, int n_groups, int g, double eps_var, double* rewards,
+                              double* adv, int* valid) {
+    const int n = n_groups * g;
+    if (n_groups <= 0 || g < 2) throw std::invalid_argument("standardize_advantages: need G >= 2");
+    if (static_cast<size_t>(n) != last_lens_.size()) throw std::invalid_argument("group_advantages: not the last rollout's shape");
+    if (n > max_rows_) throw std::invalid_argument("group_advantages: too many sequences");
+    int* dlen = misc_i_;
+    int* dplen = misc_i_ + n;
+    int* dvalid = misc_i_ + 2 * n;
+    long long* dans = misc_l_;
+    if (!adv_buf_) adv_buf_ = dalloc<double>(2 * static_cast<size_t>(max_rows_));  // n <= max_rows
+    double* dbuf = adv_buf_;
+    h2d(dlen, last_lens_.data(), n, st_);
+    h2d(dplen, last_plens_.data(), n, st_);
+    h2d(dans, answers, n_groups, st_);
+    launch_group_advantages(n_groups, g, ss_.tokens, dims_.max_seq, dlen, dplen, dans, eps_var, dbuf, dbuf + n, dvalid,
+                            st_);
+    SGB_CUDA(cudaMemcpyAsync(rewards, dbuf, sizeof(double) * n, cudaMemcpyDeviceToHost, st_));
+    SGB_CUDA(cudaMemcpyAsync(adv, dbuf + n, sizeof(double) * n, cudaMemcpyDeviceToHost, st_));
+    SGB_CUDA(cudaMemcpyAsync(valid, dvalid, sizeof(int) * n_groups, cudaMemcpyDeviceToHost, st_));
+    SGB_CUDA(cudaStreamSynchronize(st_));
 }
 
 // Shared-prefix tiles for grouped rows; SGB_ATTN_GROUP=0 runs every row alone (bit-identical,
@@ -1436,6 +1461,7 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
     }
     res.hit_eos = h_eos;
     last_lens_ = len;  // the draft update can consume this rollout straight from HBM
+    last_plens_ = plen;
     for (int s = 0; s < n_seqs; ++s) {
         res.d2h_bytes += static_cast<long long>(len[s]) * sizeof(int);
         if (a.want_features) res.d2h_bytes += static_cast<long long>(len[s] - 1) * d * sizeof(float);

@@ -194,6 +194,14 @@ class Engine {
         const std::vector<std::array<int, 4>>* groups = nullptr;
     };
     void forward(const Fwd& f);
+
+  public:
+    // rewards (grpo.cpp:99-116) and standardized advantages (grpo.cpp:121-136) of the last
+    // rollout's groups, computed from its token table in HBM; valid[b] = 0 for filtered groups
+    void group_advantages(const long long* answers, int n_groups, int g, double eps_var, double* rewards, double* adv,
+                          int* valid);
+
+  private:
     void convert_target(const float* staging);
     void convert_draft();
     void alloc_rows();
@@ -293,7 +301,9 @@ class Engine {
         GemmAct act_fuse, act_a1, act_a2, act_ctx, act_hg, act_dx, act_dxmid, act_dfch, act_dqkv, act_dlog;
         GemmWeight w2_ref, w1_ref, wo_ref, wqkv_ref_w, lm_ref_w;
     } tr2_;
-    std::vector<int> last_lens_;  // token counts of the last rollout's sequences
+    std::vector<int> last_lens_;   // token counts of the last rollout's sequences
+    std::vector<int> last_plens_;  // and their prompt lengths
+    double* adv_buf_ = nullptr;    // [2 * max_rows] rewards + advantages of group_advantages
     void train_alloc();
     void train_refresh_ref_weights();
     void wgrad(const __nv_bfloat16* dyT, int N, const __nv_bfloat16* xT, int Kfeat, int Rp, float* grad_dst, int ld);

@@ -73,6 +73,11 @@ void launch_attention(const float* q, const __nv_bfloat16* K, const __nv_bfloat1
                       const AttnRowsDev& rows, int M, int H, int d, int max_virtual_len, double total_keys,
                       const AttnScratch& sc, __nv_bfloat16* out, cudaStream_t st);
 
+// ---- rewards.cu: per-sequence task reward and per-group standardized advantages
+void launch_group_advantages(int n_groups, int g, const int* tok, long long stride, const int* len, const int* plen,
+                             const long long* answer, double eps_var, double* rewards, double* adv, int* valid,
+                             cudaStream_t st);
+
 // ---- sample.cu
 // Per-(row, chunk) records + per-row tickets of the multi-CTA row reductions.
 struct RowScratch {
