@@ -295,12 +295,20 @@ __global__ void __launch_bounds__(threads_for(BN), 1)
         pdl_wait();
         pdl_trigger();
         if (lane == 0) {
-            constexpr uint32_t idesc = idesc_bf16_m128(BN);
+            // MMA width = the tile's valid token rows rounded up to 16 (tcgen05 N granularity):
+            // a 211-row tile issues 224-wide MMAs, not 256. Output columns are independent, so
+            // the width never changes an element's bits (test_gemm_batch_invariance).
+            uint32_t idesc = idesc_bf16_m128(BN);
             StageSeq sq = seq0;
             int i = 0, it = -1, cur_c = -1, cur_u = -1;
             for (; sq.valid(); ++i) {
                 const bool chunk_start = (sq.u != cur_u || sq.c != cur_c);
                 if (chunk_start) {
+                    if (sq.u != cur_u) {
+                        const int rows = M - decode_unit(sq.u, m_tiles, S, BN).m0;
+                        const int n_eff = min(BN, max(16, (rows + 15) / 16 * 16));
+                        idesc = idesc_bf16_m128(static_cast<uint32_t>(n_eff));
+                    }
                     cur_u = sq.u;
                     cur_c = sq.c;
                     ++it;
