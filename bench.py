@@ -423,6 +423,9 @@ def main():
     roofline = {"bound": "hbm", "kernel": "attn_kernel (mma.sync tree/paged KV attention: shared-prefix tiles, bulk-DMA ring, in-kernel block merge)",
                 "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s", "frac": round(ach / hbm, 4),
                 "traffic": traffic, "traffic_algorithmic": traffic_alg, "traffic_source": traffic_src,
+                "achieved_note": "algorithmic bytes = each sequence's context K/V per layer (SURVEY 8d), prompt "
+                                 "included; at <= 16 heads the G members of a group stage their shared prompt "
+                                 "once per tile, so DRAM bytes are below the algorithmic bytes",
                 "peak_source": src,
                 "share_of_step": round(att["ms"] / total_ms, 4) if total_ms else None,
                 "measured": "per-launch CUDA events on the engine stream, one profiled rollout after the timed steps",

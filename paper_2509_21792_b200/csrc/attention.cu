@@ -133,8 +133,11 @@ __global__ void __launch_bounds__(32 * (kMaxCons + 1), 1)
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + 2 * nst * stage_bytes);
     uint64_t* empty = full + nst;
     int* flag = reinterpret_cast<int*>(empty + nst);  // [kMaxTileRows]
-    int* tsum = flag + kMaxTileRows;                   // [blockDim.x + 1]
-    int* loc = tsum + blockDim.x + 1;                  // [2] start tile, start item offset
+    int* tsum = flag + kMaxTileRows;                   // [blockDim.x + 1] item-count scan
+    int* loc = tsum + blockDim.x + 1;                  // [4] start tile, head group, block
+    long long* wsum = reinterpret_cast<long long*>(  // [blockDim.x + 1] weight scan
+        (reinterpret_cast<uintptr_t>(loc + 4) + 7) & ~uintptr_t(7));
+    long long* locl = wsum + blockDim.x + 1;          // [2] first item, end item
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n_cons = HG * QW;
@@ -156,65 +159,111 @@ __global__ void __launch_bounds__(32 * (kMaxCons + 1), 1)
     pdl_wait();
     pdl_trigger();
     const TileView tv{tiles, rows.ctx_len, rows.chain_len};
-    // ---- item counts per thread slice of tiles, exclusive scan over slices
+    // ---- work split. Items are (tile, head group, block), tiles in order; an item weighs its
+    // 16-key chunks + 1 (shared tiles 5, a tree row's boundary block as few as 2), and CTA c
+    // takes the items whose starting weight lies in [c*W/grid, (c+1)*W/grid): equal work per
+    // CTA whatever the mix of shared and per-row tiles.
     const int per = (n_tiles + nthr - 1) / nthr;
     const int t0 = min(n_tiles, static_cast<int>(threadIdx.x) * per), t1 = min(n_tiles, t0 + per);
+    auto lv_of = [&](const AttnTileDev& tl) { return rows.ctx_len[tl.row0] + rows.chain_len[tl.row0]; };
+    auto item_w = [&](const AttnTileDev& tl, int lv, int b) -> int {
+        if (tl.nrows > 1) return kBlock / kChunk + 1;
+        const int keys = min(kBlock, max(0, lv - b * kBlock));
+        return (keys + kChunk - 1) / kChunk + 1;
+    };
+    auto tile_w = [&](const AttnTileDev& tl, int lv) -> long long {
+        long long w = 0;
+        for (int b = tl.blo; b < tl.bhi; ++b) w += item_w(tl, lv, b);
+        return w;
+    };
     int own = 0;
+    long long ownw = 0;
     for (int t = t0; t < t1; ++t) {
         const AttnTileDev tl = tv.get(t);
         own += tl.bhi - tl.blo;
+        ownw += tile_w(tl, lv_of(tl));
     }
     tsum[threadIdx.x] = own;
+    wsum[threadIdx.x] = ownw;
     __syncthreads();
     if (warp == 0) {
         const int run = (nthr + 31) / 32;
-        int lsum = 0;
-        for (int t = lane * run; t < min(nthr, (lane + 1) * run); ++t) lsum += tsum[t];
-        int inc = lsum;
+        long long lsum = 0, lw = 0;
+        for (int t = lane * run; t < min(nthr, (lane + 1) * run); ++t) {
+            lsum += tsum[t];
+            lw += wsum[t];
+        }
+        long long inc = lsum, incw = lw;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= o) inc += y;
+            const long long y = __shfl_up_sync(0xffffffffu, inc, o);
+            const long long yw = __shfl_up_sync(0xffffffffu, incw, o);
+            if (lane >= o) {
+                inc += y;
+                incw += yw;
+            }
         }
-        int off = inc - lsum;
+        long long off = inc - lsum, offw = incw - lw;
         for (int t = lane * run; t < min(nthr, (lane + 1) * run); ++t) {
             const int v = tsum[t];
-            tsum[t] = off;
+            const long long vw = wsum[t];
+            tsum[t] = static_cast<int>(off);
+            wsum[t] = offw;
             off += v;
+            offw += vw;
         }
-        if (lane == 31) tsum[nthr] = inc;
+        if (lane == 31) {
+            tsum[nthr] = static_cast<int>(inc);
+            wsum[nthr] = incw;
+        }
     }
     __syncthreads();
     const long long T = static_cast<long long>(G) * tsum[nthr];
-    const long long i0 = T * blockIdx.x / gridDim.x, i1 = T * (blockIdx.x + 1) / gridDim.x;
-    if (i0 >= i1) return;
-    {
-        const long long s0 = static_cast<long long>(G) * tsum[threadIdx.x];
-        if (own > 0 && s0 <= i0 && i0 < s0 + static_cast<long long>(G) * own) {
-            long long c = s0;
-            for (int t = t0; t < t1; ++t) {
-                const AttnTileDev tl = tv.get(t);
-                const long long n = static_cast<long long>(G) * (tl.bhi - tl.blo);
-                if (i0 < c + n) {
+    const long long WT = static_cast<long long>(G) * wsum[nthr];
+    const long long w_lo = WT * blockIdx.x / gridDim.x, w_hi = WT * (blockIdx.x + 1) / gridDim.x;
+    if (threadIdx.x == 0) locl[1] = T;  // w_hi == WT: the end of the list
+    // the item holding weight position w (found by the thread whose tile slice holds it)
+    auto find = [&](long long w, bool lo) {
+        const long long c0 = static_cast<long long>(G) * wsum[threadIdx.x];
+        if (ownw == 0 || w < c0 || w >= c0 + static_cast<long long>(G) * ownw) return;
+        long long c = c0, base = static_cast<long long>(G) * tsum[threadIdx.x];
+        for (int t = t0; t < t1; ++t) {
+            const AttnTileDev tl = tv.get(t);
+            const int lv = lv_of(tl);
+            const long long wt = tile_w(tl, lv);
+            const int nb = tl.bhi - tl.blo;
+            if (w < c + static_cast<long long>(G) * wt) {
+                const int g = static_cast<int>((w - c) / wt);
+                long long rem = (w - c) - g * wt;
+                int b = tl.blo;
+                while (rem >= item_w(tl, lv, b)) rem -= item_w(tl, lv, b++);
+                const long long idx = base + static_cast<long long>(g) * nb + (b - tl.blo);
+                if (lo) {
                     loc[0] = t;
-                    loc[1] = static_cast<int>(i0 - c);
-                    break;
+                    loc[1] = g;
+                    loc[2] = b;
+                    locl[0] = idx;
+                } else {
+                    locl[1] = idx;
                 }
-                c += n;
+                return;
             }
+            c += static_cast<long long>(G) * wt;
+            base += static_cast<long long>(G) * nb;
         }
-    }
+    };
     __syncthreads();
+    if (w_lo < WT) find(w_lo, true);
+    if (w_hi < WT) find(w_hi, false);
+    __syncthreads();
+    if (w_lo >= WT || locl[1] <= locl[0]) return;
     ItemIt it0;
     it0.t = loc[0];
     it0.tl = tv.get(it0.t);
-    it0.lv = rows.ctx_len[it0.tl.row0] + rows.chain_len[it0.tl.row0];
-    {
-        const int nbt = it0.tl.bhi - it0.tl.blo;
-        it0.g = loc[1] / nbt;
-        it0.b = it0.tl.blo + loc[1] % nbt;
-    }
-    const int n_items = static_cast<int>(i1 - i0);
+    it0.lv = lv_of(it0.tl);
+    it0.g = loc[1];
+    it0.b = loc[2];
+    const int n_items = static_cast<int>(locl[1] - locl[0]);
     auto advance = [&](ItemIt& x) {
         if (++x.b == x.tl.bhi) {
             if (++x.g == G) {
@@ -457,7 +506,8 @@ void launch_impl(const float* q, const __nv_bfloat16* K, const __nv_bfloat16* V,
                  const AttnScratch& sc, __nv_bfloat16* out, cudaStream_t st) {
     auto stage_of = [&](int G) { return 2 * static_cast<size_t>(kChunk) * ((H / G) * DH * 2 + 16); };
     auto fixed_of = [&](int G) {
-        return static_cast<size_t>(8 * 8 + 4 * kMaxTileRows + 4 * (32 * (QW * H / G + 1) + 3)) + 128;
+        const size_t thr = 32 * (QW * H / G + 1);
+        return static_cast<size_t>(8 * 8 + 4 * kMaxTileRows + 4 * (thr + 5) + 8 + 8 * (thr + 3)) + 128;
     };
     auto next_div = [&](int g) {
         int g2 = g + 1;

@@ -115,19 +115,21 @@ __global__ void __launch_bounds__(kRowThreads)
             const int e = threadIdx.x + i * kRowThreads;
             acc[i] = e < d ? P[row + e] : 0.f;
         }
-        // four chunks per round of loads (w2 at the c2 shape has 12 chunks: 3 round trips)
+        // four chunks per round of loads (w2 at the c2 shape has 12 chunks: 3 round trips;
+        // eight per round measured slower), added strictly in chunk order
+        constexpr int CPR = 4;
         int s = 1;
-        for (; s + 4 <= S; s += 4) {
-            float pp[4][PER];
+        for (; s + CPR <= S; s += CPR) {
+            float pp[CPR][PER];
 #pragma unroll
-            for (int c = 0; c < 4; ++c)
+            for (int c = 0; c < CPR; ++c)
 #pragma unroll
                 for (int i = 0; i < PER; ++i) {
                     const int e = threadIdx.x + i * kRowThreads;
                     pp[c][i] = e < d ? P[(s + c) * st + row + e] : 0.f;
                 }
 #pragma unroll
-            for (int c = 0; c < 4; ++c)
+            for (int c = 0; c < CPR; ++c)
 #pragma unroll
                 for (int i = 0; i < PER; ++i) acc[i] += pp[c][i];
         }
