@@ -119,7 +119,7 @@ template <int DH>
 __global__ void __launch_bounds__(32 * (kMaxCons + 1), 1)
     attn_kernel(const float* __restrict__ q, const __nv_bfloat16* __restrict__ K, const __nv_bfloat16* __restrict__ V,
                 AttnRowsDev rows, const AttnTileDev* __restrict__ tiles, int n_tiles, int H, int d, int G, int QW,
-                int nst, int nb_max, float scale, float* __restrict__ part_acc, float* __restrict__ part_ml,
+                int nst, int nb_max, int balance, float scale, float* __restrict__ part_acc, float* __restrict__ part_ml,
                 int* __restrict__ row_ctr, __nv_bfloat16* __restrict__ out) {
     constexpr int NK = DH / 16;   // mma k-steps of S (dims) = m-tiles of O (dims)
     constexpr int DPL = DH / 32;  // merge: dims per lane
@@ -160,13 +160,14 @@ __global__ void __launch_bounds__(32 * (kMaxCons + 1), 1)
     pdl_trigger();
     const TileView tv{tiles, rows.ctx_len, rows.chain_len};
     // ---- work split. Items are (tile, head group, block), tiles in order; an item weighs its
-    // 16-key chunks + 1 (shared tiles 5, a tree row's boundary block as few as 2), and CTA c
-    // takes the items whose starting weight lies in [c*W/grid, (c+1)*W/grid): equal work per
-    // CTA whatever the mix of shared and per-row tiles.
+    // 16-key chunks + 1 (shared tiles 5, a tree row's boundary block as few as 2) -- or 1 each
+    // (balance == 0) -- and CTA c takes the items whose starting weight lies in
+    // [c*W/grid, (c+1)*W/grid).
     const int per = (n_tiles + nthr - 1) / nthr;
     const int t0 = min(n_tiles, static_cast<int>(threadIdx.x) * per), t1 = min(n_tiles, t0 + per);
     auto lv_of = [&](const AttnTileDev& tl) { return rows.ctx_len[tl.row0] + rows.chain_len[tl.row0]; };
     auto item_w = [&](const AttnTileDev& tl, int lv, int b) -> int {
+        if (!balance) return 1;  // count-based split
         if (tl.nrows > 1) return kBlock / kChunk + 1;
         const int keys = min(kBlock, max(0, lv - b * kBlock));
         return (keys + kChunk - 1) / kChunk + 1;
@@ -522,6 +523,14 @@ void launch_impl(const float* q, const __nv_bfloat16* K, const __nv_bfloat16* V,
         const char* v = getenv("SGB_ATTN_PERSM");  // tuning experiments only
         return v ? atoi(v) : 0;
     }();
+    static const int balance_env = [] {
+        const char* v = getenv("SGB_ATTN_BALANCE");  // A/B: 0 = by item count, 1 = by weight
+        return v ? atoi(v) : -1;
+    }();
+    // measured (scripts/bench_tree_attn.py, c3 rollouts): weighting pays when the shared tiles
+    // hold > 8 verify rows (B <= 16 at C_peak 211); with 2-3 rows per sequence the item count
+    // split is faster
+    const int balance = balance_env >= 0 ? balance_env : (QW >= 2 ? 1 : 0);
     static const int g_force = [] {
         const char* v = getenv("SGB_ATTN_G");  // tuning experiments only
         return v ? atoi(v) : 0;
@@ -572,7 +581,7 @@ void launch_impl(const float* q, const __nv_bfloat16* K, const __nv_bfloat16* V,
     if (static_cast<long long>(n_rows) * G > sc.ctr_cap) throw std::invalid_argument("attention: row tickets too small");
     const long long grid = std::max(1LL, std::min<long long>(est_items * G, 148LL * per_sm));
     launch_pdl(attn_kernel<DH>, dim3(static_cast<unsigned>(grid)), dim3(threads), smem, st, q, K, V, rows, tiles,
-               n_tiles, H, d, G, QW, nst, nb_max, 1.0f / sqrtf(static_cast<float>(DH)), sc.part_acc, sc.part_ml,
+               n_tiles, H, d, G, QW, nst, nb_max, balance, 1.0f / sqrtf(static_cast<float>(DH)), sc.part_acc, sc.part_ml,
                sc.row_ctr, out);
 }
 
