@@ -57,6 +57,9 @@ namespace {
 #ifndef SGB_KSUB128
 #define SGB_KSUB128 2
 #endif
+#ifndef SGB_GEMM_SMEM_KB
+#define SGB_GEMM_SMEM_KB 220  // stage ring budget: 3 x 72 KB stages for 16-32-token tiles
+#endif
 #ifndef SGB_CHUNK_MIN
 #define SGB_CHUNK_MIN 4
 #endif
@@ -74,7 +77,7 @@ struct GemmCfg {
     static constexpr int kSub = BN <= 32 ? SGB_KSUB32 : (BN == 64 ? SGB_KSUB64 : (BN == 128 ? SGB_KSUB128 : 1));
     static constexpr int kBBytes = BN * kBK * 2;
     static constexpr int kStage = kSub * (kABytes + kBBytes);
-    static constexpr int kStages = (200 * 1024) / kStage > 8 ? 8 : (200 * 1024) / kStage;
+    static constexpr int kStages = (SGB_GEMM_SMEM_KB * 1024) / kStage > 8 ? 8 : (SGB_GEMM_SMEM_KB * 1024) / kStage;
     static constexpr int kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;
     static constexpr int kSmem = kStages * kStage + 1024 /*align*/ + 256 /*barriers*/;
     static constexpr int kCQ = cq_for(BN);
