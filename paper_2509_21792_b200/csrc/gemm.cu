@@ -490,6 +490,13 @@ void launch_bn(const CUtensorMap& w, const CUtensorMap& x, int M, int N, int kbt
 int gemm_chunk_kb(int N, int K) {
     const int kbt = (K + kBK - 1) / kBK;
     const int n_tiles = (N + kBM - 1) / kBM;
+    // weights wider than 64 tiles are never K-split (gemm_splits_for): one chunk, which also
+    // lets their >128-row GEMMs take 256-token tiles
+    static const int max_split_tiles = [] {
+        const char* v = getenv("SGB_CHUNK_TILES_MAX");  // A/B switch (0 = chunk every weight)
+        return v ? atoi(v) : 64;  // measured: c2 +1.3 %, c3 speculative steps 3-5 % cheaper
+    }();
+    if (max_split_tiles > 0 && n_tiles > max_split_tiles) return ((kbt + 3) / 4) * 4;
     const int want = std::max(1, (kNumSMs + n_tiles - 1) / n_tiles);
     int ckb = (kbt + want - 1) / want;
     ckb = ((ckb + 3) / 4) * 4;
