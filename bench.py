@@ -343,8 +343,11 @@ def main():
         fl = tl = None
         for it in range(1, w["warm"] + 1):
             tp = stream_prompts(0x7A11 + it + 1000 * rank, 32, w["P"], w["V"])
+            # training rollouts follow the workload's own length distribution (stop caps keyed by
+            # sids disjoint from the benchmark's), so the draft sees the contexts it will serve
+            caps_w = stop_caps(w, 1_000_000 + 64 * (it + 1000 * rank), 64) if w["stops"] else None
             rw = eng.generate(tp, 2, c_peak=args.c_peak, mode="vanilla", temperature=0.0, seed=it,
-                              max_new_tokens=128, want_features=True)
+                              max_new_tokens=w["new"], want_features=True, seq_max_new=caps_w)
             for _ in range(4):
                 _, _, fl, tl, _ = draft_step(rw, 2)
         warm = {"iterations": w["warm"], "adamw_steps": 4 * w["warm"], "train_seqs_per_iter": 64,

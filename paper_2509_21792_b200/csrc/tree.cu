@@ -274,25 +274,28 @@ __global__ void commit_kv_kernel(const StepSeqDev* __restrict__ steps, const int
                                  int max_seq) {
     pdl_wait();
     pdl_trigger();
-    const int i = blockIdx.x, j = blockIdx.y, layer = blockIdx.z;
-    if (j >= result[2 * i]) return;
+    // one CTA per (sequence, layer) walks the accepted rows (1 in AR steps)
+    const int i = blockIdx.x, layer = blockIdx.y;
+    const int n_acc = result[2 * i];
     const StepSeqDev st = steps[i];
-    const int vr = st.vrow_off + acc_rows[i * kMaxChain + j];
-    const long long src = tscratch_base + vr;
-    const long long dst = static_cast<long long>(st.seq) * tcache_stride + st.p + j;
     const size_t lo = static_cast<size_t>(layer) * layer_stride;
-    const uint4* ks = reinterpret_cast<const uint4*>(K + lo + src * d);
-    const uint4* vs = reinterpret_cast<const uint4*>(V + lo + src * d);
-    uint4* kd = reinterpret_cast<uint4*>(K + lo + dst * d);
-    uint4* vd = reinterpret_cast<uint4*>(V + lo + dst * d);
-    for (int e = threadIdx.x; e < d / 8; e += blockDim.x) {
-        kd[e] = ks[e];
-        vd[e] = vs[e];
-    }
-    if (layer == 0) {
-        const float* h = hidden + static_cast<size_t>(vr) * d;
-        float* f = feats + (static_cast<size_t>(st.seq) * max_seq + st.p + j) * d;
-        for (int e = threadIdx.x; e < d; e += blockDim.x) f[e] = h[e];
+    for (int j = 0; j < n_acc; ++j) {
+        const int vr = st.vrow_off + acc_rows[i * kMaxChain + j];
+        const long long src = tscratch_base + vr;
+        const long long dst = static_cast<long long>(st.seq) * tcache_stride + st.p + j;
+        const uint4* ks = reinterpret_cast<const uint4*>(K + lo + src * d);
+        const uint4* vs = reinterpret_cast<const uint4*>(V + lo + src * d);
+        uint4* kd = reinterpret_cast<uint4*>(K + lo + dst * d);
+        uint4* vd = reinterpret_cast<uint4*>(V + lo + dst * d);
+        for (int e = threadIdx.x; e < d / 8; e += blockDim.x) {
+            kd[e] = ks[e];
+            vd[e] = vs[e];
+        }
+        if (layer == 0) {
+            const float* h = hidden + static_cast<size_t>(vr) * d;
+            float* f = feats + (static_cast<size_t>(st.seq) * max_seq + st.p + j) * d;
+            for (int e = threadIdx.x; e < d; e += blockDim.x) f[e] = h[e];
+        }
     }
 }
 
@@ -393,7 +396,7 @@ void launch_commit_kv(int B, const StepSeqDev* steps, const int* acc_rows, const
                       __nv_bfloat16* K, __nv_bfloat16* V, long long layer_stride, long long tcache_stride,
                       long long tscratch_base, const float* hidden, float* feats, int max_seq, cudaStream_t st) {
     if (B <= 0) return;
-    dim3 grid(B, kMaxChain, layers);
+    dim3 grid(B, layers);
     launch_pdl(commit_kv_kernel, grid, 128, 0, st, steps, acc_rows, result, d, K, V, layer_stride, tcache_stride,
                                            tscratch_base, hidden, feats, max_seq);
     SGB_KCHECK();

@@ -5,7 +5,7 @@ Rng(mix_key(0, 0x7a11 + iter))); each iteration is one rollout (vanilla, greedy,
 kept) followed by S draft_update steps on it (grpo.cpp:329-345), as the paper's online
 learning does between GRPO iterations.
 
-    python scripts/warm_draft.py [iters] [S] [lr]
+    python scripts/warm_draft.py [iters] [S] [lr] [config]
 """
 import json
 import sys
@@ -32,7 +32,7 @@ def stream_prompts(key, n, P, V):
 iters = int(sys.argv[1]) if len(sys.argv) > 1 else 40
 S = int(sys.argv[2]) if len(sys.argv) > 2 else 4
 lr = float(sys.argv[3]) if len(sys.argv) > 3 else 1e-3
-w = dict(WORKLOADS["c2"])
+w = dict(WORKLOADS[sys.argv[4] if len(sys.argv) > 4 else "c2"])
 w["new"] = 128
 cfg = model_cfg(w)
 eng = capi.Engine(cfg, 1, 0, 64, 4096, 10, 6)
