@@ -298,7 +298,9 @@ int grid_for(size_t n, int threads) {
     do {                                                                                 \
         if ((d) <= 256) KERNEL<1><<<__VA_ARGS__>>>;                                      \
         else if ((d) <= 1024) KERNEL<4><<<__VA_ARGS__>>>;                                \
+        else if ((d) <= 1536) KERNEL<6><<<__VA_ARGS__>>>;                                \
         else if ((d) <= 2048) KERNEL<8><<<__VA_ARGS__>>>;                                \
+        else if ((d) <= 3584) KERNEL<14><<<__VA_ARGS__>>>;                               \
         else if ((d) <= 4096) KERNEL<16><<<__VA_ARGS__>>>;                               \
         else KERNEL<kMaxPerThread><<<__VA_ARGS__>>>;                                     \
     } while (0)
@@ -310,7 +312,9 @@ void launch_embed_ln(const int* tokens, const int* positions, int M, int d, cons
 #define ARGS , dim3(M), dim3(kRowThreads), 0, st, tokens, positions, d, tok_emb, pos_emb, g, b, x, a
     if (d <= 256) launch_pdl(embed_ln_kernel<1> ARGS);
     else if (d <= 1024) launch_pdl(embed_ln_kernel<4> ARGS);
+    else if (d <= 1536) launch_pdl(embed_ln_kernel<6> ARGS);  // exact per-thread counts: fewer registers
     else if (d <= 2048) launch_pdl(embed_ln_kernel<8> ARGS);
+    else if (d <= 3584) launch_pdl(embed_ln_kernel<14> ARGS);
     else if (d <= 4096) launch_pdl(embed_ln_kernel<16> ARGS);
     else launch_pdl(embed_ln_kernel<kMaxPerThread> ARGS);
 #undef ARGS
@@ -324,7 +328,9 @@ void launch_reduce_residual_ln(const float* P, int S, int M, int d, float* x, bo
 #define ARGS , dim3(M), dim3(kRowThreads), 0, st, P, S, M, d, x, accumulate ? 1 : 0, pos_emb, positions, g, b, a, y
     if (d <= 256) launch_pdl(reduce_residual_ln_kernel<1> ARGS);
     else if (d <= 1024) launch_pdl(reduce_residual_ln_kernel<4> ARGS);
+    else if (d <= 1536) launch_pdl(reduce_residual_ln_kernel<6> ARGS);  // exact per-thread counts: fewer registers
     else if (d <= 2048) launch_pdl(reduce_residual_ln_kernel<8> ARGS);
+    else if (d <= 3584) launch_pdl(reduce_residual_ln_kernel<14> ARGS);
     else if (d <= 4096) launch_pdl(reduce_residual_ln_kernel<16> ARGS);
     else launch_pdl(reduce_residual_ln_kernel<kMaxPerThread> ARGS);
 #undef ARGS
