@@ -199,6 +199,11 @@ int sgb_bench_attention(int B, int ctx, int H, int dh, int iters, double* ms_out
 int sgb_debug_attention(int B, const int* n_keys, int H, int dh, const float* q, const float* k, const float* v,
                         float* out);
 
+/* target_forward_calls() (include/sgrpo/tinylm.hpp:288-291): cumulative target forward
+ * LAUNCHES of this engine (one per prefill chunk / decode step / forward_target call, not one
+ * per sequence); the draft update never runs the target (SPEC acceptance criterion 10). */
+int sgb_target_forward_calls(sgb_engine* e, long long* out);
+
 /* GRPO rewards and advantages of the LAST rollout's groups, from its token table in HBM:
  * rewards[s] = compute_reward (src/grpo.cpp:99-116) of sequence s's response (tokens after
  * its prompt, scored against answers[s / g] = a + b of query s / g, call site grpo.cpp:352-363);

@@ -61,7 +61,7 @@ EXPORTED = ["sgb_last_error", "sgb_version", "sgb_device_count", "sgb_engine_cre
             "sgb_cache_reset", "sgb_cache_len", "sgb_cache_read", "sgb_cache_gather_tail", "sgb_forward_target",
             "sgb_forward_draft_rows", "sgb_sample_rows", "sgb_topk_logsoftmax", "sgb_build_tree", "sgb_rollout",
             "sgb_debug_gemm", "sgb_profile_enable", "sgb_profile_read", "sgb_bench_gemm", "sgb_bench_attention",
-            "sgb_debug_attention", "sgb_debug_tree_attention", "sgb_bench_tree_attention", "sgb_group_advantages",
+            "sgb_debug_attention", "sgb_debug_tree_attention", "sgb_bench_tree_attention", "sgb_group_advantages", "sgb_target_forward_calls",
             "sgb_debug_group_advantages", "sgb_allgather_f64", "sgb_detect_knee", "sgb_measure_c_peak"]
 
 KERNEL_CLASSES = ["gemm_tcgen05", "attention", "rowops", "lm_head", "sample", "tree", "kv_commit"]
@@ -438,6 +438,12 @@ def _group_advantages(self, answers, g: int, eps_var: float = 1e-8):
     return r, a, v
 
 
+def _target_forward_calls(self) -> int:
+    n = C.c_longlong()
+    _check(_lib.sgb_target_forward_calls(self.h, C.byref(n)))
+    return n.value
+
+
 def _allgather_f64(self, vals, world: int):
     s = np.ascontiguousarray(vals, np.float64)
     out = np.zeros(s.size * world, np.float64)
@@ -461,6 +467,7 @@ Engine.nccl_init = _nccl_init
 Engine.allreduce_f64 = _allreduce_f64
 Engine.allreduce_i64 = _allreduce_i64
 Engine.group_advantages = _group_advantages
+Engine.target_forward_calls = _target_forward_calls
 Engine.allgather_f64 = _allgather_f64
 EXPORTED += ["sgb_nccl_unique_id", "sgb_nccl_init", "sgb_allreduce_sum_f64", "sgb_allreduce_sum_i64"]
 

@@ -335,6 +335,13 @@ int sgb_nccl_init(sgb_engine* e, int rank, int world, const unsigned char* id128
 }
 
 
+int sgb_target_forward_calls(sgb_engine* e, long long* out) {
+    return guarded([&] {
+        if (!out) throw std::invalid_argument("target_forward_calls: null output");
+        *out = E(e).target_forward_calls();
+    });
+}
+
 int sgb_group_advantages(sgb_engine* e, const long long* answers, int n_groups, int g, double eps_var,
                          double* rewards, double* advantages, int* valid) {
     return guarded([&] {

@@ -577,6 +577,7 @@ void Engine::forward(const Fwd& f) {
     if (M > max_rows_) throw std::invalid_argument("forward: rows exceed engine max_rows");
     if (f.max_vlen > max_vlen_cap_) throw std::out_of_range("forward: context beyond capacity");
     if (!target_ready_ || (f.draft && !draft_ready_)) throw std::runtime_error("weights not uploaded");
+    if (!f.draft) ++target_forward_calls_;  // target_forward_calls() (tinylm.hpp:288-291): one per launch
     const std::vector<LayerDev>& L = f.draft ? dL_ : tL_;
     KvStore& kv = f.draft ? dkv_ : tkv_;
     AttnRowsDev ar{rows_.ctx_base, rows_.ctx_len, rows_.chain_len, rows_.chain};

@@ -200,6 +200,8 @@ class Engine {
     // rollout's groups, computed from its token table in HBM; valid[b] = 0 for filtered groups
     void group_advantages(const long long* answers, int n_groups, int g, double eps_var, double* rewards, double* adv,
                           int* valid);
+    // cumulative count of target forward launches (the reference's target_forward_calls())
+    long long target_forward_calls() const { return target_forward_calls_; }
 
   private:
     void convert_target(const float* staging);
@@ -303,6 +305,7 @@ class Engine {
     } tr2_;
     std::vector<int> last_lens_;   // token counts of the last rollout's sequences
     std::vector<int> last_plens_;  // and their prompt lengths
+    long long target_forward_calls_ = 0;
     double* adv_buf_ = nullptr;    // [2 * max_rows] rewards + advantages of group_advantages
     void train_alloc();
     void train_refresh_ref_weights();
