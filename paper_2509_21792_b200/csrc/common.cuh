@@ -52,6 +52,13 @@ SGB_DEV void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c
         "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
         : "memory");
 }
+// L2-only prefetch of one box (no smem destination, no barrier)
+SGB_DEV void tma_prefetch_l2_2d(const CUtensorMap* map, int c0, int c1) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(c0), "r"(c1)
+                 : "memory");
+}
 // L2 cache-hinted variant (evict-first for streamed weights)
 SGB_DEV void tma_load_2d_hint(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, uint64_t policy) {
     asm volatile(

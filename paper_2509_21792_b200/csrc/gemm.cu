@@ -204,7 +204,7 @@ template <int BN, bool PART>
 __global__ void __launch_bounds__(threads_for(BN), 1)
     gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap mapW, const __grid_constant__ CUtensorMap mapX, int M,
                         int N, int kb_total, int n_chunks, int ckb, int cps, int S, int m_tiles, int n_tiles, GemmEpi epi,
-                        float* __restrict__ ws, int* __restrict__ ctr) {
+                        float* __restrict__ ws, int* __restrict__ ctr, int pf_boxes) {
     using Cfg = GemmCfg<BN>;
     constexpr int SUB = Cfg::kSub;
     extern __shared__ uint8_t smem_raw[];
@@ -268,6 +268,17 @@ __global__ void __launch_bounds__(threads_for(BN), 1)
                 pre_ns[npre] = ns;
                 pre_m0[npre] = un.m0;
                 sq.next(SUB);
+            }
+            // (1b) HBM-bound token tiles: the following weight boxes go to L2 as well, so the
+            // weight stream keeps running while the previous kernel drains (pf_boxes per CTA,
+            // sized by the host to a fraction of L2; the smem loads then hit in L2)
+            {
+                StageSeq pq = sq;
+                for (int n = 0; n < pf_boxes && pq.valid(); pq.next(SUB)) {
+                    const int ns = min(SUB, pq.hi - pq.kb);
+                    const Unit un = decode_unit(pq.u, m_tiles, S, BN);
+                    for (int j = 0; j < ns; ++j, ++n) tma_prefetch_l2_2d(&mapW, (pq.kb + j) * kBK, un.n0);
+                }
             }
             // (2) activations are produced by the previous kernel
             pdl_wait();
@@ -477,8 +488,17 @@ void launch_bn(const CUtensorMap& w, const CUtensorMap& x, int M, int N, int kbt
     const int m_tiles = (M + BN - 1) / BN, n_tiles = (N + kBM - 1) / kBM;
     const int units = m_tiles * n_tiles * S;
     const int grid = std::min(units, kNumSMs);
+    // L2 prefetch budget for the weight stream of HBM-bound (<= 32-token) tiles, in MB over
+    // the whole grid. A/B switch only, off by default: measured at the 7B shape, 48 MB made
+    // the one-token QKV GEMM 17.4 -> 19.6 us and the B = 1 AR step 3.19 -> 3.50 ms
+    // (profiles/r01_tail_b1_c3.txt)
+    static const int pf_mb = [] {
+        const char* v = getenv("SGB_L2_PF_MB");
+        return v ? atoi(v) : 0;
+    }();
+    const int pf_boxes = BN <= 32 ? static_cast<int>((static_cast<long long>(pf_mb) << 20) / grid / kABytes) : 0;
     launch_pdl(gemm_bf16_tn_kernel<BN, PART>, dim3(grid), dim3(Cfg::kThreads), Cfg::kSmem, st, w, x, M, N, kbt, n_chunks, ckb,
-               cps, S, m_tiles, n_tiles, epi, ws, ctr);
+               cps, S, m_tiles, n_tiles, epi, ws, ctr, pf_boxes);
 }
 
 }  // namespace
@@ -497,7 +517,10 @@ int gemm_chunk_kb(int N, int K) {
         return v ? atoi(v) : 64;  // measured: c2 +1.3 %, c3 speculative steps 3-5 % cheaper
     }();
     if (max_split_tiles > 0 && n_tiles > max_split_tiles) return ((kbt + 3) / 4) * 4;
-    const int want = std::max(1, (kNumSMs + n_tiles - 1) / n_tiles);
+    // at most floor(148 / n_tiles) splits fit one wave (gemm_splits_for), so the chunk count
+    // aims at that: a ceil here gave the 7B w2 six chunks, which only split 3 ways (84 CTAs,
+    // 104 k-blocks each); five chunks split 5 ways (140 CTAs, 60 k-blocks): M = 1 w2 31 -> ~22 us
+    const int want = std::max(1, kNumSMs / n_tiles);
     int ckb = (kbt + want - 1) / want;
     ckb = ((ckb + 3) / 4) * 4;
     ckb = std::max(ckb, SGB_CHUNK_MIN);

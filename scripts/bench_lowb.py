@@ -1,8 +1,9 @@
-"""Low-concurrency regime at the c2 shape: per-step device time of AR vs speculative steps
+"""Low-concurrency regime at the c2 (or --config c3) shape: per-step device time of AR vs speculative steps
 for B sequences (diagnostic for the concurrency-sweep tail). Timing runs are unprofiled; a
 second, profiled run gives the per-class split (events around every launch inflate it).
 
-    python scripts/bench_lowb.py [B ...] [--ncu]   (--ncu: one short run per mode, for ncu)
+    python scripts/bench_lowb.py [B ...] [--ncu] [--config=c3] [--vanilla]
+      (--ncu: one short run per mode, for ncu; --vanilla: AR steps only)
 """
 import json
 import sys
@@ -13,14 +14,16 @@ from paper_2509_21792_b200 import capi  # noqa: E402
 
 args = [a for a in sys.argv[1:] if not a.startswith("--")]
 ncu = "--ncu" in sys.argv
-w = dict(WORKLOADS["c2"])
+conf = next((a.split("=", 1)[1] for a in sys.argv[1:] if a.startswith("--config=")), "c2")
+modes = ("vanilla",) if "--vanilla" in sys.argv else ("vanilla", "adaptive_spec")
+w = dict(WORKLOADS[conf])
 cfg = model_cfg(w)
 eng = capi.Engine(cfg, 1, 0, 128, 2048, 10, 6)
 eng.init_random(1234)
 prompts = make_prompts(w, 0)
 for B in [int(x) for x in (args or ["1", "4", "16", "64"])]:
     pr = prompts[:B]
-    for mode in ("vanilla", "adaptive_spec"):
+    for mode in modes:
         kw = dict(c_peak=211, temperature=0.0, seed=7, max_new_tokens=8 if ncu else 48, want_features=False)
         eng.generate(pr, 1, mode=mode, **kw)  # warm
         if ncu:
