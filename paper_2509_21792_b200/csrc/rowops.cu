@@ -68,6 +68,39 @@ __device__ void block_ln(const float* xs, int d, const float* __restrict__ g, co
     }
 }
 
+// Same, gamma/beta already in registers (gs[i] = g[threadIdx.x + i*256]); identical bits.
+template <int PER>
+__device__ void block_ln_regs(const float* xs, int d, const float* gs, const float* bs, __nv_bfloat16* out_bf,
+                              float* out_f, float* red) {
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+        const int e = threadIdx.x + i * kRowThreads;
+        if (e < d) s += xs[i];
+    }
+    const float mu = block_sum(s, red) / static_cast<float>(d);
+    float v = 0.f;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+        const int e = threadIdx.x + i * kRowThreads;
+        if (e < d) {
+            const float dv = xs[i] - mu;
+            v += dv * dv;
+        }
+    }
+    const float var = block_sum(v, red) / static_cast<float>(d);
+    const float rstd = 1.0f / sqrtf(var + 1e-5f);
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+        const int e = threadIdx.x + i * kRowThreads;
+        if (e < d) {
+            const float y = gs[i] * (xs[i] - mu) * rstd + bs[i];
+            if (out_bf) out_bf[e] = __float2bfloat16(y);
+            if (out_f) out_f[e] = y;
+        }
+    }
+}
+
 template <int PER>
 __global__ void __launch_bounds__(kRowThreads) embed_ln_kernel(const int* __restrict__ tokens,
                                                              const int* __restrict__ positions, int d,
@@ -98,27 +131,58 @@ __global__ void __launch_bounds__(kRowThreads)
                               const float* __restrict__ pos_emb, const int* __restrict__ positions,
                               const float* __restrict__ g, const float* __restrict__ b, __nv_bfloat16* __restrict__ a,
                               float* __restrict__ y) {
+    __shared__ float red[kRowThreads / 32];
+    // LN parameters are weights, never written by the previous kernel: load them before the
+    // PDL wait, so that a one-row launch (the decode tail) pays one dependent round trip for
+    // partials + residual instead of four
+    float gs[PER], bs[PER];
+    if (g) {
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int e = threadIdx.x + i * kRowThreads;
+            gs[i] = e < d ? g[e] : 0.f;
+            bs[i] = e < d ? b[e] : 0.f;
+        }
+    }
     pdl_wait();
     pdl_trigger();
-    __shared__ float red[kRowThreads / 32];
     const int r = blockIdx.x;
     float xs[PER];
     const float* pe = pos_emb ? pos_emb + static_cast<size_t>(positions[r]) * d : nullptr;
     const size_t row = static_cast<size_t>(r) * d;
     if (P) {
-        // chunk partials, strictly in chunk order per element; the loads of two chunks for
-        // all of this thread's elements are in flight together
+        // chunk partials, strictly in chunk order per element: acc = P0, acc += P1, ... The
+        // first round loads chunks 0..CPR-1 together with the residual row; later rounds load
+        // CPR chunks at a time (w2 at the c2 shape has 12 chunks: 3 round trips; eight per
+        // round measured slower)
         const size_t st = static_cast<size_t>(M) * d;
-        float acc[PER];
-#pragma unroll
-        for (int i = 0; i < PER; ++i) {
-            const int e = threadIdx.x + i * kRowThreads;
-            acc[i] = e < d ? P[row + e] : 0.f;
-        }
-        // four chunks per round of loads (w2 at the c2 shape has 12 chunks: 3 round trips;
-        // eight per round measured slower), added strictly in chunk order
         constexpr int CPR = 4;
-        int s = 1;
+        float acc[PER], xr[PER];
+        {
+            const int n0 = min(S, CPR);
+            float pp[CPR][PER];
+#pragma unroll
+            for (int i = 0; i < PER; ++i) {
+                const int e = threadIdx.x + i * kRowThreads;
+                xr[i] = (accumulate && e < d) ? x[row + e] : 0.f;
+            }
+#pragma unroll
+            for (int c = 0; c < CPR; ++c)
+#pragma unroll
+                for (int i = 0; i < PER; ++i) {
+                    const int e = threadIdx.x + i * kRowThreads;
+                    pp[c][i] = (c < n0 && e < d) ? P[c * st + row + e] : 0.f;
+                }
+#pragma unroll
+            for (int i = 0; i < PER; ++i) acc[i] = pp[0][i];
+#pragma unroll
+            for (int c = 1; c < CPR; ++c)
+                if (c < n0) {
+#pragma unroll
+                    for (int i = 0; i < PER; ++i) acc[i] += pp[c][i];
+                }
+        }
+        int s = min(S, CPR);
         for (; s + CPR <= S; s += CPR) {
             float pp[CPR][PER];
 #pragma unroll
@@ -158,7 +222,7 @@ __global__ void __launch_bounds__(kRowThreads)
         for (int i = 0; i < PER; ++i) {
             const int e = threadIdx.x + i * kRowThreads;
             if (e < d) {
-                float v = accumulate ? x[row + e] + acc[i] : acc[i];
+                float v = accumulate ? xr[i] + acc[i] : acc[i];
                 if (pe) v += pe[e];
                 x[row + e] = v;
                 xs[i] = v;
@@ -174,8 +238,8 @@ __global__ void __launch_bounds__(kRowThreads)
         }
     }
     if (g)
-        block_ln<PER>(xs, d, g, b, a ? a + static_cast<size_t>(r) * d : nullptr, y ? y + static_cast<size_t>(r) * d : nullptr,
-                      red);
+        block_ln_regs<PER>(xs, d, gs, bs, a ? a + static_cast<size_t>(r) * d : nullptr,
+                           y ? y + static_cast<size_t>(r) * d : nullptr, red);
 }
 
 __device__ __forceinline__ float gelu_tanh(float x) {
