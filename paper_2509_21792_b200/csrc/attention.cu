@@ -105,14 +105,14 @@ struct TileView {
     __device__ int row_blocks(int r) const { return (ctx_len[r] + chain_len[r] + kBlock - 1) / kBlock; }
     __device__ AttnTileDev get(int t) const {
         if (tiles) return tiles[t];
-        return AttnTileDev{t, 1, 0, row_blocks(t)};
+        return AttnTileDev{t, 1, 0, row_blocks(t), -1};
     }
 };
 
 struct ItemIt {
     int t, g, b;
     AttnTileDev tl;
-    int lv;  // virtual length of the tile's first row (1-row tiles: the row's key count)
+    int lv;  // the longest virtual length among the tile's rows (1-row tiles: the row's key count)
 };
 
 template <int DH>
@@ -165,9 +165,21 @@ __global__ void __launch_bounds__(32 * (kMaxCons + 1), 1)
     // [c*W/grid, (c+1)*W/grid).
     const int per = (n_tiles + nthr - 1) / nthr;
     const int t0 = min(n_tiles, static_cast<int>(threadIdx.x) * per), t1 = min(n_tiles, t0 + per);
-    auto lv_of = [&](const AttnTileDev& tl) { return rows.ctx_len[tl.row0] + rows.chain_len[tl.row0]; };
+    auto lv_of = [&](const AttnTileDev& tl) {
+        int lv = rows.ctx_len[tl.row0] + rows.chain_len[tl.row0];
+        if (tl.bsh >= 0)
+            for (int j = 1; j < tl.nrows; ++j) lv = max(lv, rows.ctx_len[tl.row0 + j] + rows.chain_len[tl.row0 + j]);
+        return lv;
+    };
     auto item_w = [&](const AttnTileDev& tl, int lv, int b) -> int {
         if (!balance) return 1;  // count-based split
+        if (tl.nrows > 1 && tl.bsh >= 0 && b == tl.bhi - 1) {
+            // boundary block: chunks inside the common prefix once, the rest once per row
+            const int kb = b * kBlock, ve = min(kb + kBlock, lv);
+            const int nsh = min(max(0, (tl.bsh - kb) / kChunk), (ve - kb + kChunk - 1) / kChunk);
+            const int ncp = (ve - kb + kChunk - 1) / kChunk;
+            return nsh + (ncp - nsh) * tl.nrows + 1;
+        }
         if (tl.nrows > 1) return kBlock / kChunk + 1;
         const int keys = min(kBlock, max(0, lv - b * kBlock));
         return (keys + kChunk - 1) / kChunk + 1;
@@ -272,7 +284,7 @@ __global__ void __launch_bounds__(32 * (kMaxCons + 1), 1)
                 ++x.t;
                 if (x.t < n_tiles) {
                     x.tl = tv.get(x.t);
-                    x.lv = rows.ctx_len[x.tl.row0] + rows.chain_len[x.tl.row0];
+                    x.lv = lv_of(x.tl);
                 }
             }
             x.b = x.tl.blo;
@@ -281,8 +293,13 @@ __global__ void __launch_bounds__(32 * (kMaxCons + 1), 1)
     // the keys of item x: virtual [64b, v_end); v_end <= 64b when the row has no such block
     auto item_end = [&](const ItemIt& x) -> int {
         const int kb = x.b * kBlock;
-        if (x.tl.nrows > 1) return kb + kBlock;  // shared blocks lie inside the committed prefix
+        if (x.tl.nrows > 1 && !(x.tl.bsh >= 0 && x.b == x.tl.bhi - 1))
+            return kb + kBlock;  // shared blocks lie inside the committed prefix
         return min(kb + kBlock, x.lv);
+    };
+    // a chunk of a boundary block past the common prefix: staged once per tile row
+    auto per_row_chunk = [&](const ItemIt& x, int v0) {
+        return x.tl.nrows > 1 && x.tl.bsh >= 0 && x.b == x.tl.bhi - 1 && v0 + kChunk > x.tl.bsh;
     };
 
     if (warp == n_cons) {
@@ -305,20 +322,35 @@ __global__ void __launch_bounds__(32 * (kMaxCons + 1), 1)
                 pre_base = rows.pre_len ? rows.pre_base[r] : 0;
             }
             const size_t col = static_cast<size_t>(x.g) * HG * DH;
-            for (int v0 = x.b * kBlock; v0 < ve; v0 += kChunk, ++i) {
+            // one stage: keys [v0, v0 + nk) of a row with the given key map
+            auto stage = [&](int v0, int nk, int c_len, long long c_base, int p_len, long long p_base,
+                             const long long* ch) {
                 const int s = i % nst;
                 if (i >= nst) mbar_wait(&empty[s], ((i / nst) & 1) ^ 1);
-                const int nk = min(kChunk, ve - v0);
                 if (lane == 0) mbar_arrive_expect_tx(&full[s], 2u * row_bytes * nk);
                 __syncwarp();
                 if (lane < nk) {
                     const int v = v0 + lane;
-                    const long long slot = v < ctx_len ? (v < pre_len ? pre_base : ctx_base) + v : chain[v - ctx_len];
+                    const long long slot = v < c_len ? (v < p_len ? p_base : c_base) + v : ch[v - c_len];
                     const size_t src = static_cast<size_t>(slot) * d + col;
                     bulk_g2s(Ks + static_cast<size_t>(s) * stage_bytes + static_cast<size_t>(lane) * rowb, K + src,
                              row_bytes, &full[s]);
                     bulk_g2s(Vs + static_cast<size_t>(s) * stage_bytes + static_cast<size_t>(lane) * rowb, V + src,
                              row_bytes, &full[s]);
+                }
+                ++i;
+            };
+            for (int v0 = x.b * kBlock; v0 < ve; v0 += kChunk) {
+                if (!per_row_chunk(x, v0)) {
+                    stage(v0, min(kChunk, ve - v0), ctx_len, ctx_base, pre_len, pre_base, chain);
+                    continue;
+                }
+                for (int j = 0; j < x.tl.nrows; ++j) {
+                    const int rj = r + j;
+                    const int cl = rows.ctx_len[rj];
+                    const int nk = max(0, min(kChunk, cl + rows.chain_len[rj] - v0));
+                    stage(v0, nk, cl, rows.ctx_base[rj], rows.pre_len ? rows.pre_len[rj] : 0,
+                          rows.pre_len ? rows.pre_base[rj] : 0, rows.chain_slots + static_cast<size_t>(rj) * kMaxChain);
                 }
             }
         }
@@ -364,7 +396,8 @@ __global__ void __launch_bounds__(32 * (kMaxCons + 1), 1)
             float o[NK][4];
 #pragma unroll
             for (int mt = 0; mt < NK; ++mt) o[mt][0] = o[mt][1] = o[mt][2] = o[mt][3] = 0.f;
-            for (int v0 = kb; v0 < ve; v0 += kChunk, ++i) {
+            // one staged chunk; e0 / e1 = key end of this lane's query columns 2t4 / 2t4+1
+            auto chunk = [&](int v0, int e0, int e1) {
                 const int s = i % nst;
                 mbar_wait(&full[s], (i / nst) & 1);
                 const uint32_t kst = ks_base + static_cast<uint32_t>(s * stage_bytes);
@@ -377,11 +410,11 @@ __global__ void __launch_bounds__(32 * (kMaxCons + 1), 1)
                     ldsm_x4(kst + k_lane + ks * 32, a);
                     mma16816(sc, a, qf[ks][0], qf[ks][1]);
                 }
-                const bool va = v0 + g8 < ve, vb = v0 + g8 + 8 < ve;
-                const float s0 = va ? attn_scale(sc[0], scale) : -INFINITY;  // key g8,   query 2t
-                const float s1 = va ? attn_scale(sc[1], scale) : -INFINITY;  // key g8,   query 2t+1
-                const float s2 = vb ? attn_scale(sc[2], scale) : -INFINITY;  // key g8+8, query 2t
-                const float s3 = vb ? attn_scale(sc[3], scale) : -INFINITY;  // key g8+8, query 2t+1
+                const bool va0 = v0 + g8 < e0, va1 = v0 + g8 < e1, vb0 = v0 + g8 + 8 < e0, vb1 = v0 + g8 + 8 < e1;
+                const float s0 = va0 ? attn_scale(sc[0], scale) : -INFINITY;  // key g8,   query 2t
+                const float s1 = va1 ? attn_scale(sc[1], scale) : -INFINITY;  // key g8,   query 2t+1
+                const float s2 = vb0 ? attn_scale(sc[2], scale) : -INFINITY;  // key g8+8, query 2t
+                const float s3 = vb1 ? attn_scale(sc[3], scale) : -INFINITY;  // key g8+8, query 2t+1
                 float c0 = fmaxf(s0, s2), c1 = fmaxf(s1, s3);
 #pragma unroll
                 for (int o2 = 4; o2 < 32; o2 <<= 1) {
@@ -390,8 +423,8 @@ __global__ void __launch_bounds__(32 * (kMaxCons + 1), 1)
                 }
                 const float n0 = fmaxf(m0, c0), n1 = fmaxf(m1, c1);
                 const float a0 = attn_alpha(m0, n0), a1 = attn_alpha(m1, n1);
-                const float p0 = va ? attn_p(s0, n0) : 0.f, p1 = va ? attn_p(s1, n1) : 0.f;
-                const float p2 = vb ? attn_p(s2, n0) : 0.f, p3 = vb ? attn_p(s3, n1) : 0.f;
+                const float p0 = va0 ? attn_p(s0, n0) : 0.f, p1 = va1 ? attn_p(s1, n1) : 0.f;
+                const float p2 = vb0 ? attn_p(s2, n0) : 0.f, p3 = vb1 ? attn_p(s3, n1) : 0.f;
                 float ps0 = __fadd_rn(p0, p2), ps1 = __fadd_rn(p1, p3);
 #pragma unroll
                 for (int o2 = 4; o2 < 32; o2 <<= 1) {
@@ -417,6 +450,31 @@ __global__ void __launch_bounds__(32 * (kMaxCons + 1), 1)
                     o[mt][2] = __fmul_rn(o[mt][2], a0);
                     o[mt][3] = __fmul_rn(o[mt][3], a1);
                     mma16816(o[mt], va4[mt], b0, b1);
+                }
+                ++i;
+            };
+            for (int v0 = kb; v0 < ve; v0 += kChunk) {
+                if (!per_row_chunk(x, v0)) {
+                    chunk(v0, ve, ve);
+                    continue;
+                }
+                // boundary chunk past the common prefix: one stage per tile row, row j's keys.
+                // Only row j's query column is live (the others see -inf scores: alpha = 1,
+                // p = 0, an exact no-op on their state), so every column runs exactly the
+                // chunks its own 1-row item would, in the same order (identical bits).
+                for (int j = 0; j < x.tl.nrows; ++j) {
+                    const int cj = j - kQT * qt;
+                    if (cj < 0 || cj >= kQT) {
+                        const int s = i % nst;
+                        mbar_wait(&full[s], (i / nst) & 1);
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&empty[s]);
+                        ++i;
+                        continue;
+                    }
+                    const int rj = x.tl.row0 + j;
+                    const int lvj = rows.ctx_len[rj] + rows.chain_len[rj];
+                    chunk(v0, 2 * t4 == cj ? lvj : v0, 2 * t4 + 1 == cj ? lvj : v0);
                 }
             }
             // publish the block partial of every real query column
@@ -613,26 +671,39 @@ int attn_tile_qw(const std::vector<std::array<int, 4>>& groups) {
     return std::min(cap, (mx + kQT - 1) / kQT);
 }
 
-long long build_attn_tiles(const std::vector<std::array<int, 4>>& groups, std::vector<AttnTileDev>& out, int qw) {
+long long build_attn_tiles(const std::vector<std::array<int, 4>>& groups, std::vector<AttnTileDev>& out, int qw,
+                           bool boundary) {
     out.clear();
     long long n = 0;
     const int rows_per_tile = kQT * qw;
+    static const int bnd_env = [] {
+        const char* v = getenv("SGB_ATTN_BOUNDARY");  // A/B switch (0 = boundary blocks per row)
+        return v ? atoi(v) : 1;
+    }();
+    boundary = boundary && bnd_env != 0;
     for (const auto& g : groups) {
         const int row0 = g[0], nr = g[1], ctx_len = g[2], vmax = g[3];
         const int nb = attn_splits_for(vmax);
-        // blocks entirely inside the committed prefix are shared by the tile's rows
-        const int nsb = nr > 1 ? std::min(nb, ctx_len / kBlock) : 0;
+        // blocks entirely inside the committed prefix are shared by the tile's rows; with
+        // `boundary` so is the block holding the end of the prefix (its path chunks per row).
+        // Measured (scripts/bench_tree_attn.py, profiles/r01_tree_boundary.txt): it pays when
+        // that block starts with >= 1 whole prefix chunk, or with many rows per group; with
+        // a few rows and no shared chunk the per-row items run in parallel instead (12 heads,
+        // 16 x 13 rows, ctx 1100: 0.099 vs 0.123 ms)
+        const bool bnd = boundary && nr > 1 && (ctx_len % kBlock >= kChunk || nr > 2 * kQT);
+        const int nsb = nr > 1 ? std::min(nb, ctx_len / kBlock + (bnd ? 1 : 0)) : 0;
+        const int bsh = bnd ? ctx_len : -1;
         // ... and the blocks that reach into each row's own tree path run per row, listed
         // right after the row's shared tile so every CTA's slice mixes heavy and light items
         for (int o = 0; o < nr; o += rows_per_tile) {
             const int nt = std::min(rows_per_tile, nr - o);
             if (nsb > 0) {
-                out.push_back(AttnTileDev{row0 + o, nt, 0, nsb});
+                out.push_back(AttnTileDev{row0 + o, nt, 0, nsb, bsh});
                 n += nsb;
             }
             if (nb > nsb)
                 for (int r = o; r < o + nt; ++r) {
-                    out.push_back(AttnTileDev{row0 + r, 1, nsb, nb});
+                    out.push_back(AttnTileDev{row0 + r, 1, nsb, nb, -1});
                     n += nb - nsb;
                 }
         }

@@ -852,7 +852,7 @@ struct TreeAttnCase {
             cbase += ctx_len[g];
         }
         qw = sgb::attn_tile_qw(groups);
-        items = sgb::build_attn_tiles(groups, ht, qw);
+        items = sgb::build_attn_tiles(groups, ht, qw, true);
         n_tiles = static_cast<int>(ht.size());
         const int ns = sgb::attn_splits_for(max_vlen);
         K = static_cast<__nv_bfloat16*>(dev(static_cast<size_t>(slots) * d * 2));

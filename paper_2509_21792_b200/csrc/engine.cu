@@ -602,7 +602,7 @@ void Engine::forward(const Fwd& f) {
     long long n_items = 0;
     if (f.groups && group_attn_enabled(static_cast<int>(f.groups->size()), M)) {
         qw = attn_tile_qw(*f.groups);
-        n_items = build_attn_tiles(*f.groups, htiles_, qw);
+        n_items = build_attn_tiles(*f.groups, htiles_, qw, f.groups_exact);
         n_tiles = static_cast<int>(htiles_.size());
         if (n_tiles > 2 * max_rows_) throw std::logic_error("forward: attention tiles exceed capacity");
         h2d(tiles_, htiles_.data(), htiles_.size(), st_);
@@ -1317,6 +1317,7 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
                                 {drow[static_cast<size_t>(level - 2) * B + i], hs[i].k, hs[i].p, hs[i].p + level});
                         }
                     f.groups = &groups_;
+                    f.groups_exact = true;
                     forward(f);
                     res.draft_forwards++;
                     stat.draft_rows += R;
@@ -1352,6 +1353,7 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
                 {hs[i].vrow_off, hs[i].nsel, hs[i].p, hs[i].p + 1 + std::min(hs[i].l, hs[i].nsel - 1)});
             all_ar = all_ar && hs[i].nsel == 1;
         }
+        f.groups_exact = true;
         // measured A/B (SGB_PROMPT_TILES, bench.py vanilla): +5 % at 12 heads (c2), -13 % at
         // 28 heads (c3, where the per-row kernel already hits the prompt pages in L2)
         static const int prompt_tiles = [] {
@@ -1360,6 +1362,7 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
         }();
         const bool use_prompt_tiles = prompt_tiles < 0 ? dims_.heads <= 16 : prompt_tiles != 0;
         if (all_ar && a.g > 1 && use_prompt_tiles) {
+            f.groups_exact = false;  // members share only their prompt
             // AR step: the live members of a query group (consecutive rows) read their prompt's
             // K/V from the leader's copy, so they share the prompt blocks as one tile
             groups_.clear();

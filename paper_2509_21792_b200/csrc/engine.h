@@ -192,6 +192,9 @@ class Engine {
         // rows sharing one committed prefix: (row0, nrows, ctx_len, max virtual length); the
         // prefix blocks then run as shared tiles of up to 8 rows (attention.cu)
         const std::vector<std::array<int, 4>>* groups = nullptr;
+        // the groups' rows share exactly ctx_len keys (tree verify, draft levels; not the
+        // AR prompt groups): shared tiles also cover the prefix-end block (attention.cu)
+        bool groups_exact = false;
     };
     void forward(const Fwd& f);
 

@@ -55,14 +55,21 @@ int attn_splits_for(int max_virtual_len);
 // 64-key blocks [blo, bhi) -- one row, or up to 8*qw verify rows of one sequence over the
 // blocks inside its committed prefix (kAttnTileRows queries per mma tile).
 constexpr int kAttnTileRows = 8;
+// bsh >= 0 marks a boundary tile: its last block bhi-1 holds the end of the common prefix
+// (bsh keys) and then each row's own tree path; 16-key chunks inside [0, bsh) are staged
+// once for all rows, the chunks past it once per row (the row's own keys), so the tile's
+// rows no longer re-stream the prefix tail of that block one by one.
 struct AttnTileDev {
-    int row0, nrows, blo, bhi;
+    int row0, nrows, blo, bhi, bsh;
 };
 // groups: (row0, nrows, ctx_len, max virtual length) of rows sharing one committed prefix.
 // attn_tile_qw: 8-query tiles per CTA item for these groups; build_attn_tiles returns the
 // number of (tile, block) items of tiles of up to 8*qw rows
 int attn_tile_qw(const std::vector<std::array<int, 4>>& groups);
-long long build_attn_tiles(const std::vector<std::array<int, 4>>& groups, std::vector<AttnTileDev>& out, int qw);
+// boundary: the rows of a group share their first ctx_len keys exactly (tree verify, draft
+// levels), so shared tiles also take the block holding the end of the prefix (bsh)
+long long build_attn_tiles(const std::vector<std::array<int, 4>>& groups, std::vector<AttnTileDev>& out, int qw,
+                           bool boundary = false);
 void launch_attention_tiles(const float* q, const __nv_bfloat16* K, const __nv_bfloat16* V, long long kv_slots,
                             const AttnRowsDev& rows, int M, const AttnTileDev* tiles, int n_tiles, long long n_items,
                             int qw, int H, int d, int max_virtual_len, const AttnScratch& sc, __nv_bfloat16* out,
