@@ -571,6 +571,12 @@ static bool group_attn_enabled(int n_groups, int M) {
     return M >= 2 * n_groups;
 }
 
+// Prefix-end blocks inside the shared verify / draft-level tiles (attention.cu): measured
+// faster at 28 heads (B = 16 x 13 rows, ctx 680: 0.129 -> 0.098 ms per layer), slower at 12
+// heads, where fewer head groups leave the longer boundary item on the critical path (0.076 ->
+// 0.099 ms; profiles/r01_tree_boundary.txt)
+bool Engine::boundary_tiles() const { return dims_.heads > 16; }
+
 void Engine::forward(const Fwd& f) {
     const int M = f.M, d = dims_.d, F = dims_.dff, H = dims_.heads;
     if (M <= 0) return;
@@ -1317,7 +1323,7 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
                                 {drow[static_cast<size_t>(level - 2) * B + i], hs[i].k, hs[i].p, hs[i].p + level});
                         }
                     f.groups = &groups_;
-                    f.groups_exact = true;
+                    f.groups_exact = boundary_tiles();
                     forward(f);
                     res.draft_forwards++;
                     stat.draft_rows += R;
@@ -1353,7 +1359,7 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
                 {hs[i].vrow_off, hs[i].nsel, hs[i].p, hs[i].p + 1 + std::min(hs[i].l, hs[i].nsel - 1)});
             all_ar = all_ar && hs[i].nsel == 1;
         }
-        f.groups_exact = true;
+        f.groups_exact = boundary_tiles();
         // measured A/B (SGB_PROMPT_TILES, bench.py vanilla): +5 % at 12 heads (c2), -13 % at
         // 28 heads (c3, where the per-row kernel already hits the prompt pages in L2)
         static const int prompt_tiles = [] {

@@ -197,6 +197,7 @@ class Engine {
         bool groups_exact = false;
     };
     void forward(const Fwd& f);
+    bool boundary_tiles() const;
 
   public:
     // rewards (grpo.cpp:99-116) and standardized advantages (grpo.cpp:121-136) of the last
