@@ -2,7 +2,9 @@
 
     python scripts/bench_gemm.py                # c2 shapes x M sweep, auto split vs S=1
     python scripts/bench_gemm.py 211x1536x8960  # explicit MxNxK
+    SPLITS=-1,0 python scripts/bench_gemm.py ...  # -1 = kEpiPartials (raw chunk sums, the engine's wo/w2)
 """
+import os
 import ctypes as C
 import json
 import sys
@@ -17,7 +19,7 @@ if not shapes:
         for N, K in ((4608, 1536), (1536, 1536), (8960, 1536), (1536, 8960), (151936, 1536)):
             shapes.append((M, N, K))
 for M, N, K in shapes:
-    for sp in (0, 1):
+    for sp in [int(v) for v in os.environ.get("SPLITS", "0,1").split(",")]:
         ms = C.c_double()
         rc = lib.sgb_bench_gemm(M, N, K, sp, 30, C.byref(ms))
         if rc:

@@ -32,3 +32,26 @@ def test_random_rollouts_lossless():
             spec = e.generate(prompts, g, c_peak=int(rng.integers(8, 300)), mode="adaptive_spec", **kw)
         assert spec.tokens == van.tokens, trial
         assert spec.hit_eos == van.hit_eos, trial
+
+
+def test_wide_head_rollouts_lossless():
+    """> 16 heads: tree-verify and draft-level tiles also take the prefix-end block (attention.cu,
+    AttnTileDev.bsh), whose chunks past the common prefix are staged once per row. Prompt lengths
+    put the prefix end at every offset inside a 64-key block; spec must equal vanilla bit for bit."""
+    from oracle import oracle as O
+    from tests.gpu_common import capi
+    cfg = O.ModelConfig(vocab_size=512, d_model=28 * 64, n_layers=2, n_heads=28, d_ff=1024, max_seq_len=320, seed=2)
+    c = capi()
+    e = c.Engine(cfg, 1, 0, 16, 2048, 10, 6)
+    e.init_random(2024)
+    rng = np.random.default_rng(7)
+    for trial in range(8):
+        n_q = int(rng.integers(1, 4))
+        g = int(rng.choice([1, 2, 4]))
+        plen = int(rng.integers(60, 200))
+        prompts = [rng.integers(2, cfg.vocab_size, size=plen).tolist() for _ in range(n_q)]
+        kw = dict(temperature=float(trial % 2), seed=trial, max_new_tokens=int(rng.integers(20, 60)), want_features=False)
+        van = e.generate(prompts, g, c_peak=4, mode="vanilla", **kw)
+        spec = e.generate(prompts, g, c_peak=int(rng.choice([64, 211, 300])), mode="adaptive_spec", **kw)
+        assert spec.tokens == van.tokens, trial
+        assert sum(1 for s in spec.steps if s[1] > 1) > 0, trial  # speculative steps ran
