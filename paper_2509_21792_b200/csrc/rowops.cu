@@ -11,6 +11,8 @@
 //   tinylm.hpp:519-533  draft fuse concat(tok_emb, feature)          -> gather_fuse_kernel
 // Every kernel is row-local with a fixed reduction order, so a row's bits do not depend
 // on how many rows share the launch (batch invariance, SURVEY.md §7 hard part 1).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "util.h"
@@ -125,7 +127,8 @@ __global__ void __launch_bounds__(kRowThreads) embed_ln_kernel(const int* __rest
 }
 
 // x = (mode==0 ? 0 : x) + sum_s P[s][r] (+ pos_emb[pos[r]]); then LN -> a (bf16) / y (fp32).
-template <int PER>
+// FR: chunks loaded in the first round (with the residual row); CPR per later round.
+template <int PER, int FR = 4>
 __global__ void __launch_bounds__(kRowThreads)
     reduce_residual_ln_kernel(const float* __restrict__ P, int S, int M, int d, float* __restrict__ x, int accumulate,
                               const float* __restrict__ pos_emb, const int* __restrict__ positions,
@@ -159,15 +162,15 @@ __global__ void __launch_bounds__(kRowThreads)
         constexpr int CPR = 4;
         float acc[PER], xr[PER];
         {
-            const int n0 = min(S, CPR);
-            float pp[CPR][PER];
+            const int n0 = min(S, FR);
+            float pp[FR][PER];
 #pragma unroll
             for (int i = 0; i < PER; ++i) {
                 const int e = threadIdx.x + i * kRowThreads;
                 xr[i] = (accumulate && e < d) ? x[row + e] : 0.f;
             }
 #pragma unroll
-            for (int c = 0; c < CPR; ++c)
+            for (int c = 0; c < FR; ++c)
 #pragma unroll
                 for (int i = 0; i < PER; ++i) {
                     const int e = threadIdx.x + i * kRowThreads;
@@ -176,13 +179,13 @@ __global__ void __launch_bounds__(kRowThreads)
 #pragma unroll
             for (int i = 0; i < PER; ++i) acc[i] = pp[0][i];
 #pragma unroll
-            for (int c = 1; c < CPR; ++c)
+            for (int c = 1; c < FR; ++c)
                 if (c < n0) {
 #pragma unroll
                     for (int i = 0; i < PER; ++i) acc[i] += pp[c][i];
                 }
         }
-        int s = min(S, CPR);
+        int s = min(S, FR);
         for (; s + CPR <= S; s += CPR) {
             float pp[CPR][PER];
 #pragma unroll
@@ -392,7 +395,15 @@ void launch_reduce_residual_ln(const float* P, int S, int M, int d, float* x, bo
 #define ARGS , dim3(M), dim3(kRowThreads), 0, st, P, S, M, d, x, accumulate ? 1 : 0, pos_emb, positions, g, b, a, y
     if (d <= 256) launch_pdl(reduce_residual_ln_kernel<1> ARGS);
     else if (d <= 1024) launch_pdl(reduce_residual_ln_kernel<4> ARGS);
-    else if (d <= 1536) launch_pdl(reduce_residual_ln_kernel<6> ARGS);  // exact per-thread counts: fewer registers
+    else if (d <= 1536) {  // exact per-thread counts: fewer registers
+        static const int fr = [] {
+            const char* v = getenv("SGB_ROW_FR");  // A/B: chunks in the first load round
+            return v ? atoi(v) : 4;
+        }();
+        if (fr >= 12) launch_pdl(reduce_residual_ln_kernel<6, 12> ARGS);
+        else if (fr >= 6) launch_pdl(reduce_residual_ln_kernel<6, 6> ARGS);
+        else launch_pdl(reduce_residual_ln_kernel<6> ARGS);
+    }
     else if (d <= 2048) launch_pdl(reduce_residual_ln_kernel<8> ARGS);
     else if (d <= 3584) launch_pdl(reduce_residual_ln_kernel<14> ARGS);
     else if (d <= 4096) launch_pdl(reduce_residual_ln_kernel<16> ARGS);
