@@ -397,8 +397,11 @@ void launch_reduce_residual_ln(const float* P, int S, int M, int d, float* x, bo
     else if (d <= 1024) launch_pdl(reduce_residual_ln_kernel<4> ARGS);
     else if (d <= 1536) {  // exact per-thread counts: fewer registers
         static const int fr = [] {
-            const char* v = getenv("SGB_ROW_FR");  // A/B: chunks in the first load round
-            return v ? atoi(v) : 4;
+            // A/B: chunks in the first load round. Measured at c2 (profiles/r01_row_fr_c2.txt):
+            // 6 -> 45.1 k tok/s, rowops 682 ms/step; 4 -> 44.9 k, 798 ms; 12 -> 43.6 k (162
+            // registers: one CTA per SM)
+            const char* v = getenv("SGB_ROW_FR");
+            return v ? atoi(v) : 6;
         }();
         if (fr >= 12) launch_pdl(reduce_residual_ln_kernel<6, 12> ARGS);
         else if (fr >= 6) launch_pdl(reduce_residual_ln_kernel<6, 6> ARGS);
