@@ -408,7 +408,14 @@ void launch_reduce_residual_ln(const float* P, int S, int M, int d, float* x, bo
         else launch_pdl(reduce_residual_ln_kernel<6> ARGS);
     }
     else if (d <= 2048) launch_pdl(reduce_residual_ln_kernel<8> ARGS);
-    else if (d <= 3584) launch_pdl(reduce_residual_ln_kernel<14> ARGS);
+    else if (d <= 3584) {
+        static const int fr14 = [] {
+            const char* v = getenv("SGB_ROW_FR14");  // A/B: 5 = the 7B wo / w2 partials in one trip
+            return v ? atoi(v) : 4;
+        }();
+        if (fr14 >= 5) launch_pdl(reduce_residual_ln_kernel<14, 5> ARGS);
+        else launch_pdl(reduce_residual_ln_kernel<14> ARGS);
+    }
     else if (d <= 4096) launch_pdl(reduce_residual_ln_kernel<16> ARGS);
     else launch_pdl(reduce_residual_ln_kernel<kMaxPerThread> ARGS);
 #undef ARGS
