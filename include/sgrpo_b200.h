@@ -107,6 +107,18 @@ int sgb_forward_draft_rows(sgb_engine* e, int slot, const int* tokens, const flo
  * (the key verify derives, drafttree.cpp:184-190). */
 int sgb_sample_rows(sgb_engine* e, const float* logits, int rows, int vocab, double temperature,
                     const unsigned long long* seeds, const int* key_pos, int* out);
+/* sample_token<T> (tinylm.hpp:591-628) with the draw's uniform SUPPLIED per row (u = uniforms[i]
+ * * sum instead of Rng(key).uniform() * sum): the "identical logits and supplied uniforms" parity
+ * mode. Every CDF term is glibc's exp bit for bit; rows whose u lies within the fast path's
+ * summation-order error bound of a CDF boundary are redone in the reference's sequential order
+ * (exact_rows[i] = 1, optional). */
+int sgb_sample_rows_u(sgb_engine* e, const float* logits, int rows, int vocab, double temperature,
+                      const double* uniforms, int* out, int* exact_rows);
+/* Count of T > 0 draws (rollouts and sample calls) the engine resolved by the exact pass. */
+int sgb_exact_draws(sgb_engine* e, unsigned long long* out);
+/* The device's exp(): the restatement of glibc's exp (csrc/glibc_exp.cuh), for parity tests. */
+int sgb_debug_exp(sgb_engine* e, const double* x, size_t n, double* out);
+
 /* log_softmax_row<double> + topk_tokens (nn.hpp:172-180, drafttree.cpp:20-30). */
 int sgb_topk_logsoftmax(sgb_engine* e, const float* logits, int rows, int vocab, int k, int* tokens,
                         double* log_probs);

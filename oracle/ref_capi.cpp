@@ -214,6 +214,48 @@ int sgref_sample_token(const float* logits, int n, double temp, unsigned long lo
     return guarded([&] { *out = sample_token<float>(std::span<const float>(logits, n), temp, key); });
 }
 
+// Supplied-uniform mode (the exception to "forward only"): sample_token derives u from a key,
+// so the parity tests that place u at a chosen CDF boundary need lines 614-627 of tinylm.hpp
+// with `rng.uniform()` replaced by the supplied U -- nothing else changes (same std::exp, same
+// sequential sums, same comparison). Pinned against the real sample_token by the tests (U =
+// Rng(key).uniform() must give sample_token's token for every key).
+int sgref_sample_token_u(const float* logits, int n, double temperature, double U, int* out,
+                         double* sum_out, double* prefix_out) {
+    return guarded([&] {
+        double mx = -std::numeric_limits<double>::infinity();
+        for (int i = 0; i < n; ++i) mx = std::max(mx, double(logits[i]));
+        std::vector<double> p(n);
+        double sum = 0;
+        for (int i = 0; i < n; ++i) {
+            p[i] = std::exp((double(logits[i]) - mx) / temperature);
+            sum += p[i];
+        }
+        double u = U * sum;
+        double acc = 0;
+        if (prefix_out)
+            for (int i = 0; i < n; ++i) prefix_out[i] = acc += p[i];
+        acc = 0;
+        int tok = n - 1;
+        for (int i = 0; i < n; ++i) {
+            acc += p[i];
+            if (u < acc) {
+                tok = i;
+                break;
+            }
+        }
+        *out = tok;
+        if (sum_out) *sum_out = sum;
+    });
+}
+
+// std::exp of the reference's libm over an array (the host exp the device restates).
+void sgref_exp_array(const double* x, long long n, double* y) {
+    for (long long i = 0; i < n; ++i) y[i] = std::exp(x[i]);
+}
+
+// Rng(key).uniform() (rng.hpp:28-41)
+double sgref_uniform(unsigned long long key) { return Rng(key).uniform(); }
+
 // ---- drafttree (drafttree.cpp) ----------------------------------------------------
 long long sgref_max_candidates(int k, int l) { return max_candidates(k, l); }
 

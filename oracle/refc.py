@@ -190,6 +190,32 @@ def sample_token(logits, temp, key):
     return out.value
 
 
+def sample_token_u(logits, temp, U, want_prefix=False):
+    """tinylm.hpp:614-627 with the uniform supplied: (token, sum, sequential prefixes|None)."""
+    l = np.ascontiguousarray(logits, np.float32)
+    out = C.c_int()
+    s = C.c_double()
+    pre = np.zeros(l.size, np.float64) if want_prefix else None
+    check(lib().sgref_sample_token_u(_p(l, C.c_float), l.size, C.c_double(temp), C.c_double(U), C.byref(out),
+                                     C.byref(s), _p(pre, C.c_double)))
+    return out.value, s.value, pre
+
+
+def exp_array(x):
+    """std::exp (the reference host's libm) elementwise."""
+    xx = np.ascontiguousarray(x, np.float64)
+    y = np.zeros_like(xx)
+    lib().sgref_exp_array(_p(xx, C.c_double), C.c_longlong(xx.size), _p(y, C.c_double))
+    return y
+
+
+def uniform(key):
+    """Rng(key).uniform() (rng.hpp:28-41)."""
+    f = lib().sgref_uniform
+    f.restype = C.c_double
+    return f(C.c_ulonglong(key))
+
+
 def tree_arrays(tree):
     tok = np.array([n.token for n in tree], np.int32)
     par = np.array([n.parent for n in tree], np.int32)

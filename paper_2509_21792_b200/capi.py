@@ -529,3 +529,35 @@ def gen_stats_jsonl(r: "Rollout") -> str:
         out.append(json.dumps({"step": i, "b_cur": b, "spec_config": {"n_verify": n, "k_draft": k, "l_draft": l},
                                "accepted_total": acc, "sim_latency_s": sec}, separators=(",", ":")))
     return "".join(x + "\n" for x in out)
+
+
+def _sample_rows_u(self, logits, temperature: float, uniforms):
+    """sample_token with supplied uniforms (u = uniforms[i] * sum). Returns (tokens, exact_rows):
+    exact_rows[i] = 1 where the draw was resolved by the exact sequential pass."""
+    lg = np.ascontiguousarray(logits, np.float32)
+    rows, V = lg.shape
+    u = np.ascontiguousarray(uniforms, np.float64)
+    out = np.zeros(rows, np.int32)
+    ex = np.zeros(rows, np.int32)
+    _check(_lib.sgb_sample_rows_u(self.h, _p(lg, C.c_float), rows, V, C.c_double(temperature), _p(u, C.c_double),
+                                  _p(out, C.c_int), _p(ex, C.c_int)))
+    return out, ex
+
+
+def _exact_draws(self) -> int:
+    n = C.c_ulonglong()
+    _check(_lib.sgb_exact_draws(self.h, C.byref(n)))
+    return n.value
+
+
+def _debug_exp(self, x):
+    xx = np.ascontiguousarray(x, np.float64)
+    out = np.zeros_like(xx)
+    _check(_lib.sgb_debug_exp(self.h, _p(xx, C.c_double), C.c_size_t(xx.size), _p(out, C.c_double)))
+    return out
+
+
+Engine.sample_rows_u = _sample_rows_u
+Engine.exact_draws = _exact_draws
+Engine.debug_exp = _debug_exp
+EXPORTED += ["sgb_sample_rows_u", "sgb_exact_draws", "sgb_debug_exp"]

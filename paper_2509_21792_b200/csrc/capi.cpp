@@ -216,6 +216,22 @@ int sgb_sample_rows(sgb_engine* e, const float* logits, int rows, int vocab, dou
     return guarded([&] { E(e).emit(logits, rows, vocab, temperature, seeds, key_pos, out); });
 }
 
+int sgb_sample_rows_u(sgb_engine* e, const float* logits, int rows, int vocab, double temperature,
+                      const double* uniforms, int* out, int* exact_rows) {
+    return guarded([&] {
+        if (!uniforms) throw std::invalid_argument("sample_rows_u: uniforms required");
+        E(e).emit(logits, rows, vocab, temperature, nullptr, nullptr, out, uniforms, exact_rows);
+    });
+}
+
+int sgb_exact_draws(sgb_engine* e, unsigned long long* out) {
+    return guarded([&] { *out = E(e).exact_draws(); });
+}
+
+int sgb_debug_exp(sgb_engine* e, const double* x, size_t n, double* out) {
+    return guarded([&] { E(e).debug_exp(x, n, out); });
+}
+
 int sgb_topk_logsoftmax(sgb_engine* e, const float* logits, int rows, int vocab, int k, int* tokens,
                         double* log_probs) {
     return guarded([&] { E(e).topk_logsoftmax(logits, rows, vocab, k, tokens, log_probs); });

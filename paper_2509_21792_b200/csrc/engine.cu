@@ -253,7 +253,11 @@ Engine::Engine(const ModelDims& dims, int draft_layers, int device, int max_seqs
     rsc_.buf = dalloc<unsigned char>(rsc_.bytes);
     rsc_.ctr = dalloc<int>(R);
     rsc_.rowmax = dalloc<float>(R);
+    rsc_.exact = dalloc<int>(R);
+    rsc_.n_exact = dalloc<unsigned long long>(1);
     SGB_CUDA(cudaMemset(rsc_.ctr, 0, sizeof(int) * R));
+    SGB_CUDA(cudaMemset(rsc_.exact, 0, sizeof(int) * R));
+    SGB_CUDA(cudaMemset(rsc_.n_exact, 0, sizeof(unsigned long long)));
     max_vlen_cap_ = static_cast<int>(T) + kMaxChain;
     const int ns = attn_splits_for(max_vlen_cap_);
     pacc_ = dalloc<float>(R * d * ns);
@@ -310,7 +314,7 @@ Engine::~Engine() {
                     a2_, h_, fuse_, ws_.buf, ws_.ctr, logits_, pacc_, pml_, rows_.tok, rows_.pos, rows_.kv_dst,
                     rows_.ctx_base, rows_.ctx_len, rows_.chain_len, rows_.chain, rows_.feat_off, rows_.out_off,
                     rows_.key_pos, rows_.seed, rows_.par_row, rows_.pre_base, rows_.pre_len, lm_idx_, topk_tok_, topk_lp_, emitted_, acc_rows_,
-                    result_, err_, steps_, drow_, misc_i_, misc_l_, mask_dbg_, rsc_.buf, rsc_.ctr, rsc_.rowmax, asc_.row_ctr, gpart_};
+                    result_, err_, steps_, drow_, misc_i_, misc_l_, mask_dbg_, rsc_.buf, rsc_.ctr, rsc_.rowmax, rsc_.exact, rsc_.n_exact, asc_.row_ctr, gpart_};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (h_result_) cudaFreeHost(h_result_);
@@ -905,21 +909,51 @@ void Engine::forward_draft(int slot, const int* tokens, const float* prev_feat, 
 }
 
 void Engine::emit(const float* logits, int rows, int vocab, double temperature, const unsigned long long* seeds,
-                  const int* key_pos, int* out) {
+                  const int* key_pos, int* out, const double* uniforms, int* exact_rows) {
     if (vocab != dims_.vocab) throw std::invalid_argument("emit: vocab mismatch");
     if (rows <= 0 || rows > max_rows_) throw std::invalid_argument("emit: bad row count");
     if (temperature < 0) throw std::invalid_argument("sample_token: negative temperature");
     h2d(logits_, logits, static_cast<size_t>(rows) * vocab, st_);
-    h2d(rows_.seed, seeds, rows, st_);
-    h2d(rows_.key_pos, key_pos, rows, st_);
+    double* du = nullptr;
+    if (uniforms) {
+        for (int i = 0; i < rows; ++i)
+            if (!(uniforms[i] >= 0.0 && uniforms[i] < 1.0)) throw std::invalid_argument("sample: uniform outside [0, 1)");
+        du = reinterpret_cast<double*>(misc_l_);  // 2R + 2S words
+        h2d(du, uniforms, rows, st_);
+    } else {
+        h2d(rows_.seed, seeds, rows, st_);
+        h2d(rows_.key_pos, key_pos, rows, st_);
+    }
     SGB_CUDA(cudaMemsetAsync(err_, 0, sizeof(int), st_));
-    launch_emit(logits_, vocab, nullptr, rows_.seed, rows_.key_pos, rows, temperature, emitted_, err_, rsc_, st_);
+    launch_emit(logits_, vocab, nullptr, rows_.seed, rows_.key_pos, rows, temperature, emitted_, err_, rsc_, st_, du);
     d2h(out, emitted_, rows, st_);
+    if (exact_rows) {
+        if (temperature > 0) d2h(exact_rows, rsc_.exact, rows, st_);
+        else std::fill(exact_rows, exact_rows + rows, 0);
+    }
     int err = 0;
     d2h(&err, err_, 1, st_);
     SGB_CUDA(cudaStreamSynchronize(st_));
     if (err & 2) throw std::domain_error("sample_token: NaN logit");
     if (err & 4) throw std::domain_error("sample_token: all logits are -inf");
+}
+
+void Engine::debug_exp(const double* x, size_t n, double* y) {
+    double* dx = dalloc<double>(n);
+    double* dy = dalloc<double>(n);
+    h2d(dx, x, n, st_);
+    launch_debug_exp(dx, n, dy, st_);
+    d2h(y, dy, n, st_);
+    SGB_CUDA(cudaStreamSynchronize(st_));
+    cudaFree(dx);
+    cudaFree(dy);
+}
+
+unsigned long long Engine::exact_draws() {
+    unsigned long long n = 0;
+    SGB_CUDA(cudaMemcpyAsync(&n, rsc_.n_exact, sizeof(n), cudaMemcpyDeviceToHost, st_));
+    SGB_CUDA(cudaStreamSynchronize(st_));
+    return n;
 }
 
 void Engine::topk_logsoftmax(const float* logits, int rows, int vocab, int k, int* tok, double* lp) {
@@ -1051,8 +1085,13 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
     {
         int pi = 0;
         while (pi < P) {
+            // a chunk is bounded by its prompt rows AND by its np * g first-token emissions (both
+            // index row-sized buffers: lm_idx_, rows_.seed, the sampling scratch)
+            if (a.g > max_rows_) throw std::invalid_argument("generate: group size exceeds engine max_rows");
             int rows = 0, pe = pi;
-            while (pe < P && rows + static_cast<int>(a.prompts[pe].size()) <= max_rows_) rows += a.prompts[pe++].size();
+            while (pe < P && rows + static_cast<int>(a.prompts[pe].size()) <= max_rows_ &&
+                   (pe - pi + 1) * a.g <= max_rows_)
+                rows += a.prompts[pe++].size();
             if (pe == pi) throw std::invalid_argument("generate: prompt longer than engine max_rows");
             std::vector<int> tok, pos, cl, chl, last_rows;
             std::vector<long long> kvd, cb;

@@ -119,8 +119,12 @@ class Engine {
                         float* logits, float* hidden);
     void forward_draft(int slot, const int* tokens, const float* prev_feat, const int* positions, int rows, bool extend,
                        float* feats, float* logits);
+    // sample_token per row; uniforms (optional) replace the keyed Rng(key).uniform() draws;
+    // exact_rows (optional) receives 1 for rows resolved by the exact sequential pass
     void emit(const float* logits, int rows, int vocab, double temperature, const unsigned long long* seeds,
-              const int* key_pos, int* out);
+              const int* key_pos, int* out, const double* uniforms = nullptr, int* exact_rows = nullptr);
+    void debug_exp(const double* x, size_t n, double* y);
+    unsigned long long exact_draws();  // T > 0 draws resolved by the exact sequential pass so far
     void topk_logsoftmax(const float* logits, int rows, int vocab, int k, int* tok, double* lp);
 
     // ---- the rollout (generate_dynamic_batch drop-in)

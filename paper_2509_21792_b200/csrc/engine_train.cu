@@ -169,9 +169,12 @@ Engine::DraftLossTerms Engine::draft_update(const DraftUpdateArgs& A) {
     const auto& lo = dlay_.layers[0];
     const LayerDev& W = dL_[0];
     DraftLossTerms terms;
-    cudaEvent_t e0, e1;
-    SGB_CUDA(cudaEventCreate(&e0));
-    SGB_CUDA(cudaEventCreate(&e1));
+    struct Ev {  // RAII: no leaked events on early return / exception
+        cudaEvent_t e = nullptr;
+        Ev() { SGB_CUDA(cudaEventCreate(&e)); }
+        ~Ev() { cudaEventDestroy(e); }
+    } ev0, ev1;
+    cudaEvent_t e0 = ev0.e, e1 = ev1.e;
     SGB_CUDA(cudaEventRecord(e0, st_));
 
     // ---- sequence table + feature source
@@ -211,10 +214,16 @@ Engine::DraftLossTerms Engine::draft_update(const DraftUpdateArgs& A) {
     for (int L : lens) rows_local += std::max(0, L - 2);
     terms.rows = rows_local;
     const long long rows_norm = A.rows_total > 0 ? A.rows_total : rows_local;
-    if (lens.empty() || (rows_norm == 0)) return terms;
+    SGB_CUDA(cudaMemsetAsync(t.grad, 0, dlay_.total * 4, st_));
+    if (lens.empty() || rows_norm == 0) {
+        // a data-parallel rank with no rows still joins the gradient all-reduce (zero
+        // contribution), or the other ranks would wait in ncclAllReduce forever
+        if (A.grad_hook) A.grad_hook(t.grad, dlay_.total, st_, A.hook_ctx);
+        SGB_CUDA(cudaStreamSynchronize(st_));
+        return terms;
+    }
     const double inv_r = 1.0 / static_cast<double>(rows_norm);
     const double scale_feat = A.w_feat * inv_r / d, scale_tok = A.w_tok * inv_r;
-    SGB_CUDA(cudaMemsetAsync(t.grad, 0, dlay_.total * 4, st_));
 
     // host tokens of the last rollout are needed to build the row tables
     std::vector<int> dev_tok_copy;
@@ -399,8 +408,6 @@ Engine::DraftLossTerms Engine::draft_update(const DraftUpdateArgs& A) {
     float ms = 0.f;
     SGB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
     terms.seconds = ms * 1e-3;
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
     return terms;
 }
 

@@ -92,11 +92,18 @@ struct RowScratch {
     size_t bytes;
     int* ctr;       // [rows], zero between launches
     float* rowmax;  // [rows]
+    int* exact;     // [rows] T > 0: 1 = the row's draw was resolved by the exact sequential pass
+    unsigned long long* n_exact;  // running count of such rows (diagnostics)
     int rows;
 };
 size_t row_scratch_bytes(int rows, int V);
+// uniforms (optional, [R]): the draw's Rng(key).uniform() supplied by the caller instead of
+// derived from (seeds, key_pos) -- the "identical logits and supplied uniforms" parity mode
 void launch_emit(const float* logits, int V, const int* row_idx, const unsigned long long* seeds, const int* key_pos,
-                 int R, double temperature, int* out, int* err, const RowScratch& sc, cudaStream_t st);
+                 int R, double temperature, int* out, int* err, const RowScratch& sc, cudaStream_t st,
+                 const double* uniforms = nullptr);
+// device evaluation of the glibc exp restatement (glibc_exp.cuh), for the parity tests
+void launch_debug_exp(const double* x, size_t n, double* out, cudaStream_t st);
 int emit_launches(double temperature);
 void launch_topk_lsm(const float* logits, int V, int R, int k, int* out_tok, double* out_lp, const RowScratch& sc,
                      cudaStream_t st);

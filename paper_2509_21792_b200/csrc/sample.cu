@@ -17,6 +17,7 @@
 #include <cfloat>
 
 #include "common.cuh"
+#include "glibc_exp.cuh"
 #include "kernels.h"
 #include "util.h"
 
@@ -266,39 +267,69 @@ __global__ void __launch_bounds__(kT) emit_max_kernel(const float* __restrict__ 
     if (temperature == 0.0) out[r] = b.i;
 }
 
-// T > 0: thread t of chunk p owns the kPer contiguous logits base + t*kPer ...; sums are
-// sequential in fp64 inside a thread, then in thread order, then in chunk order.
-__device__ __forceinline__ double thread_expsum(const float* L, int V, int lo, double mx, double temperature) {
+// T > 0. Every CDF term is glibc's exp of (l - max) / T, bit for bit (glibc_exp.cuh), so the
+// only difference to the reference's sequential fp64 sum is the summation ORDER: thread t of
+// chunk p sums its kPer contiguous logits sequentially, then threads in order, then chunks in
+// order. Summing n non-negative terms in any order is within (n - 1) * 2^-53 * S of the exact
+// sum, so the reference's prefixes P'_i and u' = U * S' differ from ours by less than
+// (2V + 1024) * 2^-53 * S (first order). The draw is taken from the fast path only when u lies
+// more than kMarginUlps(V) * 2^-53 * S (twice that bound) inside the chosen token's interval
+// [P_{i-1}, P_i); otherwise the row is flagged and emit_exact_kernel redoes it with the
+// reference's own sequential order (tinylm.hpp:614-627), which then gives the same bits.
+__device__ __forceinline__ double margin_bound(int V, double S) { return (4.0 * V + 4096.0) * 0x1p-53 * S; }
+
+__device__ const uint64_t kExpTab[256] = SGB_GLIBC_EXP_TAB;
+
+__device__ __forceinline__ void load_exp_tab(uint64_t* sh) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) sh[i] = kExpTab[i];
+    __syncthreads();
+}
+
+__device__ __forceinline__ double thread_expsum(const float* L, int V, int lo, double mx, double temperature,
+                                                const uint64_t* tab) {
     double s = 0.0;
     const int hi = min(V, lo + kPer);
-    for (int i = lo; i < hi; ++i) s += exp((static_cast<double>(L[i]) - mx) / temperature);
+    for (int i = lo; i < hi; ++i) s = __dadd_rn(s, gx::cdf_term(L[i], mx, temperature, tab));
     return s;
+}
+
+__device__ __forceinline__ double row_uniform(const unsigned long long* seeds, const int* key_pos,
+                                              const double* uniforms, int r) {
+    if (uniforms) return uniforms[r];
+    return rng_first_uniform(mix_key(seeds[r], static_cast<uint64_t>(key_pos[r])));
 }
 
 __global__ void __launch_bounds__(kT) emit_sample_kernel(const float* __restrict__ logits, int V, int P,
                                                          const int* __restrict__ row_idx,
                                                          const unsigned long long* __restrict__ seeds,
-                                                         const int* __restrict__ key_pos, double temperature,
+                                                         const int* __restrict__ key_pos,
+                                                         const double* __restrict__ uniforms, double temperature,
                                                          EmitRec* __restrict__ rec, int* __restrict__ ctr,
-                                                         const float* __restrict__ rowmax, int* __restrict__ out) {
+                                                         const float* __restrict__ rowmax, int* __restrict__ out,
+                                                         int* __restrict__ exact) {
     pdl_wait();
     pdl_trigger();
+    __shared__ uint64_t tab[256];
     __shared__ double ts[kT];
     __shared__ VI shv[kT / 32];
     __shared__ int flag;
-    __shared__ double sh_u;
+    __shared__ double sh_u, sh_S;
     __shared__ int sh_p;
     const int p = blockIdx.x, r = blockIdx.y;
     const float mxf = rowmax[r];
-    if (mxf == -INFINITY) return;  // emit_max flagged the row (domain_error)
+    if (mxf == -INFINITY) {  // emit_max flagged the row (domain_error)
+        if (p == 0 && threadIdx.x == 0) exact[r] = 0;
+        return;
+    }
+    load_exp_tab(tab);
     const double mx = static_cast<double>(mxf);
     const float* L = logits + static_cast<size_t>(row_idx ? row_idx[r] : r) * V;
     const int lo = p * kCH + static_cast<int>(threadIdx.x) * kPer;
-    ts[threadIdx.x] = thread_expsum(L, V, lo, mx, temperature);
+    ts[threadIdx.x] = thread_expsum(L, V, lo, mx, temperature, tab);
     __syncthreads();
     if (threadIdx.x == 0) {
         double acc = 0.0;
-        for (int t = 0; t < kT; ++t) acc += ts[t];
+        for (int t = 0; t < kT; ++t) acc = __dadd_rn(acc, ts[t]);
         rec[static_cast<size_t>(r) * (((P + kCPC - 1) / kCPC) * kCPC) + p].s = acc;
     }
     if (!last_of_row(ctr, r, P, &flag)) return;
@@ -307,18 +338,18 @@ __global__ void __launch_bounds__(kT) emit_sample_kernel(const float* __restrict
         // chunk prefixes in order; the winner chunk is the last non-empty one whose
         // exclusive prefix is <= u
         double acc = 0.0;
-        for (int q = 0; q < P; ++q) acc += __ldcg(&rr[q].s);
-        const uint64_t key = mix_key(seeds[r], static_cast<uint64_t>(key_pos[r]));
-        const double u = rng_first_uniform(key) * acc;
+        for (int q = 0; q < P; ++q) acc = __dadd_rn(acc, __ldcg(&rr[q].s));
+        const double u = __dmul_rn(row_uniform(seeds, key_pos, uniforms, r), acc);
         double pre = 0.0;
         int win = 0;
         for (int q = 0; q < P; ++q) {
             if (pre <= u) win = q;
-            pre += __ldcg(&rr[q].s);
+            pre = __dadd_rn(pre, __ldcg(&rr[q].s));
         }
         double wpre = 0.0;
-        for (int q = 0; q < win; ++q) wpre += __ldcg(&rr[q].s);
+        for (int q = 0; q < win; ++q) wpre = __dadd_rn(wpre, __ldcg(&rr[q].s));
         sh_u = u;
+        sh_S = acc;
         ts[0] = wpre;  // reused below after the barrier
         sh_p = win;
     }
@@ -329,14 +360,14 @@ __global__ void __launch_bounds__(kT) emit_sample_kernel(const float* __restrict
     __syncthreads();
     // recompute the winner chunk's per-thread sums (same arithmetic, same bits)
     const int wlo = win * kCH + static_cast<int>(threadIdx.x) * kPer;
-    ts[threadIdx.x] = thread_expsum(L, V, wlo, mx, temperature);
+    ts[threadIdx.x] = thread_expsum(L, V, wlo, mx, temperature, tab);
     __syncthreads();
     if (threadIdx.x == 0) {
         double acc = cpre;
         for (int t = 0; t < kT; ++t) {
             const double c = ts[t];
             ts[t] = acc;  // exclusive prefix of thread t (chunk prefix included)
-            acc += c;
+            acc = __dadd_rn(acc, c);
         }
     }
     __syncthreads();
@@ -347,18 +378,97 @@ __global__ void __launch_bounds__(kT) emit_sample_kernel(const float* __restrict
     if (static_cast<int>(threadIdx.x) == cv.i) {
         double acc = ts[threadIdx.x];
         const int hi = min(V, wlo + kPer);
-        int tok = hi - 1;
+        int tok = -1;
+        double margin = 0.0;
         for (int i = wlo; i < hi; ++i) {
-            acc += exp((static_cast<double>(L[i]) - mx) / temperature);
+            const double before = acc;
+            acc = __dadd_rn(acc, gx::cdf_term(L[i], mx, temperature, tab));
             if (u < acc) {
                 tok = i;
+                margin = fmin(u - before, acc - u);
                 break;
             }
         }
-        out[r] = tok;
+        const bool sure = tok >= 0 && margin > margin_bound(V, sh_S);
+        out[r] = tok >= 0 ? tok : V - 1;
+        exact[r] = sure ? 0 : 1;
     } else if (cv.i < 0 && threadIdx.x == 0) {
         out[r] = V - 1;
+        exact[r] = 1;
     }
+}
+
+// The rows flagged above, redone exactly as sample_token does (tinylm.hpp:614-627): the
+// terms in index order into ONE sequential fp64 sum, u = uniform * sum, then the sequential
+// walk to the first prefix above u. Terms are computed by the whole CTA into shared memory,
+// the additions (the only order-sensitive step) by one thread. Rare by construction (the
+// probability that u lands inside the margin is ~1e-10 per row), so its serial cost is moot;
+// unflagged rows exit at once.
+constexpr int kExT = 256;
+constexpr int kExChunk = 4096;
+
+__global__ void __launch_bounds__(kExT) emit_exact_kernel(const float* __restrict__ logits, int V,
+                                                          const int* __restrict__ row_idx,
+                                                          const unsigned long long* __restrict__ seeds,
+                                                          const int* __restrict__ key_pos,
+                                                          const double* __restrict__ uniforms, double temperature,
+                                                          const float* __restrict__ rowmax, int* __restrict__ out,
+                                                          int* __restrict__ exact,
+                                                          unsigned long long* __restrict__ n_exact) {
+    pdl_wait();
+    pdl_trigger();
+    const int r = blockIdx.x;
+    if (!exact[r]) return;
+    __shared__ uint64_t tab[256];
+    __shared__ double e[kExChunk];
+    __shared__ double sh_acc;
+    __shared__ int sh_tok;
+    load_exp_tab(tab);
+    const double mx = static_cast<double>(rowmax[r]);
+    const float* L = logits + static_cast<size_t>(row_idx ? row_idx[r] : r) * V;
+    double sum = 0.0;  // thread 0's running sum
+    for (int base = 0; base < V; base += kExChunk) {
+        const int n = min(kExChunk, V - base);
+        for (int j = threadIdx.x; j < n; j += kExT) e[j] = gx::cdf_term(L[base + j], mx, temperature, tab);
+        __syncthreads();
+        if (threadIdx.x == 0)
+            for (int j = 0; j < n; ++j) sum = __dadd_rn(sum, e[j]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        sh_acc = __dmul_rn(row_uniform(seeds, key_pos, uniforms, r), sum);  // u
+        sh_tok = -1;
+    }
+    __syncthreads();
+    const double u = sh_acc;
+    double acc = 0.0;
+    for (int base = 0; base < V; base += kExChunk) {
+        const int n = min(kExChunk, V - base);
+        for (int j = threadIdx.x; j < n; j += kExT) e[j] = gx::cdf_term(L[base + j], mx, temperature, tab);
+        __syncthreads();
+        if (threadIdx.x == 0)
+            for (int j = 0; j < n; ++j) {
+                acc = __dadd_rn(acc, e[j]);
+                if (u < acc) {
+                    sh_tok = base + j;
+                    break;
+                }
+            }
+        __syncthreads();
+        if (sh_tok >= 0) break;
+    }
+    if (threadIdx.x == 0) {
+        out[r] = sh_tok >= 0 ? sh_tok : V - 1;
+        atomicAdd(n_exact, 1ull);
+    }
+}
+
+__global__ void debug_exp_kernel(const double* __restrict__ x, size_t n, double* __restrict__ y) {
+    __shared__ uint64_t tab[256];
+    load_exp_tab(tab);
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x)
+        y[i] = gx::exp(x[i], tab);
 }
 
 int chunks_for(int V) {
@@ -374,7 +484,8 @@ size_t row_scratch_bytes(int rows, int V) {
 }
 
 void launch_emit(const float* logits, int V, const int* row_idx, const unsigned long long* seeds, const int* key_pos,
-                 int R, double temperature, int* out, int* err, const RowScratch& sc, cudaStream_t st) {
+                 int R, double temperature, int* out, int* err, const RowScratch& sc, cudaStream_t st,
+                 const double* uniforms) {
     if (R <= 0) return;
     const int P = chunks_for(V);
     if (R > sc.rows || static_cast<size_t>(R) * (((P + kCPC - 1) / kCPC) * kCPC) * sizeof(EmitRec) > sc.bytes)
@@ -385,13 +496,22 @@ void launch_emit(const float* logits, int V, const int* row_idx, const unsigned 
                sc.rowmax, out, err);
     SGB_KCHECK();
     if (temperature != 0.0) {
-        launch_pdl(emit_sample_kernel, dim3(P, R), dim3(kT), 0, st, logits, V, P, row_idx, seeds, key_pos, temperature,
-                   rec, sc.ctr, static_cast<const float*>(sc.rowmax), out);
+        launch_pdl(emit_sample_kernel, dim3(P, R), dim3(kT), 0, st, logits, V, P, row_idx, seeds, key_pos, uniforms,
+                   temperature, rec, sc.ctr, static_cast<const float*>(sc.rowmax), out, sc.exact);
+        SGB_KCHECK();
+        launch_pdl(emit_exact_kernel, dim3(R), dim3(kExT), 0, st, logits, V, row_idx, seeds, key_pos, uniforms,
+                   temperature, static_cast<const float*>(sc.rowmax), out, sc.exact, sc.n_exact);
         SGB_KCHECK();
     }
 }
 
-int emit_launches(double temperature) { return temperature != 0.0 ? 2 : 1; }
+int emit_launches(double temperature) { return temperature != 0.0 ? 3 : 1; }
+
+void launch_debug_exp(const double* x, size_t n, double* out, cudaStream_t st) {
+    if (n == 0) return;
+    debug_exp_kernel<<<296, 256, 0, st>>>(x, n, out);
+    SGB_KCHECK();
+}
 
 void launch_topk_lsm(const float* logits, int V, int R, int k, int* out_tok, double* out_lp, const RowScratch& sc,
                      cudaStream_t st) {
