@@ -67,14 +67,14 @@ def env_rank():
 
 
 def model_cfg(w):
-    from oracle.oracle import ModelConfig  # plain config record (no oracle compute)
+    from paper_2509_21792_b200.capi import ModelConfig
     return ModelConfig(w["V"], w["d"], w["L"], w["H"], w["dff"], w["P"] + w["new"], 1)
 
 
 def make_prompts(w, rank):
     """Uniform ids in [2, V) from a splitmix stream keyed by (run_seed=0, 0x9a01), SURVEY §8d;
     rank r takes global queries [r*Q, (r+1)*Q)."""
-    from oracle.oracle import mix_key  # integer key derivation only
+    from paper_2509_21792_b200.capi import mix_key
     seed = mix_key(0, 0x9A01)
     n = (rank + 1) * w["Q"] * w["P"]
     with np.errstate(over="ignore"):
@@ -98,7 +98,7 @@ def _splitmix_stream(seed, n):
 def stream_prompts(key, n, P, V):
     """Training prompts for online draft learning, disjoint from the benchmark prompts:
     Rng(mix_key(0, key)) (key = 0x7a11 + iteration)."""
-    from oracle.oracle import mix_key  # integer key derivation only
+    from paper_2509_21792_b200.capi import mix_key
     z = _splitmix_stream(mix_key(0, key), n * P)
     return (z % np.uint64(V - 2) + np.uint64(2)).astype(np.int64).reshape(n, P).tolist()
 
@@ -106,7 +106,7 @@ def stream_prompts(key, n, P, V):
 def stop_caps(w, sid0, n):
     """c3 variable-length stops: per-sequence max_new from Rng(mix_key(0, 0x5709 + sid)),
     uniform in [new/4, new] (max/min = 4x), keyed by GLOBAL sequence id."""
-    from oracle.oracle import mix_key
+    from paper_2509_21792_b200.capi import mix_key
     lo, hi = w["new"] // 4, w["new"]
     caps = []
     for sid in range(sid0, sid0 + n):

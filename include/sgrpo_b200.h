@@ -188,6 +188,13 @@ int sgb_draft_update(sgb_engine* e, int n_seqs, const int* tokens, const int* le
 int sgb_draft_update_last(sgb_engine* e, const sgb_adamw* opt, float* grad_out, sgb_draft_terms* terms);
 /* Reset the AdamW moments and step counter (a fresh AdamW object). */
 int sgb_adamw_reset(sgb_engine* e);
+/* AdamW::m, AdamW::v, AdamW::t (grpo.hpp:97-103) of the device draft optimizer: upload = 1
+ * installs a caller's optimizer state (m / v NULL = zeros), 0 reads it back (NULL = skip). */
+int sgb_adamw_state(sgb_engine* e, float* m, float* v, long long* t, int upload);
+/* GenStats.events (scheduler.hpp:73-86, scheduler.cpp:326) of the engine's last sgb_rollout:
+ * (step, seq, accepted) triples, min(n, cap) written; the measured prefill seconds
+ * (GenStats.prefill_sim_s). */
+int sgb_rollout_events(sgb_engine* e, int* triples, long long cap, long long* n, double* prefill_seconds);
 
 /* ---- hardware profile: C_peak calibration (Alg. 2, src/roofline.cpp:39-108) ------------- */
 /* detect_knee (roofline.cpp:39-76): farthest point from the chord of the unit-normalised

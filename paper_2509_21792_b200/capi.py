@@ -28,6 +28,36 @@ if not os.path.exists(LIB_PATH):
 _lib = C.CDLL(LIB_PATH)
 
 
+@dataclass
+class ModelConfig:
+    """ModelConfig (include/sgrpo/tinylm.hpp:16-37), as the engine needs it."""
+    vocab_size: int
+    d_model: int
+    n_layers: int
+    n_heads: int
+    d_ff: int
+    max_seq_len: int
+    seed: int = 0
+
+
+_M64 = (1 << 64) - 1
+
+
+def _splitmix64(state: int):
+    state = (state + 0x9E3779B97F4A7C15) & _M64
+    z = state
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _M64
+    return z ^ (z >> 31)
+
+
+def mix_key(a: int, b: int) -> int:
+    """mix_key (include/sgrpo/rng.hpp:17-20): the keyed-stream combiner the engine derives
+    sequence seeds and emission keys with (host integer work, no compute)."""
+    s = (a ^ ((b + 0x9E3779B97F4A7C15 + ((a << 6) & _M64) + (a >> 2)) & _M64)) & _M64
+    return _splitmix64(s)
+
+
 class ModelConfigC(C.Structure):
     _fields_ = [("vocab_size", C.c_int), ("d_model", C.c_int), ("n_layers", C.c_int), ("n_heads", C.c_int),
                 ("d_ff", C.c_int), ("max_seq_len", C.c_int), ("seed", C.c_ulonglong)]

@@ -31,6 +31,8 @@ struct sgb_engine {
     std::unique_ptr<sgb::Engine> eng;
     sgb_model_config cfg{};  // as created (checkpoint headers carry it)
     int draft_layers = 1;
+    std::vector<int> last_events;  // (step, seq, accepted) of the last rollout
+    double last_prefill_s = 0;
 };
 
 namespace {
@@ -287,6 +289,8 @@ int sgb_rollout(sgb_engine* e, const int* prompts, const int* prompt_lens, int n
         a.sid_offset = opt->sid_offset;
         if (a.want_features) a.features_out = features;
         sgb::RolloutResult r = en.rollout(a);
+        e->last_events = r.events;
+        e->last_prefill_s = r.prefill_seconds;
         const int T = en.dims().max_seq;
         const int ns = static_cast<int>(r.tokens.size());
         for (int s = 0; s < ns; ++s) {
@@ -672,6 +676,20 @@ int sgb_save_draft_checkpoint(sgb_engine* e, const char* path) {
                   std::fwrite(h.data(), 1, hl, f) == hl && std::fwrite(flat.data(), 4, nd, f) == nd;
         ok = (std::fclose(f) == 0) && ok;
         if (!ok) throw std::runtime_error(std::string("checkpoint write failed: ") + path);
+    });
+}
+
+int sgb_adamw_state(sgb_engine* e, float* m, float* v, long long* t, int upload) {
+    return guarded([&] { E(e).adamw_state(m, v, t, upload != 0); });
+}
+
+int sgb_rollout_events(sgb_engine* e, int* triples, long long cap, long long* n, double* prefill_seconds) {
+    return guarded([&] {
+        if (!e) throw std::invalid_argument("null engine");
+        const long long m = static_cast<long long>(e->last_events.size() / 3);
+        if (n) *n = m;
+        if (triples) std::copy(e->last_events.begin(), e->last_events.begin() + 3 * std::min(m, cap), triples);
+        if (prefill_seconds) *prefill_seconds = e->last_prefill_s;
     });
 }
 

@@ -163,6 +163,7 @@ class Engine {
     };
     DraftLossTerms draft_update(const DraftUpdateArgs& a);
     void adamw_reset();
+    void adamw_state(float* m, float* v, long long* t, bool upload);
     // measure_c_peak's latency_fn on the device (roofline.cpp:78-108 / tools/sgrpo.cpp:38-49):
     // one batched target forward of b rows (EOS token, position 0, self-only attention),
     // median device seconds over `reps` after `warmup` untimed launches.

@@ -129,6 +129,26 @@ void Engine::adamw_reset() {
     tr2_.adam_t = 0;
 }
 
+// AdamW moments + step count (grpo.hpp:97-103) between the device and a caller's AdamW object:
+// upload (m, v nullptr = a fresh optimizer's zeros) or download.
+void Engine::adamw_state(float* m, float* v, long long* t, bool upload) {
+    if (!target_ready_ || !draft_ready_) throw std::runtime_error("weights not uploaded");
+    train_alloc();
+    const size_t n = dlay_.total;
+    if (upload) {
+        if (m) SGB_CUDA(cudaMemcpyAsync(tr2_.m, m, n * 4, cudaMemcpyHostToDevice, st_));
+        else SGB_CUDA(cudaMemsetAsync(tr2_.m, 0, n * 4, st_));
+        if (v) SGB_CUDA(cudaMemcpyAsync(tr2_.v, v, n * 4, cudaMemcpyHostToDevice, st_));
+        else SGB_CUDA(cudaMemsetAsync(tr2_.v, 0, n * 4, st_));
+        tr2_.adam_t = t ? *t : 0;
+    } else {
+        if (m) SGB_CUDA(cudaMemcpyAsync(m, tr2_.m, n * 4, cudaMemcpyDeviceToHost, st_));
+        if (v) SGB_CUDA(cudaMemcpyAsync(v, tr2_.v, n * 4, cudaMemcpyDeviceToHost, st_));
+        if (t) *t = tr2_.adam_t;
+    }
+    SGB_CUDA(cudaStreamSynchronize(st_));
+}
+
 // bf16 copies of the draft master in the reference [in][out] layout: the K-major operands
 // of the dgrad GEMMs (dX = dY . W^T).
 void Engine::train_refresh_ref_weights() {

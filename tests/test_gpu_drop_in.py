@@ -38,3 +38,48 @@ def test_reference_api_caller_runs_on_b200():
     kw = dict(c_peak=64, mode="adaptive_spec", seed=7, max_new_tokens=64, want_features=False)
     assert e.generate(r["prompts"], 4, temperature=0.0, **kw).tokens == r["tokens_t0"]
     assert e.generate(r["prompts"], 4, temperature=1.0, **kw).tokens == r["tokens_t1"]
+
+
+BUILD = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "integration", "_build")
+CFG = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "integration", "configs",
+                   "drop_in_bench.json")
+STRATEGIES = ["vanilla", "vanilla+early_term", "fixed_spec", "adaptive_spec", "adaptive_spec+online_draft"]
+
+
+def _run_bench(binary):
+    p = subprocess.run([binary, CFG, *STRATEGIES], capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, (p.returncode, p.stdout[-3000:], p.stderr[-3000:])
+    return p.stdout, json.loads(p.stdout.strip().splitlines()[-1])
+
+
+def test_reference_bench_runs_unmodified_reference_on_b200():
+    """The reference's own bench() (harness.cpp:89-154) -> train_loop (grpo.cpp:280-410) ->
+    pretrain_draft / generate_dynamic_batch / draft_update / policy_update, from the UNMODIFIED
+    reference objects, with generate_dynamic_batch and draft_update bound to the B200 drop-in
+    (weakened reference definitions, integration/Makefile). Every strategy must emit identical
+    tokens (the reference's own check), and the shim's counters prove every rollout and draft
+    step of train_loop ran on the device."""
+    binary = os.path.join(BUILD, "ref_bench")
+    if not os.path.exists(binary):
+        pytest.skip("integration/_build/ref_bench not built (needs /root/reference at build time)")
+    table, r = _run_bench(binary)
+    print(table)
+    assert r["tokens_identical"] is True
+    cfg = json.load(open(CFG))
+    iters = cfg["grpo"]["iterations"]
+    dev = r["device"]
+    # one rollout per strategy per iteration + bench()'s pretrain_draft corpus rollout
+    assert dev["rollouts"] == len(STRATEGIES) * iters + 1
+    # pretrain_draft's steps + one per iteration of the online-draft strategy
+    assert dev["draft_updates"] == cfg["init"]["draft_pretrain_steps"] + iters
+    # the draft is re-uploaded only when the host copy differs from the device copy (each
+    # train_loop starts from bench()'s draft0 again); the target only if policy_update moved it
+    assert dev["draft_uploads"] <= len(STRATEGIES) + 1
+    ent = {e["name"]: e for e in r["entries"]}
+    assert all(e["iterations"] == iters for e in ent.values())
+    assert ent["adaptive_spec"]["tau"] >= 1.0 and ent["fixed_spec"]["tau"] >= 1.0
+    assert len({e["tokens_hash"] for e in ent.values()}) == 1
+    cpu = os.path.join(BUILD, "ref_bench_cpu")
+    if os.path.exists(cpu):
+        _, rc = _run_bench(cpu)
+        print("CPU reference tokens_hash", rc["entries"][0]["tokens_hash"], "B200", r["entries"][0]["tokens_hash"])
