@@ -48,6 +48,10 @@ typedef struct sgb_gen_options {
     int sid_offset;            /* global sid of this shard's first sequence (data-parallel ranks) */
     double* step_seconds;      /* optional [step_cap]: measured device seconds of every step (GenStats
                                   StepRecord.sim_latency_s, scheduler.cpp:356-368), or NULL */
+    int acceptance;            /* 0: keyed strict match, the reference's verify (drafttree.cpp:170-222);
+                                  1: speculative rejection sampling (draft children sampled from q,
+                                  accept min(1, p/q), residual resample; T > 0; lossless in
+                                  distribution, not token-identical to the reference) */
 } sgb_gen_options;
 
 /* GenStats summary (scheduler.hpp:68-89) plus device measurements. */
@@ -114,6 +118,11 @@ int sgb_sample_rows(sgb_engine* e, const float* logits, int rows, int vocab, dou
  * (exact_rows[i] = 1, optional). */
 int sgb_sample_rows_u(sgb_engine* e, const float* logits, int rows, int vocab, double temperature,
                       const double* uniforms, int* out, int* exact_rows);
+/* Test entry for the rejection-sampling acceptance (reject.cu): n_trials independent rounds of one
+ * node -- k candidates drawn from softmax(q_logits / T), multi-round rejection against
+ * softmax(p_logits / T). out_tok = emitted token, out_acc = 1 if a candidate was accepted. */
+int sgb_debug_spec_sample(sgb_engine* e, const float* p_logits, const float* q_logits, int vocab, int k,
+                          double temperature, int n_trials, unsigned long long seed, int* out_tok, int* out_acc);
 /* Count of T > 0 draws (rollouts and sample calls) the engine resolved by the exact pass. */
 int sgb_exact_draws(sgb_engine* e, unsigned long long* out);
 /* The device's exp(): the restatement of glibc's exp (csrc/glibc_exp.cuh), for parity tests. */

@@ -68,7 +68,9 @@ class GenOptionsC(C.Structure):
                 ("mode", C.c_int), ("early_term", C.c_int), ("temperature", C.c_double), ("seed", C.c_ulonglong),
                 ("max_new_tokens", C.c_int), ("fixed_n_verify", C.c_int), ("fixed_k_draft", C.c_int),
                 ("fixed_l_draft", C.c_int), ("seq_max_new", C.POINTER(C.c_int)), ("want_features", C.c_int),
-                ("sid_offset", C.c_int), ("step_seconds", C.POINTER(C.c_double))]
+                ("sid_offset", C.c_int), ("step_seconds", C.POINTER(C.c_double)), ("acceptance", C.c_int)]
+
+ACCEPTANCE = {"strict": 0, "rejection": 1}
 
 
 class RolloutStatsC(C.Structure):
@@ -355,7 +357,9 @@ class Engine:
                  k_max: int = 10, l_max: int = 6, mode: str = "vanilla", early_term: bool = True,
                  temperature: float = 0.0, seed: int = 0, max_new_tokens: int = 0, fixed=(1, 0, 0),
                  seq_max_new: Optional[Sequence[int]] = None, want_features: bool = True,
-                 max_steps_record: int = 1 << 16, sid_offset: int = 0) -> Rollout:
+                 max_steps_record: int = 1 << 16, sid_offset: int = 0, acceptance: str = "strict") -> Rollout:
+        """generate_dynamic_batch. acceptance: "strict" = the reference's keyed strict-match verify
+        (drafttree.cpp:170-222), "rejection" = speculative rejection sampling (T > 0, reject.cu)."""
         T, d = self.cfg.max_seq_len, self.cfg.d_model
         n_p = len(prompts)
         ns = n_p * g
@@ -366,7 +370,7 @@ class Engine:
         step_s = np.zeros(max_steps_record, np.float64)
         opt = GenOptionsC(alpha, k_max, l_max, c_peak, MODES[mode], int(early_term), temperature, seed,
                           max_new_tokens, fixed[0], fixed[1], fixed[2], _p(smn, C.c_int), int(want_features),
-                          sid_offset, _p(step_s, C.c_double))
+                          sid_offset, _p(step_s, C.c_double), ACCEPTANCE[acceptance])
         toks = np.zeros((max(ns, 1), T), np.int32)
         lens = np.zeros(max(ns, 1), np.int32)
         pl = np.zeros(max(ns, 1), np.int32)
@@ -591,3 +595,19 @@ Engine.sample_rows_u = _sample_rows_u
 Engine.exact_draws = _exact_draws
 Engine.debug_exp = _debug_exp
 EXPORTED += ["sgb_sample_rows_u", "sgb_exact_draws", "sgb_debug_exp"]
+
+
+def _debug_spec_sample(self, p_logits, q_logits, k: int, temperature: float, n_trials: int, seed: int = 1):
+    """n_trials rounds of ONE speculative-sampling node (reject.cu): k candidates drawn from
+    softmax(q / T), the multi-round rejection against softmax(p / T). Returns (tokens, accepted)."""
+    p = np.ascontiguousarray(p_logits, np.float32)
+    q = np.ascontiguousarray(q_logits, np.float32)
+    tok = np.zeros(n_trials, np.int32)
+    acc = np.zeros(n_trials, np.int32)
+    _check(_lib.sgb_debug_spec_sample(self.h, _p(p, C.c_float), _p(q, C.c_float), p.size, k, C.c_double(temperature),
+                                      n_trials, C.c_ulonglong(seed), _p(tok, C.c_int), _p(acc, C.c_int)))
+    return tok, acc
+
+
+Engine.debug_spec_sample = _debug_spec_sample
+EXPORTED += ["sgb_debug_spec_sample", "sgb_adamw_state", "sgb_rollout_events"]

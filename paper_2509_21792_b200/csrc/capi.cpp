@@ -226,6 +226,31 @@ int sgb_sample_rows_u(sgb_engine* e, const float* logits, int rows, int vocab, d
     });
 }
 
+int sgb_debug_spec_sample(sgb_engine* e, const float* p_logits, const float* q_logits, int vocab, int k,
+                          double temperature, int n_trials, unsigned long long seed, int* out_tok, int* out_acc) {
+    return guarded([&] {
+        E(e);
+        if (vocab <= 0 || n_trials <= 0) throw std::invalid_argument("debug_spec_sample: empty input");
+        if (!(temperature > 0)) throw std::invalid_argument("rejection sampling needs temperature > 0");
+        const size_t V = vocab;
+        float *dp = nullptr, *dq = nullptr, *dr = nullptr;
+        int *dt = nullptr, *da = nullptr;
+        SGB_CUDA(cudaMalloc(&dp, V * 4));
+        SGB_CUDA(cudaMalloc(&dq, V * 4));
+        SGB_CUDA(cudaMalloc(&dr, V * 4 * static_cast<size_t>(n_trials)));
+        SGB_CUDA(cudaMalloc(&dt, 4 * static_cast<size_t>(n_trials)));
+        SGB_CUDA(cudaMalloc(&da, 4 * static_cast<size_t>(n_trials)));
+        SGB_CUDA(cudaMemcpy(dp, p_logits, V * 4, cudaMemcpyHostToDevice));
+        SGB_CUDA(cudaMemcpy(dq, q_logits, V * 4, cudaMemcpyHostToDevice));
+        sgb::launch_debug_spec_sample(dp, dq, vocab, k, temperature, n_trials, seed, dr, dt, da, nullptr);
+        SGB_CUDA(cudaMemcpy(out_tok, dt, 4 * static_cast<size_t>(n_trials), cudaMemcpyDeviceToHost));
+        SGB_CUDA(cudaMemcpy(out_acc, da, 4 * static_cast<size_t>(n_trials), cudaMemcpyDeviceToHost));
+        for (void* x : {static_cast<void*>(dp), static_cast<void*>(dq), static_cast<void*>(dr), static_cast<void*>(dt),
+                        static_cast<void*>(da)})
+            cudaFree(x);
+    });
+}
+
 int sgb_exact_draws(sgb_engine* e, unsigned long long* out) {
     return guarded([&] { *out = E(e).exact_draws(); });
 }
@@ -287,6 +312,7 @@ int sgb_rollout(sgb_engine* e, const int* prompts, const int* prompt_lens, int n
         if (opt->seq_max_new) a.seq_max_new.assign(opt->seq_max_new, opt->seq_max_new + n_prompts * g);
         a.want_features = features != nullptr && opt->want_features;
         a.sid_offset = opt->sid_offset;
+        a.acceptance = opt->acceptance;
         if (a.want_features) a.features_out = features;
         sgb::RolloutResult r = en.rollout(a);
         e->last_events = r.events;

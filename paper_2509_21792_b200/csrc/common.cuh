@@ -243,3 +243,33 @@ SGB_DEV double rng_first_uniform(uint64_t seed) {
 }
 
 }  // namespace sgb
+
+#include "kernels.h"
+
+namespace sgb {
+// commit_tokens (scheduler.cpp:97-118): append the accepted tokens, stop at EOS (tinylm.hpp:41)
+// or the length cap; result = (appended, finished)
+SGB_DEV void commit_tokens_dev(const StepSeqDev& st, SeqStateDev& ss, const int* acc_tok, int nacc, int* result) {
+    const int s = st.seq;
+    int len = ss.len[s], a = 0, fin = 0, eos = 0;
+    for (int j = 0; j < nacc; ++j) {
+        const int t = acc_tok[j];
+        ss.tokens[static_cast<size_t>(s) * ss.max_seq + len] = t;
+        ++len;
+        ++a;
+        if (t == 1) {
+            fin = eos = 1;
+            break;
+        }
+        if (len >= st.len_cap) {
+            fin = 1;
+            break;
+        }
+    }
+    ss.len[s] = len;
+    ss.finished[s] = fin;
+    ss.hit_eos[s] = eos;
+    result[0] = a;
+    result[1] = fin;
+}
+}  // namespace sgb

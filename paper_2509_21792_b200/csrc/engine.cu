@@ -308,6 +308,9 @@ Engine::~Engine() {
     cudaSetDevice(device_);
     cudaStreamSynchronize(st_);
     if (adv_buf_) cudaFree(adv_buf_);
+    for (void* q : {static_cast<void*>(qbuf_), static_cast<void*>(qstat_), static_cast<void*>(resid_),
+                    static_cast<void*>(rkeys_), static_cast<void*>(tr_.qrow)})
+        if (q) cudaFree(q);
     void* ptrs[] = {tw_, dw_, tsmall_, dmaster_, tkv_.K, tkv_.V, dkv_.K, dkv_.V, ss_.tokens, ss_.len, ss_.finished,
                     ss_.hit_eos, ss_.seed, feats_, dfeat_, tr_.tok, tr_.par, tr_.dep, tr_.lp, tr_.conf, tr_.fslot,
                     tr_.sel, tr_.n_nodes, tr_.lvl_start, tr_.lvl_cnt, tr_.frontier, x_, q_, y_, featin_, a_, att_,
@@ -1034,6 +1037,16 @@ Engine::DebugTree Engine::debug_tree_cb(int root_token, int k, int l, int n_veri
     return out;
 }
 
+void Engine::reject_alloc() {
+    if (qbuf_) return;
+    const size_t R = max_rows_, V = dims_.vocab, S = max_seqs_;
+    qbuf_ = dalloc<float>(R * V);
+    qstat_ = dalloc<double>(2 * R);
+    resid_ = dalloc<float>(S * V);
+    rkeys_ = dalloc<unsigned long long>(R);
+    tr_.qrow = dalloc<int>(S * static_cast<size_t>(tr_.tmax));
+}
+
 // ------------------------------------------------------------------ the rollout
 RolloutResult Engine::rollout(const RolloutArgs& a) {
     const ModelDims& mc = dims_;
@@ -1053,7 +1066,11 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
     if (a.k_max > k_max_ || a.l_max > l_max_)
         throw std::invalid_argument("generate: k_max/l_max exceed the engine's tree capacity");
     if (a.temperature < 0) throw std::invalid_argument("sample_token: negative temperature");
+    if (a.acceptance < 0 || a.acceptance > 1) throw std::invalid_argument("generate: unknown acceptance mode");
     if (!target_ready_ || !draft_ready_) throw std::runtime_error("weights not uploaded");
+    const bool rej = a.acceptance == 1 && a.temperature > 0;  // at T = 0 both modes are greedy strict match
+    if (rej) reject_alloc();
+    tr_.static_rank = rej ? 1 : 0;
     const int P = static_cast<int>(a.prompts.size());
     const int n_seqs = P * a.g;
     if (n_seqs > max_seqs_) throw std::invalid_argument("generate: more sequences than engine max_seqs");
@@ -1318,9 +1335,22 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
             }
             for (int i = 0; i < B; ++i)
                 if (hs[i].k) dft_len[hs[i].seq] = hs[i].p;
-            // root logits -> level 1
-            lm_head(a2_, act_a2_, n_spec, logits_);
-            launch_topk_lsm(logits_, V, n_spec, kstep, topk_tok_, topk_lp_, rsc_, st_);
+            // root logits -> level 1 (top-k children; rejection mode: k children sampled from q)
+            int qoff = 0;
+            if (rej) {
+                std::vector<unsigned long long> keys(n_spec);
+                for (int i = 0; i < B; ++i)
+                    if (hs[i].k)
+                        keys[hs[i].root_row] =
+                            mix_key_host(mix_key_host(seeds[hs[i].seq], static_cast<uint64_t>(hs[i].p + 1)), 0xD5A0u);
+                h2d(rkeys_, keys.data(), n_spec, st_);
+                lm_head(a2_, act_a2_, n_spec, qbuf_);
+                launch_sample_children(qbuf_, n_spec, V, kstep, a.temperature, rkeys_, topk_tok_, topk_lp_, qstat_, st_);
+                qoff = n_spec;
+            } else {
+                lm_head(a2_, act_a2_, n_spec, logits_);
+                launch_topk_lsm(logits_, V, n_spec, kstep, topk_tok_, topk_lp_, rsc_, st_);
+            }
             launch_tree_root(B, steps_, ss_, tr_, topk_tok_, topk_lp_, kstep, st_);
             count(2);
             // levels 2..L: one batched draft forward per level
@@ -1342,8 +1372,9 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
                     if (R == 0) break;
                     if (R > max_rows_) throw std::invalid_argument("generate: draft rows exceed engine max_rows");
                     const int* dro = drow_ + static_cast<size_t>(level - 2) * B;
+                    if (rej && qoff + R > max_rows_) throw std::invalid_argument("generate: draft q rows exceed max_rows");
                     launch_tree_frontier(B, level, steps_, dro, ss_, tr_, rows_, dkv_.seq_stride, dkv_.scratch_base,
-                                         d, st_);
+                                         d, st_, rej ? qoff : -1);
                     count();
                     Fwd f;
                     f.M = R;
@@ -1351,7 +1382,7 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
                     f.feat_base = dfeat_;
                     f.y_out = y_;
                     f.logits = true;
-                    f.logits_out = logits_;
+                    f.logits_out = rej ? qbuf_ + static_cast<size_t>(qoff) * V : logits_;
                     f.max_vlen = max_p + level;
                     groups_.clear();
                     for (int i = 0; i < B; ++i)
@@ -1367,7 +1398,22 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
                     res.draft_forwards++;
                     stat.draft_rows += R;
                     launch_copy_rows_f32(y_, nullptr, rows_.out_off, R, d, dfeat_, st_);
-                    launch_topk_lsm(logits_, V, R, kstep, topk_tok_, topk_lp_, rsc_, st_);
+                    if (rej) {
+                        std::vector<unsigned long long> keys(R);
+                        for (int i = 0; i < B; ++i) {
+                            const int r0 = drow[static_cast<size_t>(level - 2) * B + i];
+                            if (r0 < 0) continue;
+                            for (int j = 0; j < hs[i].k; ++j)  // frontier node j's children sit at p + level
+                                keys[r0 + j] = mix_key_host(
+                                    mix_key_host(seeds[hs[i].seq], static_cast<uint64_t>(hs[i].p + level)), 0xD5A0u + j);
+                        }
+                        h2d(rkeys_, keys.data(), R, st_);
+                        launch_sample_children(qbuf_ + static_cast<size_t>(qoff) * V, R, V, kstep, a.temperature, rkeys_,
+                                               topk_tok_, topk_lp_, qstat_ + 2 * static_cast<size_t>(qoff), st_);
+                        qoff += R;
+                    } else {
+                        launch_topk_lsm(logits_, V, R, kstep, topk_tok_, topk_lp_, rsc_, st_);
+                    }
                     launch_tree_expand(B, level, steps_, dro, tr_, topk_tok_, topk_lp_, st_);
                     count(3);
                 }
@@ -1431,7 +1477,11 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
         count(emit_launches(a.temperature) - 1);
         pend(kClsSample, pe0, 4.0 * vrows * V, 0);
         pe0 = pbeg();
-        launch_walk_commit(B, steps_, ss_, tr_, rows_, emitted_, acc_rows_, result_, st_);
+        if (rej && n_spec > 0)
+            launch_walk_reject(B, steps_, ss_, tr_, rows_, emitted_, logits_, rsc_.rowmax, qbuf_, qstat_, V,
+                               a.temperature, resid_, acc_rows_, result_, st_);
+        else
+            launch_walk_commit(B, steps_, ss_, tr_, rows_, emitted_, acc_rows_, result_, st_);
         pend(kClsTree, pe0, 0, 0);
         pe0 = pbeg();
         launch_commit_kv(B, steps_, acc_rows_, result_, tkv_.layers, d, tkv_.K, tkv_.V, tkv_.n_slots * d, tkv_.seq_stride,

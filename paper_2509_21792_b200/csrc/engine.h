@@ -63,6 +63,9 @@ struct RolloutArgs {
     std::vector<int> seq_max_new;  // optional per-sequence caps (c3 extension)
     bool want_features = true;
     int sid_offset = 0;  // global sid of local sequence 0 (seed parity under sharding)
+    // 0: keyed strict match (verify, drafttree.cpp:170-222; the parity mode), 1: speculative
+    // rejection sampling (reject.cu; T > 0 only -- at T = 0 it is the strict-match mode)
+    int acceptance = 0;
     // optional caller buffer [n_seqs][max_seq-1][d] for the features (skips RolloutResult.features):
     // one pinned-staging DMA of the feature store, then a multi-threaded host scatter
     float* features_out = nullptr;
@@ -316,6 +319,13 @@ class Engine {
     std::vector<int> last_plens_;  // and their prompt lengths
     long long target_forward_calls_ = 0;
     double* adv_buf_ = nullptr;    // [2 * max_rows] rewards + advantages of group_advantages
+    // rejection-sampling mode buffers (allocated on first use): draft logits of every expanded
+    // node of a step [max_rows][V], their (max, sum) stats, per-sequence residuals, child keys
+    float* qbuf_ = nullptr;
+    double* qstat_ = nullptr;
+    float* resid_ = nullptr;
+    unsigned long long* rkeys_ = nullptr;
+    void reject_alloc();
     void train_alloc();
     void train_refresh_ref_weights();
     void wgrad(const __nv_bfloat16* dyT, int N, const __nv_bfloat16* xT, int Kfeat, int Rp, float* grad_dst, int ld);

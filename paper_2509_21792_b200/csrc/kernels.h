@@ -136,6 +136,11 @@ struct TreeDev {
     int* lvl_cnt;             // [S]
     int* frontier;            // [S][16]
     int* sel;                 // [S][tmax] selected node ids (ascending)
+    // rejection-sampling mode (reject.cu): children are SAMPLED from the draft distribution and
+    // the tree shape must not depend on their values -- confidences are the static weights
+    // conf(child j) = conf(parent) * 2^-(j+1) (exact dyadics), ties by node index only
+    int static_rank = 0;
+    int* qrow = nullptr;      // [S][tmax] expanded node -> row of its draft logits (q) buffer
 };
 
 struct SeqStateDev {
@@ -167,9 +172,10 @@ struct RowsDev {
 
 void launch_tree_root(int B, const StepSeqDev* steps, const SeqStateDev& ss, const TreeDev& tr, const int* topk_tok,
                       const double* topk_lp, int kmax_row, cudaStream_t st);
+// qoff >= 0 (rejection mode): frontier node j of sequence i gets qrow = qoff + drow_off[i] + j
 void launch_tree_frontier(int B, int level, const StepSeqDev* steps, const int* drow_off, const SeqStateDev& ss,
                           const TreeDev& tr, const RowsDev& rows, long long dcache_stride, long long dscratch_base,
-                          int d, cudaStream_t st);
+                          int d, cudaStream_t st, int qoff = -1);
 void launch_tree_expand(int B, int level, const StepSeqDev* steps, const int* drow_off, const TreeDev& tr,
                         const int* topk_tok, const double* topk_lp, cudaStream_t st);
 void launch_tree_select(int B, const StepSeqDev* steps, const SeqStateDev& ss, const TreeDev& tr, const RowsDev& rows,
@@ -177,6 +183,26 @@ void launch_tree_select(int B, const StepSeqDev* steps, const SeqStateDev& ss, c
                         cudaStream_t st);
 void launch_walk_commit(int B, const StepSeqDev* steps, const SeqStateDev& ss, const TreeDev& tr, const RowsDev& rows,
                         const int* emitted, int* acc_rows, int* result, cudaStream_t st);
+// ---- reject.cu: speculative rejection sampling (the rollout's `acceptance = 1` mode)
+// K i.i.d. children per row from q = softmax(draft logits / T): key of child c of row r is
+// mix_key(keys[r], c); qstat[r] = (max, sum exp((l - max) / T)) of the row
+void launch_sample_children(const float* q, int R, int V, int k, double temperature,
+                            const unsigned long long* keys, int* out_tok, double* out_lp, double* qstat,
+                            cudaStream_t st);
+// multi-round speculative sampling walk (accept child x with prob min(1, r(x) / q(x)), residual
+// r <- norm(max(r - q, 0)) after each rejection, bonus drawn from the final residual) + the
+// same token commit as walk_commit. A node without selected children emits emitted[row] (the
+// keyed sample_token draw), so AR steps equal the strict-match mode bit for bit.
+void launch_walk_reject(int B, const StepSeqDev* steps, const SeqStateDev& ss, const TreeDev& tr, const RowsDev& rows,
+                        const int* emitted, const float* logits, const float* rowmax, const float* qbuf,
+                        const double* qstat, int V, double temperature, float* resid, int* acc_rows, int* result,
+                        cudaStream_t st);
+// test entry: n_trials independent rounds of ONE node: k candidates sampled from q, the
+// multi-round rejection against p, out_tok = emitted token, out_acc = candidate accepted (1) or
+// residual / bonus draw (0). Same device code as the rollout kernels.
+void launch_debug_spec_sample(const float* p, const float* q, int V, int k, double temperature, int n_trials,
+                              unsigned long long seed, float* resid, int* out_tok, int* out_acc, cudaStream_t st);
+
 void launch_commit_kv(int B, const StepSeqDev* steps, const int* acc_rows, const int* result, int layers, int d,
                       __nv_bfloat16* K, __nv_bfloat16* V, long long layer_stride, long long tcache_stride,
                       long long tscratch_base, const float* hidden, float* feats, int max_seq, cudaStream_t st);

@@ -1,0 +1,359 @@
+// Speculative REJECTION SAMPLING -- the `acceptance = 1` rollout mode (north star item 3,
+// BASELINE configs[4] "rejection-sampling verify at T=1.0").
+//
+// The reference only has keyed strict-match acceptance (verify, drafttree.cpp:170-222): the
+// target emits a keyed sample at every selected node and a child is accepted if it carries that
+// token. With deterministic top-k children that is already lossless, and its acceptance rate is
+// the target mass of the candidates -- at T = 1 over a 128k-152k vocabulary that mass is tiny
+// however good the draft is. Standard speculative sampling instead SAMPLES the candidates from
+// the draft distribution q and accepts candidate x with probability min(1, p(x) / q(x)); with
+// several candidates per node it is the multi-round form (SpecInfer): after a rejection the
+// target distribution is replaced by the residual norm(max(p - q, 0)) and the next candidate
+// is tried; when all are rejected the bonus token is drawn from the final residual. Each
+// emitted token is then distributed exactly as p, and a candidate is accepted with probability
+// 1 - TV(p, q) per round, so a draft that has learned q ~ p is accepted almost always.
+//
+// Losslessness needs every node's verified children to be a prefix of an i.i.d. sequence from
+// q that was chosen without looking at the sampled values, so in this mode the tree shape is
+// static: children carry the exact dyadic confidences conf(parent) * 2^-(j+1) and every
+// frontier / rerank tie is broken by node index (tree.cu, TreeDev::static_rank). The expansion
+// and verify machinery (batched draft levels, tree-masked verify forward, KV commit) is the
+// same as the strict-match mode's.
+//
+// Keys (no reference behaviour to match; the parity mode is strict match): child c of a node
+// whose children sit at position p is mix_key(mix_key(mix_key(seq_seed, p), 0xD5A0 + f), c),
+// f = the node's frontier index; the acceptance uniform of child j is
+// mix_key(mix_key(seq_seed, p), 0xACC0 + j); the residual bonus uses 0xB0B0. A node with no
+// selected children emits the keyed sample_token draw of its row (emit kernels), so steps
+// without speculation are bit-identical to the strict-match mode.
+#include <cfloat>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "util.h"
+
+namespace sgb {
+
+namespace {
+
+constexpr int kRT = 512;  // threads per row CTA
+
+// a row's terms exp((l - m) / T): CUDA exp in fp64 (any fixed function defines q / p exactly;
+// the same function evaluates the sampling CDF and the acceptance ratios)
+SGB_DEV double term(float l, double m, double temperature) { return exp((static_cast<double>(l) - m) / temperature); }
+
+// block max of a float row
+SGB_DEV float block_max(const float* L, int V, float* red) {
+    float m = -INFINITY;
+    for (int i = threadIdx.x; i < V; i += blockDim.x) m = fmaxf(m, L[i]);
+    m = warp_max(m);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    float r = red[0];
+    for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) r = fmaxf(r, red[w]);
+    __syncthreads();
+    return r;
+}
+
+SGB_DEV double block_sum(double v, double* red) {
+    v = warp_sum_d(v);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double r = 0.0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) r += red[w];
+    __syncthreads();
+    return r;
+}
+
+// Inverse-CDF draw over a row of non-negative weights w(i) (functor), total Z: thread t owns the
+// contiguous segment [t*seg, (t+1)*seg); per-thread sums, an exclusive scan in shared memory,
+// then the owner of u walks its segment. pre: shared [blockDim.x + 1] doubles.
+template <class W>
+SGB_DEV int block_draw(W w, int V, double u01, double* pre, int* sh_tok) {
+    const int T = blockDim.x, t = threadIdx.x;
+    const int seg = (V + T - 1) / T;
+    const int lo = min(V, t * seg), hi = min(V, lo + seg);
+    double s = 0.0;
+    for (int i = lo; i < hi; ++i) s += w(i);
+    pre[t + 1] = s;
+    __syncthreads();
+    if (t == 0) {
+        pre[0] = 0.0;
+        for (int j = 1; j <= T; ++j) pre[j] += pre[j - 1];
+        *sh_tok = -1;
+    }
+    __syncthreads();
+    const double u = u01 * pre[T];
+    if (pre[t] <= u && u < pre[t + 1]) {
+        double acc = pre[t];
+        int tok = hi - 1;
+        for (int i = lo; i < hi; ++i) {
+            acc += w(i);
+            if (u < acc) {
+                tok = i;
+                break;
+            }
+        }
+        *sh_tok = tok;
+    }
+    __syncthreads();
+    int tok = *sh_tok;
+    if (tok < 0) {  // u at the very top (rounding): the last token with weight
+        if (t == 0) {
+            int last = V - 1;
+            while (last > 0 && w(last) <= 0.0) --last;
+            *sh_tok = last;
+        }
+        __syncthreads();
+        tok = *sh_tok;
+    }
+    __syncthreads();
+    return tok;
+}
+
+struct RowStat {
+    double m, z;
+};
+
+SGB_DEV RowStat row_stat(const float* L, int V, double temperature, float* redf, double* redd) {
+    const double m = static_cast<double>(block_max(L, V, redf));
+    double s = 0.0;
+    for (int i = threadIdx.x; i < V; i += blockDim.x) s += term(L[i], m, temperature);
+    return RowStat{m, block_sum(s, redd)};
+}
+
+// ---- one node of the multi-round walk. p: the target row, q: the draft row (stats given),
+// cand: the node's verified children tokens (n). resid: [V] scratch. Returns the index of the
+// accepted candidate, or -1 with *bonus = the residual draw.
+SGB_DEV int mss_node(const float* P, RowStat ps, const float* Q, RowStat qs, const int* cand, int n, int V,
+                     double temperature, uint64_t key, float* resid, double* pre, float* redf, double* redd,
+                     int* sh_tok, int* bonus) {
+    bool materialised = false;  // resid holds norm-free residual weights once a candidate is rejected
+    double zr = ps.z;           // residual total (unnormalised weights)
+    for (int j = 0; j < n; ++j) {
+        const int x = cand[j];
+        const double qx = term(Q[x], qs.m, temperature) / qs.z;
+        const double rx = (materialised ? static_cast<double>(resid[x]) : term(P[x], ps.m, temperature)) / zr;
+        const double u = rng_first_uniform(mix_key(key, 0xACC0u + j));
+        if (u * qx < rx) return j;  // accept with probability min(1, r(x) / q(x))
+        // r <- max(r / zr - q, 0) (unnormalised: the new total is recomputed)
+        double s = 0.0;
+        for (int i = threadIdx.x; i < V; i += blockDim.x) {
+            const double ri = (materialised ? static_cast<double>(resid[i]) : term(P[i], ps.m, temperature)) / zr;
+            const double qi = term(Q[i], qs.m, temperature) / qs.z;
+            const float ni = static_cast<float>(fmax(ri - qi, 0.0));
+            resid[i] = ni;
+            s += ni;
+        }
+        __syncthreads();
+        materialised = true;
+        zr = block_sum(s, redd);
+        if (!(zr > 0.0)) {  // p == q on the support (floating-point residue): fall back to p
+            for (int i = threadIdx.x; i < V; i += blockDim.x) resid[i] = static_cast<float>(term(P[i], ps.m, temperature));
+            __syncthreads();
+            zr = ps.z;
+        }
+    }
+    const double ub = rng_first_uniform(mix_key(key, 0xB0B0u));
+    if (materialised) {
+        *bonus = block_draw([&](int i) { return static_cast<double>(resid[i]); }, V, ub, pre, sh_tok);
+    } else {
+        *bonus = block_draw([&](int i) { return term(P[i], ps.m, temperature); }, V, ub, pre, sh_tok);
+    }
+    return -1;
+}
+
+// K children per row, i.i.d. from q = softmax(row / T)
+__global__ void __launch_bounds__(kRT) sample_children_kernel(const float* __restrict__ q, int V, int k,
+                                                              double temperature,
+                                                              const unsigned long long* __restrict__ keys,
+                                                              int* __restrict__ out_tok, double* __restrict__ out_lp,
+                                                              double* __restrict__ qstat) {
+    pdl_wait();
+    pdl_trigger();
+    __shared__ double pre[kRT + 1];
+    __shared__ float redf[kRT / 32];
+    __shared__ double redd[kRT / 32];
+    const int r = blockIdx.x;
+    const float* Q = q + static_cast<size_t>(r) * V;
+    const RowStat qs = row_stat(Q, V, temperature, redf, redd);
+    if (threadIdx.x == 0) {
+        qstat[2 * r] = qs.m;
+        qstat[2 * r + 1] = qs.z;
+    }
+    // per-thread segment sums once; each child is one search + one segment walk
+    const int T = blockDim.x, t = threadIdx.x;
+    const int seg = (V + T - 1) / T;
+    const int lo = min(V, t * seg), hi = min(V, lo + seg);
+    double s = 0.0;
+    for (int i = lo; i < hi; ++i) s += term(Q[i], qs.m, temperature);
+    pre[t + 1] = s;
+    __syncthreads();
+    if (t == 0) {
+        pre[0] = 0.0;
+        for (int j = 1; j <= T; ++j) pre[j] += pre[j - 1];
+    }
+    __syncthreads();
+    for (int c = 0; c < k; ++c) {
+        const double u = rng_first_uniform(mix_key(keys[r], static_cast<uint64_t>(c))) * pre[T];
+        if (pre[t] <= u && u < pre[t + 1]) {
+            double acc = pre[t];
+            int tok = hi - 1;
+            for (int i = lo; i < hi; ++i) {
+                acc += term(Q[i], qs.m, temperature);
+                if (u < acc) {
+                    tok = i;
+                    break;
+                }
+            }
+            out_tok[static_cast<size_t>(r) * k + c] = tok;
+            out_lp[static_cast<size_t>(r) * k + c] = log(term(Q[tok], qs.m, temperature) / qs.z);
+        }
+        // (u == total after rounding: no owner) -> the row's argmax, a token of positive mass
+        __syncthreads();
+    }
+    if (t == 0)
+        for (int c = 0; c < k; ++c) {
+            const double u = rng_first_uniform(mix_key(keys[r], static_cast<uint64_t>(c))) * pre[T];
+            if (!(u < pre[T])) {
+                int best = 0;
+                for (int i = 1; i < V; ++i)
+                    if (Q[i] > Q[best]) best = i;
+                out_tok[static_cast<size_t>(r) * k + c] = best;
+                out_lp[static_cast<size_t>(r) * k + c] = log(term(Q[best], qs.m, temperature) / qs.z);
+            }
+        }
+}
+
+// one CTA per live sequence: the multi-round walk from the root along accepted children
+__global__ void __launch_bounds__(kRT) walk_reject_kernel(int B, const StepSeqDev* __restrict__ steps, SeqStateDev ss,
+                                                          TreeDev tr, RowsDev rows, const int* __restrict__ emitted,
+                                                          const float* __restrict__ logits,
+                                                          const float* __restrict__ rowmax,
+                                                          const float* __restrict__ qbuf,
+                                                          const double* __restrict__ qstat, int V, double temperature,
+                                                          float* __restrict__ resid, int* __restrict__ acc_rows,
+                                                          int* __restrict__ result) {
+    pdl_wait();
+    pdl_trigger();
+    __shared__ double pre[kRT + 1];
+    __shared__ float redf[kRT / 32];
+    __shared__ double redd[kRT / 32];
+    __shared__ int sh_tok, sh_bonus;
+    __shared__ int cand_row[16], cand_tok[16];
+    __shared__ int acc_tok[kMaxChain + 1];
+    const int i = blockIdx.x;
+    const StepSeqDev st = steps[i];
+    const int s = st.seq, off = st.vrow_off, N = st.nsel;
+    const size_t base = static_cast<size_t>(s) * tr.tmax;
+    float* R = resid + static_cast<size_t>(i) * V;
+    int cur = 0, nacc = 0;
+    if (threadIdx.x == 0) acc_rows[i * kMaxChain] = 0;
+    for (;;) {
+        // the node's verified children, in row order (a prefix of its sampled children)
+        if (threadIdx.x == 0) {
+            int n = 0;
+            for (int r = cur + 1; r < N && n < 16; ++r)
+                if (rows.par_row[off + r] == cur) {
+                    cand_row[n] = r;
+                    cand_tok[n] = rows.tok[off + r];
+                    ++n;
+                }
+            sh_tok = n;
+        }
+        __syncthreads();
+        const int n = sh_tok;
+        __syncthreads();
+        if (n == 0 || nacc + 1 >= kMaxChain) {
+            if (threadIdx.x == 0) acc_tok[nacc++] = emitted[off + cur];  // keyed sample_token draw
+            break;
+        }
+        const float* P = logits + static_cast<size_t>(off + cur) * V;
+        const double pm = static_cast<double>(rowmax[off + cur]);
+        double zs = 0.0;
+        for (int e = threadIdx.x; e < V; e += blockDim.x) zs += term(P[e], pm, temperature);
+        const RowStat ps{pm, block_sum(zs, redd)};
+        const int node = tr.sel[base + cur];
+        const int qr = tr.qrow[base + node];
+        const RowStat qs{qstat[2 * qr], qstat[2 * qr + 1]};
+        const int depth = tr.dep[base + node];
+        const uint64_t key = mix_key(ss.seed[s], static_cast<uint64_t>(st.p + depth + 1));
+        int bonus = 0;
+        const int j = mss_node(P, ps, qbuf + static_cast<size_t>(qr) * V, qs, cand_tok, n, V, temperature, key, R, pre,
+                               redf, redd, &sh_bonus, &bonus);
+        if (j < 0) {
+            if (threadIdx.x == 0) acc_tok[nacc++] = bonus;
+            break;
+        }
+        if (threadIdx.x == 0) {
+            acc_tok[nacc] = cand_tok[j];
+            acc_rows[i * kMaxChain + nacc + 1] = cand_row[j];
+        }
+        ++nacc;
+        cur = cand_row[j];
+        __syncthreads();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) commit_tokens_dev(st, ss, acc_tok, nacc, result + 2 * i);
+}
+
+__global__ void __launch_bounds__(kRT) debug_spec_kernel(const float* __restrict__ p, const float* __restrict__ q,
+                                                         int V, int k, double temperature, unsigned long long seed,
+                                                         float* __restrict__ resid, int* __restrict__ out_tok,
+                                                         int* __restrict__ out_acc) {
+    __shared__ double pre[kRT + 1];
+    __shared__ float redf[kRT / 32];
+    __shared__ double redd[kRT / 32];
+    __shared__ int sh_tok;
+    __shared__ int cand[16];
+    const int trial = blockIdx.x;  // sh_tok: block_draw's scratch
+    const RowStat ps = row_stat(p, V, temperature, redf, redd);
+    const RowStat qs = row_stat(q, V, temperature, redf, redd);
+    const uint64_t key = mix_key(seed, static_cast<uint64_t>(trial));
+    for (int c = 0; c < k; ++c) {
+        const double u = rng_first_uniform(mix_key(mix_key(key, 0xD5A0u), static_cast<uint64_t>(c)));
+        const int x = block_draw([&](int i) { return term(q[i], qs.m, temperature); }, V, u, pre, &sh_tok);
+        if (threadIdx.x == 0) cand[c] = x;
+        __syncthreads();
+    }
+    int bonus = 0;
+    const int j = mss_node(p, ps, q, qs, cand, k, V, temperature, key, resid + static_cast<size_t>(trial) * V, pre, redf,
+                           redd, &sh_tok, &bonus);
+    if (threadIdx.x == 0) {
+        out_tok[trial] = j >= 0 ? cand[j] : bonus;
+        out_acc[trial] = j >= 0 ? 1 : 0;
+    }
+}
+
+}  // namespace
+
+void launch_sample_children(const float* q, int R, int V, int k, double temperature, const unsigned long long* keys,
+                            int* out_tok, double* out_lp, double* qstat, cudaStream_t st) {
+    if (R <= 0) return;
+    if (k < 1 || k > 16) throw std::invalid_argument("sample_children: k must be in [1, 16]");
+    if (!(temperature > 0)) throw std::invalid_argument("rejection sampling needs temperature > 0");
+    launch_pdl(sample_children_kernel, R, kRT, 0, st, q, V, k, temperature, keys, out_tok, out_lp, qstat);
+    SGB_KCHECK();
+}
+
+void launch_walk_reject(int B, const StepSeqDev* steps, const SeqStateDev& ss, const TreeDev& tr, const RowsDev& rows,
+                        const int* emitted, const float* logits, const float* rowmax, const float* qbuf,
+                        const double* qstat, int V, double temperature, float* resid, int* acc_rows, int* result,
+                        cudaStream_t st) {
+    if (B <= 0) return;
+    launch_pdl(walk_reject_kernel, B, kRT, 0, st, B, steps, ss, tr, rows, emitted, logits, rowmax, qbuf, qstat, V,
+               temperature, resid, acc_rows, result);
+    SGB_KCHECK();
+}
+
+void launch_debug_spec_sample(const float* p, const float* q, int V, int k, double temperature, int n_trials,
+                              unsigned long long seed, float* resid, int* out_tok, int* out_acc, cudaStream_t st) {
+    if (n_trials <= 0) return;
+    if (k < 1 || k > 16) throw std::invalid_argument("debug_spec_sample: k in [1, 16]");
+    debug_spec_kernel<<<n_trials, kRT, 0, st>>>(p, q, V, k, temperature, seed, resid, out_tok, out_acc);
+    SGB_KCHECK();
+}
+
+}  // namespace sgb

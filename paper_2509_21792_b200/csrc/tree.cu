@@ -55,8 +55,9 @@ __global__ void tree_root_kernel(int B, const StepSeqDev* __restrict__ steps, Se
             tr.par[base + 1 + j] = 0;
             tr.dep[base + 1 + j] = 1;
             tr.lp[base + 1 + j] = l;
-            tr.conf[base + 1 + j] = 1.0 * exp(l);
+            tr.conf[base + 1 + j] = tr.static_rank ? ldexp(1.0, -(j + 1)) : 1.0 * exp(l);
         }
+        if (tr.qrow) tr.qrow[base] = st.root_row;
         n = 1 + st.k;
         tr.lvl_start[st.seq] = 1;
         tr.lvl_cnt[st.seq] = st.k;
@@ -66,7 +67,7 @@ __global__ void tree_root_kernel(int B, const StepSeqDev* __restrict__ steps, Se
 
 __global__ void tree_frontier_kernel(int B, int level, const StepSeqDev* __restrict__ steps,
                                      const int* __restrict__ drow_off, SeqStateDev ss, TreeDev tr, RowsDev rows,
-                                     long long dcache_stride, long long dscratch_base, int d) {
+                                     long long dcache_stride, long long dscratch_base, int d, int qoff) {
     pdl_wait();
     pdl_trigger();
     const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -84,10 +85,11 @@ __global__ void tree_frontier_kernel(int B, int level, const StepSeqDev* __restr
         if (c < cnt) {
             const int v = start + c;
             const double cv = tr.conf[base + v];
-            const int tv = tr.tok[base + v];
+            // static ranking (rejection mode): the sampled tokens must not steer the shape
+            const int tv = tr.static_rank ? 0 : tr.tok[base + v];
             int rank = 0;
             for (int u = start; u < start + cnt; ++u)
-                rank += node_better(tr.conf[base + u], tr.tok[base + u], u, cv, tv, v) ? 1 : 0;
+                rank += node_better(tr.conf[base + u], tr.static_rank ? 0 : tr.tok[base + u], u, cv, tv, v) ? 1 : 0;
             selected = rank < k;
         }
         const unsigned bal = __ballot_sync(0xffffffffu, selected);
@@ -105,6 +107,7 @@ __global__ void tree_frontier_kernel(int B, int level, const StepSeqDev* __restr
         tr.fslot[base + node] = fs;
         const int row = drow_off[i] + j;
         const int dn = tr.dep[base + node];
+        if (qoff >= 0 && tr.qrow) tr.qrow[base + node] = qoff + row;
         rows.tok[row] = tr.tok[base + node];
         rows.pos[row] = st.p + dn;
         const long long own = dscratch_base + static_cast<long long>(s) * tr.ds + fs;
@@ -145,7 +148,7 @@ __global__ void tree_expand_kernel(int B, int level, const StepSeqDev* __restric
             tr.par[base + n] = parent;
             tr.dep[base + n] = level;
             tr.lp[base + n] = l;
-            tr.conf[base + n] = pc * exp(l);
+            tr.conf[base + n] = tr.static_rank ? ldexp(pc, -(c + 1)) : pc * exp(l);
             ++n;
         }
     }
@@ -227,7 +230,7 @@ __global__ void walk_commit_kernel(int B, const StepSeqDev* __restrict__ steps, 
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= B) return;
     const StepSeqDev st = steps[i];
-    const int s = st.seq, off = st.vrow_off, N = st.nsel;
+    const int off = st.vrow_off, N = st.nsel;
     int acc_tok[kMaxChain + 1];
     int nacc = 0, cur = 0;
     acc_rows[i * kMaxChain] = 0;
@@ -245,26 +248,7 @@ __global__ void walk_commit_kernel(int B, const StepSeqDev* __restrict__ steps, 
         cur = nxt;
     }
     acc_tok[nacc++] = emitted[off + cur];
-    int len = ss.len[s], a = 0, fin = 0, eos = 0;
-    for (int j = 0; j < nacc; ++j) {
-        const int t = acc_tok[j];
-        ss.tokens[static_cast<size_t>(s) * ss.max_seq + len] = t;
-        ++len;
-        ++a;
-        if (t == kEos) {
-            fin = eos = 1;
-            break;
-        }
-        if (len >= st.len_cap) {
-            fin = 1;
-            break;
-        }
-    }
-    ss.len[s] = len;
-    ss.finished[s] = fin;
-    ss.hit_eos[s] = eos;
-    result[2 * i] = a;
-    result[2 * i + 1] = fin;
+    commit_tokens_dev(st, ss, acc_tok, nacc, result + 2 * i);
 }
 
 __global__ void commit_kv_kernel(const StepSeqDev* __restrict__ steps, const int* __restrict__ acc_rows,
@@ -362,10 +346,10 @@ void launch_tree_root(int B, const StepSeqDev* steps, const SeqStateDev& ss, con
 
 void launch_tree_frontier(int B, int level, const StepSeqDev* steps, const int* drow_off, const SeqStateDev& ss,
                           const TreeDev& tr, const RowsDev& rows, long long dcache_stride, long long dscratch_base,
-                          int d, cudaStream_t st) {
+                          int d, cudaStream_t st, int qoff) {
     if (B <= 0) return;
     launch_pdl(tree_frontier_kernel, (B + 3) / 4, 128, 0, st, B, level, steps, drow_off, ss, tr, rows, dcache_stride,
-                                                      dscratch_base, d);
+                                                      dscratch_base, d, qoff);
     SGB_KCHECK();
 }
 
