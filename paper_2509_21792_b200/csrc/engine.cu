@@ -547,6 +547,7 @@ void Engine::group_advantages(const long long* answers, int n_groups, int g, dou
                               double* adv, int* valid) {
     const int n = n_groups * g;
     if (n_groups <= 0 || g < 2) throw std::invalid_argument("standardize_advantages: need G >= 2");
+    if (last_waves_) throw std::invalid_argument("group_advantages: the last rollout ran in waves (not resident)");
     if (static_cast<size_t>(n) != last_lens_.size()) throw std::invalid_argument("group_advantages: not the last rollout's shape");
     if (n > max_rows_) throw std::invalid_argument("group_advantages: too many sequences");
     int* dlen = misc_i_;
@@ -1073,7 +1074,9 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
     tr_.static_rank = rej ? 1 : 0;
     const int P = static_cast<int>(a.prompts.size());
     const int n_seqs = P * a.g;
-    if (n_seqs > max_seqs_) throw std::invalid_argument("generate: more sequences than engine max_seqs");
+    const int G = a.g;
+    if (G > max_seqs_) throw std::invalid_argument("generate: group size exceeds engine max_seqs");
+    if (G > max_rows_) throw std::invalid_argument("generate: group size exceeds engine max_rows");
     if (!a.seq_max_new.empty() && static_cast<int>(a.seq_max_new.size()) != n_seqs)
         throw std::invalid_argument("generate: seq_max_new size mismatch");
 
@@ -1081,40 +1084,71 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
     const long long launches0 = launches_;
     SGB_CUDA(cudaMemsetAsync(err_, 0, sizeof(int), st_));
 
-    // ---------------- sequence setup
-    std::vector<int> len(n_seqs), len_cap(n_seqs), fin(n_seqs, 0), dft_len(n_seqs, 0), plen(n_seqs);
-    std::vector<unsigned long long> seeds(n_seqs);
-    for (int pi = 0; pi < P; ++pi)
-        for (int r = 0; r < a.g; ++r) {
-            const int sid = pi * a.g + r;
-            const int q = static_cast<int>(a.prompts[pi].size());
-            plen[sid] = q;
-            seeds[sid] = mix_key_host(a.seed, static_cast<uint64_t>(sid + a.sid_offset) + 1);
-            const int mn = a.seq_max_new.empty() ? a.max_new_tokens : a.seq_max_new[sid];
-            len_cap[sid] = mn > 0 ? std::min(T, q + mn) : T;
-            h2d(ss_.tokens + static_cast<size_t>(sid) * T, a.prompts[pi].data(), q, st_);
-        }
-    h2d(ss_.seed, seeds.data(), n_seqs, st_);
+    // ---------------- sequences, KV regions and admission
+    // The reference admits every sequence at once with its own KvCache (scheduler.cpp:259-294).
+    // Here the KV store holds max_seqs_ sequence REGIONS (one region = max_seq_len slots of every
+    // layer), handed out in aligned blocks of G to whole query groups (the members read their
+    // prompt K/V from the group leader's region). When a rollout has more sequences than
+    // regions it runs in waves: a group's regions are recycled once all its members finished
+    // (their tokens and features copied out first) and the next pending group is admitted and
+    // prefilled at that step boundary. Sequence ids, seeds and caps stay global (sid order).
+    const int S = max_seqs_;
+    const int n_gslots = S / G;
+    std::vector<int> sid_of(S, -1), len(S, 0), len_cap(S, 0), fin(S, 1), dft_len(S, 0), plen(S, 0);
+    std::vector<unsigned long long> seeds(S, 0);
+    std::vector<int> sid_cap(n_seqs), sid_len(n_seqs, 0), sid_eos(n_seqs, 0);
+    std::vector<unsigned long long> sid_seed(n_seqs);
+    for (int sid = 0; sid < n_seqs; ++sid) {
+        const int q = static_cast<int>(a.prompts[sid / G].size());
+        sid_seed[sid] = mix_key_host(a.seed, static_cast<uint64_t>(sid + a.sid_offset) + 1);
+        const int mn = a.seq_max_new.empty() ? a.max_new_tokens : a.seq_max_new[sid];
+        sid_cap[sid] = mn > 0 ? std::min(T, q + mn) : T;
+    }
+    res.tokens.resize(n_seqs);
+    res.prompt_len.resize(n_seqs);
+    res.hit_eos.assign(n_seqs, 0);
+    if (a.want_features && !a.features_out) res.features.resize(n_seqs);
+    std::vector<int> gslot_group(n_gslots, -1);  // query group held by a block of G regions
+    int next_group = 0;
+    bool waves = false;
     for (const auto& pr : a.prompts) res.h2d_bytes += static_cast<long long>(pr.size()) * sizeof(int);
     SGB_CUDA(cudaEventRecord(ev0_, st_));  // inputs resident in HBM from here on
 
-    // ---------------- prefill: one forward per chunk of distinct prompts (scheduler.cpp:259-294)
-    {
-        int pi = 0;
-        while (pi < P) {
+    // copy a retired sequence's tokens (+ features) to the host result (scheduler.cpp:343-353)
+    auto retire = [&](int slot) {
+        const int sid = sid_of[slot];
+        auto& tk = res.tokens[sid];
+        tk.resize(len[slot]);
+        d2h(tk.data(), ss_.tokens + static_cast<size_t>(slot) * T, len[slot], st_);
+        if (a.want_features) {
+            const size_t nf = static_cast<size_t>(len[slot] - 1) * d;
+            float* dst = a.features_out ? a.features_out + static_cast<size_t>(sid) * (T - 1) * d
+                                        : (res.features[sid].resize(nf), res.features[sid].data());
+            d2h(dst, feats_ + static_cast<size_t>(slot) * T * d, nf, st_);
+        }
+        d2h(&sid_eos[sid], ss_.hit_eos + slot, 1, st_);
+        sid_len[sid] = len[slot];
+        sid_of[slot] = -1;
+    };
+
+    // ---------------- prefill of newly admitted groups: one forward per chunk of distinct
+    // prompts (scheduler.cpp:259-294); the prompt K/V is copied to the G members
+    auto prefill = [&](const std::vector<std::pair<int, int>>& adm) {  // (query group, gslot)
+        const int NA = static_cast<int>(adm.size());
+        int ai = 0;
+        while (ai < NA) {
             // a chunk is bounded by its prompt rows AND by its np * g first-token emissions (both
             // index row-sized buffers: lm_idx_, rows_.seed, the sampling scratch)
-            if (a.g > max_rows_) throw std::invalid_argument("generate: group size exceeds engine max_rows");
-            int rows = 0, pe = pi;
-            while (pe < P && rows + static_cast<int>(a.prompts[pe].size()) <= max_rows_ &&
-                   (pe - pi + 1) * a.g <= max_rows_)
-                rows += a.prompts[pe++].size();
-            if (pe == pi) throw std::invalid_argument("generate: prompt longer than engine max_rows");
+            int rows = 0, ae = ai;
+            while (ae < NA && rows + static_cast<int>(a.prompts[adm[ae].first].size()) <= max_rows_ &&
+                   (ae - ai + 1) * G <= max_rows_)
+                rows += a.prompts[adm[ae++].first].size();
+            if (ae == ai) throw std::invalid_argument("generate: prompt longer than engine max_rows");
             std::vector<int> tok, pos, cl, chl, last_rows;
             std::vector<long long> kvd, cb;
             int maxq = 0;
-            for (int p2 = pi; p2 < pe; ++p2) {
-                const int s0 = p2 * a.g;
+            for (int x = ai; x < ae; ++x) {
+                const int p2 = adm[x].first, s0 = adm[x].second * G;
                 const int q = static_cast<int>(a.prompts[p2].size());
                 maxq = std::max(maxq, q);
                 for (int t = 0; t < q; ++t) {
@@ -1128,7 +1162,7 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
                 last_rows.push_back(static_cast<int>(tok.size()) - 1);
             }
             upload_rows_host(rows, tok, pos, kvd, cb, cl, chl, {}, nullptr);
-            const int np = pe - pi;
+            const int np = ae - ai;
             h2d(lm_idx_, last_rows.data(), np, st_);
             Fwd f;
             f.M = rows;
@@ -1139,8 +1173,8 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
             f.logits_out = logits_;
             f.max_vlen = maxq;
             f.attn_kv_unique = rows;
-            for (int p2 = pi; p2 < pe; ++p2) {
-                const double q = static_cast<double>(a.prompts[p2].size());
+            for (int x = ai; x < ae; ++x) {
+                const double q = static_cast<double>(a.prompts[adm[x].first].size());
                 f.attn_row_keys += q * (q + 1) / 2;
             }
             forward(f);
@@ -1148,26 +1182,27 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
             // features of every member: feats[s][t] = hidden[row]
             std::vector<int> src_row;
             std::vector<long long> dst_off;
-            std::vector<int> srcs, dsts, pl, ems, emseq, emq, emcap, emrow, emkey;
+            std::vector<int> srcs, dsts, pl, emseq, emq, emcap, emrow, emkey;
             std::vector<unsigned long long> emseed;
             int row0 = 0;
-            for (int p2 = pi; p2 < pe; ++p2) {
+            for (int x = ai; x < ae; ++x) {
+                const int p2 = adm[x].first, s0 = adm[x].second * G;
                 const int q = static_cast<int>(a.prompts[p2].size());
-                for (int r = 0; r < a.g; ++r) {
-                    const int s = p2 * a.g + r;
+                for (int r = 0; r < G; ++r) {
+                    const int s = s0 + r;
                     for (int t = 0; t < q; ++t) {
                         src_row.push_back(row0 + t);
                         dst_off.push_back((static_cast<long long>(s) * T + t) * d);
                     }
                     if (r > 0) {
-                        srcs.push_back(p2 * a.g);
+                        srcs.push_back(s0);
                         dsts.push_back(s);
                         pl.push_back(q);
                     }
                     emseq.push_back(s);
                     emq.push_back(q);
                     emcap.push_back(len_cap[s]);
-                    emrow.push_back(p2 - pi);
+                    emrow.push_back(x - ai);
                     emseed.push_back(seeds[s]);
                     emkey.push_back(q);
                 }
@@ -1206,17 +1241,46 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
             launch_prefill_commit(ne, b + 2 * ne, b + 3 * ne, lm_idx_, emitted_, ss_, st_);
             count(2);
             SGB_CUDA(cudaStreamSynchronize(st_));
-            pi = pe;
+            ai = ae;
         }
-        std::vector<int> t1(n_seqs), f1(n_seqs);
-        d2h(t1.data(), ss_.len, n_seqs, st_);
-        d2h(f1.data(), ss_.finished, n_seqs, st_);
+        std::vector<int> t1(S), f1(S);
+        d2h(t1.data(), ss_.len, S, st_);
+        d2h(f1.data(), ss_.finished, S, st_);
         SGB_CUDA(cudaStreamSynchronize(st_));
-        for (int s = 0; s < n_seqs; ++s) {
-            len[s] = t1[s];
-            fin[s] = f1[s];
+        for (const auto& g2 : adm)
+            for (int r = 0; r < G; ++r) {
+                const int s = g2.second * G + r;
+                len[s] = t1[s];
+                fin[s] = f1[s];
+            }
+    };
+
+    // admit pending query groups into free region blocks, then prefill them
+    auto admit = [&]() {
+        std::vector<std::pair<int, int>> adm;
+        for (int gs = 0; gs < n_gslots && next_group < P; ++gs) {
+            if (gslot_group[gs] >= 0) continue;
+            const int pi = next_group++;
+            gslot_group[gs] = pi;
+            const int q = static_cast<int>(a.prompts[pi].size());
+            for (int r = 0; r < G; ++r) {
+                const int s = gs * G + r, sid = pi * G + r;
+                sid_of[s] = sid;
+                plen[s] = q;
+                seeds[s] = sid_seed[sid];
+                len_cap[s] = sid_cap[sid];
+                dft_len[s] = 0;
+                fin[s] = 0;
+                res.prompt_len[sid] = q;
+                h2d(ss_.tokens + static_cast<size_t>(s) * T, a.prompts[pi].data(), q, st_);
+            }
+            h2d(ss_.seed + gs * G, seeds.data() + gs * G, G, st_);
+            adm.emplace_back(pi, gs);
         }
-    }
+        if (!adm.empty()) prefill(adm);
+    };
+    admit();
+    if (next_group < P) waves = true;
 
     // ---------------- step loop (scheduler.cpp:299-341)
     SGB_CUDA(cudaEventRecord(evs_a_, st_));  // prefill done; each step's end is timed against the last
@@ -1230,10 +1294,10 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
     std::vector<int> drow, live;
     for (int step = 0;; ++step) {
         live.clear();
-        for (int s = 0; s < n_seqs; ++s)
-            if (!fin[s]) live.push_back(s);
+        for (int s = 0; s < S; ++s)
+            if (sid_of[s] >= 0 && !fin[s]) live.push_back(s);
         const int B = static_cast<int>(live.size());
-        if (B == 0) break;
+        if (B == 0) break;  // (pending groups are admitted at the end of the step that frees regions)
         const int eff_b = a.early_term ? B : n_seqs;
         SpecCfg cfg;
         if (a.mode == 0) cfg = SpecCfg{1, 0, 0};
@@ -1509,27 +1573,48 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
             fin[s] = h_result_[2 * i + 1];
             stat.accepted += acc;
             res.events.push_back(step);
-            res.events.push_back(s);
+            res.events.push_back(sid_of[s]);
             res.events.push_back(acc);
         }
         res.steps.push_back(stat);
         res.total_accepted += stat.accepted;
         res.total_verify_slots += B;
+        if (next_group < P) {  // waves: recycle the regions of finished groups, admit the next groups
+            bool freed = false;
+            for (int gs = 0; gs < n_gslots; ++gs) {
+                if (gslot_group[gs] < 0) continue;
+                bool done = true;
+                for (int r = 0; r < G && done; ++r) done = fin[gs * G + r] != 0;
+                if (!done) continue;
+                for (int r = 0; r < G; ++r) retire(gs * G + r);
+                gslot_group[gs] = -1;
+                freed = true;
+            }
+            if (freed) {
+                SGB_CUDA(cudaStreamSynchronize(st_));
+                admit();
+                SGB_CUDA(cudaEventRecord(evs_a_, st_));  // the next step is timed after the admission prefill
+            }
+        }
     }
     SGB_CUDA(cudaEventRecord(ev1_, st_));
 
-    // ---------------- results (scheduler.cpp:343-353)
-    std::vector<int> h_eos(n_seqs);
-    d2h(h_eos.data(), ss_.hit_eos, n_seqs, st_);
-    res.tokens.resize(n_seqs);
-    res.prompt_len = plen;
-    for (int s = 0; s < n_seqs; ++s) {
-        res.tokens[s].resize(len[s]);
-        d2h(res.tokens[s].data(), ss_.tokens + static_cast<size_t>(s) * T, len[s], st_);
+    // ---------------- results (scheduler.cpp:343-353) of the sequences still resident
+    std::vector<int> h_eos(S);
+    d2h(h_eos.data(), ss_.hit_eos, S, st_);
+    std::vector<int> resident;
+    for (int s2 = 0; s2 < S; ++s2)
+        if (sid_of[s2] >= 0) resident.push_back(s2);
+    for (int s2 : resident) {
+        const int sid = sid_of[s2];
+        res.tokens[sid].resize(len[s2]);
+        d2h(res.tokens[sid].data(), ss_.tokens + static_cast<size_t>(s2) * T, len[s2], st_);
+        sid_len[sid] = len[s2];
     }
-    if (a.want_features && a.features_out) {
-        // one DMA of the whole feature store into pinned staging at full link rate ...
-        const size_t n = static_cast<size_t>(n_seqs) * T * d;
+    const int slot_hi = resident.empty() ? 0 : resident.back() + 1;
+    if (a.want_features && a.features_out && slot_hi > 0) {
+        // one DMA of the resident feature store into pinned staging at full link rate ...
+        const size_t n = static_cast<size_t>(slot_hi) * T * d;
         if (feats_host_cap_ < n) {
             if (feats_host_) cudaFreeHost(feats_host_);
             feats_host_ = nullptr;
@@ -1538,33 +1623,46 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
         }
         SGB_CUDA(cudaMemcpyAsync(feats_host_, feats_, n * sizeof(float), cudaMemcpyDeviceToHost, st_));
     } else if (a.want_features) {
-        res.features.resize(n_seqs);
-        for (int s = 0; s < n_seqs; ++s) {
-            res.features[s].resize(static_cast<size_t>(len[s] - 1) * d);
-            d2h(res.features[s].data(), feats_ + static_cast<size_t>(s) * T * d, res.features[s].size(), st_);
+        for (int s2 : resident) {
+            const int sid = sid_of[s2];
+            res.features[sid].resize(static_cast<size_t>(len[s2] - 1) * d);
+            d2h(res.features[sid].data(), feats_ + static_cast<size_t>(s2) * T * d, res.features[sid].size(), st_);
         }
     }
     SGB_CUDA(cudaStreamSynchronize(st_));
-    if (a.want_features && a.features_out) {
-        // ... then the per-sequence scatter into the caller's layout on several host threads
+    if (a.want_features && a.features_out && slot_hi > 0) {
+        // ... then the per-sequence scatter into the caller's layout (sid order) on host threads
         const int nth = std::max(1, std::min(16, static_cast<int>(std::thread::hardware_concurrency())));
         std::vector<std::thread> pool;
+        const int nres = static_cast<int>(resident.size());
         for (int w = 0; w < nth; ++w)
             pool.emplace_back([&, w] {
-                for (int s = w; s < n_seqs; s += nth)
-                    std::memcpy(a.features_out + static_cast<size_t>(s) * (T - 1) * d,
-                                feats_host_ + static_cast<size_t>(s) * T * d,
-                                static_cast<size_t>(len[s] - 1) * d * sizeof(float));
+                for (int k = w; k < nres; k += nth) {
+                    const int s2 = resident[k];
+                    std::memcpy(a.features_out + static_cast<size_t>(sid_of[s2]) * (T - 1) * d,
+                                feats_host_ + static_cast<size_t>(s2) * T * d,
+                                static_cast<size_t>(len[s2] - 1) * d * sizeof(float));
+                }
             });
         for (auto& t : pool) t.join();
     }
-    res.hit_eos = h_eos;
-    last_lens_ = len;  // the draft update can consume this rollout straight from HBM
-    last_plens_ = plen;
-    for (int s = 0; s < n_seqs; ++s) {
-        res.d2h_bytes += static_cast<long long>(len[s]) * sizeof(int);
-        if (a.want_features) res.d2h_bytes += static_cast<long long>(len[s] - 1) * d * sizeof(float);
+    for (int s2 : resident) sid_eos[sid_of[s2]] = h_eos[s2];
+    res.hit_eos = sid_eos;
+    // the draft update / group advantages can consume this rollout straight from HBM when every
+    // sequence is still resident at region == sid (no waves)
+    last_waves_ = waves;
+    if (!waves) {
+        last_lens_ = sid_len;
+        last_plens_ = res.prompt_len;
+    } else {
+        last_lens_.clear();
+        last_plens_.clear();
     }
+    for (int sid = 0; sid < n_seqs; ++sid) {
+        res.d2h_bytes += static_cast<long long>(sid_len[sid]) * sizeof(int);
+        if (a.want_features) res.d2h_bytes += static_cast<long long>(sid_len[sid] - 1) * d * sizeof(float);
+    }
+    res.waves = waves;
     float ms = 0.f;
     SGB_CUDA(cudaEventElapsedTime(&ms, ev0_, ev1_));
     res.seconds = ms * 1e-3;

@@ -94,6 +94,7 @@ struct RolloutResult {
     double prefill_seconds = 0;
     std::vector<double> step_seconds;  // device time of every decode step (CUDA events)
     long long h2d_bytes = 0, d2h_bytes = 0;
+    bool waves = false;  // more sequences than KV regions: groups were admitted as regions freed
 };
 
 class Engine {
@@ -317,6 +318,7 @@ class Engine {
     } tr2_;
     std::vector<int> last_lens_;   // token counts of the last rollout's sequences
     std::vector<int> last_plens_;  // and their prompt lengths
+    bool last_waves_ = false;      // the last rollout recycled KV regions (its data left HBM)
     long long target_forward_calls_ = 0;
     double* adv_buf_ = nullptr;    // [2 * max_rows] rewards + advantages of group_advantages
     // rejection-sampling mode buffers (allocated on first use): draft logits of every expanded

@@ -204,6 +204,7 @@ Engine::DraftLossTerms Engine::draft_update(const DraftUpdateArgs& A) {
     const int* tok_base_dev = nullptr;
     std::vector<int> host_tokens;
     if (A.use_last_rollout) {
+        if (last_waves_) throw std::invalid_argument("draft_update: the last rollout ran in waves (not resident in HBM)");
         lens = last_lens_;
         for (size_t s = 0; s < lens.size(); ++s) {
             tok_off.push_back(static_cast<long long>(s) * dims_.max_seq);

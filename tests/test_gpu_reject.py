@@ -78,12 +78,13 @@ def test_rollout_marginals_match_ar_sampling(eng):
     for it in range(48):
         a = eng.generate(prompt, 64, mode="vanilla", seed=10_000 + it, **kw)
         r = eng.generate(prompt, 64, mode="adaptive_spec", seed=20_000 + it, acceptance="rejection", **kw)
-        ar += [t[q + 1] for t in a.tokens]
-        sp += [t[q + 1] for t in r.tokens]
+        # EOS at the first generated token ends a sequence: its own bin (index V)
+        ar += [t[q + 1] if len(t) > q + 1 else SMALL.vocab_size for t in a.tokens]
+        sp += [t[q + 1] if len(t) > q + 1 else SMALL.vocab_size for t in r.tokens]
         spec_steps += sum(1 for s in r.steps if s[1] > 1)
         acc += r.total_accepted
         slots += r.total_verify_slots
-    V = SMALL.vocab_size
+    V = SMALL.vocab_size + 1
     ca = np.bincount(ar, minlength=V).astype(np.float64)
     cs = np.bincount(sp, minlength=V).astype(np.float64)
     keep = (ca + cs) >= 10
