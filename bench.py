@@ -48,14 +48,16 @@ WORKLOADS = {
                desc="Qwen2.5-7B-shaped GRPO rollout, data-parallel by query group, 16 queries x group 8 per GPU, "
                     "variable-length stops 256..1024, adaptive spec + one online draft-learning AdamW step with "
                     "NCCL gradient all-reduce per step"),
-    # c5 (BASELINE configs[4]): Llama-3-8B shape, T=1.0 keyed sampling (the reference's strict-match
-    # verify at T>0, the parity mode), group 16, 4096 new tokens. The full per-GPU
-    # shard (32 queries x 16 = 512 sequences x 4224 positions) needs ~1.1 TB of KV at 524 KB per
-    # token, beyond one GPU's 180 GB: this shard runs 2 queries x 16 = 32 sequences (71 GB of KV)
-    "c5": dict(V=128256, d=4096, L=32, H=32, dff=14336, P=128, G=16, Q=2, new=4096, stops=False, online=False,
-               warm=0, temp=1.0,
-               desc="Llama-3-8B-shaped target + 1-layer draft, T=1.0 keyed sampling, 2 queries x group 16 per GPU "
-                    "(memory-bounded shard of 256 x 16 over 8 GPUs), 128-token prompts, 4096 new tokens, adaptive spec"),
+    # c5 (BASELINE configs[4]): Llama-3-8B shape, rejection-sampling verify at T=1.0, 256 queries x
+    # group 16 over 8 GPUs = the full per-GPU shard of 32 queries x 16 = 512 sequences x 4224
+    # positions. Its KV (524 KB per token, 1.1 TB) is 6x one GPU's HBM, so the rollout runs in
+    # waves over `regions` resident KV regions (engine admission); features are not
+    # returned (35 GB per rollout), tokens are
+    "c5": dict(V=128256, d=4096, L=32, H=32, dff=14336, P=128, G=16, Q=32, new=4096, stops=False, online=False,
+               warm=0, temp=1.0, acceptance="rejection", features=False, regions=48, rows=1024,
+               desc="Llama-3-8B-shaped target + 1-layer draft, rejection-sampling verify at T=1.0, 32 queries x "
+                    "group 16 per GPU (the full 256 x 16 shard of 8 GPUs), 128-token prompts, 4096 new tokens, "
+                    "adaptive spec, KV-region waves (48 resident sequences)"),
     "c1": dict(V=512, d=256, L=2, H=4, dff=1024, P=32, G=4, Q=8, new=128, stops=False, online=False, warm=0,
                desc="2-layer d=256 target + 1-layer draft, 8 queries x group 4, 32-token prompts, 128 new tokens"),
 }
@@ -274,12 +276,19 @@ def main():
     ap.add_argument("--max-new", type=int, default=0, help="override new tokens (profiling runs)")
     ap.add_argument("--warm-iters", type=int, default=-1, help="online draft-warming iterations (default per config)")
     ap.add_argument("--c-peak", type=int, default=C_PEAK)
+    ap.add_argument("--acceptance", default=None, choices=["strict", "rejection"],
+                    help="verify acceptance (default per config: c5 rejection sampling, else strict match)")
+    ap.add_argument("--warmup-max-new", type=int, default=0,
+                    help="new tokens of the warm-up rollouts (0: the workload's); long workloads (c5) warm up short")
+    ap.add_argument("--no-profile", action="store_true", help="skip the per-kernel-class profiled rollout")
     args = ap.parse_args()
     w = dict(WORKLOADS[args.config])
     if args.max_new:
         w["new"] = args.max_new
     if args.warm_iters >= 0:
         w["warm"] = args.warm_iters
+    if args.acceptance:
+        w["acceptance"] = args.acceptance
     if args.impl == "reference":
         return reference_arm(args, w)
 
@@ -292,7 +301,8 @@ def main():
     from paper_2509_21792_b200 import capi
     cfg = model_cfg(w)
     n_seq = w["Q"] * w["G"]
-    eng = capi.Engine(cfg, 1, local, max(n_seq, 64 if w["warm"] > 0 else 1), 2048, 10, 6)
+    regions = w.get("regions", n_seq)  # resident KV regions (fewer than sequences: waves)
+    eng = capi.Engine(cfg, 1, local, max(min(n_seq, regions), 64 if w["warm"] > 0 else 1), w.get("rows", 2048), 10, 6)
     eng.init_random(1234)
     # NCCL data-parallel group over NVLink (C1 gradient all-reduce, C2 statistics)
     uid = [capi.nccl_unique_id() if rank == 0 else None]
@@ -302,12 +312,13 @@ def main():
     prompts = make_prompts(w, rank)
     caps = stop_caps(w, rank * n_seq, n_seq) if w["stops"] else None
     gen = dict(c_peak=args.c_peak, alpha=2.0, k_max=10, l_max=6, temperature=w.get("temp", 0.0), seed=7,
-               max_new_tokens=w["new"],
-               sid_offset=rank * n_seq, seq_max_new=caps)
+               max_new_tokens=w["new"], sid_offset=rank * n_seq, seq_max_new=caps,
+               acceptance=w.get("acceptance", "strict"))
+    want_feats = w.get("features", True)
 
-    def rollout(mode):
+    def rollout(mode, **over):
         t0 = time.perf_counter()
-        r = eng.generate(prompts, w["G"], mode=mode, want_features=True, **gen)
+        r = eng.generate(prompts, w["G"], mode=mode, want_features=want_feats, **dict(gen, **over))
         return r, time.perf_counter() - t0
 
     adv_stats = {"ms": 0.0, "calls": 0, "groups": 0, "filtered": 0, "reward_mean": 0.0}
@@ -354,7 +365,10 @@ def main():
                 "feature_loss": round(fl, 5), "token_loss": round(tl, 4), "seconds": round(time.perf_counter() - t0, 1)}
 
     for _ in range(args.warmup):
-        r, _ = rollout(args.mode)
+        wover = {}
+        if args.warmup_max_new:
+            wover = dict(max_new_tokens=args.warmup_max_new, seq_max_new=None)
+        r, _ = rollout(args.mode, **wover)
         if w["online"]:
             draft_step(r, w["G"])
     eng.read_profile(reset=True)
@@ -365,8 +379,10 @@ def main():
     dev_s, wall_s, toks, launches, acc, slots, h2d, d2h = 0.0, 0.0, 0, 0, 0, 0, 0, 0
     spec_steps, upd_s, upd_wall, upd_rows = 0, 0.0, 0.0, 0
     terms = None
+    last = None
     for _ in range(args.steps):
         r, wall = rollout(args.mode)
+        last = r
         dev_s += r.seconds
         wall_s += wall
         if w["online"]:
@@ -400,7 +416,7 @@ def main():
             ar = {"value": tok_all / t_max, "unit": "tokens/s", "speedup": 1.0,
                   "note": "every step had B_cur > C_peak, so Eqs. 1-3 planned N_verify=1 (AR) throughout"}
         else:
-            rs, _ = rollout(args.mode)
+            rs = last  # the last timed rollout
             ra, _ = rollout("vanilla")
             same = all(list(a) == list(b) for a, b in zip(rs.tokens, ra.tokens))
             ar = {"value": ra.generated() / ra.seconds, "unit": "tokens/s",
@@ -409,9 +425,10 @@ def main():
                   "tokens_identical": same, "note": "rollout only (no draft step), this rank"}
     # kernel-class breakdown: one more rollout of the same workload with a CUDA-event pair
     # around every launch (kept out of the timed steps: events between launches defeat PDL)
-    eng.profile(True)
-    rollout(args.mode)
-    eng.profile(False)
+    if not args.no_profile:
+        eng.profile(True)
+        rollout(args.mode)
+        eng.profile(False)
     prof = eng.read_profile(reset=True)
     if rank != 0:
         eng.close()
@@ -440,7 +457,9 @@ def main():
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(w, max(1, min(os.cpu_count() or 1, 64)))
     config = {"workload": f"{args.config}: {w['desc']}", "mode": args.mode, "c_peak": args.c_peak,
-              "sequences_per_gpu": n_seq, "new_tokens": w["new"], "prompt_len": w["P"],
+              "acceptance": w.get("acceptance", "strict"), "temperature": w.get("temp", 0.0),
+              "sequences_per_gpu": n_seq, "resident_kv_regions": min(n_seq, regions), "new_tokens": w["new"],
+              "prompt_len": w["P"], "features_returned": want_feats,
               "l2": "inputs larger than L2 (KV cache of the shard >> 126 MB L2)",
               "parallelism": f"dp{world} (query groups)", "weights": "random init on device"}
     if caps:
