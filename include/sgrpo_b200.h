@@ -261,6 +261,14 @@ int sgb_debug_tree_attention(int n_groups, const int* ctx_len, const int* n_rows
                              const float* q, const float* kctx, const float* vctx, const float* knode,
                              const float* vnode, float* out_row, float* out_group);
 
+/* The same self-test through attention_tree.cu (the engine's tree-verify / draft-level kernel:
+ * one CTA per row tile and head over the whole key range); out_tree [rows][H*dh]. */
+int sgb_debug_tree_attention_tree(int n_groups, const int* ctx_len, const int* n_rows, const int* parent, int H, int dh,
+                                  const float* q, const float* kctx, const float* vctx, const float* knode,
+                                  const float* vnode, float* out_tree);
+/* Tree-verify microbenchmark of attention_tree.cu (same shapes as sgb_bench_tree_attention). */
+int sgb_bench_tree_attention_tree(int B, int N, int ctx, int H, int dh, int iters, double* ms_tree);
+
 /* Tree-verify attention microbenchmark: B sequences x (ctx committed keys + an EAGLE-shaped
  * tree of N rows); ms per launch of the per-row and of the prefix-shared group kernel. */
 int sgb_bench_tree_attention(int B, int N, int ctx, int H, int dh, int iters, double* ms_row, double* ms_group);

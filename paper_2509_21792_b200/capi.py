@@ -611,3 +611,23 @@ def _debug_spec_sample(self, p_logits, q_logits, k: int, temperature: float, n_t
 
 Engine.debug_spec_sample = _debug_spec_sample
 EXPORTED += ["sgb_debug_spec_sample", "sgb_adamw_state", "sgb_rollout_events"]
+
+
+def debug_tree_attention_tree(ctx_len, parents, q, kctx, vctx, knode, vnode, n_heads: int):
+    """attention_tree.cu on the debug_tree_attention inputs: out [rows][d] (bf16 values)."""
+    cl = np.ascontiguousarray(ctx_len, np.int32)
+    nr = np.array([len(p) for p in parents], np.int32)
+    par = np.ascontiguousarray(np.concatenate([np.asarray(p, np.int32) for p in parents]), np.int32)
+    q = np.ascontiguousarray(q, np.float32)
+    out = np.zeros_like(q)
+    _check(_lib.sgb_debug_tree_attention_tree(len(cl), _p(cl, C.c_int), _p(nr, C.c_int), _p(par, C.c_int), n_heads,
+                                              q.shape[1] // n_heads, _p(q, C.c_float),
+                                              _p(np.ascontiguousarray(kctx, np.float32), C.c_float),
+                                              _p(np.ascontiguousarray(vctx, np.float32), C.c_float),
+                                              _p(np.ascontiguousarray(knode, np.float32), C.c_float),
+                                              _p(np.ascontiguousarray(vnode, np.float32), C.c_float),
+                                              _p(out, C.c_float)))
+    return out
+
+
+EXPORTED += ["sgb_debug_tree_attention_tree", "sgb_bench_tree_attention_tree"]

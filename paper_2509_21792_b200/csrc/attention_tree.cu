@@ -1,0 +1,390 @@
+// Tree-verify attention: the rows of one sequence's draft tree against its committed prefix
+// plus each row's own ancestor path -- the verify forward of a speculative step and the batched
+// draft-level forwards (decode_blocks, include/sgrpo/tinylm.hpp:335-395, with the tree mask of
+// build_tree_mask, drafttree.cpp:145-168).
+//
+// Why a separate kernel. attention.cu serves every row shape through one persistent work list
+// of (tile <= 16 rows, head group, 64-key block) items whose block partials are merged through
+// global memory; for ~200 tree rows over a few hundred prefix keys that list is thousands of
+// tiny items and the kernel is latency-bound (ncu: DRAM 0.8 %, 23 % occupancy,
+// profiles/r01_verify_attn_c3_m211.txt). Here one CTA owns (sequence, head, tile of up to 64
+// rows) for the WHOLE key range: the prefix streams once per tile through a TMA ring (16-key x
+// 64-dim SWIZZLE_128B boxes straight from the paged K/V store), the tree nodes' own K/V rows
+// (the keys of every row's path) are loaded once into shared memory, and the per-64-key-block
+// partials are merged in registers -- no partials in HBM, no tickets.
+//
+// Bit-identical to attention.cu (batch invariance): a row's virtual key sequence
+// is [prefix 0..P) then its path (ancestors root-first, then itself), chunked in 16-key steps
+// of 64-key blocks at the same virtual offsets; the chunk arithmetic (mma.sync S^T = K.Q^T with
+// keys in M, online softmax with the same explicit-rounding steps and shuffle trees, P^T via
+// movmatrix, O^T += V^T.P^T) and the in-order block merge (attn_merge from the identity) are
+// the same operations on the same operands. Chunks wholly inside the prefix are shared by all
+// rows of the tile (every column live); a chunk that reaches past P is run once per row with
+// only that row's query column live (-inf scores on the others are exact no-ops, as in
+// attention.cu's boundary tiles), its key rows gathered per lane by ldmatrix addresses: prefix
+// keys from the staged ring, path keys from the node table.
+#include <algorithm>
+#include <cfloat>
+
+#include "attn_numerics.cuh"
+#include "common.cuh"
+#include "kernels.h"
+#include "util.h"
+
+namespace sgb {
+
+namespace {
+
+constexpr int kTBlock = kAttnBlock;  // 64 keys per softmax partial
+constexpr int kTChunk = 16;          // keys per staged chunk
+constexpr int kTMaxWarps = 8;        // consumer warps (8 query rows each)
+constexpr int kTSmem = 227 * 1024;
+
+SGB_DEV void ldsm_x4(uint32_t addr, uint32_t* r) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(addr));
+}
+SGB_DEV void ldsm_x4_t(uint32_t addr, uint32_t* r) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(addr));
+}
+SGB_DEV uint32_t movm_t(uint32_t x) {
+    uint32_t y;
+    asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
+    return y;
+}
+SGB_DEV void mma16816(float* d, const uint32_t* a, uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+SGB_DEV uint32_t pack_bf16(float lo, float hi) {
+    const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<const uint32_t*>(&v);
+}
+SGB_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+// smem address of dims [dd, dd+8) of key row kr in a staged chunk: DH/64 SWIZZLE_128B boxes of
+// 16 rows x 128 B (16-byte unit u of row r stored at unit u ^ (r & 7))
+SGB_DEV uint32_t ring_addr(uint32_t stage, int kr, int dd) {
+    const int box = dd >> 6, u = (dd & 63) >> 3;
+    return stage + static_cast<uint32_t>(box * 2048 + kr * 128 + ((u ^ (kr & 7)) << 4));
+}
+
+template <int DH>
+__global__ void __launch_bounds__(32 * (kTMaxWarps + 1), 1)
+    tree_attn_kernel(const float* __restrict__ q, const __grid_constant__ CUtensorMap kmap,
+                     const __grid_constant__ CUtensorMap vmap, long long layer_row0, const __nv_bfloat16* __restrict__ K,
+                     const __nv_bfloat16* __restrict__ V, AttnRowsDev rows, const TreeGroupDev* __restrict__ groups,
+                     const TreeTileDev* __restrict__ tiles, int d, int nst, int tbl_cap, float scale,
+                     __nv_bfloat16* __restrict__ out) {
+    constexpr int NK = DH / 16;
+    constexpr uint32_t kStageK = static_cast<uint32_t>(kTChunk) * DH * 2;  // one of K or V per stage
+    constexpr int kRowB = DH * 2 + 16;                                    // padded node-table row
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // SWIZZLE_128B TMA destinations need 1024-byte alignment
+    uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+    const int W = static_cast<int>(blockDim.x >> 5) - 1;  // consumer warps
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const TreeTileDev tt = tiles[blockIdx.x];
+    const TreeGroupDev gr = groups[tt.group];
+    const int h = blockIdx.y;
+    const int P = gr.ctx_len;
+    uint8_t* ringK = smem;                                    // [nst][16][DH] swizzled
+    uint8_t* ringV = smem + static_cast<size_t>(nst) * kStageK;
+    uint8_t* tblK = ringV + static_cast<size_t>(nst) * kStageK;  // [tbl_cap][kRowB]
+    uint8_t* tblV = tblK + static_cast<size_t>(tbl_cap) * kRowB;
+    uint64_t* full = reinterpret_cast<uint64_t*>(tblV + static_cast<size_t>(tbl_cap) * kRowB);
+    uint64_t* empty = full + nst;
+    uint64_t* tbar = empty + nst;
+    const int n_prefix_chunks = (P + kTChunk - 1) / kTChunk;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < nst; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], W);
+        }
+        mbar_init(tbar, 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+    pdl_wait();  // q and this layer's K/V (incl. the tree rows') come from the previous kernels
+    pdl_trigger();
+
+    if (warp == W) {
+        // ---------------- producer: node table (bulk rows), then the prefix chunks (TMA ring)
+        const int nn = gr.n_nodes;
+        const uint32_t rowbytes = DH * 2;
+        if (lane == 0) mbar_arrive_expect_tx(tbar, 2u * rowbytes * nn);
+        __syncwarp();
+        for (int i = lane; i < nn; i += 32) {
+            const size_t src = static_cast<size_t>(gr.node_base + i) * d + static_cast<size_t>(h) * DH;
+            bulk_g2s(tblK + static_cast<size_t>(i) * kRowB, K + src, rowbytes, tbar);
+            bulk_g2s(tblV + static_cast<size_t>(i) * kRowB, V + src, rowbytes, tbar);
+        }
+        if (lane == 0) {
+            for (int c = 0; c < n_prefix_chunks; ++c) {
+                const int s = c % nst;
+                if (c >= nst) mbar_wait(&empty[s], ((c / nst) & 1) ^ 1);
+                const int v0 = c * kTChunk;
+                // the shared prompt copy (identical values) while the whole box lies in it
+                const long long slot0 = (v0 + kTChunk <= gr.pre_len ? gr.pre_base : gr.ctx_base) + v0;
+                const int row = static_cast<int>(layer_row0 + slot0);
+                mbar_arrive_expect_tx(&full[s], 2 * kStageK);
+#pragma unroll
+                for (int b = 0; b < DH / 64; ++b) {
+                    tma_load_2d(ringK + static_cast<size_t>(s) * kStageK + b * 2048, &kmap, &full[s], h * DH + 64 * b, row);
+                    tma_load_2d(ringV + static_cast<size_t>(s) * kStageK + b * 2048, &vmap, &full[s], h * DH + 64 * b, row);
+                }
+            }
+        }
+        return;
+    }
+
+    // ---------------- consumers: warp w owns tile rows [8w, 8w + 8) as the 8 query columns
+    const int g8 = lane >> 2, t4 = lane & 3;
+    const int li = lane >> 3, lr = lane & 7;
+    const int row0 = gr.row0 + tt.r0 + 8 * warp;
+    const int nrows = max(0, min(8, tt.nr - 8 * warp));
+    uint32_t qf[NK][2];
+    {
+        const int qrow = nrows > 0 ? row0 + min(g8, nrows - 1) : gr.row0;
+        const float* qr = q + static_cast<size_t>(qrow) * d + h * DH + 2 * t4;
+#pragma unroll
+        for (int ks = 0; ks < NK; ++ks) {
+            const float2 a = __ldg(reinterpret_cast<const float2*>(qr + 16 * ks));
+            const float2 b = __ldg(reinterpret_cast<const float2*>(qr + 16 * ks + 8));
+            qf[ks][0] = pack_bf16(a.x, a.y);
+            qf[ks][1] = pack_bf16(b.x, b.y);
+        }
+    }
+    // virtual lengths of this lane's two query columns, and of the warp's rows
+    const int c0 = 2 * t4, c1 = 2 * t4 + 1;
+    const int lv0 = c0 < nrows ? P + rows.chain_len[row0 + c0] : 0;
+    const int lv1 = c1 < nrows ? P + rows.chain_len[row0 + c1] : 0;
+    int lvmax = max(lv0, lv1);
+#pragma unroll
+    for (int o2 = 1; o2 < 4; o2 <<= 1) lvmax = max(lvmax, __shfl_xor_sync(0xffffffffu, lvmax, o2));
+    const uint32_t ringK0 = smem_u32(ringK), ringV0 = smem_u32(ringV);
+    const uint32_t tblK0 = smem_u32(tblK), tblV0 = smem_u32(tblV);
+    // merged state of the two columns (attn_merge from the identity), o layout as attention.cu
+    float M0 = -INFINITY, M1 = -INFINITY, L0 = 0.f, L1 = 0.f;
+    float A[NK][4];
+#pragma unroll
+    for (int mt = 0; mt < NK; ++mt) A[mt][0] = A[mt][1] = A[mt][2] = A[mt][3] = 0.f;
+    bool tbl_ready = false;
+    int i = 0;  // staged chunk counter
+    const int nb = (lvmax + kTBlock - 1) / kTBlock;
+    const int nbp = (P + kTBlock - 1) / kTBlock;  // blocks holding prefix keys: every warp runs them
+    for (int b = 0; b < max(nb, nbp); ++b) {
+        float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+        float o[NK][4];
+#pragma unroll
+        for (int mt = 0; mt < NK; ++mt) o[mt][0] = o[mt][1] = o[mt][2] = o[mt][3] = 0.f;
+        // one chunk: kaddr / vaddr give the smem row of key slot kr; e0 / e1 = key end of the
+        // lane's two query columns
+        auto chunk = [&](auto kaddr, auto vaddr, int v0, int e0, int e1) {
+            float sc[4] = {0.f, 0.f, 0.f, 0.f};
+            const int kr_k = lr + 8 * (li & 1);
+#pragma unroll
+            for (int ks = 0; ks < NK; ++ks) {
+                uint32_t a[4];
+                ldsm_x4(kaddr(kr_k, 16 * ks + 8 * (li >> 1)), a);
+                mma16816(sc, a, qf[ks][0], qf[ks][1]);
+            }
+            const bool va0 = v0 + g8 < e0, va1 = v0 + g8 < e1, vb0 = v0 + g8 + 8 < e0, vb1 = v0 + g8 + 8 < e1;
+            const float s0 = va0 ? attn_scale(sc[0], scale) : -INFINITY;
+            const float s1 = va1 ? attn_scale(sc[1], scale) : -INFINITY;
+            const float s2 = vb0 ? attn_scale(sc[2], scale) : -INFINITY;
+            const float s3 = vb1 ? attn_scale(sc[3], scale) : -INFINITY;
+            float x0 = fmaxf(s0, s2), x1 = fmaxf(s1, s3);
+#pragma unroll
+            for (int o2 = 4; o2 < 32; o2 <<= 1) {
+                x0 = fmaxf(x0, __shfl_xor_sync(0xffffffffu, x0, o2));
+                x1 = fmaxf(x1, __shfl_xor_sync(0xffffffffu, x1, o2));
+            }
+            const float n0 = fmaxf(m0, x0), n1 = fmaxf(m1, x1);
+            const float a0 = attn_alpha(m0, n0), a1 = attn_alpha(m1, n1);
+            const float p0 = va0 ? attn_p(s0, n0) : 0.f, p1 = va1 ? attn_p(s1, n1) : 0.f;
+            const float p2 = vb0 ? attn_p(s2, n0) : 0.f, p3 = vb1 ? attn_p(s3, n1) : 0.f;
+            float ps0 = __fadd_rn(p0, p2), ps1 = __fadd_rn(p1, p3);
+#pragma unroll
+            for (int o2 = 4; o2 < 32; o2 <<= 1) {
+                ps0 = __fadd_rn(ps0, __shfl_xor_sync(0xffffffffu, ps0, o2));
+                ps1 = __fadd_rn(ps1, __shfl_xor_sync(0xffffffffu, ps1, o2));
+            }
+            l0 = attn_l(l0, a0, ps0);
+            l1 = attn_l(l1, a1, ps1);
+            m0 = n0;
+            m1 = n1;
+            uint32_t va4[NK][4];
+            const int kr_v = lr + 8 * (li >> 1);
+#pragma unroll
+            for (int mt = 0; mt < NK; ++mt) ldsm_x4_t(vaddr(kr_v, 16 * mt + 8 * (li & 1)), va4[mt]);
+            const uint32_t b0 = movm_t(pack_bf16(p0, p1)), b1 = movm_t(pack_bf16(p2, p3));
+#pragma unroll
+            for (int mt = 0; mt < NK; ++mt) {
+                o[mt][0] = __fmul_rn(o[mt][0], a0);
+                o[mt][1] = __fmul_rn(o[mt][1], a1);
+                o[mt][2] = __fmul_rn(o[mt][2], a0);
+                o[mt][3] = __fmul_rn(o[mt][3], a1);
+                mma16816(o[mt], va4[mt], b0, b1);
+            }
+        };
+        for (int c = 0; c < kTBlock / kTChunk; ++c) {
+            const int v0 = b * kTBlock + c * kTChunk;
+            if (v0 >= max(lvmax, P)) break;
+            const bool staged = v0 < P;
+            uint32_t sK = 0, sV = 0;
+            int s = 0;
+            if (staged) {
+                s = i % nst;
+                mbar_wait(&full[s], (i / nst) & 1);
+                sK = ringK0 + static_cast<uint32_t>(s) * kStageK;
+                sV = ringV0 + static_cast<uint32_t>(s) * kStageK;
+            }
+            if (v0 + kTChunk <= P) {
+                // shared prefix chunk: every query column live
+                auto ka = [&](int kr, int dd) { return ring_addr(sK, kr, dd); };
+                auto vaa = [&](int kr, int dd) { return ring_addr(sV, kr, dd); };
+                chunk(ka, vaa, v0, lv0, lv1);
+            } else if (nrows > 0) {
+                // past the prefix: once per row, its own path keys gathered from the node table
+                if (!tbl_ready) {
+                    mbar_wait(tbar, 0);
+                    tbl_ready = true;
+                }
+                for (int j = 0; j < nrows; ++j) {
+                    const int rj = row0 + j;
+                    const int lvj = P + rows.chain_len[rj];
+                    if (lvj <= v0) continue;
+                    const long long* ch = rows.chain_slots + static_cast<size_t>(rj) * kMaxChain;
+                    // smem row of key slot kr for row j: prefix from the ring, path from the table,
+                    // past the row's end any finite row (masked: p = 0)
+                    auto row_of = [&](int kr, uint32_t ring, uint32_t tbl, int dd) -> uint32_t {
+                        const int v = v0 + kr;
+                        if (v < P) return ring_addr(ring, kr, dd);
+                        const int node = v < lvj ? static_cast<int>(ch[v - P] - gr.node_base) : 0;
+                        return tbl + static_cast<uint32_t>(node * kRowB + dd * 2);
+                    };
+                    auto ka = [&](int kr, int dd) { return row_of(kr, sK, tblK0, dd); };
+                    auto vaa = [&](int kr, int dd) { return row_of(kr, sV, tblV0, dd); };
+                    chunk(ka, vaa, v0, c0 == j ? lvj : v0, c1 == j ? lvj : v0);
+                }
+            }
+            if (staged) {
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[s]);
+                ++i;
+            }
+        }
+        // ordered merge of this block's partial (rows whose keys reach into block b)
+        const bool h0 = b * kTBlock < lv0, h1 = b * kTBlock < lv1;
+        if (h0) {
+            const float Mn = fmaxf(M0, m0);
+            const float ca = M0 == -INFINITY ? 0.f : expf(__fsub_rn(M0, Mn));
+            const float cb = expf(__fsub_rn(m0, Mn));
+            L0 = fmaf(L0, ca, __fmul_rn(l0, cb));
+#pragma unroll
+            for (int mt = 0; mt < NK; ++mt) {
+                A[mt][0] = fmaf(A[mt][0], ca, __fmul_rn(o[mt][0], cb));
+                A[mt][2] = fmaf(A[mt][2], ca, __fmul_rn(o[mt][2], cb));
+            }
+            M0 = Mn;
+        }
+        if (h1) {
+            const float Mn = fmaxf(M1, m1);
+            const float ca = M1 == -INFINITY ? 0.f : expf(__fsub_rn(M1, Mn));
+            const float cb = expf(__fsub_rn(m1, Mn));
+            L1 = fmaf(L1, ca, __fmul_rn(l1, cb));
+#pragma unroll
+            for (int mt = 0; mt < NK; ++mt) {
+                A[mt][1] = fmaf(A[mt][1], ca, __fmul_rn(o[mt][1], cb));
+                A[mt][3] = fmaf(A[mt][3], ca, __fmul_rn(o[mt][3], cb));
+            }
+            M1 = Mn;
+        }
+    }
+    // outputs of the real columns
+#pragma unroll
+    for (int cc = 0; cc < 2; ++cc) {
+        const int qc = 2 * t4 + cc;
+        if (qc >= nrows) continue;
+        const float Lx = cc ? L1 : L0;
+        __nv_bfloat16* orow = out + static_cast<size_t>(row0 + qc) * d + h * DH;
+#pragma unroll
+        for (int mt = 0; mt < NK; ++mt) {
+            orow[16 * mt + g8] = __float2bfloat16(__fdiv_rn(A[mt][cc], Lx));
+            orow[16 * mt + g8 + 8] = __float2bfloat16(__fdiv_rn(A[mt][2 + cc], Lx));
+        }
+    }
+}
+
+template <int DH>
+void launch_tree_impl(const float* q, const CUtensorMap& kmap, const CUtensorMap& vmap, long long layer_row0,
+                      const __nv_bfloat16* K, const __nv_bfloat16* V, const AttnRowsDev& rows, const TreeGroupDev* groups,
+                      const TreeTileDev* tiles, int n_tiles, int W, int H, int d, int max_nodes, __nv_bfloat16* out,
+                      cudaStream_t st) {
+    constexpr size_t stageK = static_cast<size_t>(kTChunk) * DH * 2;
+    const size_t tbl = static_cast<size_t>(max_nodes) * (DH * 2 + 16) * 2;
+    const size_t fixed = tbl + 8 * 24 + 1024;  // barriers + alignment slack
+    int nst = 6;
+    while (nst > 2 && 2 * stageK * nst + fixed > static_cast<size_t>(kTSmem)) --nst;
+    const size_t smem = 2 * stageK * nst + fixed;
+    if (smem > static_cast<size_t>(kTSmem)) throw std::invalid_argument("tree attention: tree too large for shared memory");
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(tree_attn_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTSmem);
+        attr = true;
+    }
+    launch_pdl(tree_attn_kernel<DH>, dim3(n_tiles, H), dim3(32 * (W + 1)), smem, st, q, kmap, vmap, layer_row0, K, V,
+               rows, groups, tiles, d, nst, max_nodes, 1.0f / sqrtf(static_cast<float>(DH)), out);
+}
+
+}  // namespace
+
+int tree_attn_warps(int max_rows_per_group, int n_groups, int H) {
+    // 8 query rows per warp; fewer warps per tile when that is what it takes to cover the SMs
+    int w = std::max(1, std::min(kTMaxWarps, (max_rows_per_group + 7) / 8));
+    while (w > 1) {
+        const int rows_per_tile = 8 * w;
+        const long long ctas = static_cast<long long>(n_groups) * ((max_rows_per_group + rows_per_tile - 1) / rows_per_tile) * H;
+        if (ctas >= 148) break;
+        w = (w + 1) / 2;
+    }
+    return w;
+}
+
+void build_tree_tiles(const std::vector<TreeGroupDev>& groups, int W, std::vector<TreeTileDev>& out) {
+    out.clear();
+    const int rt = 8 * W;
+    for (size_t g = 0; g < groups.size(); ++g)
+        for (int r = 0; r < groups[g].nrows; r += rt)
+            out.push_back(TreeTileDev{static_cast<int>(g), r, std::min(rt, groups[g].nrows - r)});
+}
+
+void launch_attention_tree(const float* q, const CUtensorMap& kmap, const CUtensorMap& vmap, long long layer_row0,
+                           const __nv_bfloat16* K, const __nv_bfloat16* V, const AttnRowsDev& rows,
+                           const TreeGroupDev* groups, const TreeTileDev* tiles, int n_tiles, int W, int H, int d,
+                           int max_nodes, __nv_bfloat16* out, cudaStream_t st) {
+    if (n_tiles <= 0) return;
+    if (W < 1 || W > kTMaxWarps) throw std::invalid_argument("tree attention: warps per tile in [1, 8]");
+    const int dh = d / H;
+    if (dh == 128)
+        launch_tree_impl<128>(q, kmap, vmap, layer_row0, K, V, rows, groups, tiles, n_tiles, W, H, d, max_nodes, out, st);
+    else if (dh == 64)
+        launch_tree_impl<64>(q, kmap, vmap, layer_row0, K, V, rows, groups, tiles, n_tiles, W, H, d, max_nodes, out, st);
+    else
+        throw std::invalid_argument("tree attention: head dim must be 64 or 128");
+    SGB_KCHECK();
+}
+
+}  // namespace sgb

@@ -864,6 +864,11 @@ struct TreeAttnCase {
     sgb::AttnRowsDev ar{};
     sgb::AttnScratch sc{};
     sgb::AttnTileDev* tiles = nullptr;
+    std::vector<sgb::TreeGroupDev> tg;
+    sgb::TreeGroupDev* dtg = nullptr;
+    sgb::TreeTileDev* dtt = nullptr;
+    int tw = 1, n_ttiles = 0, max_nodes = 1;
+    CUtensorMap kmap, vmap;
 
     void* dev(size_t bytes) {
         void* p = nullptr;
@@ -945,6 +950,28 @@ struct TreeAttnCase {
         auto* dcl = static_cast<int*>(dev(M * 4));
         auto* dchl = static_cast<int*>(dev(M * 4));
         tiles = static_cast<sgb::AttnTileDev*>(dev(ht.size() * sizeof(sgb::AttnTileDev)));
+        // attention_tree.cu: one group per sequence (node rows = its tree rows' own slots)
+        {
+            long long cb = 0;
+            int r = 0, mx = 1;
+            for (int g = 0; g < n_groups; ++g) {
+                tg.push_back(sgb::TreeGroupDev{r, n_rows[g], ctx_len[g], n_rows[g], n_ctx + r, cb, cb, 0, 0});
+                max_nodes = std::max(max_nodes, n_rows[g]);
+                mx = std::max(mx, n_rows[g]);
+                cb += ctx_len[g];
+                r += n_rows[g];
+            }
+            tw = sgb::tree_attn_warps(mx, n_groups, H);
+            std::vector<sgb::TreeTileDev> tt;
+            sgb::build_tree_tiles(tg, tw, tt);
+            n_ttiles = static_cast<int>(tt.size());
+            dtg = static_cast<sgb::TreeGroupDev*>(dev(tg.size() * sizeof(sgb::TreeGroupDev)));
+            dtt = static_cast<sgb::TreeTileDev*>(dev(tt.size() * sizeof(sgb::TreeTileDev)));
+            SGB_CUDA(cudaMemcpy(dtg, tg.data(), tg.size() * sizeof(sgb::TreeGroupDev), cudaMemcpyHostToDevice));
+            SGB_CUDA(cudaMemcpy(dtt, tt.data(), tt.size() * sizeof(sgb::TreeTileDev), cudaMemcpyHostToDevice));
+            kmap = sgb::make_kmajor_map(K, static_cast<int>(slots), d, 16);
+            vmap = sgb::make_kmajor_map(V, static_cast<int>(slots), d, 16);
+        }
         sc = sgb::AttnScratch{pacc, pml, nullptr, static_cast<long long>(M) * H};  // >= rows x head groups
         sc.row_ctr = static_cast<int*>(dev(sc.ctr_cap * 4));
         SGB_CUDA(cudaMemset(sc.row_ctr, 0, sc.ctr_cap * 4));
@@ -959,6 +986,9 @@ struct TreeAttnCase {
         for (void* p : ptrs) cudaFree(p);
     }
     void run_row() { sgb::launch_attention(q, K, V, n_slots, ar, M, H, d, max_vlen, keys, sc, o1, 0); }
+    void run_tree() {
+        sgb::launch_attention_tree(q, kmap, vmap, 0, K, V, ar, dtg, dtt, n_ttiles, tw, H, d, max_nodes, o2, 0);
+    }
     void run_group() { sgb::launch_attention_tiles(q, K, V, n_slots, ar, M, tiles, n_tiles, items, qw, H, d, max_vlen, sc, o2,
                                                     0); }
     void read(const __nv_bfloat16* o, float* out) const {
@@ -980,6 +1010,50 @@ int sgb_debug_tree_attention(int n_groups, const int* ctx_len, const int* n_rows
         SGB_CUDA(cudaDeviceSynchronize());
         c.read(c.o1, out_row);
         c.read(c.o2, out_group);
+    });
+}
+
+int sgb_debug_tree_attention_tree(int n_groups, const int* ctx_len, const int* n_rows, const int* parent, int H, int dh,
+                                  const float* q, const float* kctx, const float* vctx, const float* knode,
+                                  const float* vnode, float* out_tree) {
+    return guarded([&] {
+        if (!q) throw std::invalid_argument("debug_tree_attention: null inputs");
+        TreeAttnCase c(n_groups, ctx_len, n_rows, parent, H, dh, q, kctx, vctx, knode, vnode);
+        c.run_tree();
+        SGB_CUDA(cudaDeviceSynchronize());
+        c.read(c.o2, out_tree);
+    });
+}
+
+int sgb_bench_tree_attention_tree(int B, int N, int ctx, int H, int dh, int iters, double* ms_tree) {
+    return guarded([&] {
+        if (B <= 0 || N <= 0 || iters <= 0) throw std::invalid_argument("bench_tree_attention: bad shape");
+        std::vector<int> cl(B, ctx), nr(B, N), par;
+        for (int b = 0; b < B; ++b) {
+            std::vector<int> dep(N, 0);
+            for (int i = 0; i < N; ++i) {
+                int p = i == 0 ? -1 : (i - 1) / 10;
+                if (i) {
+                    while (dep[p] + 1 >= sgb::kMaxChain) p = (p - 1) / 10;
+                    dep[i] = dep[p] + 1;
+                }
+                par.push_back(p);
+            }
+        }
+        TreeAttnCase c(B, cl.data(), nr.data(), par.data(), H, dh, nullptr, nullptr, nullptr, nullptr, nullptr);
+        cudaEvent_t a, b;
+        SGB_CUDA(cudaEventCreate(&a));
+        SGB_CUDA(cudaEventCreate(&b));
+        for (int i = 0; i < 2; ++i) c.run_tree();
+        SGB_CUDA(cudaEventRecord(a, 0));
+        for (int i = 0; i < iters; ++i) c.run_tree();
+        SGB_CUDA(cudaEventRecord(b, 0));
+        SGB_CUDA(cudaEventSynchronize(b));
+        float ms = 0.f;
+        SGB_CUDA(cudaEventElapsedTime(&ms, a, b));
+        *ms_tree = ms / iters;
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
     });
 }
 

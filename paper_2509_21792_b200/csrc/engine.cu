@@ -194,6 +194,16 @@ Engine::Engine(const ModelDims& dims, int draft_layers, int device, int max_seqs
     dkv_.n_slots = dkv_.scratch_base + static_cast<long long>(S) * ds;
     dkv_.K = dalloc<__nv_bfloat16>(static_cast<size_t>(dkv_.n_slots) * d * draft_layers);
     dkv_.V = dalloc<__nv_bfloat16>(static_cast<size_t>(dkv_.n_slots) * d * draft_layers);
+    // every KV slot holds finite values from the start: attention stages whole 16-key boxes and
+    // masks the keys past a row's end (p = 0), which must not meet NaN bit patterns
+    SGB_CUDA(cudaMemset(tkv_.K, 0, static_cast<size_t>(tkv_.n_slots) * d * dims.layers * 2));
+    SGB_CUDA(cudaMemset(tkv_.V, 0, static_cast<size_t>(tkv_.n_slots) * d * dims.layers * 2));
+    SGB_CUDA(cudaMemset(dkv_.K, 0, static_cast<size_t>(dkv_.n_slots) * d * draft_layers * 2));
+    SGB_CUDA(cudaMemset(dkv_.V, 0, static_cast<size_t>(dkv_.n_slots) * d * draft_layers * 2));
+    tkmap_ = make_kmajor_map(tkv_.K, static_cast<int>(tkv_.n_slots * dims.layers), static_cast<int>(d), 16);
+    tvmap_ = make_kmajor_map(tkv_.V, static_cast<int>(tkv_.n_slots * dims.layers), static_cast<int>(d), 16);
+    dkmap_ = make_kmajor_map(dkv_.K, static_cast<int>(dkv_.n_slots * draft_layers), static_cast<int>(d), 16);
+    dvmap_ = make_kmajor_map(dkv_.V, static_cast<int>(dkv_.n_slots * draft_layers), static_cast<int>(d), 16);
     // sequences
     ss_.max_seq = static_cast<int>(T);
     ss_.tokens = dalloc<int>(S * T);
@@ -298,6 +308,8 @@ void Engine::alloc_rows() {
     err_ = dalloc<int>(1);
     steps_ = dalloc<StepSeqDev>(S);
     tiles_ = dalloc<AttnTileDev>(2 * R);
+    d_tgroups_ = dalloc<TreeGroupDev>(S + R);
+    d_ttiles_ = dalloc<TreeTileDev>(S + R);
     drow_ = dalloc<int>(S * std::max(1, l_max_));
     misc_i_ = dalloc<int>(4 * R + 4 * S);
     misc_l_ = dalloc<long long>(2 * R + 2 * S);
@@ -317,7 +329,7 @@ Engine::~Engine() {
                     a2_, h_, fuse_, ws_.buf, ws_.ctr, logits_, pacc_, pml_, rows_.tok, rows_.pos, rows_.kv_dst,
                     rows_.ctx_base, rows_.ctx_len, rows_.chain_len, rows_.chain, rows_.feat_off, rows_.out_off,
                     rows_.key_pos, rows_.seed, rows_.par_row, rows_.pre_base, rows_.pre_len, lm_idx_, topk_tok_, topk_lp_, emitted_, acc_rows_,
-                    result_, err_, steps_, drow_, misc_i_, misc_l_, mask_dbg_, rsc_.buf, rsc_.ctr, rsc_.rowmax, rsc_.exact, rsc_.n_exact, asc_.row_ctr, gpart_};
+                    result_, err_, steps_, drow_, misc_i_, misc_l_, mask_dbg_, d_tgroups_, d_ttiles_, rsc_.buf, rsc_.ctr, rsc_.rowmax, rsc_.exact, rsc_.n_exact, asc_.row_ctr, gpart_};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (h_result_) cudaFreeHost(h_result_);
@@ -579,6 +591,18 @@ static bool group_attn_enabled(int n_groups, int M) {
     return M >= 2 * n_groups;
 }
 
+// attention_tree.cu for tree verify / draft levels (SGB_TREE_ATTN=0: attention.cu, A/B), when
+// the node table of the largest tree fits the kernel's shared memory
+bool Engine::tree_attn_ok(int max_nodes) const {
+    static const int env = [] {
+        const char* v = getenv("SGB_TREE_ATTN");
+        return v ? atoi(v) : 1;
+    }();
+    const int dh = dims_.d / dims_.heads;
+    return env != 0 && (dh == 64 || dh == 128) &&
+           static_cast<size_t>(max_nodes) * (dh * 2 + 16) * 2 + 4 * 16 * dh * 2 + 2048 <= 227 * 1024;
+}
+
 // Prefix-end blocks inside the shared verify / draft-level tiles (attention.cu): measured
 // faster at 28 heads (B = 16 x 13 rows, ctx 680: 0.129 -> 0.098 ms per layer), slower at 12
 // heads, where fewer head groups leave the longer boundary item on the critical path (0.076 ->
@@ -611,10 +635,27 @@ void Engine::forward(const Fwd& f) {
         count();
         gemm_resid_ln(w_fuse_, act_fuse_, M, false, true, L[0].ln1_g, L[0].ln1_b, nullptr);
     }
+    // tree verify / draft levels: attention_tree.cu (one CTA per row tile and head)
+    int tree_w = 0, n_ttiles = 0, tree_nodes = 0;
+    if (f.tree) {
+        int mx = 1;
+        for (const auto& g : *f.tree) {
+            mx = std::max(mx, g.nrows);
+            tree_nodes = std::max(tree_nodes, g.n_nodes);
+        }
+        tree_w = tree_attn_warps(mx, static_cast<int>(f.tree->size()), dims_.heads);
+        build_tree_tiles(*f.tree, tree_w, ttiles_);
+        n_ttiles = static_cast<int>(ttiles_.size());
+        if (f.tree->size() > static_cast<size_t>(max_seqs_ + max_rows_) ||
+            ttiles_.size() > static_cast<size_t>(max_seqs_ + max_rows_))
+            throw std::logic_error("forward: tree attention tables exceed capacity");
+        h2d(d_tgroups_, f.tree->data(), f.tree->size(), st_);
+        h2d(d_ttiles_, ttiles_.data(), ttiles_.size(), st_);
+    }
     // rows sharing a committed prefix (tree verify, draft levels): shared tiles of <= 8 rows
     int n_tiles = 0, qw = 1;
     long long n_items = 0;
-    if (f.groups && group_attn_enabled(static_cast<int>(f.groups->size()), M)) {
+    if (!f.tree && f.groups && group_attn_enabled(static_cast<int>(f.groups->size()), M)) {
         qw = attn_tile_qw(*f.groups);
         n_items = build_attn_tiles(*f.groups, htiles_, qw, f.groups_exact);
         n_tiles = static_cast<int>(htiles_.size());
@@ -636,7 +677,11 @@ void Engine::forward(const Fwd& f) {
         eq.d = d;
         gemm(W.qkv, act_a_, M, eq, kClsGemm, 8.0 / 3.0);
         e0 = pbeg();
-        if (n_tiles)
+        if (f.tree)
+            launch_attention_tree(q_, f.draft ? dkmap_ : tkmap_, f.draft ? dvmap_ : tvmap_,
+                                  static_cast<long long>(l) * kv.n_slots, eq.K, eq.V, ar, d_tgroups_, d_ttiles_, n_ttiles,
+                                  tree_w, H, d, tree_nodes, att_, st_);
+        else if (n_tiles)
             launch_attention_tiles(q_, eq.K, eq.V, kv.n_slots, ar, M, tiles_, n_tiles, n_items, qw, H, d, f.max_vlen,
                                    asc_, att_, st_);
         else
@@ -1449,15 +1494,23 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
                     f.logits_out = rej ? qbuf_ + static_cast<size_t>(qoff) * V : logits_;
                     f.max_vlen = max_p + level;
                     groups_.clear();
+                    tgroups_.clear();
                     for (int i = 0; i < B; ++i)
                         if (hs[i].k && hs[i].l >= level) {
                             f.attn_kv_unique += hs[i].p + level - 1;
                             f.attn_row_keys += static_cast<double>(hs[i].k) * (hs[i].p + level - 1);
-                            groups_.push_back(
-                                {drow[static_cast<size_t>(level - 2) * B + i], hs[i].k, hs[i].p, hs[i].p + level});
+                            const int r0 = drow[static_cast<size_t>(level - 2) * B + i];
+                            groups_.push_back({r0, hs[i].k, hs[i].p, hs[i].p + level});
+                            const int s = hs[i].seq;
+                            // frontier rows: draft prefix (p keys), paths in the sequence's draft scratch
+                            tgroups_.push_back(TreeGroupDev{r0, hs[i].k, hs[i].p, tr_.ds,
+                                                            dkv_.scratch_base + static_cast<long long>(s) * tr_.ds,
+                                                            static_cast<long long>(s) * dkv_.seq_stride,
+                                                            static_cast<long long>(s) * dkv_.seq_stride, 0, 0});
                         }
                     f.groups = &groups_;
                     f.groups_exact = boundary_tiles();
+                    if (tree_attn_ok(tr_.ds)) f.tree = &tgroups_;
                     forward(f);
                     res.draft_forwards++;
                     stat.draft_rows += R;
@@ -1500,15 +1553,25 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
         f.logits_out = logits_;
         f.max_vlen = max_p + max_l + 1;
         groups_.clear();
+        tgroups_.clear();
         bool all_ar = true;
+        int max_sel = 1;
         for (int i = 0; i < B; ++i) {
             f.attn_kv_unique += hs[i].p + hs[i].nsel;
             f.attn_row_keys += static_cast<double>(hs[i].nsel) * (hs[i].p + 1);
             groups_.push_back(
                 {hs[i].vrow_off, hs[i].nsel, hs[i].p, hs[i].p + 1 + std::min(hs[i].l, hs[i].nsel - 1)});
             all_ar = all_ar && hs[i].nsel == 1;
+            max_sel = std::max(max_sel, hs[i].nsel);
+            // verify rows: committed prefix (p keys; the prompt part from the group leader's
+            // copy), paths = the sequence's own verify rows in the scratch region
+            const long long cb = static_cast<long long>(hs[i].seq) * tkv_.seq_stride;
+            tgroups_.push_back(TreeGroupDev{hs[i].vrow_off, hs[i].nsel, hs[i].p, hs[i].nsel,
+                                            tkv_.scratch_base + hs[i].vrow_off, cb, a.g > 1 ? hs[i].pre_base : cb,
+                                            a.g > 1 ? std::min(hs[i].pre_len, hs[i].p) : 0, 0});
         }
         f.groups_exact = boundary_tiles();
+        if (!all_ar && tree_attn_ok(max_sel)) f.tree = &tgroups_;
         // measured A/B (SGB_PROMPT_TILES, bench.py vanilla): +5 % at 12 heads (c2), -13 % at
         // 28 heads (c3, where the per-row kernel already hits the prompt pages in L2)
         static const int prompt_tiles = [] {

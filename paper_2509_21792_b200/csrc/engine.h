@@ -204,6 +204,8 @@ class Engine {
         // the groups' rows share exactly ctx_len keys (tree verify, draft levels; not the
         // AR prompt groups): shared tiles also cover the prefix-end block (attention.cu)
         bool groups_exact = false;
+        // tree-verify / draft-level groups for attention_tree.cu (nullptr: attention.cu)
+        const std::vector<TreeGroupDev>* tree = nullptr;
     };
     void forward(const Fwd& f);
     bool boundary_tiles() const;
@@ -293,6 +295,12 @@ class Engine {
     AttnTileDev* tiles_ = nullptr;  // [2 * max_rows] attention tiles of the current forward
     std::vector<AttnTileDev> htiles_;
     std::vector<std::array<int, 4>> groups_;
+    std::vector<TreeGroupDev> tgroups_;
+    std::vector<TreeTileDev> ttiles_;
+    TreeGroupDev* d_tgroups_ = nullptr;
+    TreeTileDev* d_ttiles_ = nullptr;
+    CUtensorMap tkmap_, tvmap_, dkmap_, dvmap_;  // [layers * n_slots][d] views of the KV stores
+    bool tree_attn_ok(int max_nodes) const;
     int* drow_ = nullptr;
     int* misc_i_ = nullptr;
     long long* misc_l_ = nullptr;

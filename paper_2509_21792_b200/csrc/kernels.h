@@ -1,6 +1,7 @@
 // Launchers of the sm_100a kernels (rowops.cu, attention.cu, sample.cu, tree.cu).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -79,6 +80,27 @@ void launch_attention_tiles(const float* q, const __nv_bfloat16* K, const __nv_b
 void launch_attention(const float* q, const __nv_bfloat16* K, const __nv_bfloat16* V, long long kv_slots,
                       const AttnRowsDev& rows, int M, int H, int d, int max_virtual_len, double total_keys,
                       const AttnScratch& sc, __nv_bfloat16* out, cudaStream_t st);
+
+// ---- attention_tree.cu: tree-verify / draft-level attention, one CTA per (tile of <= 64 rows
+// of one sequence, head) over the whole key range (prefix through a TMA ring, path keys from a
+// node table in shared memory), bit-identical to launch_attention / launch_attention_tiles
+struct TreeGroupDev {
+    int row0, nrows, ctx_len, n_nodes;  // rows share keys [0, ctx_len); paths = node slots
+    long long node_base;                // first KV slot of the group's node rows
+    long long ctx_base, pre_base;       // committed prefix slots (pre_base for v < pre_len)
+    int pre_len, pad;
+};
+struct TreeTileDev {
+    int group, r0, nr;
+};
+int tree_attn_warps(int max_rows_per_group, int n_groups, int H);
+void build_tree_tiles(const std::vector<TreeGroupDev>& groups, int W, std::vector<TreeTileDev>& out);
+// kmap / vmap: 2-D TMA maps over the store viewed as [layers * n_slots][d] (16 x 64 boxes,
+// SWIZZLE_128B); layer_row0 = layer * n_slots; K / V: this layer's [n_slots][d] base
+void launch_attention_tree(const float* q, const CUtensorMap& kmap, const CUtensorMap& vmap, long long layer_row0,
+                           const __nv_bfloat16* K, const __nv_bfloat16* V, const AttnRowsDev& rows,
+                           const TreeGroupDev* groups, const TreeTileDev* tiles, int n_tiles, int W, int H, int d,
+                           int max_nodes, __nv_bfloat16* out, cudaStream_t st);
 
 // ---- rewards.cu: per-sequence task reward and per-group standardized advantages
 void launch_group_advantages(int n_groups, int g, const int* tok, long long stride, const int* len, const int* plen,

@@ -70,6 +70,9 @@ def test_group_attention_bitwise_equals_per_row_kernel(H, dh):
     vn = rng.standard_normal((M, d)).astype(np.float32)
     o_row, o_grp = c.debug_tree_attention(ctx, parents, q, kc, vc, kn, vn, H)
     assert np.array_equal(o_row, o_grp), np.argwhere(o_row != o_grp)[:5]
+    # attention_tree.cu (the engine's tree-verify / draft-level kernel) -- same bits
+    o_tree = c.debug_tree_attention_tree(ctx, parents, q, kc, vc, kn, vn, H)
+    assert np.array_equal(o_row, o_tree), np.argwhere(o_row != o_tree)[:5]
     # spot-check groups against fp64
     r0 = c0 = 0
     for (cl, n), par in zip(groups, parents):
