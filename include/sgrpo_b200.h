@@ -205,6 +205,29 @@ int sgb_adamw_state(sgb_engine* e, float* m, float* v, long long* t, int upload)
  * (GenStats.prefill_sim_s). */
 int sgb_rollout_events(sgb_engine* e, int* triples, long long cap, long long* n, double* prefill_seconds);
 
+/* ---- GRPO policy update on the device (policy_update, grpo.cpp:163-175) -------------------- */
+/* Keep the fp32 target master on the device from the next sgb_upload_target / sgb_init_random
+ * (the policy update trains it; 4 bytes per parameter). */
+int sgb_policy_enable(sgb_engine* e);
+/* The fp32 target master (reference flat layout), e.g. to mirror Model::flat after an update. */
+int sgb_download_target(sgb_engine* e, float* flat, size_t n);
+typedef struct sgb_policy_terms {
+    double loss;      /* policy_loss_grad's return value (grpo.hpp:235-276) */
+    long long tokens; /* response tokens of these sequences (the loss normaliser unless rows_total) */
+    long long rows;   /* training rows (n - 1 per sequence with a response) */
+    double seconds;
+    int skipped;      /* no response tokens: nothing to do (policy_update returns false) */
+} sgb_policy_terms;
+/* policy_loss_grad (grpo.hpp:235-276: target_train_forward / backward, tinylm.hpp:804-866) over
+ * TrainSeq{tokens, prompt_len, weight = advantage} and one AdamW::step (grpo.cpp:142-161) on the
+ * device master, then the bf16 inference weights are rebuilt. opt->rows_total > 0: global
+ * response-token count of a data-parallel shard; opt->allreduce_grad: NCCL sum of the gradient.
+ * opt->w_feat / w_tok are unused. */
+int sgb_policy_update(sgb_engine* e, int n_seqs, const int* tokens, const int* lens, const int* prompt_lens,
+                      const double* weights, const sgb_adamw* opt, float* grad_out, sgb_policy_terms* terms);
+/* AdamW::m / v / t of the device policy optimizer (upload = 1 installs, 0 reads back). */
+int sgb_policy_adamw_state(sgb_engine* e, float* m, float* v, long long* t, int upload);
+
 /* ---- hardware profile: C_peak calibration (Alg. 2, src/roofline.cpp:39-108) ------------- */
 /* detect_knee (roofline.cpp:39-76): farthest point from the chord of the unit-normalised
  * curve; confidence in [0, 1]. n >= 4 (else SGB_EINVAL). */

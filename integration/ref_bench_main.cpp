@@ -19,7 +19,7 @@
 #include "sgrpo/grpo.hpp"
 #include "sgrpo/harness.hpp"
 
-extern "C" __attribute__((weak)) void sgb_shim_counters(long long*, long long*, long long*, long long*);
+extern "C" __attribute__((weak)) void sgb_shim_counters(long long*, long long*, long long*, long long*, long long*);
 
 using namespace sgrpo;
 
@@ -59,11 +59,15 @@ int main(int argc, char** argv) {
                     e.result.trace.empty() ? 0.0 : e.result.trace.back().reward_mean);
     }
     std::printf("]");
+    long long pol = 0;
+    for (const auto& e : r.entries)
+        for (const auto& it : e.result.trace) pol += it.policy_skipped ? 0 : 1;
+    std::printf(", \"policy_steps\": %lld", pol);
     if (sgb_shim_counters) {
-        long long ro, up, tu, du;
-        sgb_shim_counters(&ro, &up, &tu, &du);
+        long long ro, up, tu, du, pu;
+        sgb_shim_counters(&ro, &up, &tu, &du, &pu);
         std::printf(", \"device\": {\"rollouts\": %lld, \"draft_updates\": %lld, \"target_uploads\": %lld, "
-                    "\"draft_uploads\": %lld}", ro, up, tu, du);
+                    "\"draft_uploads\": %lld, \"policy_updates\": %lld}", ro, up, tu, du, pu);
     }
     std::printf("}\n");
     return r.tokens_identical ? 0 : 3;

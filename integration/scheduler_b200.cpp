@@ -4,6 +4,7 @@
 //
 //   generate_dynamic_batch  scheduler.hpp:99-102 / scheduler.cpp:236-354
 //   draft_update            grpo.hpp:115-116 / grpo.cpp:177-186
+//   policy_update           grpo.hpp:106-108 / grpo.cpp:163-175 (target train step on the device)
 //
 // Everything else -- plan_step / compute_* / SpecConfig::validate / decode_mode_from_string /
 // to_string / GenStats::tau / gen_stats_to_jsonl (scheduler.cpp:14-75,356-388), train_loop,
@@ -75,14 +76,16 @@ struct Device {
     int k_max = 0, l_max = 0;  // tree capacity the engine was created with
     uint64_t target_hash = 0, draft_hash = 0;
     bool target_ok = false, draft_ok = false;
-    const AdamW* opt_owner = nullptr;  // whose optimizer state the device holds
+    const AdamW* opt_owner = nullptr;  // whose optimizer state the device holds (draft)
     long long opt_t = -1;
-    long long rollouts = 0, updates = 0, target_uploads = 0, draft_uploads = 0;
+    const AdamW* pol_owner = nullptr;  // ... and the policy optimizer's
+    long long pol_t = -1;
+    long long rollouts = 0, updates = 0, target_uploads = 0, draft_uploads = 0, policy_updates = 0;
 };
 Device g;
 
-sgb_engine* engine_for(const Model& t, const Draft& d, size_t n_seqs, int k_max = 10, int l_max = 6) {
-    const int dl = static_cast<int>(d.layers.size());
+sgb_engine* engine_for(const Model& t, const Draft* d, size_t n_seqs, int k_max = 10, int l_max = 6) {
+    const int dl = d ? static_cast<int>(d->layers.size()) : (g.e ? g.draft_layers : 1);
     k_max = std::max(k_max, g.e ? g.k_max : 10);
     l_max = std::max(l_max, g.e ? g.l_max : 6);
     if (g.e && (n_seqs > g.cap || !(g.cfg == t.config) || g.draft_layers != dl || k_max > g.k_max || l_max > g.l_max)) {
@@ -92,6 +95,7 @@ sgb_engine* engine_for(const Model& t, const Draft& d, size_t n_seqs, int k_max 
         fresh.updates = g.updates;
         fresh.target_uploads = g.target_uploads;
         fresh.draft_uploads = g.draft_uploads;
+        fresh.policy_updates = g.policy_updates;
         g = fresh;
     }
     if (!g.e) {
@@ -100,6 +104,7 @@ sgb_engine* engine_for(const Model& t, const Draft& d, size_t n_seqs, int k_max 
         g.cap = std::max<size_t>(n_seqs, 64);
         check(sgb_engine_create(&mc, dl, /*device=*/0, static_cast<int>(g.cap), /*max_rows=*/2048, k_max, l_max,
                                 &g.e));
+        check(sgb_policy_enable(g.e));  // keep the fp32 target master: policy_update trains it on the device
         g.cfg = c;
         g.draft_layers = dl;
         g.k_max = k_max;
@@ -112,12 +117,14 @@ sgb_engine* engine_for(const Model& t, const Draft& d, size_t n_seqs, int k_max 
         g.target_ok = true;
         ++g.target_uploads;
     }
-    const uint64_t hd = content_hash(d.flat);
-    if (!g.draft_ok || hd != g.draft_hash) {
-        check(sgb_upload_draft(g.e, d.flat.data(), d.flat.size()));
-        g.draft_hash = hd;
-        g.draft_ok = true;
-        ++g.draft_uploads;
+    if (d) {
+        const uint64_t hd = content_hash(d->flat);
+        if (!g.draft_ok || hd != g.draft_hash) {
+            check(sgb_upload_draft(g.e, d->flat.data(), d->flat.size()));
+            g.draft_hash = hd;
+            g.draft_ok = true;
+            ++g.draft_uploads;
+        }
     }
     return g.e;
 }
@@ -137,7 +144,7 @@ BatchState generate_dynamic_batch(const Model& target, const Draft& draft, const
               d = target.config.d_model;
     const int km = opts.mode == DecodeMode::fixed_spec ? std::max(sched.k_max, opts.fixed.k_draft) : sched.k_max;
     const int lm = opts.mode == DecodeMode::fixed_spec ? std::max(sched.l_max, opts.fixed.l_draft) : sched.l_max;
-    sgb_engine* e = engine_for(target, draft, static_cast<size_t>(std::max(n, 1)), km, lm);
+    sgb_engine* e = engine_for(target, &draft, static_cast<size_t>(std::max(n, 1)), km, lm);
     sgb_gen_options o{sched.alpha, sched.k_max, sched.l_max, sched.c_peak, static_cast<int>(opts.mode),
                       opts.early_term ? 1 : 0, opts.temperature, opts.seed, opts.max_new_tokens,
                       opts.fixed.n_verify, opts.fixed.k_draft, opts.fixed.l_draft, nullptr, 1, 0, nullptr};
@@ -194,7 +201,7 @@ DraftLossTerms draft_update(Draft& draft, const Model& target, const DraftTrainB
                             double w_tok) {
     DraftLossTerms terms;
     if (batch.seqs.empty()) return terms;  // grpo.cpp:180
-    sgb_engine* e = engine_for(target, draft, std::max<size_t>(batch.seqs.size(), 1));
+    sgb_engine* e = engine_for(target, &draft, std::max<size_t>(batch.seqs.size(), 1));
     std::vector<int> toks, lens;
     std::vector<float> feats;
     for (const SeqResult* s : batch.seqs) {
@@ -227,13 +234,54 @@ DraftLossTerms draft_update(Draft& draft, const Model& target, const DraftTrainB
     return terms;
 }
 
+bool policy_update(Model& params, const std::vector<GroupBatch>& groups, AdamW& opt) {
+    // TrainSeq per member of every unfiltered group (grpo.cpp:164-169)
+    std::vector<int> toks, lens, plens;
+    std::vector<double> w;
+    for (const auto& gb : groups) {
+        if (gb.filtered) continue;
+        for (size_t i = 0; i < gb.members.size(); ++i) {
+            const auto& m = gb.members[i];
+            toks.insert(toks.end(), m.tokens.begin(), m.tokens.end());
+            lens.push_back(static_cast<int>(m.tokens.size()));
+            plens.push_back(m.prompt_len);
+            w.push_back(gb.advantages[i]);
+        }
+    }
+    if (lens.empty()) return false;  // grpo.cpp:170
+    sgb_engine* e = engine_for(params, nullptr, lens.size());
+    const size_t n = params.flat.size();
+    if (opt.m.size() != n || opt.v.size() != n) {  // AdamW::step's fresh start (grpo.cpp:144-148)
+        long long t0 = 0;
+        check(sgb_policy_adamw_state(e, nullptr, nullptr, &t0, 1));
+    } else if (g.pol_owner != &opt || g.pol_t != opt.t) {
+        check(sgb_policy_adamw_state(e, opt.m.data(), opt.v.data(), &opt.t, 1));
+    }
+    sgb_adamw a{opt.lr, opt.beta1, opt.beta2, opt.eps, opt.weight_decay, 1.0, 0.1, 0, 1, 0};
+    sgb_policy_terms t{};
+    check(sgb_policy_update(e, static_cast<int>(lens.size()), toks.data(), lens.data(), plens.data(), w.data(), &a,
+                            nullptr, &t));
+    if (t.skipped) return true;  // the reference steps AdamW with a zero gradient here; tokens > 0 always
+    // mirror the updated master and the optimizer state into the caller's objects
+    check(sgb_download_target(e, params.flat.data(), n));
+    g.target_hash = content_hash(params.flat);
+    opt.m.resize(n);
+    opt.v.resize(n);
+    check(sgb_policy_adamw_state(e, opt.m.data(), opt.v.data(), &opt.t, 0));
+    g.pol_owner = &opt;
+    g.pol_t = opt.t;
+    ++g.policy_updates;
+    return true;
+}
+
 }  // namespace sgrpo
 
 // Counters of the shim (tests / ref_bench print them to prove the device path ran).
 extern "C" void sgb_shim_counters(long long* rollouts, long long* updates, long long* target_uploads,
-                                  long long* draft_uploads) {
+                                  long long* draft_uploads, long long* policy_updates) {
     *rollouts = sgrpo::g.rollouts;
     *updates = sgrpo::g.updates;
     *target_uploads = sgrpo::g.target_uploads;
     *draft_uploads = sgrpo::g.draft_uploads;
+    *policy_updates = sgrpo::g.policy_updates;
 }

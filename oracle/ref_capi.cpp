@@ -537,6 +537,25 @@ int sgref_draft_loss_grad(void* draft, void* model, int nseq, const int* tokens,
     });
 }
 
+// policy_loss_grad<float> (grpo.hpp:235-276): the GRPO policy objective's loss and gradient
+int sgref_policy_loss_grad(void* model, int nseq, const int* tokens, const int* lens, const int* prompt_lens,
+                           const double* weights, float* grad, double* loss) {
+    return guarded([&] {
+        const Model& m = *static_cast<Model*>(model);
+        std::vector<std::vector<int>> toks(nseq);
+        std::vector<TrainSeq> ts(nseq);
+        size_t off = 0;
+        for (int i = 0; i < nseq; ++i) {
+            toks[i].assign(tokens + off, tokens + off + lens[i]);
+            off += lens[i];
+        }
+        for (int i = 0; i < nseq; ++i) ts[i] = TrainSeq{&toks[i], prompt_lens[i], weights[i]};
+        std::vector<float> g(m.flat.size(), 0.f);
+        *loss = policy_loss_grad<float>(m, ts, g);
+        std::memcpy(grad, g.data(), g.size() * sizeof(float));
+    });
+}
+
 struct AdamC {
     double lr, beta1, beta2, eps, wd;
 };

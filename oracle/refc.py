@@ -344,6 +344,21 @@ def generate_threaded(model, draft, prompts, g, threads, **kw):
     return int(n), secs.value
 
 
+def policy_loss_grad(model: RefModel, seqs):
+    """policy_loss_grad<float> (grpo.hpp:235-276) of the compiled reference. seqs: list of
+    (tokens, prompt_len, weight). Returns (loss, grad[param_count])."""
+    toks = np.ascontiguousarray(np.concatenate([np.asarray(t, np.int32) for t, _, _ in seqs]), np.int32)
+    lens = np.array([len(t) for t, _, _ in seqs], np.int32)
+    pl = np.array([q for _, q, _ in seqs], np.int32)
+    w = np.array([x for _, _, x in seqs], np.float64)
+    n = lib().sgref_param_count(C.byref(cfg_c(model.cfg)))
+    grad = np.zeros(n, np.float32)
+    loss = C.c_double()
+    check(lib().sgref_policy_loss_grad(C.c_void_p(model.h), len(seqs), _p(toks, C.c_int), _p(lens, C.c_int),
+                                       _p(pl, C.c_int), _p(w, C.c_double), _p(grad, C.c_float), C.byref(loss)))
+    return loss.value, grad
+
+
 def _seq_arrays(seqs, d):
     toks = np.ascontiguousarray(np.concatenate([np.asarray(s.tokens, np.int32) for s in seqs]), np.int32)
     lens = np.array([len(s.tokens) for s in seqs], np.int32)

@@ -631,3 +631,42 @@ def debug_tree_attention_tree(ctx_len, parents, q, kctx, vctx, knode, vnode, n_h
 
 
 EXPORTED += ["sgb_debug_tree_attention_tree", "sgb_bench_tree_attention_tree"]
+
+
+class PolicyTermsC(C.Structure):
+    _fields_ = [("loss", C.c_double), ("tokens", C.c_longlong), ("rows", C.c_longlong), ("seconds", C.c_double),
+                ("skipped", C.c_int)]
+
+
+def _policy_enable(self):
+    """Keep the fp32 target master on the device from the next upload (policy updates)."""
+    _check(_lib.sgb_policy_enable(self.h))
+
+
+def _policy_update(self, seqs, lr=2e-4, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.0, tokens_total=0,
+                   apply_step=True, want_grad=False, allreduce_grad=False):
+    """policy_update (grpo.cpp:163-175) on the device. seqs: list of (tokens, prompt_len, advantage).
+    Returns (loss, tokens, rows, seconds, skipped) and the fp32 gradient if want_grad."""
+    toks = np.ascontiguousarray(np.concatenate([np.asarray(t, np.int32) for t, _, _ in seqs]) if seqs
+                                else np.zeros(0, np.int32), np.int32)
+    lens = np.array([len(t) for t, _, _ in seqs], np.int32)
+    pl = np.array([q for _, q, _ in seqs], np.int32)
+    w = np.array([x for _, _, x in seqs], np.float64)
+    opt = AdamWC(lr, beta1, beta2, eps, weight_decay, 1.0, 0.1, tokens_total, int(apply_step), int(allreduce_grad))
+    grad = np.zeros(self.n_target, np.float32) if want_grad else None
+    t = PolicyTermsC()
+    _check(_lib.sgb_policy_update(self.h, len(seqs), _p(toks, C.c_int), _p(lens, C.c_int), _p(pl, C.c_int),
+                                  _p(w, C.c_double), C.byref(opt), _p(grad, C.c_float), C.byref(t)))
+    return (t.loss, t.tokens, t.rows, t.seconds, bool(t.skipped)), grad
+
+
+def _download_target(self):
+    out = np.zeros(self.n_target, np.float32)
+    _check(_lib.sgb_download_target(self.h, _p(out, C.c_float), C.c_size_t(out.size)))
+    return out
+
+
+Engine.policy_enable = _policy_enable
+Engine.policy_update = _policy_update
+Engine.download_target = _download_target
+EXPORTED += ["sgb_policy_enable", "sgb_policy_update", "sgb_download_target", "sgb_policy_adamw_state"]

@@ -492,6 +492,53 @@ int sgb_draft_update(sgb_engine* e, int n_seqs, const int* tokens, const int* le
     });
 }
 
+int sgb_policy_enable(sgb_engine* e) {
+    return guarded([&] { E(e).policy_enable(); });
+}
+
+int sgb_download_target(sgb_engine* e, float* flat, size_t n) {
+    return guarded([&] { E(e).download_target(flat, n); });
+}
+
+int sgb_policy_update(sgb_engine* e, int n_seqs, const int* tokens, const int* lens, const int* prompt_lens,
+                      const double* weights, const sgb_adamw* opt, float* grad_out, sgb_policy_terms* terms) {
+    return guarded([&] {
+        if (!opt) throw std::invalid_argument("null AdamW options");
+        if (n_seqs < 0 || (n_seqs > 0 && (!tokens || !lens || !prompt_lens || !weights)))
+            throw std::invalid_argument("policy_update: null sequence arrays");
+        sgb::Engine::PolicyArgs a;
+        a.n_seqs = n_seqs;
+        a.tokens = tokens;
+        a.lens = lens;
+        a.prompt_lens = prompt_lens;
+        a.weights = weights;
+        a.lr = opt->lr;
+        a.beta1 = opt->beta1;
+        a.beta2 = opt->beta2;
+        a.eps = opt->eps;
+        a.weight_decay = opt->weight_decay;
+        a.tokens_total = opt->rows_total;
+        a.apply_step = opt->apply_step != 0;
+        a.grad_out = grad_out;
+        if (opt->allreduce_grad) {
+            a.grad_hook = grad_allreduce_hook;
+            a.hook_ctx = &group_of(e);
+        }
+        const auto t = E(e).policy_update(a);
+        if (terms) {
+            terms->loss = t.loss;
+            terms->tokens = t.tokens;
+            terms->rows = t.rows;
+            terms->seconds = t.seconds;
+            terms->skipped = t.skipped ? 1 : 0;
+        }
+    });
+}
+
+int sgb_policy_adamw_state(sgb_engine* e, float* m, float* v, long long* t, int upload) {
+    return guarded([&] { E(e).policy_adamw_state(m, v, t, upload != 0); });
+}
+
 int sgb_draft_update_last(sgb_engine* e, const sgb_adamw* opt, float* grad_out, sgb_draft_terms* terms) {
     return guarded([&] {
         auto a = draft_args(opt, grad_out);

@@ -320,6 +320,8 @@ Engine::~Engine() {
     cudaSetDevice(device_);
     cudaStreamSynchronize(st_);
     if (adv_buf_) cudaFree(adv_buf_);
+    for (void* q : pol_ptrs_) cudaFree(q);
+    if (tmaster_) cudaFree(tmaster_);
     for (void* q : {static_cast<void*>(qbuf_), static_cast<void*>(qstat_), static_cast<void*>(resid_),
                     static_cast<void*>(rkeys_), static_cast<void*>(tr_.qrow)})
         if (q) cudaFree(q);
@@ -435,10 +437,16 @@ void Engine::convert_draft() {
 
 void Engine::upload_target(const float* flat, size_t n) {
     if (n != tlay_.total) throw std::invalid_argument("upload_target: param count mismatch");
-    float* stg = dalloc<float>(n);
+    float* stg = tmaster_ ? tmaster_ : dalloc<float>(n);
     SGB_CUDA(cudaMemcpy(stg, flat, n * sizeof(float), cudaMemcpyHostToDevice));
     convert_target(stg);
-    cudaFree(stg);
+    draft_lm_stale_ = tr2_.ready;  // the draft update's frozen copy of the LM head
+    if (keep_master_) {
+        tmaster_ = stg;  // the policy update's fp32 master
+        if (pol_.ready) policy_refresh_ref_weights();
+    } else {
+        cudaFree(stg);
+    }
 }
 
 void Engine::upload_draft(const float* flat, size_t n) {
@@ -480,7 +488,14 @@ void Engine::init_random(uint64_t seed) {
     one(tlay_.lnf_b, d, 0.f);
     nrm(tlay_.lm_head, static_cast<size_t>(d) * V, 0.02f);
     convert_target(stg);
-    cudaFree(stg);
+    draft_lm_stale_ = tr2_.ready;
+    if (keep_master_) {
+        if (tmaster_) cudaFree(tmaster_);
+        tmaster_ = stg;
+        if (pol_.ready) policy_refresh_ref_weights();
+    } else {
+        cudaFree(stg);
+    }
     const float res_d = static_cast<float>(0.02 / std::sqrt(2.0 * dlayers_));
     float* m = dmaster_;
     launch_init_normal(m + dlay_.w_fuse, 2 * static_cast<size_t>(d) * d, splitmix_host(s), 0.02f, st_);

@@ -166,6 +166,32 @@ class Engine {
         double seconds = 0;
     };
     DraftLossTerms draft_update(const DraftUpdateArgs& a);
+
+    // ---- GRPO policy update on the device (policy_update, grpo.cpp:163-175)
+    struct PolicyArgs {
+        int n_seqs = 0;
+        const int* tokens = nullptr;       // concatenated
+        const int* lens = nullptr;         // [n_seqs]
+        const int* prompt_lens = nullptr;  // [n_seqs]
+        const double* weights = nullptr;   // [n_seqs] TrainSeq::weight (the advantage)
+        double lr = 2e-4, beta1 = 0.9, beta2 = 0.999, eps = 1e-8, weight_decay = 0.0;
+        long long tokens_total = 0;  // > 0: global response-token normaliser (data-parallel shard)
+        bool apply_step = true;
+        float* grad_out = nullptr;  // optional host copy of the gradient (reference flat layout)
+        void (*grad_hook)(float* dgrad, size_t n, cudaStream_t st, void* ctx) = nullptr;
+        void* hook_ctx = nullptr;
+    };
+    struct PolicyTerms {
+        double loss = 0;
+        long long tokens = 0, rows = 0;
+        double seconds = 0;
+        bool skipped = false;
+    };
+    // keep the fp32 target master on the device from the next upload (needed by policy_update)
+    void policy_enable();
+    PolicyTerms policy_update(const PolicyArgs& a);
+    void download_target(float* flat, size_t n);
+    void policy_adamw_state(float* m, float* v, long long* t, bool upload);
     void adamw_reset();
     void adamw_state(float* m, float* v, long long* t, bool upload);
     // measure_c_peak's latency_fn on the device (roofline.cpp:78-108 / tools/sgrpo.cpp:38-49):
@@ -338,6 +364,36 @@ class Engine {
     void reject_alloc();
     void train_alloc();
     void train_refresh_ref_weights();
+    // ---- policy update state (engine_policy.cu)
+    bool keep_master_ = false;
+    float* tmaster_ = nullptr;  // fp32 target master (reference flat layout)
+    bool draft_lm_stale_ = false;
+    std::vector<void*> pol_ptrs_;
+    struct Pol {
+        bool ready = false;
+        int rmax = 0, lc = 0;
+        long long adam_t = 0;
+        float *grad = nullptr, *m = nullptr, *v = nullptr;
+        __nv_bfloat16 *flat_b = nullptr, *wqkv_ref = nullptr;
+        struct Layer {
+            float *x_in, *mu1, *rs1, *qkv, *ctx, *lse, *xmid, *mu2, *rs2, *fch;
+            __nv_bfloat16 *a1, *ctxb, *a2, *hg;
+            GemmAct act_a1, act_ctx, act_a2, act_hg;
+        };
+        std::vector<Layer> L;
+        struct Refs {
+            GemmWeight wqkv, wo, w1, w2;
+        };
+        std::vector<Refs> refs;
+        GemmWeight lm_ref;
+        float *xfin, *fhat, *muf, *rsf, *dlnf, *dx, *dxmid, *da, *dctx, *dqkv, *dhg, *dgb, *Drow, *logits;
+        __nv_bfloat16 *fhat_b, *dfch_b, *dx_b, *dxmid_b, *dqkv_b, *dlog, *tA, *tB;
+        int *tok, *pos, *next, *seq_first, *seq_last, *tiles, *csr;
+        double *rscale, *loss_row;
+        GemmAct act_fhat, act_dx, act_dxmid, act_dfch, act_dqkv, act_dlog;
+    } pol_;
+    void policy_alloc();
+    void policy_refresh_ref_weights();
     void wgrad(const __nv_bfloat16* dyT, int N, const __nv_bfloat16* xT, int Kfeat, int Rp, float* grad_dst, int ld);
     cudaEvent_t ev0_ = nullptr, ev1_ = nullptr, evs_a_ = nullptr, evs_b_ = nullptr;  // rollout / per-step
 };

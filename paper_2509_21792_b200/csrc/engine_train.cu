@@ -185,6 +185,10 @@ Engine::DraftLossTerms Engine::draft_update(const DraftUpdateArgs& A) {
     if (!target_ready_ || !draft_ready_) throw std::runtime_error("weights not uploaded");
     train_alloc();
     Train& t = tr2_;
+    if (draft_lm_stale_) {  // the target's LM head changed (policy update / re-upload)
+        launch_transpose_bf16(lm_head_.ptr, dims_.vocab, dims_.d, dims_.d, t.lm_ref, dims_.vocab, st_);
+        draft_lm_stale_ = false;
+    }
     const int d = dims_.d, F = dims_.dff, V = dims_.vocab, H = dims_.heads;
     const auto& lo = dlay_.layers[0];
     const LayerDev& W = dL_[0];

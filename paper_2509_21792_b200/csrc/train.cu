@@ -166,7 +166,8 @@ __global__ void __launch_bounds__(kT) smoothl1_kernel(const float* __restrict__ 
 // Cross entropy vs the next token through the frozen LM head (grpo.hpp:323-338):
 // loss row and dlogits = scale * (softmax - onehot) in bf16.
 __global__ void __launch_bounds__(kT) ce_kernel(const float* __restrict__ logits, int V, const int* __restrict__ tgt,
-                                                double scale, __nv_bfloat16* __restrict__ dlog, double* __restrict__ loss_row) {
+                                                double scale, const double* __restrict__ row_scale,
+                                                __nv_bfloat16* __restrict__ dlog, double* __restrict__ loss_row) {
     // Two passes over the 608 KB row: (1) online max + sum of exp with per-thread rescaling
     // (fp32 exps, fp64 sums), (2) the bf16 gradient scale * (softmax - onehot). The gradient
     // is stored in bf16, so its exps are fp32; the loss keeps an fp64 log-sum-exp.
@@ -206,6 +207,7 @@ __global__ void __launch_bounds__(kT) ce_kernel(const float* __restrict__ logits
     const double s = block_sum_dd(mt == -INFINITY ? 0.0 : st * static_cast<double>(expf(mt - m2)), redd);
     const double lse = static_cast<double>(m2) + log(s);
     const float lse_f = static_cast<float>(lse);
+    if (row_scale) scale = row_scale[r];  // policy loss: advantage / N on response rows, 0 on prompt rows
     const float sc = static_cast<float>(scale);
     const int t = tgt[r];
     __nv_bfloat16* D = dlog + static_cast<size_t>(r) * V;
@@ -281,6 +283,31 @@ __global__ void adamw_kernel(float* __restrict__ p, const float* __restrict__ g,
     }
 }
 
+// x0[r] = tok_emb[tok[r]] + pos_emb[pos[r]] (target_train_forward, tinylm.hpp:813-819)
+__global__ void embed_sum_kernel(const int* __restrict__ tok, const int* __restrict__ pos, int d,
+                                 const float* __restrict__ te, const float* __restrict__ pe, float* __restrict__ x) {
+    const int r = blockIdx.x;
+    const float* a = te + static_cast<size_t>(tok[r]) * d;
+    const float* b = pe + static_cast<size_t>(pos[r]) * d;
+    float* o = x + static_cast<size_t>(r) * d;
+    for (int e = threadIdx.x; e < d; e += blockDim.x) o[e] = a[e] + b[e];
+}
+
+// embedding gradients (tinylm.hpp:857-865), deterministic: one CTA per distinct embedding row,
+// which adds the dx rows that hit it (CSR, ascending row order) -- grad[key[k]] += sum dx[rows]
+__global__ void embed_grad_kernel(const int* __restrict__ key, const int* __restrict__ ptr,
+                                  const int* __restrict__ rows, int d, const float* __restrict__ dx,
+                                  float* __restrict__ grad) {
+    const int k = blockIdx.x;
+    float* o = grad + static_cast<size_t>(key[k]) * d;
+    const int j0 = ptr[k], j1 = ptr[k + 1];
+    for (int e = threadIdx.x; e < d; e += blockDim.x) {
+        float acc = o[e];
+        for (int j = j0; j < j1; ++j) acc += dx[static_cast<size_t>(rows[j]) * d + e];
+        o[e] = acc;
+    }
+}
+
 int grid_n(size_t n) {
     size_t b = (n + 255) / 256;
     if (b > 148 * 32) b = 148 * 32;
@@ -321,9 +348,9 @@ void launch_smoothl1(const float* fhat, const float* feat_base, const long long*
     SGB_KCHECK();
 }
 void launch_ce(const float* logits, int R, int V, const int* tgt, double scale, __nv_bfloat16* dlog, double* loss_row,
-               cudaStream_t st) {
+               cudaStream_t st, const double* row_scale) {
     if (R <= 0) return;
-    ce_kernel<<<R, kT, 0, st>>>(logits, V, tgt, scale, dlog, loss_row);
+    ce_kernel<<<R, kT, 0, st>>>(logits, V, tgt, scale, row_scale, dlog, loss_row);
     SGB_KCHECK();
 }
 void launch_transpose_bf16(const float* src, int rows, int cols, int src_ld, __nv_bfloat16* dst, int ld,
@@ -347,6 +374,19 @@ void launch_adamw(float* p, const float* g, float* m, float* v, size_t n, double
     const double bc1 = 1.0 - pow(b1, static_cast<double>(t));
     const double bc2 = 1.0 - pow(b2, static_cast<double>(t));
     adamw_kernel<<<grid_n(n), 256, 0, st>>>(p, g, m, v, n, lr, b1, b2, eps, wd, bc1, bc2);
+    SGB_KCHECK();
+}
+
+void launch_embed_sum(const int* tok, const int* pos, int R, int d, const float* te, const float* pe, float* x,
+                      cudaStream_t st) {
+    if (R <= 0) return;
+    embed_sum_kernel<<<R, 256, 0, st>>>(tok, pos, d, te, pe, x);
+    SGB_KCHECK();
+}
+void launch_embed_grad(const int* key, const int* ptr, const int* rows, int n_keys, int d, const float* dx,
+                       float* grad, cudaStream_t st) {
+    if (n_keys <= 0) return;
+    embed_grad_kernel<<<n_keys, 256, 0, st>>>(key, ptr, rows, d, dx, grad);
     SGB_KCHECK();
 }
 

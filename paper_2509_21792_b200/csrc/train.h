@@ -26,8 +26,14 @@ void launch_train_attn_bwd(const float* qkv, const float* ctx, const float* dctx
                            int H, float* Drow, float* dqkv, cudaStream_t st);
 void launch_smoothl1(const float* fhat, const float* feat_base, const long long* tgt_off, int R, int d, double scale,
                      float* dfeat, double* loss_row, cudaStream_t st);
+// row_scale (optional, [R]) replaces scale per row
 void launch_ce(const float* logits, int R, int V, const int* tgt, double scale, __nv_bfloat16* dlog, double* loss_row,
-               cudaStream_t st);
+               cudaStream_t st, const double* row_scale = nullptr);
+void launch_embed_sum(const int* tok, const int* pos, int R, int d, const float* te, const float* pe, float* x,
+                      cudaStream_t st);
+// grad[key[k]][:] += sum over rows[ptr[k] .. ptr[k+1]) of dx[row][:] (fixed order: deterministic)
+void launch_embed_grad(const int* key, const int* ptr, const int* rows, int n_keys, int d, const float* dx,
+                       float* grad, cudaStream_t st);
 void launch_transpose_bf16(const float* src, int rows, int cols, int src_ld, __nv_bfloat16* dst, int ld,
                            cudaStream_t st);
 void launch_transpose_bf16(const __nv_bfloat16* src, int rows, int cols, int src_ld, __nv_bfloat16* dst, int ld,

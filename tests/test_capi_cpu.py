@@ -68,15 +68,16 @@ def test_drop_in_links_the_unmodified_reference():
     subprocess.run(["make", "-C", os.path.join(ROOT, "oracle"), "-s"], check=True)
     subprocess.run(["make", "-C", os.path.join(ROOT, "integration"), "-s"], check=True)
     weak = {}
-    for obj, part in (("scheduler.o", "generate_dynamic_batch"), ("grpo.o", "draft_update")):
+    for obj, part in (("scheduler.o", "generate_dynamic_batch"), ("grpo.o", "draft_update"),
+                      ("grpo.o", "policy_update")):
         out = subprocess.run(["nm", os.path.join(build, "weak", obj)], capture_output=True, text=True).stdout
         kinds = {l.split()[1] for l in out.splitlines() if part in l and not l.split()[-1].endswith(".cold")
                  and len(l.split()) == 3}
         weak[part] = kinds
-    assert weak == {"generate_dynamic_batch": {"W"}, "draft_update": {"W"}}, weak
-    # the reference's strong definitions survive everywhere else (e.g. plan_step, policy_update)
+    assert weak == {"generate_dynamic_batch": {"W"}, "draft_update": {"W"}, "policy_update": {"W"}}, weak
+    # the reference's strong definitions survive everywhere else (e.g. train_loop, plan_step)
     out = subprocess.run(["nm", os.path.join(build, "weak", "grpo.o")], capture_output=True, text=True).stdout
-    assert any("policy_update" in l and " T " in l for l in out.splitlines())
+    assert any("train_loop" in l and " T " in l for l in out.splitlines())
     cfg = os.path.join(ROOT, "integration", "configs", "drop_in_bench.json")
     p = subprocess.run([os.path.join(build, "ref_bench_cpu"), cfg, "vanilla", "adaptive_spec"], capture_output=True,
                        text=True, timeout=300)

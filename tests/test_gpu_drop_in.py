@@ -46,8 +46,8 @@ CFG = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), 
 STRATEGIES = ["vanilla", "vanilla+early_term", "fixed_spec", "adaptive_spec", "adaptive_spec+online_draft"]
 
 
-def _run_bench(binary):
-    p = subprocess.run([binary, CFG, *STRATEGIES], capture_output=True, text=True, timeout=600)
+def _run_bench(binary, cfg=CFG):
+    p = subprocess.run([binary, cfg, *STRATEGIES], capture_output=True, text=True, timeout=600)
     assert p.returncode == 0, (p.returncode, p.stdout[-3000:], p.stderr[-3000:])
     return p.stdout, json.loads(p.stdout.strip().splitlines()[-1])
 
@@ -83,3 +83,19 @@ def test_reference_bench_runs_unmodified_reference_on_b200():
     if os.path.exists(cpu):
         _, rc = _run_bench(cpu)
         print("CPU reference tokens_hash", rc["entries"][0]["tokens_hash"], "B200", r["entries"][0]["tokens_hash"])
+
+
+def test_reference_train_loop_with_device_policy_updates():
+    """The same through a configuration whose supervised warm-up (the reference's own host
+    code) makes rewards vary, so groups survive the zero-variance filter and train_loop calls
+    policy_update: every such step runs on the B200 (policy_update drop-in, engine_policy.cu)
+    and the reference's token-identity check still passes across all five strategies."""
+    binary = os.path.join(BUILD, "ref_bench")
+    if not os.path.exists(binary):
+        pytest.skip("integration/_build/ref_bench not built (needs /root/reference at build time)")
+    cfg = CFG.replace("drop_in_bench.json", "drop_in_bench_policy.json")
+    table, r = _run_bench(binary, cfg)
+    print(table)
+    assert r["tokens_identical"] is True
+    assert r["policy_steps"] > 0
+    assert r["device"]["policy_updates"] == r["policy_steps"]
