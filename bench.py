@@ -262,6 +262,51 @@ def reference_arm(args, w):
     return 0
 
 
+def per_b_table(rs, ra):
+    """Per live-concurrency bucket: mean device seconds of a speculative step vs an AR step at the
+    same B, tau there, the break-even tau (= t_spec / t_ar) and the per-step speedup
+    tau * t_ar / t_spec (SURVEY §7 hard part 8's table, measured)."""
+    def buckets(r):
+        out = {}
+        for (b, n, k, l, acc), sec in zip(r.steps, r.step_seconds):
+            lo = 1 << (max(1, b).bit_length() - 1)  # power-of-two bucket [lo, 2lo)
+            e = out.setdefault(lo, [0, 0.0, 0, 0, (n, k, l)])
+            e[0] += 1
+            e[1] += sec
+            e[2] += acc
+            e[3] += b
+        return out
+    bs, ba = buckets(rs), buckets(ra)
+    rows = []
+    for lo in sorted(bs):
+        if lo not in ba:
+            continue
+        ns, ss, acs, bsum, nkl = bs[lo]
+        na, sa, _, _, _ = ba[lo]
+        ts, ta = ss / ns, sa / na
+        tau = acs / bsum if bsum else None
+        rows.append({"B": f"{lo}-{2 * lo - 1}", "nkl": list(nkl), "spec_ms": round(1e3 * ts, 3),
+                     "ar_ms": round(1e3 * ta, 3), "tau": round(tau, 3) if tau else None,
+                     "break_even_tau": round(ts / ta, 3), "step_speedup": round(tau * ta / ts, 3) if tau else None,
+                     "spec_steps": ns, "ar_steps": na})
+    return rows
+
+
+def rollout_roofline(eng, hbm, tf):
+    """SURVEY §8(d) rollout-level roofline of the last rollout: sum over decode steps of
+    max(bytes_t / BW, flops_t / F) vs the measured device time of those steps."""
+    b, f, s = eng.rollout_roofline()
+    if len(b) == 0:
+        return None
+    roof = float(np.sum(np.maximum(b / (hbm * 1e9), f / (tf * 1e12))))
+    meas = float(np.sum(s))
+    return {"roofline_s": round(roof, 4), "measured_s": round(meas, 4), "frac": round(roof / meas, 4) if meas else None,
+            "bytes": float(np.sum(b)), "flops": float(np.sum(f)), "steps": int(len(b)),
+            "definition": "sum_t max(bytes_t/HBM, flops_t/bf16_sustained) over decode steps (prefill excluded) / "
+                          "their CUDA-event time; bytes/flops per SURVEY 8(d): bf16 weights once per target / draft "
+                          "pass, every sequence's K/V, verify-row K/V writes, logits"}
+
+
 # ------------------------------------------------------------------------------ GPU arm
 def main():
     ap = argparse.ArgumentParser()
@@ -380,9 +425,12 @@ def main():
     spec_steps, upd_s, upd_wall, upd_rows = 0, 0.0, 0.0, 0
     terms = None
     last = None
+    hbm0, tf0, _ = measured_peaks()
+    roof_last = None
     for _ in range(args.steps):
         r, wall = rollout(args.mode)
         last = r
+        roof_last = rollout_roofline(eng, hbm0, tf0)
         dev_s += r.seconds
         wall_s += wall
         if w["online"]:
@@ -422,7 +470,11 @@ def main():
             ar = {"value": ra.generated() / ra.seconds, "unit": "tokens/s",
                   "spec_value": rs.generated() / rs.seconds,
                   "speedup": (rs.generated() / rs.seconds) / (ra.generated() / ra.seconds),
-                  "tokens_identical": same, "note": "rollout only (no draft step), this rank"}
+                  "tokens_identical": same, "note": "rollout only (no draft step), this rank",
+                  "per_concurrency": per_b_table(rs, ra)}
+            if gen["acceptance"] == "rejection":
+                ar["note"] += ("; rejection sampling is lossless in distribution: token streams differ from "
+                               "AR sampling by design (the strict-match mode is the token-identical one)")
     # kernel-class breakdown: one more rollout of the same workload with a CUDA-event pair
     # around every launch (kept out of the timed steps: events between launches defeat PDL)
     if not args.no_profile:
@@ -475,6 +527,8 @@ def main():
                 "d2h_bytes_per_step": d2h // args.steps},
         "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk,
     }
+    if roof_last:
+        line["roofline"]["rollout"] = roof_last
     if w["online"]:
         line["online_draft_step"] = {"device_ms_per_step": round(1e3 * upd_s / args.steps, 2),
                                      "wall_ms_per_step": round(1e3 * upd_wall / args.steps, 2),

@@ -204,6 +204,10 @@ int sgb_adamw_state(sgb_engine* e, float* m, float* v, long long* t, int upload)
  * (step, seq, accepted) triples, min(n, cap) written; the measured prefill seconds
  * (GenStats.prefill_sim_s). */
 int sgb_rollout_events(sgb_engine* e, int* triples, long long cap, long long* n, double* prefill_seconds);
+/* Per-step algorithmic work of the last rollout (bf16 weight + K/V bytes, GEMM +
+ * attention flops, target and draft passes) and the measured device seconds of each step:
+ * roofline time = sum_t max(bytes_t / BW, flops_t / F). min(n, cap) entries written. */
+int sgb_rollout_roofline(sgb_engine* e, double* bytes, double* flops, double* seconds, long long cap, long long* n);
 
 /* ---- GRPO policy update on the device (policy_update, grpo.cpp:163-175) -------------------- */
 /* Keep the fp32 target master on the device from the next sgb_upload_target / sgb_init_random

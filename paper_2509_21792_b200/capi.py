@@ -670,3 +670,19 @@ Engine.policy_enable = _policy_enable
 Engine.policy_update = _policy_update
 Engine.download_target = _download_target
 EXPORTED += ["sgb_policy_enable", "sgb_policy_update", "sgb_download_target", "sgb_policy_adamw_state"]
+
+
+def _rollout_roofline(self):
+    """Per-step (algorithmic bytes, flops, measured seconds) of the last rollout."""
+    n = C.c_longlong()
+    _check(_lib.sgb_rollout_roofline(self.h, None, None, None, 0, C.byref(n)))
+    b = np.zeros(n.value, np.float64)
+    f = np.zeros(n.value, np.float64)
+    s = np.zeros(n.value, np.float64)
+    _check(_lib.sgb_rollout_roofline(self.h, _p(b, C.c_double), _p(f, C.c_double), _p(s, C.c_double), n.value,
+                                     C.byref(n)))
+    return b, f, s
+
+
+Engine.rollout_roofline = _rollout_roofline
+EXPORTED += ["sgb_rollout_roofline"]

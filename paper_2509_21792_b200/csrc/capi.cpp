@@ -33,6 +33,7 @@ struct sgb_engine {
     int draft_layers = 1;
     std::vector<int> last_events;  // (step, seq, accepted) of the last rollout
     double last_prefill_s = 0;
+    std::vector<double> last_bytes, last_flops, last_secs;  // per-step algorithmic work + device time
 };
 
 namespace {
@@ -317,6 +318,9 @@ int sgb_rollout(sgb_engine* e, const int* prompts, const int* prompt_lens, int n
         sgb::RolloutResult r = en.rollout(a);
         e->last_events = r.events;
         e->last_prefill_s = r.prefill_seconds;
+        e->last_bytes = r.step_bytes;
+        e->last_flops = r.step_flops;
+        e->last_secs = r.step_seconds;
         const int T = en.dims().max_seq;
         const int ns = static_cast<int>(r.tokens.size());
         for (int s = 0; s < ns; ++s) {
@@ -763,6 +767,18 @@ int sgb_rollout_events(sgb_engine* e, int* triples, long long cap, long long* n,
         if (n) *n = m;
         if (triples) std::copy(e->last_events.begin(), e->last_events.begin() + 3 * std::min(m, cap), triples);
         if (prefill_seconds) *prefill_seconds = e->last_prefill_s;
+    });
+}
+
+int sgb_rollout_roofline(sgb_engine* e, double* bytes, double* flops, double* seconds, long long cap, long long* n) {
+    return guarded([&] {
+        if (!e) throw std::invalid_argument("null engine");
+        const long long m = static_cast<long long>(e->last_bytes.size());
+        if (n) *n = m;
+        const long long k = std::min(m, cap);
+        if (bytes) std::copy(e->last_bytes.begin(), e->last_bytes.begin() + k, bytes);
+        if (flops) std::copy(e->last_flops.begin(), e->last_flops.begin() + k, flops);
+        if (seconds) std::copy(e->last_secs.begin(), e->last_secs.begin() + std::min<long long>(k, e->last_secs.size()), seconds);
     });
 }
 

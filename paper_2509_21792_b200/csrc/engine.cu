@@ -1586,7 +1586,14 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
                                             a.g > 1 ? std::min(hs[i].pre_len, hs[i].p) : 0, 0});
         }
         f.groups_exact = boundary_tiles();
-        if (!all_ar && tree_attn_ok(max_sel)) f.tree = &tgroups_;
+        // attention_tree.cu for speculative steps, and for AR steps of few rows (one CTA per row
+        // and head streams the whole context: no work-list prologue, no partials); wide AR
+        // batches keep attention.cu's head-grouped persistent kernel (98 % of HBM at c2)
+        static const int tree_ar_max = [] {
+            const char* v = getenv("SGB_TREE_AR_MAX");  // A/B switch
+            return v ? atoi(v) : 64;
+        }();
+        if ((!all_ar || vrows <= tree_ar_max) && tree_attn_ok(max_sel)) f.tree = &tgroups_;
         // measured A/B (SGB_PROMPT_TILES, bench.py vanilla): +5 % at 12 heads (c2), -13 % at
         // 28 heads (c3, where the per-row kernel already hits the prompt pages in L2)
         static const int prompt_tiles = [] {
@@ -1655,6 +1662,29 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
             res.events.push_back(acc);
         }
         res.steps.push_back(stat);
+        {
+            // SURVEY §8(d) algorithmic work of this step (bf16 weights and K/V): the target
+            // forward streams its non-embedding weights once and every sequence's context K/V,
+            // writes the verify rows' K/V; each draft pass (catch-up + levels) streams the draft
+            // layer + fuse + the shared LM head and the draft context K/V
+            const double dd = d, L = mc.layers, Fd = mc.dff, Vv = V;
+            const double Pt = L * (4 * dd * dd + 2 * dd * Fd) + dd * Vv;
+            const double Pd = dlayers_ * (4 * dd * dd + 2 * dd * Fd) + 2 * dd * dd + dd * Vv;
+            const double kvb = 4.0 * L * dd;
+            double ctx = 0, rowsN = 0, ctxrows = 0, spec_ctx = 0;
+            for (int i = 0; i < B; ++i) {
+                ctx += hs[i].p;
+                rowsN += hs[i].nsel;
+                ctxrows += static_cast<double>(hs[i].nsel) * (hs[i].p + hs[i].nsel);
+                if (hs[i].k) spec_ctx += hs[i].p;
+            }
+            const double passes = n_spec > 0 ? 1.0 + std::max(0, max_l - 1) : 0.0;
+            const double bytes = 2 * Pt + ctx * kvb + rowsN * kvb + passes * (2 * Pd + spec_ctx * 4 * dd) +
+                                 rowsN * Vv * 4 * (a.temperature > 0 ? 2 : 1);
+            const double flops = 2 * Pt * rowsN + 4 * L * dd * ctxrows + 2 * Pd * stat.draft_rows;
+            res.step_bytes.push_back(bytes);
+            res.step_flops.push_back(flops);
+        }
         res.total_accepted += stat.accepted;
         res.total_verify_slots += B;
         if (next_group < P) {  // waves: recycle the regions of finished groups, admit the next groups

@@ -93,6 +93,7 @@ struct RolloutResult {
     double seconds = 0;  // device time of the step loop incl. prefill (CUDA events)
     double prefill_seconds = 0;
     std::vector<double> step_seconds;  // device time of every decode step (CUDA events)
+    std::vector<double> step_bytes, step_flops;  // SURVEY §8(d) algorithmic bytes / flops per step
     long long h2d_bytes = 0, d2h_bytes = 0;
     bool waves = false;  // more sequences than KV regions: groups were admitted as regions freed
 };
