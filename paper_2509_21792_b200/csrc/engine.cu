@@ -1455,7 +1455,7 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
                     launch_gather_rows_bf16(a_, lm_idx_, nl, d, a2_ + static_cast<size_t>(lasts[0]) * d, st_);
                     count(2);
                 }
-                SGB_CUDA(cudaStreamSynchronize(st_));
+                // no host sync: the next chunk's uploads and launches are stream-ordered after this one
             }
             for (int i = 0; i < B; ++i)
                 if (hs[i].k) dft_len[hs[i].seq] = hs[i].p;
