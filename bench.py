@@ -54,10 +54,12 @@ WORKLOADS = {
     # waves over `regions` resident KV regions (engine admission); features are not
     # returned (35 GB per rollout), tokens are
     "c5": dict(V=128256, d=4096, L=32, H=32, dff=14336, P=128, G=16, Q=32, new=4096, stops=False, online=False,
-               warm=0, temp=1.0, acceptance="rejection", features=False, regions=48, rows=1024,
+               warm=24, warm_new=256, warm_prompts=24, temp=1.0, acceptance="rejection", features=False, regions=48,
+               rows=1024,
                desc="Llama-3-8B-shaped target + 1-layer draft, rejection-sampling verify at T=1.0, 32 queries x "
                     "group 16 per GPU (the full 256 x 16 shard of 8 GPUs), 128-token prompts, 4096 new tokens, "
-                    "adaptive spec, KV-region waves (48 resident sequences)"),
+                    "adaptive spec, KV-region waves (48 resident sequences), draft warmed online (T=1 rollouts of "
+                    "256 tokens on a disjoint prompt stream)"),
     "c1": dict(V=512, d=256, L=2, H=4, dff=1024, P=32, G=4, Q=8, new=128, stops=False, online=False, warm=0,
                desc="2-layer d=256 target + 1-layer draft, 8 queries x group 4, 32-token prompts, 128 new tokens"),
 }
@@ -347,7 +349,8 @@ def main():
     cfg = model_cfg(w)
     n_seq = w["Q"] * w["G"]
     regions = w.get("regions", n_seq)  # resident KV regions (fewer than sequences: waves)
-    eng = capi.Engine(cfg, 1, local, max(min(n_seq, regions), 64 if w["warm"] > 0 else 1), w.get("rows", 2048), 10, 6)
+    max_seqs = min(n_seq, regions) if "regions" in w else max(n_seq, 64 if w["warm"] > 0 else 1)
+    eng = capi.Engine(cfg, 1, local, max_seqs, w.get("rows", 2048), 10, 6)
     eng.init_random(1234)
     # NCCL data-parallel group over NVLink (C1 gradient all-reduce, C2 statistics)
     uid = [capi.nccl_unique_id() if rank == 0 else None]
@@ -398,15 +401,15 @@ def main():
         t0 = time.perf_counter()
         fl = tl = None
         for it in range(1, w["warm"] + 1):
-            tp = stream_prompts(0x7A11 + it + 1000 * rank, 32, w["P"], w["V"])
+            tp = stream_prompts(0x7A11 + it + 1000 * rank, w.get("warm_prompts", 32), w["P"], w["V"])
             # training rollouts follow the workload's own length distribution (stop caps keyed by
             # sids disjoint from the benchmark's), so the draft sees the contexts it will serve
             caps_w = stop_caps(w, 1_000_000 + 64 * (it + 1000 * rank), 64) if w["stops"] else None
-            rw = eng.generate(tp, 2, c_peak=args.c_peak, mode="vanilla", temperature=0.0, seed=it,
-                              max_new_tokens=w["new"], want_features=True, seq_max_new=caps_w)
+            rw = eng.generate(tp, 2, c_peak=args.c_peak, mode="vanilla", temperature=w.get("temp", 0.0), seed=it,
+                              max_new_tokens=w.get("warm_new", w["new"]), want_features=True, seq_max_new=caps_w)
             for _ in range(4):
                 _, _, fl, tl, _ = draft_step(rw, 2)
-        warm = {"iterations": w["warm"], "adamw_steps": 4 * w["warm"], "train_seqs_per_iter": 64,
+        warm = {"iterations": w["warm"], "adamw_steps": 4 * w["warm"], "train_seqs_per_iter": 2 * w.get("warm_prompts", 32),
                 "feature_loss": round(fl, 5), "token_loss": round(tl, 4), "seconds": round(time.perf_counter() - t0, 1)}
 
     for _ in range(args.warmup):

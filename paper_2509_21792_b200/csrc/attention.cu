@@ -115,8 +115,16 @@ struct ItemIt {
     int lv;  // the longest virtual length among the tile's rows (1-row tiles: the row's key count)
 };
 
-template <int DH>
-__global__ void __launch_bounds__(32 * (kMaxCons + 1), 1)
+// MERGE: a CTA's run of a tile's blocks that starts at block 0 merges its block partials in
+// registers (attn_merge in block order, the same arithmetic the finisher would run) instead of
+// publishing each of them: a row whose blocks the run covers completely is written straight out
+// (no partials, no ticket); otherwise the merged prefix goes into block slot 0 and slots
+// 1..k-1 get an m = -inf marker (an exact no-op in the finisher's merge). Used for the shared
+// tree-verify / draft-level tiles (many blocks per tile); the per-row decode path keeps the
+// 96-register variant.
+constexpr int kMaxConsMerge = 8;  // consumer warps of the MERGE variant (its running state needs registers)
+template <int DH, bool MERGE>
+__global__ void __launch_bounds__(32 * ((MERGE ? kMaxConsMerge : kMaxCons) + 1), 1)
     attn_kernel(const float* __restrict__ q, const __nv_bfloat16* __restrict__ K, const __nv_bfloat16* __restrict__ V,
                 AttnRowsDev rows, const AttnTileDev* __restrict__ tiles, int n_tiles, int H, int d, int G, int QW,
                 int nst, int nb_max, int balance, float scale, float* __restrict__ part_acc, float* __restrict__ part_ml,
@@ -297,6 +305,7 @@ __global__ void __launch_bounds__(32 * (kMaxCons + 1), 1)
             return kb + kBlock;  // shared blocks lie inside the committed prefix
         return min(kb + kBlock, x.lv);
     };
+    auto nrows_of = [&](const ItemIt& y, int qtile) { return max(0, min(kQT, y.tl.nrows - kQT * qtile)); };
     // a chunk of a boundary block past the common prefix: staged once per tile row
     auto per_row_chunk = [&](const ItemIt& x, int v0) {
         return x.tl.nrows > 1 && x.tl.bsh >= 0 && x.b == x.tl.bhi - 1 && v0 + kChunk > x.tl.bsh;
@@ -371,6 +380,10 @@ __global__ void __launch_bounds__(32 * (kMaxCons + 1), 1)
     ItemIt x = it0;
     int i = 0;
     int cur_t = -1, cur_g = -1, seg = 0;
+    // MERGE: running merged state of this warp's two columns over the current run
+    bool run0 = false;
+    float RM0 = -INFINITY, RM1 = -INFINITY, RL0 = 0.f, RL1 = 0.f;
+    float RA[MERGE ? NK : 1][4];
     for (int n = 0; n < n_items; ++n) {
         const int ve = item_end(x);
         const int kb = x.b * kBlock;
@@ -380,6 +393,13 @@ __global__ void __launch_bounds__(32 * (kMaxCons + 1), 1)
         if (x.t != cur_t || x.g != cur_g) {
             cur_t = x.t;
             cur_g = x.g;
+            if constexpr (MERGE) {
+                run0 = x.b == 0;
+                RM0 = RM1 = -INFINITY;
+                RL0 = RL1 = 0.f;
+#pragma unroll
+                for (int mt = 0; mt < NK; ++mt) RA[mt][0] = RA[mt][1] = RA[mt][2] = RA[mt][3] = 0.f;
+            }
             // Q^T as the B operand: query column g8 (tile row, clamped), dims 16ks + {2t, 2t+1, 2t+8, 2t+9}
             const int qrow = nrows > 0 ? qrow0 + min(g8, nrows - 1) : x.tl.row0;
             const float* qr = q + static_cast<size_t>(qrow) * d + h * DH + 2 * t4;
@@ -477,22 +497,60 @@ __global__ void __launch_bounds__(32 * (kMaxCons + 1), 1)
                     chunk(v0, 2 * t4 == cj ? lvj : v0, 2 * t4 + 1 == cj ? lvj : v0);
                 }
             }
-            // publish the block partial of every real query column
+            if (MERGE && run0) {
+                // ordered in-register merge of this block partial (attn_merge, per column)
+                if (x.b == 0) {  // from the identity: reproduces the partial exactly
+                    RM0 = m0;
+                    RM1 = m1;
+                    RL0 = l0;
+                    RL1 = l1;
 #pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                const int qc = 2 * t4 + c;
-                if (qc < nrows) {
-                    const int r = qrow0 + qc;
-                    const size_t pidx = (static_cast<size_t>(r) * nb_max + x.b) * H + h;
-                    float* pa = part_acc + pidx * DH;
+                    for (int mt = 0; mt < NK; ++mt)
 #pragma unroll
-                    for (int mt = 0; mt < NK; ++mt) {
-                        pa[16 * mt + g8] = o[mt][c];
-                        pa[16 * mt + g8 + 8] = o[mt][2 + c];
+                        for (int e = 0; e < 4; ++e) RA[mt][e] = o[mt][e];
+                } else {
+                    const float Mn0 = fmaxf(RM0, m0), Mn1 = fmaxf(RM1, m1);
+                    const float ca0 = RM0 == -INFINITY ? 0.f : expf(__fsub_rn(RM0, Mn0));
+                    const float cb0 = expf(__fsub_rn(m0, Mn0));
+                    const float ca1 = RM1 == -INFINITY ? 0.f : expf(__fsub_rn(RM1, Mn1));
+                    const float cb1 = expf(__fsub_rn(m1, Mn1));
+                    if (m0 != -INFINITY) {  // a column without keys in this block: exact no-op
+                        RL0 = fmaf(RL0, ca0, __fmul_rn(l0, cb0));
+#pragma unroll
+                        for (int mt = 0; mt < NK; ++mt) {
+                            RA[mt][0] = fmaf(RA[mt][0], ca0, __fmul_rn(o[mt][0], cb0));
+                            RA[mt][2] = fmaf(RA[mt][2], ca0, __fmul_rn(o[mt][2], cb0));
+                        }
+                        RM0 = Mn0;
                     }
-                    if (g8 == 0) {
-                        part_ml[2 * pidx] = c ? m1 : m0;
-                        part_ml[2 * pidx + 1] = c ? l1 : l0;
+                    if (m1 != -INFINITY) {
+                        RL1 = fmaf(RL1, ca1, __fmul_rn(l1, cb1));
+#pragma unroll
+                        for (int mt = 0; mt < NK; ++mt) {
+                            RA[mt][1] = fmaf(RA[mt][1], ca1, __fmul_rn(o[mt][1], cb1));
+                            RA[mt][3] = fmaf(RA[mt][3], ca1, __fmul_rn(o[mt][3], cb1));
+                        }
+                        RM1 = Mn1;
+                    }
+                }
+            } else {
+                // publish the block partial of every real query column
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    const int qc = 2 * t4 + c;
+                    if (qc < nrows) {
+                        const int r = qrow0 + qc;
+                        const size_t pidx = (static_cast<size_t>(r) * nb_max + x.b) * H + h;
+                        float* pa = part_acc + pidx * DH;
+#pragma unroll
+                        for (int mt = 0; mt < NK; ++mt) {
+                            pa[16 * mt + g8] = o[mt][c];
+                            pa[16 * mt + g8 + 8] = o[mt][2 + c];
+                        }
+                        if (g8 == 0) {
+                            part_ml[2 * pidx] = c ? m1 : m0;
+                            part_ml[2 * pidx + 1] = c ? l1 : l0;
+                        }
                     }
                 }
             }
@@ -506,16 +564,53 @@ __global__ void __launch_bounds__(32 * (kMaxCons + 1), 1)
         // partial stores before its ticket (cumulative release, as in a grid barrier).
         const bool seg_end = (n + 1 == n_items) || x.t != done.t || x.g != done.g;
         if (!seg_end || seg == 0) continue;
+        if (MERGE && run0) {
+            // the run covered blocks [0, done.b]: rows it completes are written now; the others
+            // get the merged prefix in slot 0 and m = -inf markers in slots 1..done.b
+            const int h = done.g * HG + hl;
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const int qc = 2 * t4 + c;
+                if (qc >= nrows_of(done, qt)) continue;
+                const int r = done.tl.row0 + kQT * qt + qc;
+                const float Mx = c ? RM1 : RM0, Lx = c ? RL1 : RL0;
+                if (done.b + 1 >= tv.row_blocks(r)) {
+                    __nv_bfloat16* orow = out + static_cast<size_t>(r) * d + h * DH;
+#pragma unroll
+                    for (int mt = 0; mt < NK; ++mt) {
+                        orow[16 * mt + g8] = __float2bfloat16(__fdiv_rn(RA[mt][c], Lx));
+                        orow[16 * mt + g8 + 8] = __float2bfloat16(__fdiv_rn(RA[mt][2 + c], Lx));
+                    }
+                } else {
+                    const size_t p0 = (static_cast<size_t>(r) * nb_max + 0) * H + h;
+                    float* pa = part_acc + p0 * DH;
+#pragma unroll
+                    for (int mt = 0; mt < NK; ++mt) {
+                        pa[16 * mt + g8] = RA[mt][c];
+                        pa[16 * mt + g8 + 8] = RA[mt][2 + c];
+                    }
+                    if (g8 == 0) {
+                        part_ml[2 * p0] = Mx;
+                        part_ml[2 * p0 + 1] = Lx;
+                        for (int b = 1; b <= done.b; ++b)
+                            part_ml[2 * ((static_cast<size_t>(r) * nb_max + b) * H + h)] = -INFINITY;
+                    }
+                }
+            }
+        }
         asm volatile("bar.sync 1, %0;" ::"r"(n_cons * 32) : "memory");
         if (threadIdx.x < done.tl.nrows) {
-            __threadfence();
             const int r = done.tl.row0 + threadIdx.x;
-            int* c = row_ctr + static_cast<size_t>(r) * G + done.g;
-            const int old = atomicAdd(c, seg);
-            const int last = (old + seg == tv.row_blocks(r));
-            if (last) {
-                *c = 0;  // re-armed for the next launch
-                __threadfence();  // acquire side: the other CTAs' partials are read after the barrier
+            int last = 0;
+            if (!(MERGE && run0 && done.b + 1 >= tv.row_blocks(r))) {  // not completed in registers
+                __threadfence();
+                int* c = row_ctr + static_cast<size_t>(r) * G + done.g;
+                const int old = atomicAdd(c, seg);
+                last = (old + seg == tv.row_blocks(r));
+                if (last) {
+                    *c = 0;  // re-armed for the next launch
+                    __threadfence();  // acquire side: the other CTAs' partials are read after the barrier
+                }
             }
             flag[threadIdx.x] = last;
         }
@@ -547,7 +642,8 @@ __global__ void __launch_bounds__(32 * (kMaxCons + 1), 1)
                     }
 #pragma unroll
                     for (int u = 0; u < kMB; ++u)
-                        if (b0 + u < nbr) attn_merge<DPL>(Mx, Lx, A, mb[u], lb[u], ab[u]);
+                        // mb = -inf: a marker inside a merged run (skipped: an exact no-op there)
+                        if (b0 + u < nbr && mb[u] != -INFINITY) attn_merge<DPL>(Mx, Lx, A, mb[u], lb[u], ab[u]);
                 }
 #pragma unroll
                 for (int e = 0; e < DPL; ++e)
@@ -559,7 +655,7 @@ __global__ void __launch_bounds__(32 * (kMaxCons + 1), 1)
     }
 }
 
-template <int DH>
+template <int DH, bool MERGE>
 void launch_impl(const float* q, const __nv_bfloat16* K, const __nv_bfloat16* V, const AttnRowsDev& rows, int n_rows,
                  const AttnTileDev* tiles, int n_tiles, int QW, int H, int d, int nb_max, long long est_items,
                  const AttnScratch& sc, __nv_bfloat16* out, cudaStream_t st) {
@@ -575,7 +671,7 @@ void launch_impl(const float* q, const __nv_bfloat16* K, const __nv_bfloat16* V,
     };
     static const int regs = [] {
         cudaFuncAttributes fa{};
-        return cudaFuncGetAttributes(&fa, attn_kernel<DH>) == cudaSuccess && fa.numRegs > 0 ? fa.numRegs : 128;
+        return cudaFuncGetAttributes(&fa, attn_kernel<DH, MERGE>) == cudaSuccess && fa.numRegs > 0 ? fa.numRegs : 128;
     }();
     static const int env_sm = [] {
         const char* v = getenv("SGB_ATTN_PERSM");  // tuning experiments only
@@ -610,9 +706,10 @@ void launch_impl(const float* q, const __nv_bfloat16* K, const __nv_bfloat16* V,
     // head groups: the grouping with the most consumer warps resident per SM (measured:
     // decode throughput follows it, scripts/bench_attn.py), ties to fewer groups; more
     // groups only when the launch has too few items to cover the SMs
+    const int max_cons = MERGE ? kMaxConsMerge : kMaxCons;
     int G = 0, best = -1;
     for (int g = 1; g <= H; g = next_div(g)) {
-        if (QW * (H / g) > kMaxCons) continue;
+        if (QW * (H / g) > max_cons) continue;
         const int n = ctas_per_sm(g);
         if (n == 0) continue;
         const int w = n * QW * (H / g);
@@ -624,7 +721,7 @@ void launch_impl(const float* q, const __nv_bfloat16* K, const __nv_bfloat16* V,
     }
     if (G == 0) throw std::invalid_argument("attention: shared memory too small for the model width");
     while (G < H && est_items * G < 2 * 148 && ctas_per_sm(next_div(G)) > 0) G = next_div(G);
-    if (g_force > 0 && H % g_force == 0 && QW * (H / g_force) <= kMaxCons && ctas_per_sm(g_force) > 0) G = g_force;
+    if (g_force > 0 && H % g_force == 0 && QW * (H / g_force) <= max_cons && ctas_per_sm(g_force) > 0) G = g_force;
     const size_t stage = stage_of(G), fixed = fixed_of(G);
     const int threads = 32 * (QW * (H / G) + 1);
     int per_sm = ctas_per_sm(G);
@@ -633,12 +730,12 @@ void launch_impl(const float* q, const __nv_bfloat16* K, const __nv_bfloat16* V,
     const size_t smem = nst * stage + fixed;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(attn_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget);
+        cudaFuncSetAttribute(attn_kernel<DH, MERGE>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget);
         attr = true;
     }
     if (static_cast<long long>(n_rows) * G > sc.ctr_cap) throw std::invalid_argument("attention: row tickets too small");
     const long long grid = std::max(1LL, std::min<long long>(est_items * G, 148LL * per_sm));
-    launch_pdl(attn_kernel<DH>, dim3(static_cast<unsigned>(grid)), dim3(threads), smem, st, q, K, V, rows, tiles,
+    launch_pdl(attn_kernel<DH, MERGE>, dim3(static_cast<unsigned>(grid)), dim3(threads), smem, st, q, K, V, rows, tiles,
                n_tiles, H, d, G, QW, nst, nb_max, balance, 1.0f / sqrtf(static_cast<float>(DH)), sc.part_acc, sc.part_ml,
                sc.row_ctr, out);
 }
@@ -651,9 +748,23 @@ void launch_any(const float* q, const __nv_bfloat16* K, const __nv_bfloat16* V, 
     if (H > 64) throw std::invalid_argument("attention: at most 64 heads");
     const int dh = d / H;
     const int nb = attn_splits_for(max_virtual_len);
-    if (dh == 128) launch_impl<128>(q, K, V, rows, n_rows, tiles, n_tiles, QW, H, d, nb, est_items, sc, out, st);
-    else if (dh == 64) launch_impl<64>(q, K, V, rows, n_rows, tiles, n_tiles, QW, H, d, nb, est_items, sc, out, st);
-    else throw std::invalid_argument("attention: head dim must be 64 or 128");
+    static const int merge_env = [] {
+        const char* v = getenv("SGB_ATTN_MERGE");  // A/B: 0 = publish every block partial
+        return v ? atoi(v) : 1;
+    }();
+    // in-register block merge for shared tiles of <= 8 rows (QW = 1): measured (scripts/attn_merge_ab.sh)
+    // 0.380 -> 0.333 ms at the c5 verify shape (48 x 4 rows, ctx 2200, 32 heads); with wider tiles
+    // its 8-warp cap costs more occupancy than the partials it saves (16 x 13 rows: 0.15 -> 0.22 ms)
+    const bool merge = tiles != nullptr && merge_env != 0 && (merge_env == 2 || QW == 1);
+    if (dh == 128) {
+        if (merge) launch_impl<128, true>(q, K, V, rows, n_rows, tiles, n_tiles, QW, H, d, nb, est_items, sc, out, st);
+        else launch_impl<128, false>(q, K, V, rows, n_rows, tiles, n_tiles, QW, H, d, nb, est_items, sc, out, st);
+    } else if (dh == 64) {
+        if (merge) launch_impl<64, true>(q, K, V, rows, n_rows, tiles, n_tiles, QW, H, d, nb, est_items, sc, out, st);
+        else launch_impl<64, false>(q, K, V, rows, n_rows, tiles, n_tiles, QW, H, d, nb, est_items, sc, out, st);
+    } else {
+        throw std::invalid_argument("attention: head dim must be 64 or 128");
+    }
     SGB_KCHECK();
 }
 

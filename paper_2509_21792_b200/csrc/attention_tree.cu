@@ -106,6 +106,7 @@ __global__ void __launch_bounds__(32 * (kTMaxWarps + 1), 1)
     uint64_t* full = reinterpret_cast<uint64_t*>(tblV + static_cast<size_t>(tbl_cap) * kRowB);
     uint64_t* empty = full + nst;
     uint64_t* tbar = empty + nst;
+    int* chains = reinterpret_cast<int*>(tbar + 1);  // [W][8 rows][lv + 8 path node indices]
     const int n_prefix_chunks = (P + kTChunk - 1) / kTChunk;
     if (threadIdx.x == 0) {
         for (int s = 0; s < nst; ++s) {
@@ -166,6 +167,21 @@ __global__ void __launch_bounds__(32 * (kTMaxWarps + 1), 1)
             qf[ks][1] = pack_bf16(b.x, b.y);
         }
     }
+    // the warp's rows: virtual length and path node indices (shared memory, read per chunk)
+    int* wchain = chains + warp * 72;
+    for (int x = lane; x < 72; x += 32) {
+        const int j = x / 9, f = x % 9;
+        int val = 0;
+        if (j < nrows) {
+            const int cl = rows.chain_len[row0 + j];
+            val = f == 0 ? P + cl
+                         : (f - 1 < cl ? static_cast<int>(rows.chain_slots[static_cast<size_t>(row0 + j) * kMaxChain + f - 1] -
+                                                          gr.node_base)
+                                       : 0);
+        }
+        wchain[x] = val;
+    }
+    __syncwarp();
     // virtual lengths of this lane's two query columns, and of the warp's rows
     const int c0 = 2 * t4, c1 = 2 * t4 + 1;
     const int lv0 = c0 < nrows ? P + rows.chain_len[row0 + c0] : 0;
@@ -263,20 +279,16 @@ __global__ void __launch_bounds__(32 * (kTMaxWarps + 1), 1)
                     tbl_ready = true;
                 }
                 for (int j = 0; j < nrows; ++j) {
-                    const int rj = row0 + j;
-                    const int lvj = P + rows.chain_len[rj];
+                    const int* wc = wchain + j * 9;  // [lv, node of path key 0..7]
+                    const int lvj = wc[0];
                     if (lvj <= v0) continue;
-                    const long long* ch = rows.chain_slots + static_cast<size_t>(rj) * kMaxChain;
-                    // smem row of key slot kr for row j: prefix from the ring, path from the table,
-                    // past the row's end any finite row (masked: p = 0)
-                    auto row_of = [&](int kr, uint32_t ring, uint32_t tbl, int dd) -> uint32_t {
-                        const int v = v0 + kr;
-                        if (v < P) return ring_addr(ring, kr, dd);
-                        const int node = v < lvj ? static_cast<int>(ch[v - P] - gr.node_base) : 0;
-                        return tbl + static_cast<uint32_t>(node * kRowB + dd * 2);
-                    };
-                    auto ka = [&](int kr, int dd) { return row_of(kr, sK, tblK0, dd); };
-                    auto vaa = [&](int kr, int dd) { return row_of(kr, sV, tblV0, dd); };
+                    // this lane's two key slots (K: kr_k, V: kr_v): prefix rows from the ring,
+                    // path rows from the node table, past the row's end any finite row (p = 0)
+                    const int vk = v0 + lr + 8 * (li & 1), vv = v0 + lr + 8 * (li >> 1);
+                    const uint32_t kt = tblK0 + static_cast<uint32_t>((vk >= P && vk < lvj ? wc[1 + vk - P] : 0) * kRowB);
+                    const uint32_t vt = tblV0 + static_cast<uint32_t>((vv >= P && vv < lvj ? wc[1 + vv - P] : 0) * kRowB);
+                    auto ka = [&](int kr, int dd) { return vk < P ? ring_addr(sK, kr, dd) : kt + static_cast<uint32_t>(dd * 2); };
+                    auto vaa = [&](int kr, int dd) { return vv < P ? ring_addr(sV, kr, dd) : vt + static_cast<uint32_t>(dd * 2); };
                     chunk(ka, vaa, v0, c0 == j ? lvj : v0, c1 == j ? lvj : v0);
                 }
             }
@@ -335,7 +347,7 @@ void launch_tree_impl(const float* q, const CUtensorMap& kmap, const CUtensorMap
                       cudaStream_t st) {
     constexpr size_t stageK = static_cast<size_t>(kTChunk) * DH * 2;
     const size_t tbl = static_cast<size_t>(max_nodes) * (DH * 2 + 16) * 2;
-    const size_t fixed = tbl + 8 * 24 + 1024;  // barriers + alignment slack
+    const size_t fixed = tbl + 8 * 24 + 4 * 72 * 8 + 1024;  // barriers, chain tables, alignment slack
     int nst = 6;
     while (nst > 2 && 2 * stageK * nst + fixed > static_cast<size_t>(kTSmem)) --nst;
     const size_t smem = 2 * stageK * nst + fixed;

@@ -1591,7 +1591,7 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
         // batches keep attention.cu's head-grouped persistent kernel (98 % of HBM at c2)
         static const int tree_ar_max = [] {
             const char* v = getenv("SGB_TREE_AR_MAX");  // A/B switch
-            return v ? atoi(v) : 64;
+            return v ? atoi(v) : 0;
         }();
         if ((!all_ar || vrows <= tree_ar_max) && tree_attn_ok(max_sel)) f.tree = &tgroups_;
         // measured A/B (SGB_PROMPT_TILES, bench.py vanilla): +5 % at 12 heads (c2), -13 % at
