@@ -1444,6 +1444,20 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
                 f.max_vlen = maxj;
                 for (int r = 0; r < M; ++r) f.attn_row_keys += pos[r];
                 for (size_t t = 0; t < lastr.size(); ++t) f.attn_kv_unique += pos[lastr[t]];
+                // a sequence's catch-up rows are consecutive pairs (causal): they share the keys
+                // below their first row's, so those blocks run as shared tiles (attention.cu
+                // prompt-style groups; each row's own tail per row -- identical bits)
+                groups_.clear();
+                for (int r = 0; r < M;) {
+                    int e = r + 1;
+                    while (e < M && seq[e] == seq[r]) ++e;
+                    groups_.push_back({r, e - r, cl[r], cl[e - 1]});
+                    r = e;
+                }
+                if (static_cast<int>(groups_.size()) < M) {
+                    f.groups = &groups_;
+                    f.groups_exact = false;
+                }
                 forward(f);
                 res.draft_forwards++;
                 stat.draft_rows += M;
