@@ -314,7 +314,7 @@ __global__ void __launch_bounds__(32 * ((MERGE ? kMaxConsMerge : kMaxCons) + 1),
     if (warp == n_cons) {
         // ---------------- producer warp: one bulk DMA per staged K / V key row
         ItemIt x = it0;
-        int i = 0;
+        int i = 0, si = 0, ph = 0;  // staged chunk counter, ring stage, phase
         const uint32_t row_bytes = static_cast<uint32_t>(HG) * DH * 2;
         int cur_r = -1, ctx_len = 0, pre_len = 0;
         long long ctx_base = 0, pre_base = 0;
@@ -334,8 +334,8 @@ __global__ void __launch_bounds__(32 * ((MERGE ? kMaxConsMerge : kMaxCons) + 1),
             // one stage: keys [v0, v0 + nk) of a row with the given key map
             auto stage = [&](int v0, int nk, int c_len, long long c_base, int p_len, long long p_base,
                              const long long* ch) {
-                const int s = i % nst;
-                if (i >= nst) mbar_wait(&empty[s], ((i / nst) & 1) ^ 1);
+                const int s = si;
+                if (i >= nst) mbar_wait(&empty[s], ph ^ 1);
                 if (lane == 0) mbar_arrive_expect_tx(&full[s], 2u * row_bytes * nk);
                 __syncwarp();
                 if (lane < nk) {
@@ -348,6 +348,10 @@ __global__ void __launch_bounds__(32 * ((MERGE ? kMaxConsMerge : kMaxCons) + 1),
                              row_bytes, &full[s]);
                 }
                 ++i;
+                if (++si == nst) {
+                    si = 0;
+                    ph ^= 1;
+                }
             };
             for (int v0 = x.b * kBlock; v0 < ve; v0 += kChunk) {
                 if (!per_row_chunk(x, v0)) {
@@ -378,7 +382,7 @@ __global__ void __launch_bounds__(32 * ((MERGE ? kMaxConsMerge : kMaxCons) + 1),
     const uint32_t ks_base = smem_u32(Ks), vs_base = smem_u32(Vs);
     uint32_t qf[NK][2];
     ItemIt x = it0;
-    int i = 0;
+    int i = 0, si = 0, ph = 0;  // staged chunk counter, ring stage, phase
     int cur_t = -1, cur_g = -1, seg = 0;
     // MERGE: running merged state of this warp's two columns over the current run
     bool run0 = false;
@@ -418,8 +422,8 @@ __global__ void __launch_bounds__(32 * ((MERGE ? kMaxConsMerge : kMaxCons) + 1),
             for (int mt = 0; mt < NK; ++mt) o[mt][0] = o[mt][1] = o[mt][2] = o[mt][3] = 0.f;
             // one staged chunk; e0 / e1 = key end of this lane's query columns 2t4 / 2t4+1
             auto chunk = [&](int v0, int e0, int e1) {
-                const int s = i % nst;
-                mbar_wait(&full[s], (i / nst) & 1);
+                const int s = si;
+                mbar_wait(&full[s], ph);
                 const uint32_t kst = ks_base + static_cast<uint32_t>(s * stage_bytes);
                 const uint32_t vst = vs_base + static_cast<uint32_t>(s * stage_bytes);
                 // S^T = K . Q^T
@@ -472,6 +476,10 @@ __global__ void __launch_bounds__(32 * ((MERGE ? kMaxConsMerge : kMaxCons) + 1),
                     mma16816(o[mt], va4[mt], b0, b1);
                 }
                 ++i;
+                if (++si == nst) {
+                    si = 0;
+                    ph ^= 1;
+                }
             };
             for (int v0 = kb; v0 < ve; v0 += kChunk) {
                 if (!per_row_chunk(x, v0)) {
@@ -485,11 +493,15 @@ __global__ void __launch_bounds__(32 * ((MERGE ? kMaxConsMerge : kMaxCons) + 1),
                 for (int j = 0; j < x.tl.nrows; ++j) {
                     const int cj = j - kQT * qt;
                     if (cj < 0 || cj >= kQT) {
-                        const int s = i % nst;
-                        mbar_wait(&full[s], (i / nst) & 1);
+                        const int s = si;
+                        mbar_wait(&full[s], ph);
                         __syncwarp();
                         if (lane == 0) mbar_arrive(&empty[s]);
                         ++i;
+                        if (++si == nst) {
+                            si = 0;
+                            ph ^= 1;
+                        }
                         continue;
                     }
                     const int rj = x.tl.row0 + j;

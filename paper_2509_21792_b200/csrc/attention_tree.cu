@@ -132,9 +132,9 @@ __global__ void __launch_bounds__(32 * (kTMaxWarps + 1), 1)
             bulk_g2s(tblV + static_cast<size_t>(i) * kRowB, V + src, rowbytes, tbar);
         }
         if (lane == 0) {
-            for (int c = 0; c < n_prefix_chunks; ++c) {
-                const int s = c % nst;
-                if (c >= nst) mbar_wait(&empty[s], ((c / nst) & 1) ^ 1);
+            int s = 0, ph = 0;  // ring stage and its phase (no integer division in the loop)
+            for (int c = 0; c < n_prefix_chunks; ++c, s = s + 1 == nst ? 0 : s + 1, ph ^= s == 0) {
+                if (c >= nst) mbar_wait(&empty[s], ph ^ 1);
                 const int v0 = c * kTChunk;
                 // the shared prompt copy (identical values) while the whole box lies in it
                 const long long slot0 = (v0 + kTChunk <= gr.pre_len ? gr.pre_base : gr.ctx_base) + v0;
@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(32 * (kTMaxWarps + 1), 1)
 #pragma unroll
     for (int mt = 0; mt < NK; ++mt) A[mt][0] = A[mt][1] = A[mt][2] = A[mt][3] = 0.f;
     bool tbl_ready = false;
-    int i = 0;  // staged chunk counter
+    int i = 0, si = 0, ph = 0;  // staged chunk counter, its ring stage and phase
     const int nb = (lvmax + kTBlock - 1) / kTBlock;
     const int nbp = (P + kTBlock - 1) / kTBlock;  // blocks holding prefix keys: every warp runs them
     for (int b = 0; b < max(nb, nbp); ++b) {
@@ -262,8 +262,8 @@ __global__ void __launch_bounds__(32 * (kTMaxWarps + 1), 1)
             uint32_t sK = 0, sV = 0;
             int s = 0;
             if (staged) {
-                s = i % nst;
-                mbar_wait(&full[s], (i / nst) & 1);
+                s = si;
+                mbar_wait(&full[s], ph);
                 sK = ringK0 + static_cast<uint32_t>(s) * kStageK;
                 sV = ringV0 + static_cast<uint32_t>(s) * kStageK;
             }
@@ -296,6 +296,10 @@ __global__ void __launch_bounds__(32 * (kTMaxWarps + 1), 1)
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[s]);
                 ++i;
+                if (++si == nst) {
+                    si = 0;
+                    ph ^= 1;
+                }
             }
         }
         // ordered merge of this block's partial (rows whose keys reach into block b)
@@ -363,16 +367,27 @@ void launch_tree_impl(const float* q, const CUtensorMap& kmap, const CUtensorMap
 
 }  // namespace
 
-int tree_attn_warps(int max_rows_per_group, int n_groups, int H) {
-    // 8 query rows per warp; fewer warps per tile when that is what it takes to cover the SMs
-    int w = std::max(1, std::min(kTMaxWarps, (max_rows_per_group + 7) / 8));
-    while (w > 1) {
+int tree_attn_warps(int max_rows_per_group, int n_groups, int H, int dh, int max_nodes) {
+    // widest tiles (the prefix streams once per tile) unless narrower ones finish in fewer waves
+    // (CTAs resident per SM are bounded by the node table + ring in shared memory)
+    const size_t tbl = static_cast<size_t>(max_nodes) * (dh * 2 + 16) * 2;
+    const size_t per_cta = tbl + 4 * static_cast<size_t>(kTChunk) * dh * 2 * 2 + 4096;
+    const int occ_smem = std::max<int>(1, static_cast<int>(kTSmem / per_cta));
+    int best_w = 1;
+    long long best_waves = -1;
+    for (int w = std::max(1, std::min(kTMaxWarps, (max_rows_per_group + 7) / 8)); w >= 1; w = (w + 1) / 2 - (w == 1)) {
         const int rows_per_tile = 8 * w;
-        const long long ctas = static_cast<long long>(n_groups) * ((max_rows_per_group + rows_per_tile - 1) / rows_per_tile) * H;
-        if (ctas >= 148) break;
-        w = (w + 1) / 2;
+        const long long ctas =
+            static_cast<long long>(n_groups) * ((max_rows_per_group + rows_per_tile - 1) / rows_per_tile) * H;
+        const int occ = std::max(1, std::min(occ_smem, 2048 / (32 * (w + 1))));
+        const long long waves = (ctas + 148LL * occ - 1) / (148LL * occ);
+        if (best_waves < 0 || waves < best_waves) {
+            best_waves = waves;
+            best_w = w;
+        }
+        if (w == 1) break;
     }
-    return w;
+    return best_w;
 }
 
 void build_tree_tiles(const std::vector<TreeGroupDev>& groups, int W, std::vector<TreeTileDev>& out) {

@@ -1024,7 +1024,7 @@ struct TreeAttnCase {
                 cb += ctx_len[g];
                 r += n_rows[g];
             }
-            tw = sgb::tree_attn_warps(mx, n_groups, H);
+            tw = sgb::tree_attn_warps(mx, n_groups, H, dh, max_nodes);
             std::vector<sgb::TreeTileDev> tt;
             sgb::build_tree_tiles(tg, tw, tt);
             n_ttiles = static_cast<int>(tt.size());

@@ -658,7 +658,7 @@ void Engine::forward(const Fwd& f) {
             mx = std::max(mx, g.nrows);
             tree_nodes = std::max(tree_nodes, g.n_nodes);
         }
-        tree_w = tree_attn_warps(mx, static_cast<int>(f.tree->size()), dims_.heads);
+        tree_w = tree_attn_warps(mx, static_cast<int>(f.tree->size()), dims_.heads, d / H, tree_nodes);
         build_tree_tiles(*f.tree, tree_w, ttiles_);
         n_ttiles = static_cast<int>(ttiles_.size());
         if (f.tree->size() > static_cast<size_t>(max_seqs_ + max_rows_) ||

@@ -93,7 +93,7 @@ struct TreeGroupDev {
 struct TreeTileDev {
     int group, r0, nr;
 };
-int tree_attn_warps(int max_rows_per_group, int n_groups, int H);
+int tree_attn_warps(int max_rows_per_group, int n_groups, int H, int dh, int max_nodes);
 void build_tree_tiles(const std::vector<TreeGroupDev>& groups, int W, std::vector<TreeTileDev>& out);
 // kmap / vmap: 2-D TMA maps over the store viewed as [layers * n_slots][d] (16 x 64 boxes,
 // SWIZZLE_128B); layer_row0 = layer * n_slots; K / V: this layer's [n_slots][d] base
