@@ -754,7 +754,7 @@ void launch_impl(const float* q, const __nv_bfloat16* K, const __nv_bfloat16* V,
 
 void launch_any(const float* q, const __nv_bfloat16* K, const __nv_bfloat16* V, const AttnRowsDev& rows, int n_rows,
                 const AttnTileDev* tiles, int n_tiles, int QW, int H, int d, int max_virtual_len, long long est_items,
-                const AttnScratch& sc, __nv_bfloat16* out, cudaStream_t st) {
+                const AttnScratch& sc, __nv_bfloat16* out, cudaStream_t st, bool merge_ok = false) {
     if (n_tiles <= 0) return;
     if (n_tiles > kMaxScanTiles) throw std::invalid_argument("attention: too many tiles in one launch");
     if (H > 64) throw std::invalid_argument("attention: at most 64 heads");
@@ -767,7 +767,7 @@ void launch_any(const float* q, const __nv_bfloat16* K, const __nv_bfloat16* V, 
     // in-register block merge for shared tiles of <= 8 rows (QW = 1): measured (scripts/attn_merge_ab.sh)
     // 0.380 -> 0.333 ms at the c5 verify shape (48 x 4 rows, ctx 2200, 32 heads); with wider tiles
     // its 8-warp cap costs more occupancy than the partials it saves (16 x 13 rows: 0.15 -> 0.22 ms)
-    const bool merge = tiles != nullptr && merge_env != 0 && (merge_env == 2 || QW == 1);
+    const bool merge = tiles != nullptr && merge_ok && merge_env != 0 && (merge_env == 2 || QW == 1);
     if (dh == 128) {
         if (merge) launch_impl<128, true>(q, K, V, rows, n_rows, tiles, n_tiles, QW, H, d, nb, est_items, sc, out, st);
         else launch_impl<128, false>(q, K, V, rows, n_rows, tiles, n_tiles, QW, H, d, nb, est_items, sc, out, st);
@@ -845,9 +845,9 @@ void launch_attention(const float* q, const __nv_bfloat16* K, const __nv_bfloat1
 void launch_attention_tiles(const float* q, const __nv_bfloat16* K, const __nv_bfloat16* V, long long /*kv_slots*/,
                             const AttnRowsDev& rows, int M, const AttnTileDev* tiles, int n_tiles, long long n_items,
                             int qw, int H, int d, int max_virtual_len, const AttnScratch& sc, __nv_bfloat16* out,
-                            cudaStream_t st) {
+                            cudaStream_t st, bool merge) {
     if (M <= 0) return;
-    launch_any(q, K, V, rows, M, tiles, n_tiles, qw, H, d, max_virtual_len, n_items, sc, out, st);
+    launch_any(q, K, V, rows, M, tiles, n_tiles, qw, H, d, max_virtual_len, n_items, sc, out, st, merge);
 }
 
 }  // namespace sgb

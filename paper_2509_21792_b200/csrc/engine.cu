@@ -698,7 +698,7 @@ void Engine::forward(const Fwd& f) {
                                   tree_w, H, d, tree_nodes, att_, st_);
         else if (n_tiles)
             launch_attention_tiles(q_, eq.K, eq.V, kv.n_slots, ar, M, tiles_, n_tiles, n_items, qw, H, d, f.max_vlen,
-                                   asc_, att_, st_);
+                                   asc_, att_, st_, f.merge_tiles);
         else
             launch_attention(q_, eq.K, eq.V, kv.n_slots, ar, M, H, d, f.max_vlen, f.attn_row_keys, asc_, att_, st_);
         pend(kClsAttn, e0, attn_bytes, attn_flops);
@@ -1457,6 +1457,7 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
                 if (static_cast<int>(groups_.size()) < M) {
                     f.groups = &groups_;
                     f.groups_exact = false;
+                    f.merge_tiles = true;
                 }
                 forward(f);
                 res.draft_forwards++;
@@ -1539,6 +1540,7 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
                         }
                     f.groups = &groups_;
                     f.groups_exact = boundary_tiles();
+                    f.merge_tiles = true;
                     if (tree_attn_ok(tr_.ds)) f.tree = &tgroups_;
                     forward(f);
                     res.draft_forwards++;
@@ -1608,6 +1610,7 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
             return v ? atoi(v) : 0;
         }();
         if ((!all_ar || vrows <= tree_ar_max) && tree_attn_ok(max_sel)) f.tree = &tgroups_;
+        f.merge_tiles = !all_ar;  // verify tiles of a speculative step (not the AR prompt tiles)
         // measured A/B (SGB_PROMPT_TILES, bench.py vanilla): +5 % at 12 heads (c2), -13 % at
         // 28 heads (c3, where the per-row kernel already hits the prompt pages in L2)
         static const int prompt_tiles = [] {

@@ -233,6 +233,8 @@ class Engine {
         bool groups_exact = false;
         // tree-verify / draft-level groups for attention_tree.cu (nullptr: attention.cu)
         const std::vector<TreeGroupDev>* tree = nullptr;
+        // attention.cu shared tiles may merge block partials in registers (not the AR prompt tiles)
+        bool merge_tiles = false;
     };
     void forward(const Fwd& f);
     bool boundary_tiles() const;

@@ -71,10 +71,12 @@ int attn_tile_qw(const std::vector<std::array<int, 4>>& groups);
 // levels), so shared tiles also take the block holding the end of the prefix (bsh)
 long long build_attn_tiles(const std::vector<std::array<int, 4>>& groups, std::vector<AttnTileDev>& out, int qw,
                            bool boundary = false);
+// merge: allow the in-register block merge (few-row tiles over long prefixes: tree verify,
+// draft levels, catch-up rows); the AR prompt tiles keep the 16-warp kernel
 void launch_attention_tiles(const float* q, const __nv_bfloat16* K, const __nv_bfloat16* V, long long kv_slots,
                             const AttnRowsDev& rows, int M, const AttnTileDev* tiles, int n_tiles, long long n_items,
                             int qw, int H, int d, int max_virtual_len, const AttnScratch& sc, __nv_bfloat16* out,
-                            cudaStream_t st);
+                            cudaStream_t st, bool merge = true);
 // total_keys: sum over rows of keys attended (host estimate; only sizes the launch)
 // K/V: one layer of a [kv_slots][d] bf16 store
 void launch_attention(const float* q, const __nv_bfloat16* K, const __nv_bfloat16* V, long long kv_slots,
