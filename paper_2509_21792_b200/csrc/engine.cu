@@ -1541,7 +1541,7 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
                     f.groups = &groups_;
                     f.groups_exact = boundary_tiles();
                     f.merge_tiles = true;
-                    if (tree_attn_ok(tr_.ds)) f.tree = &tgroups_;
+                    if (kstep > 8 && tree_attn_ok(tr_.ds)) f.tree = &tgroups_;
                     forward(f);
                     res.draft_forwards++;
                     stat.draft_rows += R;
@@ -1609,7 +1609,10 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
             const char* v = getenv("SGB_TREE_AR_MAX");  // A/B switch
             return v ? atoi(v) : 0;
         }();
-        if ((!all_ar || vrows <= tree_ar_max) && tree_attn_ok(max_sel)) f.tree = &tgroups_;
+        // measured (scripts/attn_check.sh, profiles/r02_attn_knobs2.jsonl): attention_tree.cu wins with
+        // > 8 rows per sequence (B=1 x 211 rows: 0.057 vs 0.083 ms per layer; 16 x 13: 0.135 vs 0.166),
+        // attention.cu's merged shared tiles with fewer (48 x 4 rows over 2.2k keys: 0.324 vs 0.391)
+        if (((!all_ar && max_sel > 8) || (all_ar && vrows <= tree_ar_max)) && tree_attn_ok(max_sel)) f.tree = &tgroups_;
         f.merge_tiles = !all_ar;  // verify tiles of a speculative step (not the AR prompt tiles)
         // measured A/B (SGB_PROMPT_TILES, bench.py vanilla): +5 % at 12 heads (c2), -13 % at
         // 28 heads (c3, where the per-row kernel already hits the prompt pages in L2)
