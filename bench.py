@@ -43,6 +43,12 @@ WORKLOADS = {
                desc="Qwen2.5-7B-shaped target + 1-layer draft, 16 queries x group 8 per GPU (c3's 128 x 8 over 8 "
                     "GPUs), 128-token prompts, variable-length stops 256..1024 new tokens (concurrency sweep "
                     "128 -> 1 per GPU), greedy, adaptive spec, draft warmed online"),
+    # c3 sampled at T=1 (the reference TrainConfig default rollout temperature, grpo.hpp:142) with
+    # rejection-sampling acceptance: the same shard, stops and warm-up stream as c3
+    "c3r": dict(V=152064, d=3584, L=28, H=28, dff=18944, P=128, G=8, Q=16, new=1024, stops=True, online=False,
+                warm=24, temp=1.0, acceptance="rejection",
+                desc="Qwen2.5-7B-shaped target + 1-layer draft, 16 queries x group 8 per GPU, variable-length stops "
+                     "256..1024, T=1.0 rejection-sampling verify (GRPO's sampled rollouts), draft warmed online at T=1"),
     # c4: the c3 shard + the online draft-learning step (NCCL gradient all-reduce) in every step
     "c4": dict(V=152064, d=3584, L=28, H=28, dff=18944, P=128, G=8, Q=16, new=1024, stops=True, online=True, warm=24,
                desc="Qwen2.5-7B-shaped GRPO rollout, data-parallel by query group, 16 queries x group 8 per GPU, "
