@@ -565,6 +565,9 @@ int gemm_bn_for(int M) {
         const char* v = getenv("SGB_GEMM_MAXBN");  // tuning experiments only
         return v ? atoi(v) : 256;
     }();
+    // 257..384 rows: three 128-token tiles beat two 256-token ones (M = 384 at the c5 QKV shape:
+    // 45.6 vs 57.3 us, profiles/r02_gemm_c5_ab.jsonl); 129..256 rows keep one 256-token tile
+    if (M > 256 && M <= 384) return 128;
     return max_bn >= 256 ? 256 : 128;
 }
 
