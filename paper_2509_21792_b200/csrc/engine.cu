@@ -322,7 +322,7 @@ Engine::~Engine() {
     if (adv_buf_) cudaFree(adv_buf_);
     for (void* q : pol_ptrs_) cudaFree(q);
     if (tmaster_) cudaFree(tmaster_);
-    for (void* q : {static_cast<void*>(qbuf_), static_cast<void*>(qstat_), static_cast<void*>(resid_),
+    for (void* q : {static_cast<void*>(qbuf_), static_cast<void*>(qstat_), 
                     static_cast<void*>(rkeys_), static_cast<void*>(tr_.qrow)})
         if (q) cudaFree(q);
     void* ptrs[] = {tw_, dw_, tsmall_, dmaster_, tkv_.K, tkv_.V, dkv_.K, dkv_.V, ss_.tokens, ss_.len, ss_.finished,
@@ -1103,7 +1103,6 @@ void Engine::reject_alloc() {
     const size_t R = max_rows_, V = dims_.vocab, S = max_seqs_;
     qbuf_ = dalloc<float>(R * V);
     qstat_ = dalloc<double>(2 * R);
-    resid_ = dalloc<float>(S * V);
     rkeys_ = dalloc<unsigned long long>(R);
     tr_.qrow = dalloc<int>(S * static_cast<size_t>(tr_.tmax));
 }
@@ -1648,7 +1647,7 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
         pe0 = pbeg();
         if (rej && n_spec > 0)
             launch_walk_reject(B, steps_, ss_, tr_, rows_, emitted_, logits_, rsc_.rowmax, qbuf_, qstat_, V,
-                               a.temperature, resid_, acc_rows_, result_, st_);
+                               a.temperature, nullptr, acc_rows_, result_, st_);
         else
             launch_walk_commit(B, steps_, ss_, tr_, rows_, emitted_, acc_rows_, result_, st_);
         pend(kClsTree, pe0, 0, 0);

@@ -362,7 +362,6 @@ class Engine {
     // node of a step [max_rows][V], their (max, sum) stats, per-sequence residuals, child keys
     float* qbuf_ = nullptr;
     double* qstat_ = nullptr;
-    float* resid_ = nullptr;
     unsigned long long* rkeys_ = nullptr;
     void reject_alloc();
     void train_alloc();

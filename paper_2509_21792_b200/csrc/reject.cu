@@ -28,9 +28,13 @@
 // without speculation are bit-identical to the strict-match mode.
 #include <cfloat>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "util.h"
+
+namespace cg = cooperative_groups;
 
 namespace sgb {
 
@@ -127,44 +131,128 @@ SGB_DEV RowStat row_stat(const float* L, int V, double temperature, float* redf,
     return RowStat{m, block_sum(s, redd)};
 }
 
-// ---- one node of the multi-round walk. p: the target row, q: the draft row (stats given),
-// cand: the node's verified children tokens (n). resid: [V] scratch. Returns the index of the
-// accepted candidate, or -1 with *bonus = the residual draw.
-SGB_DEV int mss_node(const float* P, RowStat ps, const float* Q, RowStat qs, const int* cand, int n, int V,
-                     double temperature, uint64_t key, float* resid, double* pre, float* redf, double* redd,
-                     int* sh_tok, int* bonus) {
-    bool materialised = false;  // resid holds norm-free residual weights once a candidate is rejected
-    double zr = ps.z;           // residual total (unnormalised weights)
+// ---- cluster form of the walk (thread-block clusters of kCL CTAs per sequence, DSMEM reductions)
+//
+// A node's passes are full-vocabulary sweeps; one CTA per sequence streams them through one SM
+// (a 152k-logit row pair at ~150 GB/s per SM), so at low concurrency the walk took ~1.5 ms per
+// step. Here a cluster of kCL CTAs splits the vocabulary, and every sum is a cluster reduction
+// over distributed shared memory (fixed rank order: all CTAs get the same bits and take the same
+// decisions). The residual needs no buffer: after j rejections at a node it is
+// max(p - c_j q, 0) / W(c_j) with c_0 = 0, c_{j+1} = c_j + W(c_j), W(c) = sum max(p - c q, 0) --
+// the same distribution as norm(max(r - q, 0)) applied j times, recomputed on the fly.
+constexpr int kCL = 8;
+
+SGB_DEV double cluster_sum(cg::cluster_group& cl, double v_block, double* xch) {
+    if (threadIdx.x == 0) *xch = v_block;
+    cl.sync();
+    double s = 0.0;
+    for (int r = 0; r < kCL; ++r) s += *cl.map_shared_rank(xch, r);
+    cl.sync();
+    return s;
+}
+
+struct Slice {
+    int lo, hi;
+};
+SGB_DEV Slice vocab_slice(int V, int rank) {
+    const int per = (V + kCL - 1) / kCL;
+    const int lo = min(V, rank * per);
+    return Slice{lo, min(V, lo + per)};
+}
+
+// inverse-CDF draw over the vocabulary in index order from weights w(i), u01 in [0, 1): slice
+// totals -> cluster prefix -> the owner CTA walks its slice; the token is broadcast via DSMEM.
+// xch / xtok: this CTA's exchange slots (shared memory).
+template <class W>
+SGB_DEV int cluster_draw(cg::cluster_group& cl, W w, Slice sl, double u01, double* pre, double* xch, int* xtok) {
+    const int T = blockDim.x, t = threadIdx.x;
+    const int n = sl.hi - sl.lo;
+    const int seg = (n + T - 1) / T;
+    const int lo = sl.lo + min(n, t * seg), hi = min(sl.hi, lo + seg);
+    double s = 0.0;
+    for (int i = lo; i < hi; ++i) s += w(i);
+    pre[t + 1] = s;
+    __syncthreads();
+    if (t == 0) {
+        pre[0] = 0.0;
+        for (int j = 1; j <= T; ++j) pre[j] += pre[j - 1];
+        *xch = pre[T];
+        *xtok = -1;
+    }
+    cl.sync();
+    const int me = static_cast<int>(cl.block_rank());
+    double before = 0.0, total = 0.0;
+    for (int r = 0; r < kCL; ++r) {
+        const double x = *cl.map_shared_rank(xch, r);
+        if (r < me) before += x;
+        total += x;
+    }
+    const double ul = u01 * total - before;  // u relative to this slice
+    if (0.0 <= ul && ul < pre[T] && pre[t] <= ul && ul < pre[t + 1]) {
+        double acc = pre[t];
+        int tok = hi - 1;
+        for (int i = lo; i < hi; ++i) {
+            acc += w(i);
+            if (ul < acc) {
+                tok = i;
+                break;
+            }
+        }
+        for (int r = 0; r < kCL; ++r) *cl.map_shared_rank(xtok, r) = tok;
+    }
+    cl.sync();
+    int tok = *xtok;
+    if (tok < 0) {
+        // u at the very top after rounding (no owner): the last token with weight -- the last
+        // slice with mass takes its last positive index (rare; a serial scan of one slice)
+        int last_rank = -1;
+        for (int r = 0; r < kCL; ++r)
+            if (*cl.map_shared_rank(xch, r) > 0.0) last_rank = r;
+        if (me == (last_rank < 0 ? kCL - 1 : last_rank) && t == 0) {
+            int i = sl.hi - 1;
+            while (i > sl.lo && !(w(i) > 0.0)) --i;
+            for (int r = 0; r < kCL; ++r) *cl.map_shared_rank(xtok, r) = max(i, 0);
+        }
+        cl.sync();
+        tok = *xtok;
+    }
+    cl.sync();  // xch / xtok are reused by the next exchange
+    return tok;
+}
+
+// One node of the multi-round walk on a cluster. P / Q: target / draft logit rows; cand[n]: the
+// node's verified children (a prefix of its i.i.d. samples). Returns the accepted candidate's
+// index, or -1 with *bonus drawn from the final residual.
+SGB_DEV int mss_node_cluster(cg::cluster_group& cl, const float* P, double pm, const float* Q, RowStat qs,
+                             const int* cand, int n, int V, double temperature, uint64_t key, double* pre, double* redd,
+                             double* xch, int* xtok, int* bonus) {
+    const Slice sl = vocab_slice(V, static_cast<int>(cl.block_rank()));
+    double zs = 0.0;
+    for (int i = sl.lo + threadIdx.x; i < sl.hi; i += blockDim.x) zs += term(P[i], pm, temperature);
+    const double zp = cluster_sum(cl, block_sum(zs, redd), xch);
+    auto pn = [&](int i) { return term(P[i], pm, temperature) / zp; };
+    auto qn = [&](int i) { return term(Q[i], qs.m, temperature) / qs.z; };
+    double c = 0.0, wc = 1.0;  // residual max(p - c q, 0) / wc
     for (int j = 0; j < n; ++j) {
         const int x = cand[j];
-        const double qx = term(Q[x], qs.m, temperature) / qs.z;
-        const double rx = (materialised ? static_cast<double>(resid[x]) : term(P[x], ps.m, temperature)) / zr;
+        const double qx = qn(x);
+        const double rx = fmax(pn(x) - c * qx, 0.0) / wc;
         const double u = rng_first_uniform(mix_key(key, 0xACC0u + j));
         if (u * qx < rx) return j;  // accept with probability min(1, r(x) / q(x))
-        // r <- max(r / zr - q, 0) (unnormalised: the new total is recomputed)
-        double s = 0.0;
-        for (int i = threadIdx.x; i < V; i += blockDim.x) {
-            const double ri = (materialised ? static_cast<double>(resid[i]) : term(P[i], ps.m, temperature)) / zr;
-            const double qi = term(Q[i], qs.m, temperature) / qs.z;
-            const float ni = static_cast<float>(fmax(ri - qi, 0.0));
-            resid[i] = ni;
-            s += ni;
-        }
-        __syncthreads();
-        materialised = true;
-        zr = block_sum(s, redd);
-        if (!(zr > 0.0)) {  // p == q on the support (floating-point residue): fall back to p
-            for (int i = threadIdx.x; i < V; i += blockDim.x) resid[i] = static_cast<float>(term(P[i], ps.m, temperature));
-            __syncthreads();
-            zr = ps.z;
+        c += wc;
+        double ws = 0.0;
+        for (int i = sl.lo + threadIdx.x; i < sl.hi; i += blockDim.x) ws += fmax(pn(i) - c * qn(i), 0.0);
+        wc = cluster_sum(cl, block_sum(ws, redd), xch);
+        if (!(wc > 0.0)) {  // p == c q on the support (floating-point residue): back to p
+            c = 0.0;
+            wc = 1.0;
         }
     }
     const double ub = rng_first_uniform(mix_key(key, 0xB0B0u));
-    if (materialised) {
-        *bonus = block_draw([&](int i) { return static_cast<double>(resid[i]); }, V, ub, pre, sh_tok);
-    } else {
-        *bonus = block_draw([&](int i) { return term(P[i], ps.m, temperature); }, V, ub, pre, sh_tok);
-    }
+    if (c == 0.0)
+        *bonus = cluster_draw(cl, [&](int i) { return pn(i); }, sl, ub, pre, xch, xtok);
+    else
+        *bonus = cluster_draw(cl, [&](int i) { return fmax(pn(i) - c * qn(i), 0.0); }, sl, ub, pre, xch, xtok);
     return -1;
 }
 
@@ -230,30 +318,31 @@ __global__ void __launch_bounds__(kRT) sample_children_kernel(const float* __res
         }
 }
 
-// one CTA per live sequence: the multi-round walk from the root along accepted children
+// one cluster of kCL CTAs per live sequence: the multi-round walk from the root along accepted
+// children (every CTA takes the same decisions; rank 0 writes the results)
 __global__ void __launch_bounds__(kRT) walk_reject_kernel(int B, const StepSeqDev* __restrict__ steps, SeqStateDev ss,
                                                           TreeDev tr, RowsDev rows, const int* __restrict__ emitted,
                                                           const float* __restrict__ logits,
                                                           const float* __restrict__ rowmax,
                                                           const float* __restrict__ qbuf,
                                                           const double* __restrict__ qstat, int V, double temperature,
-                                                          float* __restrict__ resid, int* __restrict__ acc_rows,
-                                                          int* __restrict__ result) {
+                                                          int* __restrict__ acc_rows, int* __restrict__ result) {
     pdl_wait();
     pdl_trigger();
+    cg::cluster_group cl = cg::this_cluster();
     __shared__ double pre[kRT + 1];
-    __shared__ float redf[kRT / 32];
     __shared__ double redd[kRT / 32];
-    __shared__ int sh_tok, sh_bonus;
+    __shared__ double xch;
+    __shared__ int xtok, sh_n;
     __shared__ int cand_row[16], cand_tok[16];
     __shared__ int acc_tok[kMaxChain + 1];
-    const int i = blockIdx.x;
+    const bool lead = cl.block_rank() == 0;
+    const int i = blockIdx.x / kCL;
     const StepSeqDev st = steps[i];
     const int s = st.seq, off = st.vrow_off, N = st.nsel;
     const size_t base = static_cast<size_t>(s) * tr.tmax;
-    float* R = resid + static_cast<size_t>(i) * V;
     int cur = 0, nacc = 0;
-    if (threadIdx.x == 0) acc_rows[i * kMaxChain] = 0;
+    if (lead && threadIdx.x == 0) acc_rows[i * kMaxChain] = 0;
     for (;;) {
         // the node's verified children, in row order (a prefix of its sampled children)
         if (threadIdx.x == 0) {
@@ -264,70 +353,69 @@ __global__ void __launch_bounds__(kRT) walk_reject_kernel(int B, const StepSeqDe
                     cand_tok[n] = rows.tok[off + r];
                     ++n;
                 }
-            sh_tok = n;
+            sh_n = n;
         }
         __syncthreads();
-        const int n = sh_tok;
-        __syncthreads();
+        const int n = sh_n;
         if (n == 0 || nacc + 1 >= kMaxChain) {
             if (threadIdx.x == 0) acc_tok[nacc++] = emitted[off + cur];  // keyed sample_token draw
             break;
         }
         const float* P = logits + static_cast<size_t>(off + cur) * V;
         const double pm = static_cast<double>(rowmax[off + cur]);
-        double zs = 0.0;
-        for (int e = threadIdx.x; e < V; e += blockDim.x) zs += term(P[e], pm, temperature);
-        const RowStat ps{pm, block_sum(zs, redd)};
         const int node = tr.sel[base + cur];
         const int qr = tr.qrow[base + node];
         const RowStat qs{qstat[2 * qr], qstat[2 * qr + 1]};
         const int depth = tr.dep[base + node];
         const uint64_t key = mix_key(ss.seed[s], static_cast<uint64_t>(st.p + depth + 1));
         int bonus = 0;
-        const int j = mss_node(P, ps, qbuf + static_cast<size_t>(qr) * V, qs, cand_tok, n, V, temperature, key, R, pre,
-                               redf, redd, &sh_bonus, &bonus);
+        const int j = mss_node_cluster(cl, P, pm, qbuf + static_cast<size_t>(qr) * V, qs, cand_tok, n, V, temperature,
+                                       key, pre, redd, &xch, &xtok, &bonus);
         if (j < 0) {
             if (threadIdx.x == 0) acc_tok[nacc++] = bonus;
             break;
         }
         if (threadIdx.x == 0) {
             acc_tok[nacc] = cand_tok[j];
-            acc_rows[i * kMaxChain + nacc + 1] = cand_row[j];
+            if (lead) acc_rows[i * kMaxChain + nacc + 1] = cand_row[j];
         }
         ++nacc;
         cur = cand_row[j];
         __syncthreads();
     }
     __syncthreads();
-    if (threadIdx.x == 0) commit_tokens_dev(st, ss, acc_tok, nacc, result + 2 * i);
+    if (lead && threadIdx.x == 0) commit_tokens_dev(st, ss, acc_tok, nacc, result + 2 * i);
+    cl.sync();  // no CTA leaves while its shared memory may still be read
 }
 
 __global__ void __launch_bounds__(kRT) debug_spec_kernel(const float* __restrict__ p, const float* __restrict__ q,
                                                          int V, int k, double temperature, unsigned long long seed,
-                                                         float* __restrict__ resid, int* __restrict__ out_tok,
-                                                         int* __restrict__ out_acc) {
+                                                         int* __restrict__ out_tok, int* __restrict__ out_acc) {
+    cg::cluster_group cl = cg::this_cluster();
     __shared__ double pre[kRT + 1];
     __shared__ float redf[kRT / 32];
     __shared__ double redd[kRT / 32];
-    __shared__ int sh_tok;
+    __shared__ double xch;
+    __shared__ int xtok;
     __shared__ int cand[16];
-    const int trial = blockIdx.x;  // sh_tok: block_draw's scratch
-    const RowStat ps = row_stat(p, V, temperature, redf, redd);
+    const int trial = blockIdx.x / kCL;
+    const double pm = static_cast<double>(block_max(p, V, redf));
     const RowStat qs = row_stat(q, V, temperature, redf, redd);
     const uint64_t key = mix_key(seed, static_cast<uint64_t>(trial));
+    const Slice sl = vocab_slice(V, static_cast<int>(cl.block_rank()));
     for (int c = 0; c < k; ++c) {
         const double u = rng_first_uniform(mix_key(mix_key(key, 0xD5A0u), static_cast<uint64_t>(c)));
-        const int x = block_draw([&](int i) { return term(q[i], qs.m, temperature); }, V, u, pre, &sh_tok);
+        const int x = cluster_draw(cl, [&](int i) { return term(q[i], qs.m, temperature); }, sl, u, pre, &xch, &xtok);
         if (threadIdx.x == 0) cand[c] = x;
         __syncthreads();
     }
     int bonus = 0;
-    const int j = mss_node(p, ps, q, qs, cand, k, V, temperature, key, resid + static_cast<size_t>(trial) * V, pre, redf,
-                           redd, &sh_tok, &bonus);
-    if (threadIdx.x == 0) {
+    const int j = mss_node_cluster(cl, p, pm, q, qs, cand, k, V, temperature, key, pre, redd, &xch, &xtok, &bonus);
+    if (cl.block_rank() == 0 && threadIdx.x == 0) {
         out_tok[trial] = j >= 0 ? cand[j] : bonus;
         out_acc[trial] = j >= 0 ? 1 : 0;
     }
+    cl.sync();
 }
 
 }  // namespace
@@ -343,19 +431,43 @@ void launch_sample_children(const float* q, int R, int V, int k, double temperat
 
 void launch_walk_reject(int B, const StepSeqDev* steps, const SeqStateDev& ss, const TreeDev& tr, const RowsDev& rows,
                         const int* emitted, const float* logits, const float* rowmax, const float* qbuf,
-                        const double* qstat, int V, double temperature, float* resid, int* acc_rows, int* result,
+                        const double* qstat, int V, double temperature, float* /*resid*/, int* acc_rows, int* result,
                         cudaStream_t st) {
     if (B <= 0) return;
-    launch_pdl(walk_reject_kernel, B, kRT, 0, st, B, steps, ss, tr, rows, emitted, logits, rowmax, qbuf, qstat, V,
-               temperature, resid, acc_rows, result);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(B * kCL);
+    cfg.blockDim = dim3(kRT);
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kCL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    SGB_CUDA(cudaLaunchKernelEx(&cfg, walk_reject_kernel, B, steps, ss, tr, rows, emitted, logits, rowmax, qbuf, qstat, V,
+                                temperature, acc_rows, result));
     SGB_KCHECK();
 }
 
 void launch_debug_spec_sample(const float* p, const float* q, int V, int k, double temperature, int n_trials,
-                              unsigned long long seed, float* resid, int* out_tok, int* out_acc, cudaStream_t st) {
+                              unsigned long long seed, float* /*resid*/, int* out_tok, int* out_acc, cudaStream_t st) {
     if (n_trials <= 0) return;
     if (k < 1 || k > 16) throw std::invalid_argument("debug_spec_sample: k in [1, 16]");
-    debug_spec_kernel<<<n_trials, kRT, 0, st>>>(p, q, V, k, temperature, seed, resid, out_tok, out_acc);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(n_trials * kCL);
+    cfg.blockDim = dim3(kRT);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kCL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    SGB_CUDA(cudaLaunchKernelEx(&cfg, debug_spec_kernel, p, q, V, k, temperature, seed, out_tok, out_acc));
     SGB_KCHECK();
 }
 

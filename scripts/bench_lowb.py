@@ -2,7 +2,7 @@
 for B sequences (diagnostic for the concurrency-sweep tail). Timing runs are unprofiled; a
 second, profiled run gives the per-class split (events around every launch inflate it).
 
-    python scripts/bench_lowb.py [B ...] [--ncu] [--config=c3] [--vanilla]
+    python scripts/bench_lowb.py [B ...] [--ncu] [--config=c3|c3r|c5] [--vanilla] [--ctx=N]
       (--ncu: one short run per mode, for ncu; --vanilla: AR steps only)
 """
 import json
@@ -17,14 +17,19 @@ ncu = "--ncu" in sys.argv
 conf = next((a.split("=", 1)[1] for a in sys.argv[1:] if a.startswith("--config=")), "c2")
 modes = ("vanilla",) if "--vanilla" in sys.argv else ("vanilla", "adaptive_spec")
 w = dict(WORKLOADS[conf])
+ctx_arg = next((int(a.split("=", 1)[1]) for a in sys.argv[1:] if a.startswith("--ctx=")), 0)
+if ctx_arg:
+    w["P"] = ctx_arg  # long prompts stand in for a long generated context
+w["new"] = 64  # the engine's max_seq_len = P + new: keep the KV store small
 cfg = model_cfg(w)
-eng = capi.Engine(cfg, 1, 0, 128, 2048, 10, 6)
+eng = capi.Engine(cfg, 1, 0, 64, 2048, 10, 6)
 eng.init_random(1234)
 prompts = make_prompts(w, 0)
 for B in [int(x) for x in (args or ["1", "4", "16", "64"])]:
     pr = prompts[:B]
     for mode in modes:
-        kw = dict(c_peak=211, temperature=0.0, seed=7, max_new_tokens=8 if ncu else 48, want_features=False)
+        kw = dict(c_peak=211, temperature=w.get("temp", 0.0), seed=7, max_new_tokens=8 if ncu else 48,
+                  want_features=False, acceptance=w.get("acceptance", "strict"))
         eng.generate(pr, 1, mode=mode, **kw)  # warm
         if ncu:
             continue

@@ -1,0 +1,6 @@
+#!/bin/bash
+cd "$(dirname "$0")/.."
+mkdir -p gpurun_out
+python scripts/bench_lowb.py 4 16 48 --config=c3r > gpurun_out/r02_step_costs_c3r.jsonl 2>&1
+python scripts/bench_lowb.py 48 --config=c5 --ctx=2048 > gpurun_out/r02_step_costs_c5.jsonl 2>&1
+cat gpurun_out/r02_step_costs_c3r.jsonl gpurun_out/r02_step_costs_c5.jsonl
