@@ -74,52 +74,6 @@ SGB_DEV double block_sum(double v, double* red) {
     return r;
 }
 
-// Inverse-CDF draw over a row of non-negative weights w(i) (functor), total Z: thread t owns the
-// contiguous segment [t*seg, (t+1)*seg); per-thread sums, an exclusive scan in shared memory,
-// then the owner of u walks its segment. pre: shared [blockDim.x + 1] doubles.
-template <class W>
-SGB_DEV int block_draw(W w, int V, double u01, double* pre, int* sh_tok) {
-    const int T = blockDim.x, t = threadIdx.x;
-    const int seg = (V + T - 1) / T;
-    const int lo = min(V, t * seg), hi = min(V, lo + seg);
-    double s = 0.0;
-    for (int i = lo; i < hi; ++i) s += w(i);
-    pre[t + 1] = s;
-    __syncthreads();
-    if (t == 0) {
-        pre[0] = 0.0;
-        for (int j = 1; j <= T; ++j) pre[j] += pre[j - 1];
-        *sh_tok = -1;
-    }
-    __syncthreads();
-    const double u = u01 * pre[T];
-    if (pre[t] <= u && u < pre[t + 1]) {
-        double acc = pre[t];
-        int tok = hi - 1;
-        for (int i = lo; i < hi; ++i) {
-            acc += w(i);
-            if (u < acc) {
-                tok = i;
-                break;
-            }
-        }
-        *sh_tok = tok;
-    }
-    __syncthreads();
-    int tok = *sh_tok;
-    if (tok < 0) {  // u at the very top (rounding): the last token with weight
-        if (t == 0) {
-            int last = V - 1;
-            while (last > 0 && w(last) <= 0.0) --last;
-            *sh_tok = last;
-        }
-        __syncthreads();
-        tok = *sh_tok;
-    }
-    __syncthreads();
-    return tok;
-}
-
 struct RowStat {
     double m, z;
 };
@@ -160,89 +114,169 @@ SGB_DEV Slice vocab_slice(int V, int rank) {
     return Slice{lo, min(V, lo + per)};
 }
 
-// inverse-CDF draw over the vocabulary in index order from weights w(i), u01 in [0, 1): slice
-// totals -> cluster prefix -> the owner CTA walks its slice; the token is broadcast via DSMEM.
-// xch / xtok: this CTA's exchange slots (shared memory).
+// Block-wide exclusive scan of per-thread doubles (shuffle scan per warp, then over the warp
+// totals): pre[t] = sum of v over threads < t, pre[blockDim.x] = the block total. The owner test
+// of a draw compares against pre[t] and pre[t + 1] only, so neighbouring intervals share their
+// bounds exactly and every u in [0, total) has exactly one owner. wsum: shared [32].
+SGB_DEV void block_excl_scan(double v, double* pre, double* wsum) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    double x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    double ex = __shfl_up_sync(0xffffffffu, x, 1);
+    if (lane == 0) ex = 0.0;
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        double t = lane < nw ? wsum[lane] : 0.0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double y = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= o) t += y;
+        }
+        if (lane < nw) wsum[lane] = t;  // inclusive warp prefix
+    }
+    __syncthreads();
+    pre[threadIdx.x] = (w > 0 ? wsum[w - 1] : 0.0) + ex;
+    if (threadIdx.x == 0) pre[blockDim.x] = wsum[nw - 1];
+    __syncthreads();
+}
+
+// Inverse CDF over the vocabulary in index order, split over the cluster: rank r owns the slice
+// vocab_slice(V, r), thread t of it the contiguous segment [lo, hi). After setup every thread
+// knows its interval [before + pre[t], before + pre[t + 1]) of the cluster-wide CDF (the same
+// floating-point expressions on both sides of every boundary), so a draw u is resolved by its
+// unique owner alone -- k draws run in parallel with no further synchronisation. u >= total
+// (rounding only) goes to the last thread with mass, which returns its last positive index.
+struct ClusterCdf {
+    int lo, hi;
+    double before, total;
+    bool last_owner;
+};
+
 template <class W>
-SGB_DEV int cluster_draw(cg::cluster_group& cl, W w, Slice sl, double u01, double* pre, double* xch, int* xtok) {
+SGB_DEV ClusterCdf cluster_cdf(cg::cluster_group& cl, W w, Slice sl, double* pre, double* wsum, double* xch,
+                               int* xlast) {
     const int T = blockDim.x, t = threadIdx.x;
     const int n = sl.hi - sl.lo;
     const int seg = (n + T - 1) / T;
-    const int lo = sl.lo + min(n, t * seg), hi = min(sl.hi, lo + seg);
+    ClusterCdf c;
+    c.lo = sl.lo + min(n, t * seg);
+    c.hi = min(sl.hi, c.lo + seg);
     double s = 0.0;
-    for (int i = lo; i < hi; ++i) s += w(i);
-    pre[t + 1] = s;
+    for (int i = c.lo; i < c.hi; ++i) s += w(i);
+    if (t == 0) *xlast = -1;
     __syncthreads();
-    if (t == 0) {
-        pre[0] = 0.0;
-        for (int j = 1; j <= T; ++j) pre[j] += pre[j - 1];
-        *xch = pre[T];
-        *xtok = -1;
-    }
+    if (s > 0.0) atomicMax(xlast, t);
+    block_excl_scan(s, pre, wsum);  // (syncs: xlast complete)
+    if (t == 0) *xch = pre[T];
     cl.sync();
     const int me = static_cast<int>(cl.block_rank());
     double before = 0.0, total = 0.0;
+    int last_rank = -1;
     for (int r = 0; r < kCL; ++r) {
         const double x = *cl.map_shared_rank(xch, r);
-        if (r < me) before += x;
+        if (r == me) before = total;
         total += x;
+        if (x > 0.0) last_rank = r;
     }
-    const double ul = u01 * total - before;  // u relative to this slice
-    if (0.0 <= ul && ul < pre[T] && pre[t] <= ul && ul < pre[t + 1]) {
-        double acc = pre[t];
-        int tok = hi - 1;
-        for (int i = lo; i < hi; ++i) {
-            acc += w(i);
-            if (ul < acc) {
-                tok = i;
-                break;
-            }
-        }
+    c.before = before;
+    c.total = total;
+    c.last_owner = (me == last_rank && t == *xlast);
+    return c;
+}
+
+// the owner's walk; -1 if this thread does not own u
+template <class W>
+SGB_DEV int cdf_owner_draw(const ClusterCdf& c, W w, const double* pre, double u) {
+    const int t = threadIdx.x;
+    const double lo = c.before + pre[t], hi = c.before + pre[t + 1];
+    const bool mine = (lo <= u && u < hi) || (!(u < c.total) && c.last_owner);
+    if (!mine) return -1;
+    double acc = lo;
+    int last = c.lo;
+    for (int i = c.lo; i < c.hi; ++i) {
+        const double x = w(i);
+        if (x > 0.0) last = i;
+        acc += x;
+        if (u < acc) return i;
+    }
+    return last;
+}
+
+// one draw broadcast to the whole cluster. xtok: this CTA's exchange slot (shared memory).
+template <class W>
+SGB_DEV int cluster_draw(cg::cluster_group& cl, W w, Slice sl, double u01, double* pre, double* wsum, double* xch,
+                         int* xlast, int* xtok) {
+    if (threadIdx.x == 0) *xtok = 0;  // (total == 0 cannot happen: p and the residuals have mass)
+    const ClusterCdf c = cluster_cdf(cl, w, sl, pre, wsum, xch, xlast);
+    const int tok = cdf_owner_draw(c, w, pre, u01 * c.total);
+    if (tok >= 0)
         for (int r = 0; r < kCL; ++r) *cl.map_shared_rank(xtok, r) = tok;
-    }
     cl.sync();
-    int tok = *xtok;
-    if (tok < 0) {
-        // u at the very top after rounding (no owner): the last token with weight -- the last
-        // slice with mass takes its last positive index (rare; a serial scan of one slice)
-        int last_rank = -1;
-        for (int r = 0; r < kCL; ++r)
-            if (*cl.map_shared_rank(xch, r) > 0.0) last_rank = r;
-        if (me == (last_rank < 0 ? kCL - 1 : last_rank) && t == 0) {
-            int i = sl.hi - 1;
-            while (i > sl.lo && !(w(i) > 0.0)) --i;
-            for (int r = 0; r < kCL; ++r) *cl.map_shared_rank(xtok, r) = max(i, 0);
-        }
-        cl.sync();
-        tok = *xtok;
-    }
+    const int res = *xtok;
     cl.sync();  // xch / xtok are reused by the next exchange
-    return tok;
+    return res;
+}
+
+SGB_DEV float cluster_max(cg::cluster_group& cl, float v_block, float* xf) {
+    if (threadIdx.x == 0) *xf = v_block;
+    cl.sync();
+    float m = -INFINITY;
+    for (int r = 0; r < kCL; ++r) m = fmaxf(m, *cl.map_shared_rank(xf, r));
+    cl.sync();
+    return m;
 }
 
 // One node of the multi-round walk on a cluster. P / Q: target / draft logit rows; cand[n]: the
 // node's verified children (a prefix of its i.i.d. samples). Returns the accepted candidate's
 // index, or -1 with *bonus drawn from the final residual.
+struct ClusterSmem {
+    double pre[kRT + 1];
+    double wsum[32];
+    double redd[kRT / 32];
+    double xch;
+    float redf[kRT / 32];
+    float xf;
+    int xlast, xtok;
+};
+
+// The node's p and q terms over this CTA's slice are staged once in shared memory (stage[0..n) =
+// p terms, stage[n..2n) = q terms, fp32 exactly as term() returns them), so the residual passes
+// and the bonus CDF read shared memory; a candidate outside the slice recomputes the same term.
 SGB_DEV int mss_node_cluster(cg::cluster_group& cl, const float* P, double pm, const float* Q, RowStat qs,
-                             const int* cand, int n, int V, double temperature, uint64_t key, double* pre, double* redd,
-                             double* xch, int* xtok, int* bonus) {
+                             const int* cand, int n, int V, double temperature, uint64_t key, ClusterSmem& sm,
+                             float* stage, int* bonus) {
     const Slice sl = vocab_slice(V, static_cast<int>(cl.block_rank()));
+    const int ns = sl.hi - sl.lo;
+    float* tp = stage;
+    float* tq = stage + ns;
     double zs = 0.0;
-    for (int i = sl.lo + threadIdx.x; i < sl.hi; i += blockDim.x) zs += term(P[i], pm, temperature);
-    const double zp = cluster_sum(cl, block_sum(zs, redd), xch);
-    auto pn = [&](int i) { return term(P[i], pm, temperature) / zp; };
-    auto qn = [&](int i) { return term(Q[i], qs.m, temperature) / qs.z; };
+    for (int i = threadIdx.x; i < ns; i += blockDim.x) {
+        const double a = term(P[sl.lo + i], pm, temperature);
+        tp[i] = static_cast<float>(a);
+        tq[i] = static_cast<float>(term(Q[sl.lo + i], qs.m, temperature));
+        zs += a;
+    }
+    const double zp = cluster_sum(cl, block_sum(zs, sm.redd), &sm.xch);  // (block_sum syncs: stage complete)
+    const double izp = 1.0 / zp, iqz = 1.0 / qs.z;
+    auto pn = [&](int i) { return static_cast<double>(tp[i - sl.lo]) * izp; };
+    auto qn = [&](int i) { return static_cast<double>(tq[i - sl.lo]) * iqz; };
     double c = 0.0, wc = 1.0;  // residual max(p - c q, 0) / wc
     for (int j = 0; j < n; ++j) {
         const int x = cand[j];
-        const double qx = qn(x);
-        const double rx = fmax(pn(x) - c * qx, 0.0) / wc;
+        const double qx = term(Q[x], qs.m, temperature) * iqz;
+        const double px = term(P[x], pm, temperature) * izp;
+        const double rx = fmax(px - c * qx, 0.0) / wc;
         const double u = rng_first_uniform(mix_key(key, 0xACC0u + j));
         if (u * qx < rx) return j;  // accept with probability min(1, r(x) / q(x))
         c += wc;
         double ws = 0.0;
         for (int i = sl.lo + threadIdx.x; i < sl.hi; i += blockDim.x) ws += fmax(pn(i) - c * qn(i), 0.0);
-        wc = cluster_sum(cl, block_sum(ws, redd), xch);
+        wc = cluster_sum(cl, block_sum(ws, sm.redd), &sm.xch);
         if (!(wc > 0.0)) {  // p == c q on the support (floating-point residue): back to p
             c = 0.0;
             wc = 1.0;
@@ -250,13 +284,24 @@ SGB_DEV int mss_node_cluster(cg::cluster_group& cl, const float* P, double pm, c
     }
     const double ub = rng_first_uniform(mix_key(key, 0xB0B0u));
     if (c == 0.0)
-        *bonus = cluster_draw(cl, [&](int i) { return pn(i); }, sl, ub, pre, xch, xtok);
+        *bonus = cluster_draw(cl, pn, sl, ub, sm.pre, sm.wsum, &sm.xch, &sm.xlast, &sm.xtok);
     else
-        *bonus = cluster_draw(cl, [&](int i) { return fmax(pn(i) - c * qn(i), 0.0); }, sl, ub, pre, xch, xtok);
+        *bonus = cluster_draw(cl, [&](int i) { return fmax(pn(i) - c * qn(i), 0.0); }, sl, ub, sm.pre, sm.wsum,
+                              &sm.xch, &sm.xlast, &sm.xtok);
+    __syncthreads();  // the stage is rewritten by the next node
     return -1;
 }
 
-// K children per row, i.i.d. from q = softmax(row / T)
+// dynamic shared memory of the walk kernels: the p / q term stage of one vocabulary slice
+inline size_t walk_stage_bytes(int V) {
+    const size_t b = 2 * sizeof(float) * static_cast<size_t>((V + kCL - 1) / kCL);
+    if (b > (200u << 10)) throw std::invalid_argument("rejection sampling: vocabulary above 200k is unsupported");
+    return b;
+}
+
+// K children per row, i.i.d. from q = softmax(row / T): one cluster per row (vocabulary split
+// over kCL CTAs), one CDF pass, then every draw is resolved by its owning thread in parallel.
+// qstat[r] = (m, z) with z the cluster total of the same terms the draws use.
 __global__ void __launch_bounds__(kRT) sample_children_kernel(const float* __restrict__ q, int V, int k,
                                                               double temperature,
                                                               const unsigned long long* __restrict__ keys,
@@ -264,58 +309,34 @@ __global__ void __launch_bounds__(kRT) sample_children_kernel(const float* __res
                                                               double* __restrict__ qstat) {
     pdl_wait();
     pdl_trigger();
-    __shared__ double pre[kRT + 1];
-    __shared__ float redf[kRT / 32];
-    __shared__ double redd[kRT / 32];
-    const int r = blockIdx.x;
+    cg::cluster_group cl = cg::this_cluster();
+    __shared__ ClusterSmem sm;
+    const int r = blockIdx.x / kCL;
     const float* Q = q + static_cast<size_t>(r) * V;
-    const RowStat qs = row_stat(Q, V, temperature, redf, redd);
-    if (threadIdx.x == 0) {
-        qstat[2 * r] = qs.m;
-        qstat[2 * r + 1] = qs.z;
-    }
-    // per-thread segment sums once; each child is one search + one segment walk
-    const int T = blockDim.x, t = threadIdx.x;
-    const int seg = (V + T - 1) / T;
-    const int lo = min(V, t * seg), hi = min(V, lo + seg);
-    double s = 0.0;
-    for (int i = lo; i < hi; ++i) s += term(Q[i], qs.m, temperature);
-    pre[t + 1] = s;
+    const Slice sl = vocab_slice(V, static_cast<int>(cl.block_rank()));
+    float mloc = -INFINITY;
+    for (int i = sl.lo + threadIdx.x; i < sl.hi; i += blockDim.x) mloc = fmaxf(mloc, Q[i]);
+    mloc = warp_max(mloc);
+    if ((threadIdx.x & 31) == 0) sm.redf[threadIdx.x >> 5] = mloc;
     __syncthreads();
-    if (t == 0) {
-        pre[0] = 0.0;
-        for (int j = 1; j <= T; ++j) pre[j] += pre[j - 1];
+    float mb = sm.redf[0];
+    for (int w = 1; w < kRT / 32; ++w) mb = fmaxf(mb, sm.redf[w]);
+    const double m = static_cast<double>(cluster_max(cl, mb, &sm.xf));
+    auto wq = [&](int i) { return term(Q[i], m, temperature); };
+    const ClusterCdf c = cluster_cdf(cl, wq, sl, sm.pre, sm.wsum, &sm.xch, &sm.xlast);
+    if (cl.block_rank() == 0 && threadIdx.x == 0) {
+        qstat[2 * r] = m;
+        qstat[2 * r + 1] = c.total;
     }
-    __syncthreads();
-    for (int c = 0; c < k; ++c) {
-        const double u = rng_first_uniform(mix_key(keys[r], static_cast<uint64_t>(c))) * pre[T];
-        if (pre[t] <= u && u < pre[t + 1]) {
-            double acc = pre[t];
-            int tok = hi - 1;
-            for (int i = lo; i < hi; ++i) {
-                acc += term(Q[i], qs.m, temperature);
-                if (u < acc) {
-                    tok = i;
-                    break;
-                }
-            }
-            out_tok[static_cast<size_t>(r) * k + c] = tok;
-            out_lp[static_cast<size_t>(r) * k + c] = log(term(Q[tok], qs.m, temperature) / qs.z);
+    for (int j = 0; j < k; ++j) {
+        const double u = rng_first_uniform(mix_key(keys[r], static_cast<uint64_t>(j))) * c.total;
+        const int tok = cdf_owner_draw(c, wq, sm.pre, u);
+        if (tok >= 0) {
+            out_tok[static_cast<size_t>(r) * k + j] = tok;
+            out_lp[static_cast<size_t>(r) * k + j] = log(wq(tok) / c.total);
         }
-        // (u == total after rounding: no owner) -> the row's argmax, a token of positive mass
-        __syncthreads();
     }
-    if (t == 0)
-        for (int c = 0; c < k; ++c) {
-            const double u = rng_first_uniform(mix_key(keys[r], static_cast<uint64_t>(c))) * pre[T];
-            if (!(u < pre[T])) {
-                int best = 0;
-                for (int i = 1; i < V; ++i)
-                    if (Q[i] > Q[best]) best = i;
-                out_tok[static_cast<size_t>(r) * k + c] = best;
-                out_lp[static_cast<size_t>(r) * k + c] = log(term(Q[best], qs.m, temperature) / qs.z);
-            }
-        }
+    cl.sync();  // the slice totals in shared memory are read by the other ranks until here
 }
 
 // one cluster of kCL CTAs per live sequence: the multi-round walk from the root along accepted
@@ -330,10 +351,9 @@ __global__ void __launch_bounds__(kRT) walk_reject_kernel(int B, const StepSeqDe
     pdl_wait();
     pdl_trigger();
     cg::cluster_group cl = cg::this_cluster();
-    __shared__ double pre[kRT + 1];
-    __shared__ double redd[kRT / 32];
-    __shared__ double xch;
-    __shared__ int xtok, sh_n;
+    __shared__ ClusterSmem sm;
+    extern __shared__ float stage[];
+    __shared__ int sh_n;
     __shared__ int cand_row[16], cand_tok[16];
     __shared__ int acc_tok[kMaxChain + 1];
     const bool lead = cl.block_rank() == 0;
@@ -370,7 +390,7 @@ __global__ void __launch_bounds__(kRT) walk_reject_kernel(int B, const StepSeqDe
         const uint64_t key = mix_key(ss.seed[s], static_cast<uint64_t>(st.p + depth + 1));
         int bonus = 0;
         const int j = mss_node_cluster(cl, P, pm, qbuf + static_cast<size_t>(qr) * V, qs, cand_tok, n, V, temperature,
-                                       key, pre, redd, &xch, &xtok, &bonus);
+                                       key, sm, stage, &bonus);
         if (j < 0) {
             if (threadIdx.x == 0) acc_tok[nacc++] = bonus;
             break;
@@ -392,25 +412,23 @@ __global__ void __launch_bounds__(kRT) debug_spec_kernel(const float* __restrict
                                                          int V, int k, double temperature, unsigned long long seed,
                                                          int* __restrict__ out_tok, int* __restrict__ out_acc) {
     cg::cluster_group cl = cg::this_cluster();
-    __shared__ double pre[kRT + 1];
-    __shared__ float redf[kRT / 32];
-    __shared__ double redd[kRT / 32];
-    __shared__ double xch;
-    __shared__ int xtok;
+    __shared__ ClusterSmem sm;
+    extern __shared__ float stage[];
     __shared__ int cand[16];
     const int trial = blockIdx.x / kCL;
-    const double pm = static_cast<double>(block_max(p, V, redf));
-    const RowStat qs = row_stat(q, V, temperature, redf, redd);
+    const double pm = static_cast<double>(block_max(p, V, sm.redf));
+    const RowStat qs = row_stat(q, V, temperature, sm.redf, sm.redd);
     const uint64_t key = mix_key(seed, static_cast<uint64_t>(trial));
     const Slice sl = vocab_slice(V, static_cast<int>(cl.block_rank()));
     for (int c = 0; c < k; ++c) {
         const double u = rng_first_uniform(mix_key(mix_key(key, 0xD5A0u), static_cast<uint64_t>(c)));
-        const int x = cluster_draw(cl, [&](int i) { return term(q[i], qs.m, temperature); }, sl, u, pre, &xch, &xtok);
+        const int x = cluster_draw(cl, [&](int i) { return term(q[i], qs.m, temperature); }, sl, u, sm.pre, sm.wsum,
+                                   &sm.xch, &sm.xlast, &sm.xtok);
         if (threadIdx.x == 0) cand[c] = x;
         __syncthreads();
     }
     int bonus = 0;
-    const int j = mss_node_cluster(cl, p, pm, q, qs, cand, k, V, temperature, key, pre, redd, &xch, &xtok, &bonus);
+    const int j = mss_node_cluster(cl, p, pm, q, qs, cand, k, V, temperature, key, sm, stage, &bonus);
     if (cl.block_rank() == 0 && threadIdx.x == 0) {
         out_tok[trial] = j >= 0 ? cand[j] : bonus;
         out_acc[trial] = j >= 0 ? 1 : 0;
@@ -418,24 +436,13 @@ __global__ void __launch_bounds__(kRT) debug_spec_kernel(const float* __restrict
     cl.sync();
 }
 
-}  // namespace
-
-void launch_sample_children(const float* q, int R, int V, int k, double temperature, const unsigned long long* keys,
-                            int* out_tok, double* out_lp, double* qstat, cudaStream_t st) {
-    if (R <= 0) return;
-    if (k < 1 || k > 16) throw std::invalid_argument("sample_children: k must be in [1, 16]");
-    if (!(temperature > 0)) throw std::invalid_argument("rejection sampling needs temperature > 0");
-    launch_pdl(sample_children_kernel, R, kRT, 0, st, q, V, k, temperature, keys, out_tok, out_lp, qstat);
-    SGB_KCHECK();
-}
-
-void launch_walk_reject(int B, const StepSeqDev* steps, const SeqStateDev& ss, const TreeDev& tr, const RowsDev& rows,
-                        const int* emitted, const float* logits, const float* rowmax, const float* qbuf,
-                        const double* qstat, int V, double temperature, float* /*resid*/, int* acc_rows, int* result,
-                        cudaStream_t st) {
-    if (B <= 0) return;
+// grid of kCL-CTA clusters (+ programmatic dependent launch)
+template <class... KA, class... A>
+void launch_cluster(void (*kern)(KA...), int clusters, size_t smem, bool pdl, cudaStream_t st, A... args) {
+    if (smem > 0) SGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(B * kCL);
+    cfg.dynamicSmemBytes = smem;
+    cfg.gridDim = dim3(clusters * kCL);
     cfg.blockDim = dim3(kRT);
     cfg.stream = st;
     cudaLaunchAttribute at[2];
@@ -446,9 +453,28 @@ void launch_walk_reject(int B, const StepSeqDev* steps, const SeqStateDev& ss, c
     at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 2;
-    SGB_CUDA(cudaLaunchKernelEx(&cfg, walk_reject_kernel, B, steps, ss, tr, rows, emitted, logits, rowmax, qbuf, qstat, V,
-                                temperature, acc_rows, result));
+    cfg.numAttrs = pdl ? 2 : 1;
+    SGB_CUDA(cudaLaunchKernelEx(&cfg, kern, static_cast<KA>(args)...));
+}
+
+}  // namespace
+
+void launch_sample_children(const float* q, int R, int V, int k, double temperature, const unsigned long long* keys,
+                            int* out_tok, double* out_lp, double* qstat, cudaStream_t st) {
+    if (R <= 0) return;
+    if (k < 1 || k > 16) throw std::invalid_argument("sample_children: k must be in [1, 16]");
+    if (!(temperature > 0)) throw std::invalid_argument("rejection sampling needs temperature > 0");
+    launch_cluster(sample_children_kernel, R, 0, true, st, q, V, k, temperature, keys, out_tok, out_lp, qstat);
+    SGB_KCHECK();
+}
+
+void launch_walk_reject(int B, const StepSeqDev* steps, const SeqStateDev& ss, const TreeDev& tr, const RowsDev& rows,
+                        const int* emitted, const float* logits, const float* rowmax, const float* qbuf,
+                        const double* qstat, int V, double temperature, float* /*resid*/, int* acc_rows, int* result,
+                        cudaStream_t st) {
+    if (B <= 0) return;
+    launch_cluster(walk_reject_kernel, B, walk_stage_bytes(V), true, st, B, steps, ss, tr, rows, emitted, logits, rowmax, qbuf, qstat, V,
+                   temperature, acc_rows, result);
     SGB_KCHECK();
 }
 
@@ -456,18 +482,7 @@ void launch_debug_spec_sample(const float* p, const float* q, int V, int k, doub
                               unsigned long long seed, float* /*resid*/, int* out_tok, int* out_acc, cudaStream_t st) {
     if (n_trials <= 0) return;
     if (k < 1 || k > 16) throw std::invalid_argument("debug_spec_sample: k in [1, 16]");
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(n_trials * kCL);
-    cfg.blockDim = dim3(kRT);
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = kCL;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    SGB_CUDA(cudaLaunchKernelEx(&cfg, debug_spec_kernel, p, q, V, k, temperature, seed, out_tok, out_acc));
+    launch_cluster(debug_spec_kernel, n_trials, walk_stage_bytes(V), false, st, p, q, V, k, temperature, seed, out_tok, out_acc);
     SGB_KCHECK();
 }
 
