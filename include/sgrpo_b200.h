@@ -295,6 +295,13 @@ int sgb_debug_tree_attention_tree(int n_groups, const int* ctx_len, const int* n
                                   const float* vnode, float* out_tree);
 /* Tree-verify microbenchmark of attention_tree.cu (same shapes as sgb_bench_tree_attention). */
 int sgb_bench_tree_attention_tree(int B, int N, int ctx, int H, int dh, int iters, double* ms_tree);
+/* Cluster decode attention (AR steps, one row per group) next to attention.cu on the same
+ * inputs (debug), and an AR attention microbenchmark: ms per launch of the three kernels. */
+int sgb_debug_attention_decode(int n_groups, const int* ctx_len, int H, int dh, const float* q, const float* kctx,
+                               const float* vctx, const float* knode, const float* vnode, float* out_row,
+                               float* out_decode);
+int sgb_bench_attention_decode(int B, int ctx, int H, int dh, int iters, double* ms_row, double* ms_tree,
+                               double* ms_decode);
 
 /* Tree-verify attention microbenchmark: B sequences x (ctx committed keys + an EAGLE-shaped
  * tree of N rows); ms per launch of the per-row and of the prefix-shared group kernel. */

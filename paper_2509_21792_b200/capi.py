@@ -633,6 +633,30 @@ def debug_tree_attention_tree(ctx_len, parents, q, kctx, vctx, knode, vnode, n_h
 EXPORTED += ["sgb_debug_tree_attention_tree", "sgb_bench_tree_attention_tree"]
 
 
+def debug_attention_decode(ctx_len, q, kctx, vctx, knode, vnode, n_heads: int):
+    """attention.cu and the cluster decode kernel on one-row groups: (out_row, out_decode)."""
+    cl = np.ascontiguousarray(ctx_len, np.int32)
+    q = np.ascontiguousarray(q, np.float32)
+    o1, o2 = np.zeros_like(q), np.zeros_like(q)
+    _check(_lib.sgb_debug_attention_decode(len(cl), _p(cl, C.c_int), n_heads, q.shape[1] // n_heads, _p(q, C.c_float),
+                                           _p(np.ascontiguousarray(kctx, np.float32), C.c_float),
+                                           _p(np.ascontiguousarray(vctx, np.float32), C.c_float),
+                                           _p(np.ascontiguousarray(knode, np.float32), C.c_float),
+                                           _p(np.ascontiguousarray(vnode, np.float32), C.c_float),
+                                           _p(o1, C.c_float), _p(o2, C.c_float)))
+    return o1, o2
+
+
+def bench_attention_decode(B: int, ctx: int, n_heads: int, dh: int = 128, iters: int = 20):
+    """ms per launch: (attention.cu rows, tree kernel, cluster decode kernel)."""
+    r, t, dd = C.c_double(), C.c_double(), C.c_double()
+    _check(_lib.sgb_bench_attention_decode(B, ctx, n_heads, dh, iters, C.byref(r), C.byref(t), C.byref(dd)))
+    return r.value, t.value, dd.value
+
+
+EXPORTED += ["sgb_debug_attention_decode", "sgb_bench_attention_decode"]
+
+
 class PolicyTermsC(C.Structure):
     _fields_ = [("loss", C.c_double), ("tokens", C.c_longlong), ("rows", C.c_longlong), ("seconds", C.c_double),
                 ("skipped", C.c_int)]

@@ -26,12 +26,16 @@
 #include <algorithm>
 #include <cfloat>
 
+#include <cooperative_groups.h>
+
 #include "attn_numerics.cuh"
 #include "common.cuh"
 #include "kernels.h"
 #include "util.h"
 
 namespace sgb {
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -344,6 +348,299 @@ __global__ void __launch_bounds__(32 * (kTMaxWarps + 1), 1)
     }
 }
 
+// ------------------------------------------------------------------ few-row decode (AR steps)
+// One row per group (an AR step: the row's keys are its committed prefix plus its own new key).
+// The per-row kernels above stream a row's whole context through one warp; here the 64-key
+// blocks of a (row, head) are spread over the S CTAs of a thread-block cluster and their W warps
+// (contiguous block ranges per CTA, warp w of a CTA takes every W-th block of the range), each
+// block's partial (m, l, o) goes to shared memory, and CTA 0 of the cluster merges the partials
+// strictly in block order through distributed shared memory -- the same chunk arithmetic and
+// the same ordered merge from the identity as tree_attn_kernel / attention.cu, so the bits are
+// those of every other attention path. Each warp streams its own chunks through a private
+// NS-stage TMA ring (no producer warp: one lane issues the next chunk when a stage frees up).
+// measured (scripts/bench_decode_attn.py): 8 warps x 2 stages pushes the small-B launches to one
+// CTA per SM (two waves at B = 1); 4 x 3 keeps two CTAs per SM
+constexpr int kDW = 4;   // warps per CTA
+constexpr int kDNS = 3;  // ring stages per warp (16 keys of K and V each)
+
+template <int DH>
+struct DecodeSmem {
+    static constexpr uint32_t kStage = 2u * kTChunk * DH * 2;  // K then V, swizzled boxes
+    static constexpr int kRowB = DH * 2 + 16;
+    static size_t bytes(int max_blocks) {
+        return 1024 + static_cast<size_t>(kDW) * kDNS * kStage + 2 * kRowB +
+               static_cast<size_t>(max_blocks) * (DH + 2) * 4 + 8 * (kDW * kDNS + 1);
+    }
+};
+
+template <class KA, class VA, int NK>
+SGB_DEV void decode_chunk(KA kaddr, VA vaddr, int v0, int e0, int e1, const uint32_t (&qf)[NK][2], float scale,
+                          float& m0, float& m1, float& l0, float& l1, float (&o)[NK][4], int lane) {
+    const int g8 = lane >> 2, li = lane >> 3, lr = lane & 7;
+    float sc[4] = {0.f, 0.f, 0.f, 0.f};
+    const int kr_k = lr + 8 * (li & 1);
+#pragma unroll
+    for (int ks = 0; ks < NK; ++ks) {
+        uint32_t a[4];
+        ldsm_x4(kaddr(kr_k, 16 * ks + 8 * (li >> 1)), a);
+        mma16816(sc, a, qf[ks][0], qf[ks][1]);
+    }
+    const bool va0 = v0 + g8 < e0, va1 = v0 + g8 < e1, vb0 = v0 + g8 + 8 < e0, vb1 = v0 + g8 + 8 < e1;
+    const float s0 = va0 ? attn_scale(sc[0], scale) : -INFINITY;
+    const float s1 = va1 ? attn_scale(sc[1], scale) : -INFINITY;
+    const float s2 = vb0 ? attn_scale(sc[2], scale) : -INFINITY;
+    const float s3 = vb1 ? attn_scale(sc[3], scale) : -INFINITY;
+    float x0 = fmaxf(s0, s2), x1 = fmaxf(s1, s3);
+#pragma unroll
+    for (int o2 = 4; o2 < 32; o2 <<= 1) {
+        x0 = fmaxf(x0, __shfl_xor_sync(0xffffffffu, x0, o2));
+        x1 = fmaxf(x1, __shfl_xor_sync(0xffffffffu, x1, o2));
+    }
+    const float n0 = fmaxf(m0, x0), n1 = fmaxf(m1, x1);
+    const float a0 = attn_alpha(m0, n0), a1 = attn_alpha(m1, n1);
+    const float p0 = va0 ? attn_p(s0, n0) : 0.f, p1 = va1 ? attn_p(s1, n1) : 0.f;
+    const float p2 = vb0 ? attn_p(s2, n0) : 0.f, p3 = vb1 ? attn_p(s3, n1) : 0.f;
+    float ps0 = __fadd_rn(p0, p2), ps1 = __fadd_rn(p1, p3);
+#pragma unroll
+    for (int o2 = 4; o2 < 32; o2 <<= 1) {
+        ps0 = __fadd_rn(ps0, __shfl_xor_sync(0xffffffffu, ps0, o2));
+        ps1 = __fadd_rn(ps1, __shfl_xor_sync(0xffffffffu, ps1, o2));
+    }
+    l0 = attn_l(l0, a0, ps0);
+    l1 = attn_l(l1, a1, ps1);
+    m0 = n0;
+    m1 = n1;
+    uint32_t va4[NK][4];
+    const int kr_v = lr + 8 * (li >> 1);
+#pragma unroll
+    for (int mt = 0; mt < NK; ++mt) ldsm_x4_t(vaddr(kr_v, 16 * mt + 8 * (li & 1)), va4[mt]);
+    const uint32_t b0 = movm_t(pack_bf16(p0, p1)), b1 = movm_t(pack_bf16(p2, p3));
+#pragma unroll
+    for (int mt = 0; mt < NK; ++mt) {
+        o[mt][0] = __fmul_rn(o[mt][0], a0);
+        o[mt][1] = __fmul_rn(o[mt][1], a1);
+        o[mt][2] = __fmul_rn(o[mt][2], a0);
+        o[mt][3] = __fmul_rn(o[mt][3], a1);
+        mma16816(o[mt], va4[mt], b0, b1);
+    }
+}
+
+template <int DH>
+__global__ void __launch_bounds__(32 * kDW)
+    decode_attn_kernel(const float* __restrict__ q, const __grid_constant__ CUtensorMap kmap,
+                       const __grid_constant__ CUtensorMap vmap, long long layer_row0, const __nv_bfloat16* __restrict__ K,
+                       const __nv_bfloat16* __restrict__ V, const TreeGroupDev* __restrict__ groups, int S,
+                       int max_blocks, int d, float scale, __nv_bfloat16* __restrict__ out) {
+    constexpr int NK = DH / 16;
+    using Sm = DecodeSmem<DH>;
+    constexpr uint32_t kHalf = kTChunk * DH * 2;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = blockIdx.x / S, rank = blockIdx.x % S, h = blockIdx.y;
+    const TreeGroupDev gr = groups[g];
+    const int P = gr.ctx_len, lv = P + 1;  // prefix keys, then the row's own key (node 0)
+    const int nb = (lv + kTBlock - 1) / kTBlock;
+    const int b_lo = static_cast<int>(static_cast<long long>(rank) * nb / S);
+    const int b_hi = static_cast<int>(static_cast<long long>(rank + 1) * nb / S);
+    uint8_t* ring = smem + static_cast<size_t>(warp) * kDNS * Sm::kStage;
+    uint8_t* nodeK = smem + static_cast<size_t>(kDW) * kDNS * Sm::kStage;
+    uint8_t* nodeV = nodeK + Sm::kRowB;
+    float* part = reinterpret_cast<float*>(nodeV + Sm::kRowB);  // [max_blocks][DH + 2]: o, m, l
+    uint64_t* full = reinterpret_cast<uint64_t*>(part + static_cast<size_t>(max_blocks) * (DH + 2));
+    uint64_t* tbar = full + kDW * kDNS;
+    uint64_t* wfull = full + warp * kDNS;
+    if (threadIdx.x == 0) {
+        tma_prefetch(&kmap);
+        tma_prefetch(&vmap);
+        for (int s = 0; s < kDW * kDNS; ++s) mbar_init(&full[s], 1);
+        mbar_init(tbar, 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+    pdl_wait();
+    pdl_trigger();
+    if (threadIdx.x == 0) {
+        const size_t src = static_cast<size_t>(gr.node_base) * d + static_cast<size_t>(h) * DH;
+        mbar_arrive_expect_tx(tbar, 2u * DH * 2);
+        bulk_g2s(nodeK, K + src, DH * 2, tbar);
+        bulk_g2s(nodeV, V + src, DH * 2, tbar);
+    }
+    // this warp's staged chunks (keys below P) in order: block b_lo + warp + k * kDW, chunk c
+    auto staged_of = [&](int b) { return min(4, max(0, (P - b * kTBlock + kTChunk - 1) / kTChunk)); };
+    int ib = b_lo + warp, ic = 0;  // issue cursor
+    auto advance = [&]() {
+        if (++ic >= staged_of(ib)) {
+            ic = 0;
+            ib += kDW;
+        }
+    };
+    while (ib < b_hi && staged_of(ib) == 0) ib += kDW;
+    auto issue = [&](int st) {
+        const int v0 = ib * kTBlock + ic * kTChunk;
+        const long long slot0 = (v0 + kTChunk <= gr.pre_len ? gr.pre_base : gr.ctx_base) + v0;
+        const int row = static_cast<int>(layer_row0 + slot0);
+        uint8_t* dst = ring + static_cast<size_t>(st) * Sm::kStage;
+        mbar_arrive_expect_tx(&wfull[st], Sm::kStage);
+#pragma unroll
+        for (int bx = 0; bx < DH / 64; ++bx) {
+            tma_load_2d(dst + bx * 2048, &kmap, &wfull[st], h * DH + 64 * bx, row);
+            tma_load_2d(dst + kHalf + bx * 2048, &vmap, &wfull[st], h * DH + 64 * bx, row);
+        }
+        advance();
+        while (ib < b_hi && staged_of(ib) == 0) ib += kDW;
+    };
+    if (lane == 0)
+        for (int st = 0; st < kDNS && ib < b_hi; ++st) issue(st);
+    __syncwarp();
+    // q fragment: every column reads the row (columns past the first are dead: e = v0)
+    const int g8 = lane >> 2, t4 = lane & 3, li = lane >> 3, lr = lane & 7;
+    uint32_t qf[NK][2];
+    {
+        const float* qr = q + static_cast<size_t>(gr.row0) * d + h * DH + 2 * t4;
+#pragma unroll
+        for (int ks = 0; ks < NK; ++ks) {
+            const float2 a = __ldg(reinterpret_cast<const float2*>(qr + 16 * ks));
+            const float2 b = __ldg(reinterpret_cast<const float2*>(qr + 16 * ks + 8));
+            qf[ks][0] = pack_bf16(a.x, a.y);
+            qf[ks][1] = pack_bf16(b.x, b.y);
+        }
+    }
+    const int lv0 = t4 == 0 ? lv : 0;  // query column 0 is the row
+    const uint32_t node_k = smem_u32(nodeK), node_v = smem_u32(nodeV);
+    int i = 0, si = 0, ph = 0;  // consumed staged chunks, ring stage, phase
+    bool node_ready = false;
+    for (int b = b_lo + warp; b < b_hi; b += kDW) {
+        float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+        float o[NK][4];
+#pragma unroll
+        for (int mt = 0; mt < NK; ++mt) o[mt][0] = o[mt][1] = o[mt][2] = o[mt][3] = 0.f;
+        for (int c = 0; c < kTBlock / kTChunk; ++c) {
+            const int v0 = b * kTBlock + c * kTChunk;
+            if (v0 >= lv) break;
+            const bool staged = v0 < P;
+            uint32_t sK = 0, sV = 0;
+            if (staged) {
+                mbar_wait(&wfull[si], ph);
+                sK = smem_u32(ring) + static_cast<uint32_t>(si) * Sm::kStage;
+                sV = sK + kHalf;
+            }
+            if (v0 + kTChunk <= P) {
+                auto ka = [&](int kr, int dd) { return ring_addr(sK, kr, dd); };
+                auto vaa = [&](int kr, int dd) { return ring_addr(sV, kr, dd); };
+                decode_chunk(ka, vaa, v0, lv0, 0, qf, scale, m0, m1, l0, l1, o, lane);
+            } else {
+                if (!node_ready) {
+                    mbar_wait(tbar, 0);
+                    node_ready = true;
+                }
+                // prefix keys from the ring, the row's own key (v == P) from the node row, past it
+                // any finite row (p = 0)
+                const int vk = v0 + lr + 8 * (li & 1), vv = v0 + lr + 8 * (li >> 1);
+                auto ka = [&](int kr, int dd) { return vk < P ? ring_addr(sK, kr, dd) : node_k + static_cast<uint32_t>(dd * 2); };
+                auto vaa = [&](int kr, int dd) { return vv < P ? ring_addr(sV, kr, dd) : node_v + static_cast<uint32_t>(dd * 2); };
+                decode_chunk(ka, vaa, v0, t4 == 0 ? lv : v0, v0, qf, scale, m0, m1, l0, l1, o, lane);
+            }
+            if (staged) {
+                __syncwarp();
+                if (lane == 0 && ib < b_hi) {
+                    fence_proxy_async();  // this stage's ldmatrix reads before the TMA rewrite
+                    issue(si);
+                }
+                __syncwarp();
+                ++i;
+                if (++si == kDNS) {
+                    si = 0;
+                    ph ^= 1;
+                }
+            }
+        }
+        // block partial of query column 0 (lanes t4 == 0 hold it)
+        if (t4 == 0) {
+            float* pb = part + static_cast<size_t>(b - b_lo) * (DH + 2);
+#pragma unroll
+            for (int mt = 0; mt < NK; ++mt) {
+                pb[16 * mt + g8] = o[mt][0];
+                pb[16 * mt + g8 + 8] = o[mt][2];
+            }
+            if (g8 == 0) {
+                pb[DH] = m0;
+                pb[DH + 1] = l0;
+            }
+        }
+    }
+    // ordered merge over all blocks of the row (attn_merge from the identity), CTA 0, warp 0
+    cg::cluster_group cl = cg::this_cluster();
+    if (S > 1) cl.sync();
+    else __syncthreads();
+    if (rank == 0 && warp == 0 && t4 == 0) {
+        float M0 = -INFINITY, L0 = 0.f, A0[NK], A2[NK];
+#pragma unroll
+        for (int mt = 0; mt < NK; ++mt) A0[mt] = A2[mt] = 0.f;
+        // (measured: gathering all partials into CTA 0 first costs occupancy and was slower)
+        for (int r = 0; r < S; ++r) {
+            const int r_lo = static_cast<int>(static_cast<long long>(r) * nb / S);
+            const int r_hi = static_cast<int>(static_cast<long long>(r + 1) * nb / S);
+            const float* pr = S > 1 ? cl.map_shared_rank(part, r) : part;
+            for (int b = r_lo; b < r_hi; ++b) {
+                const float* pb = pr + static_cast<size_t>(b - r_lo) * (DH + 2);
+                const float m0 = pb[DH], l0 = pb[DH + 1];
+                const float Mn = fmaxf(M0, m0);
+                const float ca = M0 == -INFINITY ? 0.f : expf(__fsub_rn(M0, Mn));
+                const float cb = expf(__fsub_rn(m0, Mn));
+                L0 = fmaf(L0, ca, __fmul_rn(l0, cb));
+#pragma unroll
+                for (int mt = 0; mt < NK; ++mt) {
+                    A0[mt] = fmaf(A0[mt], ca, __fmul_rn(pb[16 * mt + g8], cb));
+                    A2[mt] = fmaf(A2[mt], ca, __fmul_rn(pb[16 * mt + g8 + 8], cb));
+                }
+                M0 = Mn;
+            }
+        }
+        __nv_bfloat16* orow = out + static_cast<size_t>(gr.row0) * d + h * DH;
+#pragma unroll
+        for (int mt = 0; mt < NK; ++mt) {
+            orow[16 * mt + g8] = __float2bfloat16(__fdiv_rn(A0[mt], L0));
+            orow[16 * mt + g8 + 8] = __float2bfloat16(__fdiv_rn(A2[mt], L0));
+        }
+    }
+    if (S > 1) cl.sync();  // peers keep their partials until CTA 0 has read them
+}
+
+template <int DH>
+void launch_decode_impl(const float* q, const CUtensorMap& kmap, const CUtensorMap& vmap, long long layer_row0,
+                        const __nv_bfloat16* K, const __nv_bfloat16* V, const TreeGroupDev* groups, int n_groups,
+                        int max_ctx, int H, int d, __nv_bfloat16* out, cudaStream_t st) {
+    const int nb = (max_ctx + 1 + kTBlock - 1) / kTBlock;
+    // cluster size: fill ~2 CTAs per SM, at most 8 (portable), at most one per block
+    int S = std::max(1, std::min(8, 296 / std::max(1, n_groups * H)));
+    S = std::min(S, nb);
+    const int max_blocks = (nb + S - 1) / S;
+    const size_t smem = DecodeSmem<DH>::bytes(max_blocks);
+    if (smem > static_cast<size_t>(kTSmem)) throw std::invalid_argument("decode attention: context too long");
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(decode_attn_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTSmem);
+        attr = true;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(n_groups * S, H);
+    cfg.blockDim = dim3(32 * kDW);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = S;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    SGB_CUDA(cudaLaunchKernelEx(&cfg, decode_attn_kernel<DH>, q, kmap, vmap, layer_row0, K, V, groups, S, max_blocks, d,
+                                1.0f / sqrtf(static_cast<float>(DH)), out));
+}
+
 template <int DH>
 void launch_tree_impl(const float* q, const CUtensorMap& kmap, const CUtensorMap& vmap, long long layer_row0,
                       const __nv_bfloat16* K, const __nv_bfloat16* V, const AttnRowsDev& rows, const TreeGroupDev* groups,
@@ -411,6 +708,20 @@ void launch_attention_tree(const float* q, const CUtensorMap& kmap, const CUtens
         launch_tree_impl<64>(q, kmap, vmap, layer_row0, K, V, rows, groups, tiles, n_tiles, W, H, d, max_nodes, out, st);
     else
         throw std::invalid_argument("tree attention: head dim must be 64 or 128");
+    SGB_KCHECK();
+}
+
+void launch_attention_decode(const float* q, const CUtensorMap& kmap, const CUtensorMap& vmap, long long layer_row0,
+                             const __nv_bfloat16* K, const __nv_bfloat16* V, const TreeGroupDev* groups, int n_groups,
+                             int max_ctx, int H, int d, __nv_bfloat16* out, cudaStream_t st) {
+    if (n_groups <= 0) return;
+    const int dh = d / H;
+    if (dh == 128)
+        launch_decode_impl<128>(q, kmap, vmap, layer_row0, K, V, groups, n_groups, max_ctx, H, d, out, st);
+    else if (dh == 64)
+        launch_decode_impl<64>(q, kmap, vmap, layer_row0, K, V, groups, n_groups, max_ctx, H, d, out, st);
+    else
+        throw std::invalid_argument("decode attention: head dim must be 64 or 128");
     SGB_KCHECK();
 }
 

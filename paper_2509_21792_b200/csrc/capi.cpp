@@ -1052,6 +1052,14 @@ struct TreeAttnCase {
     void run_tree() {
         sgb::launch_attention_tree(q, kmap, vmap, 0, K, V, ar, dtg, dtt, n_ttiles, tw, H, d, max_nodes, o2, 0);
     }
+    void run_decode() {
+        int mc = 0;
+        for (const auto& g : tg) {
+            if (g.nrows != 1) throw std::invalid_argument("decode attention: one row per group");
+            mc = std::max(mc, g.ctx_len);
+        }
+        sgb::launch_attention_decode(q, kmap, vmap, 0, K, V, dtg, static_cast<int>(tg.size()), mc, H, d, o2, 0);
+    }
     void run_group() { sgb::launch_attention_tiles(q, K, V, n_slots, ar, M, tiles, n_tiles, items, qw, H, d, max_vlen, sc, o2,
                                                     0); }
     void read(const __nv_bfloat16* o, float* out) const {
@@ -1085,6 +1093,51 @@ int sgb_debug_tree_attention_tree(int n_groups, const int* ctx_len, const int* n
         c.run_tree();
         SGB_CUDA(cudaDeviceSynchronize());
         c.read(c.o2, out_tree);
+    });
+}
+
+// attention_tree.cu's cluster decode kernel (AR steps: one row per group) on the same inputs
+int sgb_debug_attention_decode(int n_groups, const int* ctx_len, int H, int dh, const float* q, const float* kctx,
+                               const float* vctx, const float* knode, const float* vnode, float* out_row,
+                               float* out_decode) {
+    return guarded([&] {
+        if (!q) throw std::invalid_argument("debug_attention_decode: null inputs");
+        std::vector<int> nr(n_groups, 1), par(n_groups, -1);
+        TreeAttnCase c(n_groups, ctx_len, nr.data(), par.data(), H, dh, q, kctx, vctx, knode, vnode);
+        c.run_row();
+        c.run_decode();
+        SGB_CUDA(cudaDeviceSynchronize());
+        c.read(c.o1, out_row);
+        c.read(c.o2, out_decode);
+    });
+}
+
+// AR attention microbenchmark: B rows with ctx committed keys each; device ms per launch of
+// attention.cu (row path), the tree kernel and the cluster decode kernel
+int sgb_bench_attention_decode(int B, int ctx, int H, int dh, int iters, double* ms_row, double* ms_tree,
+                               double* ms_decode) {
+    return guarded([&] {
+        if (B <= 0 || iters <= 0) throw std::invalid_argument("bench_attention_decode: bad shape");
+        std::vector<int> cl(B, ctx), nr(B, 1), par(B, -1);
+        TreeAttnCase c(B, cl.data(), nr.data(), par.data(), H, dh, nullptr, nullptr, nullptr, nullptr, nullptr);
+        cudaEvent_t a, b;
+        SGB_CUDA(cudaEventCreate(&a));
+        SGB_CUDA(cudaEventCreate(&b));
+        auto time = [&](auto&& f) {
+            for (int i = 0; i < 2; ++i) f();
+            SGB_CUDA(cudaEventRecord(a, 0));
+            for (int i = 0; i < iters; ++i) f();
+            SGB_CUDA(cudaEventRecord(b, 0));
+            SGB_CUDA(cudaEventSynchronize(b));
+            float ms = 0.f;
+            SGB_CUDA(cudaEventElapsedTime(&ms, a, b));
+            return static_cast<double>(ms) / iters;
+        };
+        *ms_row = time([&] { c.run_row(); });
+        *ms_tree = time([&] { c.run_tree(); });
+        *ms_decode = time([&] { c.run_decode(); });
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
     });
 }
 

@@ -652,7 +652,11 @@ void Engine::forward(const Fwd& f) {
     }
     // tree verify / draft levels: attention_tree.cu (one CTA per row tile and head)
     int tree_w = 0, n_ttiles = 0, tree_nodes = 0;
-    if (f.tree) {
+    if (f.tree && f.decode) {
+        if (f.tree->size() > static_cast<size_t>(max_seqs_ + max_rows_))
+            throw std::logic_error("forward: decode attention groups exceed capacity");
+        h2d(d_tgroups_, f.tree->data(), f.tree->size(), st_);
+    } else if (f.tree) {
         int mx = 1;
         for (const auto& g : *f.tree) {
             mx = std::max(mx, g.nrows);
@@ -692,7 +696,11 @@ void Engine::forward(const Fwd& f) {
         eq.d = d;
         gemm(W.qkv, act_a_, M, eq, kClsGemm, 8.0 / 3.0);
         e0 = pbeg();
-        if (f.tree)
+        if (f.tree && f.decode)
+            launch_attention_decode(q_, f.draft ? dkmap_ : tkmap_, f.draft ? dvmap_ : tvmap_,
+                                    static_cast<long long>(l) * kv.n_slots, eq.K, eq.V, d_tgroups_,
+                                    static_cast<int>(f.tree->size()), f.decode_max_ctx, H, d, att_, st_);
+        else if (f.tree)
             launch_attention_tree(q_, f.draft ? dkmap_ : tkmap_, f.draft ? dvmap_ : tvmap_,
                                   static_cast<long long>(l) * kv.n_slots, eq.K, eq.V, ar, d_tgroups_, d_ttiles_, n_ttiles,
                                   tree_w, H, d, tree_nodes, att_, st_);
@@ -1612,6 +1620,19 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
         // > 8 rows per sequence (B=1 x 211 rows: 0.057 vs 0.083 ms per layer; 16 x 13: 0.135 vs 0.166),
         // attention.cu's merged shared tiles with fewer (48 x 4 rows over 2.2k keys: 0.324 vs 0.391)
         if (((!all_ar && max_sel > 8) || (all_ar && vrows <= tree_ar_max)) && tree_attn_ok(max_sel)) f.tree = &tgroups_;
+        // AR steps of few rows: the cluster decode kernel (attention_tree.cu) spreads each row's
+        // key blocks over up to 8 CTAs instead of one warp per row (tree kernel) or attention.cu's
+        // global-partials work list
+        static const int decode_ar_max = [] {
+            // measured crossover vs attention.cu (profiles/r02_decode_attn.jsonl): <= 4 rows
+            const char* v = getenv("SGB_DECODE_AR_MAX");  // A/B switch
+            return v ? atoi(v) : 4;
+        }();
+        if (all_ar && vrows <= decode_ar_max) {
+            f.tree = &tgroups_;
+            f.decode = true;
+            f.decode_max_ctx = max_p;
+        }
         f.merge_tiles = !all_ar;  // verify tiles of a speculative step (not the AR prompt tiles)
         // measured A/B (SGB_PROMPT_TILES, bench.py vanilla): +5 % at 12 heads (c2), -13 % at
         // 28 heads (c3, where the per-row kernel already hits the prompt pages in L2)

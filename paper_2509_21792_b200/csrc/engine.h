@@ -235,6 +235,9 @@ class Engine {
         const std::vector<TreeGroupDev>* tree = nullptr;
         // attention.cu shared tiles may merge block partials in registers (not the AR prompt tiles)
         bool merge_tiles = false;
+        // AR step of few rows: `tree` holds one group per row, run by the cluster decode kernel
+        bool decode = false;
+        int decode_max_ctx = 0;
     };
     void forward(const Fwd& f);
     bool boundary_tiles() const;

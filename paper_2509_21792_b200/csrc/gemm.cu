@@ -72,10 +72,13 @@ constexpr int cq_for(int BN) { return BN >= 256 ? 4 : 2; }
 constexpr int threads_for(int BN) { return 64 + 128 * cq_for(BN); }
 constexpr int kNumSMs = 148;
 
-template <int BN>
+// PAIR: the CTA pair (cta_group::2) form -- a 256-feature tile per 2-CTA cluster, each CTA
+// holding its 128 weight rows and half of the token rows (BN / 2) in shared memory
+template <int BN, bool PAIR = false>
 struct GemmCfg {
     static constexpr int kSub = BN <= 32 ? SGB_KSUB32 : (BN == 64 ? SGB_KSUB64 : (BN == 128 ? SGB_KSUB128 : 1));
-    static constexpr int kBBytes = BN * kBK * 2;
+    static constexpr int kBRows = PAIR ? BN / 2 : BN;
+    static constexpr int kBBytes = kBRows * kBK * 2;
     static constexpr int kStage = kSub * (kABytes + kBBytes);
     static constexpr int kStages = (SGB_GEMM_SMEM_KB * 1024) / kStage > 8 ? 8 : (SGB_GEMM_SMEM_KB * 1024) / kStage;
     static constexpr int kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;
@@ -163,15 +166,23 @@ struct Unit {
 
 // Units are tile-major (the K splits of a tile are adjacent), so the splits of a tile run
 // concurrently and the finisher work is spread over the launch instead of its last wave.
-__device__ __forceinline__ Unit decode_unit(int u, int m_tiles, int S, int BN) {
+// tw: features per tile (128, or 256 for a CTA pair), noff: this CTA's offset inside it
+__device__ __forceinline__ Unit decode_unit(int u, int m_tiles, int S, int BN, int tw = kBM, int noff = 0) {
     Unit r;
     r.tile = u / S;
     r.split = u - r.tile * S;
     const int mt = r.tile % m_tiles;
     const int nt = r.tile / m_tiles;
     r.m0 = mt * BN;
-    r.n0 = nt * kBM;
+    r.n0 = nt * tw + noff;
     return r;
+}
+
+// MMA width of a token tile: its valid rows rounded up to 16 (32 for a pair: each CTA's half
+// of B stays a multiple of 16 rows)
+__device__ __forceinline__ int mma_width(int rows, int BN, bool pair) {
+    const int g = pair ? 32 : 16;
+    return min(BN, max(g, (rows + g - 1) / g * g));
 }
 
 // The stage sequence of a CTA: units u = blockIdx.x + k*gridDim.x, each unit's chunks in
@@ -200,12 +211,13 @@ struct StageSeq {
     }
 };
 
-template <int BN, bool PART>
+template <int BN, bool PART, bool PAIR>
 __global__ void __launch_bounds__(threads_for(BN), 1)
     gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap mapW, const __grid_constant__ CUtensorMap mapX, int M,
                         int N, int kb_total, int n_chunks, int ckb, int cps, int S, int m_tiles, int n_tiles, GemmEpi epi,
                         float* __restrict__ ws, int* __restrict__ ctr, int pf_boxes) {
-    using Cfg = GemmCfg<BN>;
+    using Cfg = GemmCfg<BN, PAIR>;
+    constexpr int TW = PAIR ? 2 * kBM : kBM;
     constexpr int SUB = Cfg::kSub;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -218,29 +230,38 @@ __global__ void __launch_bounds__(threads_for(BN), 1)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n_units = m_tiles * n_tiles * S;
+    // pair: rank 0 (leader) issues the MMAs; full / tempty barriers live in the leader
+    const int rank = PAIR ? static_cast<int>(cluster_rank()) : 0;
+    const int noff = rank * kBM;
 
     if (warp == 0 && lane == 0) {
         tma_prefetch(&mapW);
         tma_prefetch(&mapX);
         for (int s = 0; s < Cfg::kStages; ++s) {
-            mbar_init(&full[s], 1);
+            mbar_init(&full[s], PAIR ? 2 : 1);
             mbar_init(&empty[s], 1);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], Cfg::kEpiThreads / 32);
+            mbar_init(&tempty[b], (PAIR ? 2 : 1) * Cfg::kEpiThreads / 32);
         }
         fence_barrier_init();
     }
-    if (warp == 1) tmem_alloc<Cfg::kTmemCols>(tmem_slot);
-    tc_fence_before();
-    __syncthreads();
+    if constexpr (PAIR) {
+        if (warp == 1) tmem_alloc_pair<Cfg::kTmemCols>(tmem_slot);
+        tc_fence_before();
+        cluster_sync_all();
+    } else {
+        if (warp == 1) tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+        tc_fence_before();
+        __syncthreads();
+    }
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     StageSeq seq0;
-    seq0.u = blockIdx.x;
+    seq0.u = PAIR ? blockIdx.x / 2 : blockIdx.x;
     seq0.n_units = n_units;
-    seq0.stride = gridDim.x;
+    seq0.stride = PAIR ? gridDim.x / 2 : gridDim.x;
     seq0.S = S;
     seq0.cps = cps;
     seq0.nc = n_chunks;
@@ -259,14 +280,22 @@ __global__ void __launch_bounds__(threads_for(BN), 1)
             int pre_kb[Cfg::kStages], pre_ns[Cfg::kStages], pre_m0[Cfg::kStages];
             for (; npre < Cfg::kStages && sq.valid(); ++npre) {
                 const int ns = min(SUB, sq.hi - sq.kb);
-                const Unit un = decode_unit(sq.u, m_tiles, S, BN);
+                const Unit un = decode_unit(sq.u, m_tiles, S, BN, TW, noff);
                 uint8_t* a = smem + npre * Cfg::kStage;
-                mbar_arrive_expect_tx(&full[npre], ns * (kABytes + Cfg::kBBytes));
-                for (int j = 0; j < ns; ++j)
-                    tma_load_2d_hint(a + j * kABytes, &mapW, &full[npre], (sq.kb + j) * kBK, un.n0, pol_w);
+                if constexpr (PAIR) {
+                    const uint32_t fb = mapa_u32(&full[npre], 0);
+                    mbar_arrive_expect_tx_remote(fb, ns * (kABytes + Cfg::kBBytes));
+                    for (int j = 0; j < ns; ++j)
+                        tma_load_2d_pair_hint(a + j * kABytes, &mapW, fb, (sq.kb + j) * kBK, un.n0, pol_w);
+                    pre_m0[npre] = un.m0 + rank * (mma_width(M - un.m0, BN, true) / 2);
+                } else {
+                    mbar_arrive_expect_tx(&full[npre], ns * (kABytes + Cfg::kBBytes));
+                    for (int j = 0; j < ns; ++j)
+                        tma_load_2d_hint(a + j * kABytes, &mapW, &full[npre], (sq.kb + j) * kBK, un.n0, pol_w);
+                    pre_m0[npre] = un.m0;
+                }
                 pre_kb[npre] = sq.kb;
                 pre_ns[npre] = ns;
-                pre_m0[npre] = un.m0;
                 sq.next(SUB);
             }
             // (1b) HBM-bound token tiles: the following weight boxes go to L2 as well, so the
@@ -276,7 +305,7 @@ __global__ void __launch_bounds__(threads_for(BN), 1)
                 StageSeq pq = sq;
                 for (int n = 0; n < pf_boxes && pq.valid(); pq.next(SUB)) {
                     const int ns = min(SUB, pq.hi - pq.kb);
-                    const Unit un = decode_unit(pq.u, m_tiles, S, BN);
+                    const Unit un = decode_unit(pq.u, m_tiles, S, BN, TW, noff);
                     for (int j = 0; j < ns; ++j, ++n) tma_prefetch_l2_2d(&mapW, (pq.kb + j) * kBK, un.n0);
                 }
             }
@@ -285,20 +314,35 @@ __global__ void __launch_bounds__(threads_for(BN), 1)
             pdl_trigger();
             for (int s = 0; s < npre; ++s) {
                 uint8_t* b = smem + s * Cfg::kStage + SUB * kABytes;
-                for (int j = 0; j < pre_ns[s]; ++j)
-                    tma_load_2d(b + j * Cfg::kBBytes, &mapX, &full[s], (pre_kb[s] + j) * kBK, pre_m0[s]);
+                for (int j = 0; j < pre_ns[s]; ++j) {
+                    if constexpr (PAIR)
+                        tma_load_2d_pair(b + j * Cfg::kBBytes, &mapX, mapa_u32(&full[s], 0), (pre_kb[s] + j) * kBK,
+                                         pre_m0[s]);
+                    else
+                        tma_load_2d(b + j * Cfg::kBBytes, &mapX, &full[s], (pre_kb[s] + j) * kBK, pre_m0[s]);
+                }
             }
             // (3) steady state
             for (int i = npre; sq.valid(); ++i, sq.next(SUB)) {
                 const int s = i % Cfg::kStages;
                 mbar_wait(&empty[s], ((i / Cfg::kStages) & 1) ^ 1);
                 const int ns = min(SUB, sq.hi - sq.kb);
-                const Unit un = decode_unit(sq.u, m_tiles, S, BN);
+                const Unit un = decode_unit(sq.u, m_tiles, S, BN, TW, noff);
                 uint8_t* a = smem + s * Cfg::kStage;
-                mbar_arrive_expect_tx(&full[s], ns * (kABytes + Cfg::kBBytes));
-                for (int j = 0; j < ns; ++j) {
-                    tma_load_2d_hint(a + j * kABytes, &mapW, &full[s], (sq.kb + j) * kBK, un.n0, pol_w);
-                    tma_load_2d(a + SUB * kABytes + j * Cfg::kBBytes, &mapX, &full[s], (sq.kb + j) * kBK, un.m0);
+                if constexpr (PAIR) {
+                    const uint32_t fb = mapa_u32(&full[s], 0);
+                    const int xm = un.m0 + rank * (mma_width(M - un.m0, BN, true) / 2);
+                    mbar_arrive_expect_tx_remote(fb, ns * (kABytes + Cfg::kBBytes));
+                    for (int j = 0; j < ns; ++j) {
+                        tma_load_2d_pair_hint(a + j * kABytes, &mapW, fb, (sq.kb + j) * kBK, un.n0, pol_w);
+                        tma_load_2d_pair(a + SUB * kABytes + j * Cfg::kBBytes, &mapX, fb, (sq.kb + j) * kBK, xm);
+                    }
+                } else {
+                    mbar_arrive_expect_tx(&full[s], ns * (kABytes + Cfg::kBBytes));
+                    for (int j = 0; j < ns; ++j) {
+                        tma_load_2d_hint(a + j * kABytes, &mapW, &full[s], (sq.kb + j) * kBK, un.n0, pol_w);
+                        tma_load_2d(a + SUB * kABytes + j * Cfg::kBBytes, &mapX, &full[s], (sq.kb + j) * kBK, un.m0);
+                    }
                 }
             }
         } else {
@@ -308,20 +352,20 @@ __global__ void __launch_bounds__(threads_for(BN), 1)
     } else if (warp == 1) {
         pdl_wait();
         pdl_trigger();
-        if (lane == 0) {
+        if (lane == 0 && rank == 0) {
             // MMA width = the tile's valid token rows rounded up to 16 (tcgen05 N granularity):
             // a 211-row tile issues 224-wide MMAs, not 256. Output columns are independent, so
             // the width never changes an element's bits (test_gemm_batch_invariance).
-            uint32_t idesc = idesc_bf16_m128(BN);
+            uint32_t idesc = PAIR ? idesc_bf16_m256(BN) : idesc_bf16_m128(BN);
             StageSeq sq = seq0;
             int i = 0, it = -1, cur_c = -1, cur_u = -1;
             for (; sq.valid(); ++i) {
                 const bool chunk_start = (sq.u != cur_u || sq.c != cur_c);
                 if (chunk_start) {
                     if (sq.u != cur_u) {
-                        const int rows = M - decode_unit(sq.u, m_tiles, S, BN).m0;
-                        const int n_eff = min(BN, max(16, (rows + 15) / 16 * 16));
-                        idesc = idesc_bf16_m128(static_cast<uint32_t>(n_eff));
+                        const int n_eff = mma_width(M - decode_unit(sq.u, m_tiles, S, BN).m0, BN, PAIR);
+                        idesc = PAIR ? idesc_bf16_m256(static_cast<uint32_t>(n_eff))
+                                     : idesc_bf16_m128(static_cast<uint32_t>(n_eff));
                     }
                     cur_u = sq.u;
                     cur_c = sq.c;
@@ -341,11 +385,22 @@ __global__ void __launch_bounds__(threads_for(BN), 1)
                 for (int j = 0; j < ns; ++j) {
                     const uint64_t adesc = sw128_desc(a + j * kABytes), bdesc = sw128_desc(b + j * Cfg::kBBytes);
 #pragma unroll
-                    for (int k = 0; k < kBK / 16; ++k)
-                        umma_bf16(tmem + buf * BN, adesc + 2 * k, bdesc + 2 * k, idesc, (!first || j != 0 || k != 0));
+                    for (int k = 0; k < kBK / 16; ++k) {
+                        if constexpr (PAIR)
+                            umma_bf16_pair(tmem + buf * BN, adesc + 2 * k, bdesc + 2 * k, idesc,
+                                           (!first || j != 0 || k != 0));
+                        else
+                            umma_bf16(tmem + buf * BN, adesc + 2 * k, bdesc + 2 * k, idesc,
+                                      (!first || j != 0 || k != 0));
+                    }
                 }
-                umma_commit(&empty[s]);
-                if (chunk_end) umma_commit(&tfull[buf]);
+                if constexpr (PAIR) {
+                    umma_commit_pair(&empty[s], 0x3);
+                    if (chunk_end) umma_commit_pair(&tfull[buf], 0x3);
+                } else {
+                    umma_commit(&empty[s]);
+                    if (chunk_end) umma_commit(&tfull[buf]);
+                }
                 sq.next(SUB);
             }
         }
@@ -359,13 +414,14 @@ __global__ void __launch_bounds__(threads_for(BN), 1)
         const int r = 32 * q + lane;
         const int j0 = h * HB;
         int it = 0;
-        for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-            const Unit un = decode_unit(u, m_tiles, S, BN);
+        for (int u = seq0.u; u < n_units; u += seq0.stride) {
+            const Unit un = decode_unit(u, m_tiles, S, BN, TW, noff);
+            const int ctile = PAIR ? 2 * un.tile + rank : un.tile;  // 128-feature tile: finisher state
             const int o = un.n0 + r;
             const int ncols = min(BN, M - un.m0);
             const int nmine = max(0, min(HB, ncols - j0));
             const int c_begin = un.split * cps, c_end = min(n_chunks, c_begin + cps);
-            float* wst = ws ? ws + static_cast<size_t>(un.tile) * n_chunks * BN * kBM : nullptr;
+            float* wst = ws ? ws + static_cast<size_t>(ctile) * n_chunks * BN * kBM : nullptr;
             // 256-token tiles run only single-chunk weights (gemm_run), so their pieces are final
             constexpr bool kOneChunk = (BN == 256);
             float run[(PART || kOneChunk) ? 1 : HB];  // the chunk-ordered running sum
@@ -402,7 +458,10 @@ __global__ void __launch_bounds__(threads_for(BN), 1)
                 }
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&tempty[buf]);
+                if (lane == 0) {
+                    if constexpr (PAIR) mbar_arrive_remote(mapa_u32(&tempty[buf], 0));
+                    else mbar_arrive(&tempty[buf]);
+                }
             }
             if constexpr (PART || kOneChunk) {
                 // raw chunk sums / single-chunk results already stored
@@ -416,7 +475,7 @@ __global__ void __launch_bounds__(threads_for(BN), 1)
                 __threadfence();
                 epi_bar<Cfg::kEpiThreads>();
                 if (threadIdx.x == 64) {
-                    const int old = atomicAdd(&ctr[un.tile], 1);
+                    const int old = atomicAdd(&ctr[ctile], 1);
                     *last_flag = (old == S - 1);
                 }
                 epi_bar<Cfg::kEpiThreads>();
@@ -453,15 +512,20 @@ __global__ void __launch_bounds__(threads_for(BN), 1)
                                 if (jb + t < j0 + nmine) epi_store(epi, un.m0 + jb + t, o, v[t]);
                         }
                     }
-                    if (threadIdx.x == 64) ctr[un.tile] = 0;
+                    if (threadIdx.x == 64) ctr[ctile] = 0;
                 }
                 epi_bar<Cfg::kEpiThreads>();  // last_flag is reused by the next unit
             }
         }
     }
     tc_fence_before();
-    __syncthreads();
-    if (warp == 1) tmem_dealloc<Cfg::kTmemCols>(tmem);
+    if constexpr (PAIR) {
+        cluster_sync_all();  // the leader's MMAs read the peer's shared memory / write its TMEM
+        if (warp == 1) tmem_dealloc_pair<Cfg::kTmemCols>(tmem);
+    } else {
+        __syncthreads();
+        if (warp == 1) tmem_dealloc<Cfg::kTmemCols>(tmem);
+    }
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
@@ -476,17 +540,40 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     return fn;
 }
 
-template <int BN, bool PART>
+template <int BN, bool PART, bool PAIR = false>
 void launch_bn(const CUtensorMap& w, const CUtensorMap& x, int M, int N, int kbt, int n_chunks, int ckb, int S, int cps,
                const GemmEpi& epi, float* ws, int* ctr, cudaStream_t st) {
-    using Cfg = GemmCfg<BN>;
+    using Cfg = GemmCfg<BN, PAIR>;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(gemm_bf16_tn_kernel<BN, PART>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
+        cudaFuncSetAttribute(gemm_bf16_tn_kernel<BN, PART, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             Cfg::kSmem);
         attr = true;
     }
-    const int m_tiles = (M + BN - 1) / BN, n_tiles = (N + kBM - 1) / kBM;
+    constexpr int TW = PAIR ? 2 * kBM : kBM;
+    const int m_tiles = (M + BN - 1) / BN, n_tiles = (N + TW - 1) / TW;
     const int units = m_tiles * n_tiles * S;
+    if constexpr (PAIR) {
+        // one unit per CTA pair per round; the 2-CTA cluster maps onto one TPC
+        const int grid = 2 * std::min(units, kNumSMs / 2);
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(Cfg::kThreads);
+        cfg.dynamicSmemBytes = Cfg::kSmem;
+        cfg.stream = st;
+        cudaLaunchAttribute at[2];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[1].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 2;
+        cudaLaunchKernelEx(&cfg, gemm_bf16_tn_kernel<BN, PART, true>, w, x, M, N, kbt, n_chunks, ckb, cps, S, m_tiles,
+                           n_tiles, epi, ws, ctr, 0);
+        return;
+    }
     const int grid = std::min(units, kNumSMs);
     // L2 prefetch budget for the weight stream of HBM-bound (<= 32-token) tiles, in MB over
     // the whole grid. A/B switch only, off by default: measured at the 7B shape, 48 MB made
@@ -497,7 +584,7 @@ void launch_bn(const CUtensorMap& w, const CUtensorMap& x, int M, int N, int kbt
         return v ? atoi(v) : 0;
     }();
     const int pf_boxes = BN <= 32 ? static_cast<int>((static_cast<long long>(pf_mb) << 20) / grid / kABytes) : 0;
-    launch_pdl(gemm_bf16_tn_kernel<BN, PART>, dim3(grid), dim3(Cfg::kThreads), Cfg::kSmem, st, w, x, M, N, kbt, n_chunks, ckb,
+    launch_pdl(gemm_bf16_tn_kernel<BN, PART, false>, dim3(grid), dim3(Cfg::kThreads), Cfg::kSmem, st, w, x, M, N, kbt, n_chunks, ckb,
                cps, S, m_tiles, n_tiles, epi, ws, ctr, pf_boxes);
 }
 
@@ -571,6 +658,20 @@ int gemm_bn_for(int M) {
     return max_bn >= 256 ? 256 : 128;
 }
 
+// CTA-pair (cta_group::2) tiles for 128- and 256-token tiles: each SM receives half of the
+// token tile (the operand bytes per MMA flop drop by a third). Bit-identical to the 1-CTA
+// kernel (test_gemm_batch_invariance, spec == AR rollouts) but not faster: measured
+// (profiles/r02_gemm_pair_sweep.jsonl, ncu in profiles/README.md) the producer waits on free
+// stages, i.e. the MMA issue rate -- not the TMA delivery -- bounds these shapes, and the pair
+// is 0-8 % slower at the c2 shapes. Off by default; SGB_GEMM_PAIR=1 selects it.
+bool gemm_pair() {
+    static const bool on = [] {
+        const char* v = getenv("SGB_GEMM_PAIR");
+        return v ? atoi(v) != 0 : false;
+    }();
+    return on;
+}
+
 // K split: which CTA computes which chunks. Any choice gives identical bits.
 int gemm_splits_for(int M, int N, int K) {
     const int bn = gemm_bn_for(M);
@@ -593,7 +694,8 @@ int gemm_splits_for(int M, int N, int K) {
 
 size_t gemm_ws_floats(int M, int N, int K) {
     const int bn = gemm_bn_for(M);
-    const size_t tiles = static_cast<size_t>((M + bn - 1) / bn) * ((N + kBM - 1) / kBM);
+    // 128-feature tiles, rounded up to whole CTA pairs
+    const size_t tiles = static_cast<size_t>((M + bn - 1) / bn) * (2 * ((N + 2 * kBM - 1) / (2 * kBM)));
     return tiles * chunks_of(N, K) * bn * kBM;
 }
 
@@ -616,6 +718,12 @@ void gemm_run(const GemmWeight& w, const GemmAct& x, int M, const GemmEpi& epi, 
             return v ? atoi(v) : 0;
         }();
         const int pbn = part_bn > 0 && M > 128 ? part_bn : (M > 384 ? 256 : std::max(64, bn));
+        if (gemm_pair() && pbn >= 128) {
+            const CUtensorMap& xm = x.map_for_bn(pbn / 2);
+            if (pbn == 256) launch_bn<256, true, true>(w.map, xm, M, w.N, kbt, nc, ckb, nc, 1, epi, nullptr, nullptr, st);
+            else launch_bn<128, true, true>(w.map, xm, M, w.N, kbt, nc, ckb, nc, 1, epi, nullptr, nullptr, st);
+            return;
+        }
         const CUtensorMap& xm = x.map_for_bn(pbn);
         if (pbn == 256) launch_bn<256, true>(w.map, xm, M, w.N, kbt, nc, ckb, nc, 1, epi, nullptr, nullptr, st);
         else if (pbn == 128) launch_bn<128, true>(w.map, xm, M, w.N, kbt, nc, ckb, nc, 1, epi, nullptr, nullptr, st);
@@ -626,6 +734,12 @@ void gemm_run(const GemmWeight& w, const GemmAct& x, int M, const GemmEpi& epi, 
     const int cps = (nc + S - 1) / S;
     S = (nc + cps - 1) / cps;
     const int bn_run = (bn == 256 && (nc > 1 || S > 1)) ? 128 : bn;  // 256-token tiles: single-chunk weights
+    if (gemm_pair() && bn_run >= 128) {
+        const CUtensorMap& xp = x.map_for_bn(bn_run / 2);
+        if (bn_run == 256) launch_bn<256, false, true>(w.map, xp, M, w.N, kbt, nc, ckb, S, cps, epi, ws.buf, ws.ctr, st);
+        else launch_bn<128, false, true>(w.map, xp, M, w.N, kbt, nc, ckb, S, cps, epi, ws.buf, ws.ctr, st);
+        return;
+    }
     const CUtensorMap& xm = x.map_for_bn(bn_run);
     switch (bn_run) {
         case 16: launch_bn<16, false>(w.map, xm, M, w.N, kbt, nc, ckb, S, cps, epi, ws.buf, ws.ctr, st); break;

@@ -99,6 +99,11 @@ int tree_attn_warps(int max_rows_per_group, int n_groups, int H, int dh, int max
 void build_tree_tiles(const std::vector<TreeGroupDev>& groups, int W, std::vector<TreeTileDev>& out);
 // kmap / vmap: 2-D TMA maps over the store viewed as [layers * n_slots][d] (16 x 64 boxes,
 // SWIZZLE_128B); layer_row0 = layer * n_slots; K / V: this layer's [n_slots][d] base
+// AR steps (one row per group): a (row, head)'s 64-key blocks over a cluster of CTAs and their
+// warps, block partials merged in order through distributed shared memory
+void launch_attention_decode(const float* q, const CUtensorMap& kmap, const CUtensorMap& vmap, long long layer_row0,
+                             const __nv_bfloat16* K, const __nv_bfloat16* V, const TreeGroupDev* groups, int n_groups,
+                             int max_ctx, int H, int d, __nv_bfloat16* out, cudaStream_t st);
 void launch_attention_tree(const float* q, const CUtensorMap& kmap, const CUtensorMap& vmap, long long layer_row0,
                            const __nv_bfloat16* K, const __nv_bfloat16* V, const AttnRowsDev& rows,
                            const TreeGroupDev* groups, const TreeTileDev* tiles, int n_tiles, int W, int H, int d,

@@ -107,3 +107,23 @@ def test_group_attention_ragged_and_repeated_launches():
     _, g2 = c.debug_tree_attention([40, 129], [par2, par], np.concatenate([q2, q]), np.concatenate([k2, kc]),
                                    np.concatenate([k2, vc]), np.concatenate([n2, kn]), np.concatenate([n2, vn]), H)
     assert np.array_equal(g2[20:], a_grp)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("H,dh", [(28, 128), (4, 64)])
+def test_decode_attention_bitwise(H, dh):
+    """The cluster decode kernel (AR steps) gives attention.cu's bits: ragged contexts around the
+    16-key chunk and 64-key block edges, up to a few thousand keys (clusters of 1..8 CTAs)."""
+    from paper_2509_21792_b200 import capi as c
+    d = H * dh
+    rng = np.random.default_rng(17)
+    for ctx in ([1, 15, 16, 17, 63, 64, 65, 127, 200], [640], [4100, 33], [1000] * 3):
+        n = sum(ctx)
+        q = rng.standard_normal((len(ctx), d)).astype(np.float32)
+        kc = rng.standard_normal((n, d)).astype(np.float32)
+        vc = rng.standard_normal((n, d)).astype(np.float32)
+        kn = rng.standard_normal((len(ctx), d)).astype(np.float32)
+        vn = rng.standard_normal((len(ctx), d)).astype(np.float32)
+        o_row, o_dec = c.debug_attention_decode(ctx, q, kc, vc, kn, vn, H)
+        assert np.array_equal(o_row, o_dec), (ctx, np.argwhere(o_row != o_dec)[:5])
+        assert np.isfinite(o_dec).all()

@@ -273,3 +273,31 @@ def test_attention_long_context_and_launch_shape_invariance(H, dh):
     big_v = vs + [rng.standard_normal((300, d)).astype(np.float32) for _ in range(40)]
     big = c.debug_attention(big_q, big_k, big_v, H)
     assert np.array_equal(big[:len(lens)], out)
+
+
+def test_gemm_pair_bitwise(tmp_path):
+    """The CTA-pair (cta_group::2) GEMM (SGB_GEMM_PAIR=1, a separate process: the switch is read
+    once) gives the 1-CTA kernel's bits, incl. a forced K split."""
+    import os
+    import subprocess
+    import sys
+    c = capi()
+    rng = np.random.default_rng(21)
+    w = rng.standard_normal((640, 1536)).astype(np.float32) * 0.05
+    x = rng.standard_normal((300, 1536)).astype(np.float32)
+    np.save(tmp_path / "w.npy", w)
+    np.save(tmp_path / "x.npy", x)
+    ref = {m: c.debug_gemm(w, x[:m])[0] for m in (65, 128, 211, 300)}
+    ref_s = c.debug_gemm(w, x[:200], splits=3)[0]
+    code = (
+        "import numpy as np, sys; sys.path.insert(0, '.')\n"
+        "from paper_2509_21792_b200 import capi as c\n"
+        f"w = np.load(r'{tmp_path / 'w.npy'}'); x = np.load(r'{tmp_path / 'x.npy'}')\n"
+        "for m in (65, 128, 211, 300): np.save(r'%s/p%%d.npy' %% m, c.debug_gemm(w, x[:m])[0])\n"
+        "np.save(r'%s/ps.npy', c.debug_gemm(w, x[:200], splits=3)[0])\n" % (tmp_path, tmp_path))
+    env = dict(os.environ, SGB_GEMM_PAIR="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    subprocess.run([sys.executable, "-c", code], check=True, env=env, cwd=root, timeout=300)
+    for m in (65, 128, 211, 300):
+        assert np.array_equal(np.load(tmp_path / f"p{m}.npy"), ref[m]), m
+    assert np.array_equal(np.load(tmp_path / "ps.npy"), ref_s)
