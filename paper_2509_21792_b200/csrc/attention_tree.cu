@@ -649,7 +649,15 @@ void launch_tree_impl(const float* q, const CUtensorMap& kmap, const CUtensorMap
     constexpr size_t stageK = static_cast<size_t>(kTChunk) * DH * 2;
     const size_t tbl = static_cast<size_t>(max_nodes) * (DH * 2 + 16) * 2;
     const size_t fixed = tbl + 8 * 24 + 4 * 72 * 8 + 1024;  // barriers, chain tables, alignment slack
-    int nst = 6;
+    // ring depth: 3 stages (measured, profiles/r02_tree_nst.jsonl): the per-chunk work of one
+    // consumer warp is latency-bound, so CTAs per SM matter more than stages per CTA -- 6 -> 3
+    // stages took the c5 verify shape (48 x 4 rows, ctx 2048, 32 heads) from 0.367 to 0.274 ms
+    // per layer (the AR launch of the same contexts: 0.277) and 16 x 13 rows from 0.134 to 0.075
+    static const int nst_env = [] {
+        const char* v = getenv("SGB_TREE_NST");  // tuning experiments only
+        return v ? std::max(2, std::min(8, atoi(v))) : 3;
+    }();
+    int nst = nst_env;
     while (nst > 2 && 2 * stageK * nst + fixed > static_cast<size_t>(kTSmem)) --nst;
     const size_t smem = 2 * stageK * nst + fixed;
     if (smem > static_cast<size_t>(kTSmem)) throw std::invalid_argument("tree attention: tree too large for shared memory");

@@ -1548,7 +1548,11 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
                     f.groups = &groups_;
                     f.groups_exact = boundary_tiles();
                     f.merge_tiles = true;
-                    if (kstep > 8 && tree_attn_ok(tr_.ds)) f.tree = &tgroups_;
+                    static const int lvl_min = [] {
+                        const char* v = getenv("SGB_TREE_LEVEL_MIN");  // A/B switch
+                        return v ? atoi(v) : 3;
+                    }();
+                    if (kstep >= lvl_min && tree_attn_ok(tr_.ds)) f.tree = &tgroups_;
                     forward(f);
                     res.draft_forwards++;
                     stat.draft_rows += R;
@@ -1616,10 +1620,15 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
             const char* v = getenv("SGB_TREE_AR_MAX");  // A/B switch
             return v ? atoi(v) : 0;
         }();
-        // measured (scripts/attn_check.sh, profiles/r02_attn_knobs2.jsonl): attention_tree.cu wins with
-        // > 8 rows per sequence (B=1 x 211 rows: 0.057 vs 0.083 ms per layer; 16 x 13: 0.135 vs 0.166),
-        // attention.cu's merged shared tiles with fewer (48 x 4 rows over 2.2k keys: 0.324 vs 0.391)
-        if (((!all_ar && max_sel > 8) || (all_ar && vrows <= tree_ar_max)) && tree_attn_ok(max_sel)) f.tree = &tgroups_;
+        // measured (profiles/r02_tree_nst.jsonl, 3-stage ring): attention_tree.cu wins from 3 rows per
+        // sequence (48 x 4 rows over 2k keys: 0.274 vs 0.364 ms per layer; 16 x 13: 0.075 vs 0.164;
+        // B=1 x 211: 0.057 vs 0.083), attention.cu's shared tiles at 2 (32 x 2 over 4k: 0.372 vs 0.471)
+        static const int tree_min_rows = [] {
+            const char* v = getenv("SGB_TREE_MIN_ROWS");  // A/B switch
+            return v ? atoi(v) : 3;
+        }();
+        if (((!all_ar && max_sel >= tree_min_rows) || (all_ar && vrows <= tree_ar_max)) && tree_attn_ok(max_sel))
+            f.tree = &tgroups_;
         // AR steps of few rows: the cluster decode kernel (attention_tree.cu) spreads each row's
         // key blocks over up to 8 CTAs instead of one warp per row (tree kernel) or attention.cu's
         // global-partials work list

@@ -1,6 +1,8 @@
 """Low-concurrency regime at the c2 (or --config c3) shape: per-step device time of AR vs speculative steps
 for B sequences (diagnostic for the concurrency-sweep tail). Timing runs are unprofiled; a
-second, profiled run gives the per-class split (events around every launch inflate it).
+second, profiled run gives the per-class split (events around every launch inflate it). Step
+times are the engine's per-decode-step CUDA-event times (prefill excluded); the class split
+subtracts a profiled prefill-only run.
 
     python scripts/bench_lowb.py [B ...] [--ncu] [--config=c3|c3r|c5] [--vanilla] [--ctx=N]
       (--ncu: one short run per mode, for ncu; --vanilla: AR steps only)
@@ -38,9 +40,17 @@ for B in [int(x) for x in (args or ["1", "4", "16", "64"])]:
         rp = eng.generate(pr, 1, mode=mode, **kw)
         eng.profile(False)
         prof = eng.read_profile(reset=True)
+        # prefill alone (no decode step), profiled: subtracted so the classes are decode-only
+        eng.profile(True)
+        eng.generate(pr, 1, mode=mode, **dict(kw, max_new_tokens=1))
+        eng.profile(False)
+        pre = eng.read_profile(reset=True)
         n = len(r.steps)
-        print(json.dumps(dict(B=B, mode=mode, steps=n, ms_per_step=round(1e3 * r.seconds / n, 3),
-                              profiled_ms_per_step=round(1e3 * rp.seconds / n, 3), tau=round(r.tau(), 3),
-                              tok_s=round(r.generated() / r.seconds, 1), nkl=r.steps[-1][1:4],
+        dec_s = sum(r.step_seconds) if r.step_seconds else r.seconds
+        cls = {k: round((v["ms"] - pre.get(k, {}).get("ms", 0.0)) / n, 3) for k, v in prof.items()}
+        print(json.dumps(dict(B=B, mode=mode, steps=n, ms_per_step=round(1e3 * dec_s / n, 3),
+                              profiled_ms_per_step=round(1e3 * sum(rp.step_seconds) / n, 3) if rp.step_seconds else None,
+                              tau=round(r.tau(), 3),
+                              tok_s=round(r.generated() / dec_s, 1), nkl=r.steps[-1][1:4],
                               launches_per_step=round(r.kernel_launches / n, 1),
-                              cls_ms_per_step={k: round(v["ms"] / n, 3) for k, v in prof.items()})), flush=True)
+                              cls_ms_per_step=cls)), flush=True)
