@@ -181,7 +181,7 @@ def ncu_traffic(name):
                 a = float(line.split()[-1])
     except OSError:
         return None, None, None
-    return t, a, (f"profiles/{name}: ncu --set full of the c2-shaped launch (512 rows x 641 keys)" if t else None)
+    return t, a, (f"profiles/{name}: ncu --set full of a c2 attention launch inside the bench workload (step 500, 512 rows x 629 keys)" if t else None)
 
 
 def measured_peaks():
@@ -500,7 +500,7 @@ def main():
     att = prof["attention"]
     ach = att["bytes"] / (att["ms"] * 1e-3) / 1e9 if att["ms"] else 0.0
     total_ms = sum(v["ms"] for v in prof.values())
-    traffic, traffic_alg, traffic_src = ncu_traffic("r01_attn_mma_c2_b512_ctx640.txt")
+    traffic, traffic_alg, traffic_src = ncu_traffic("r02_attn_c2_inworkload.txt")
     roofline = {"bound": "hbm", "kernel": "attn_kernel (mma.sync tree/paged KV attention: shared-prefix tiles, bulk-DMA ring, in-kernel block merge)",
                 "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s", "frac": round(ach / hbm, 4),
                 "traffic": traffic, "traffic_algorithmic": traffic_alg, "traffic_source": traffic_src,

@@ -303,6 +303,13 @@ int sgb_debug_attention_decode(int n_groups, const int* ctx_len, int H, int dh, 
 int sgb_bench_attention_decode(int B, int ctx, int H, int dh, int iters, double* ms_row, double* ms_tree,
                                double* ms_decode);
 
+/* Two-lane concurrency microbenchmark: one layer's attention (B rows x (ctx + 1) keys) on
+ * one stream and its four GEMMs (M rows, width H*dh, d_ff) on another, on persistent grids
+ * capped at attn_cap / gemm_cap SMs (0 = all). out[3] = ms per iteration: attention alone,
+ * GEMMs alone, both concurrently. */
+int sgb_bench_overlap(int B, int ctx, int H, int dh, int dff, int M, int attn_cap, int gemm_cap, int iters,
+                      double* out);
+
 /* Tree-verify attention microbenchmark: B sequences x (ctx committed keys + an EAGLE-shaped
  * tree of N rows); ms per launch of the per-row and of the prefix-shared group kernel. */
 int sgb_bench_tree_attention(int B, int N, int ctx, int H, int dh, int iters, double* ms_row, double* ms_group);

@@ -657,6 +657,17 @@ def bench_attention_decode(B: int, ctx: int, n_heads: int, dh: int = 128, iters:
 EXPORTED += ["sgb_debug_attention_decode", "sgb_bench_attention_decode"]
 
 
+def bench_overlap(B: int, ctx: int, n_heads: int, dff: int, M: int, attn_cap: int, gemm_cap: int, dh: int = 128,
+                  iters: int = 20):
+    """ms per iteration: (attention alone, layer GEMMs alone, both on two streams)."""
+    out = (C.c_double * 3)()
+    _check(_lib.sgb_bench_overlap(B, ctx, n_heads, dh, dff, M, attn_cap, gemm_cap, iters, out))
+    return out[0], out[1], out[2]
+
+
+EXPORTED += ["sgb_bench_overlap"]
+
+
 class PolicyTermsC(C.Structure):
     _fields_ = [("loss", C.c_double), ("tokens", C.c_longlong), ("rows", C.c_longlong), ("seconds", C.c_double),
                 ("skipped", C.c_int)]

@@ -710,7 +710,7 @@ void launch_impl(const float* q, const __nv_bfloat16* K, const __nv_bfloat16* V,
         const int threads = 32 * (QW * (H / G) + 1);
         const int by_regs = std::max(1, 65536 / (threads * ((regs + 7) / 8 * 8)));
         int n = 0;
-        while (n < std::min(by_regs, max_sm) && (n + 1) * (2 * stage_of(G) + fixed_of(G)) <= static_cast<size_t>(kSmemBudget) &&
+        while (n < std::min(by_regs, g_attn_sm_cap > 0 ? 1 : max_sm) && (n + 1) * (2 * stage_of(G) + fixed_of(G)) <= static_cast<size_t>(kSmemBudget) &&
                (n + 1) * threads <= 2048)
             ++n;
         return n;
@@ -746,7 +746,8 @@ void launch_impl(const float* q, const __nv_bfloat16* K, const __nv_bfloat16* V,
         attr = true;
     }
     if (static_cast<long long>(n_rows) * G > sc.ctr_cap) throw std::invalid_argument("attention: row tickets too small");
-    const long long grid = std::max(1LL, std::min<long long>(est_items * G, 148LL * per_sm));
+    long long grid = std::max(1LL, std::min<long long>(est_items * G, 148LL * per_sm));
+    if (g_attn_sm_cap > 0) grid = std::min<long long>(grid, g_attn_sm_cap);  // one CTA per SM on a subset of SMs
     launch_pdl(attn_kernel<DH, MERGE>, dim3(static_cast<unsigned>(grid)), dim3(threads), smem, st, q, K, V, rows, tiles,
                n_tiles, H, d, G, QW, nst, nb_max, balance, 1.0f / sqrtf(static_cast<float>(DH)), sc.part_acc, sc.part_ml,
                sc.row_ctr, out);
@@ -781,6 +782,8 @@ void launch_any(const float* q, const __nv_bfloat16* K, const __nv_bfloat16* V, 
 }
 
 }  // namespace
+
+int g_attn_sm_cap = 0;
 
 int attn_splits_for(int max_virtual_len) { return (max_virtual_len + kBlock - 1) / kBlock; }
 

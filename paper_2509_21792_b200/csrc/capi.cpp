@@ -1328,3 +1328,123 @@ int sgb_debug_gemm(const float* w, const float* x, int M, int N, int K, float* o
 }
 
 }  // extern "C"
+
+// Concurrency microbenchmark for the two-lane AR step: one decoder layer's attention
+// (B rows x (ctx + 1) keys, H heads of dh) on one stream and the layer's four GEMMs at M rows
+// (QKV, wo, w1, w2 of width d = H*dh and d_ff) on another, each on a capped persistent grid
+// (attn_cap / gemm_cap SMs, 0 = all). out[0..2] = ms per iteration: attention alone, GEMMs
+// alone, both streams concurrently.
+int sgb_bench_overlap(int B, int ctx, int H, int dh, int dff, int M, int attn_cap, int gemm_cap, int iters,
+                      double* out) {
+    return guarded([&] {
+        if (B <= 0 || M <= 0 || iters <= 0) throw std::invalid_argument("bench_overlap: bad shape");
+        const int d = H * dh;
+        const long long slots = static_cast<long long>(B) * (ctx + 1);
+        std::vector<void*> frees;
+        auto dmal = [&](size_t bytes) {
+            void* p = nullptr;
+            SGB_CUDA(cudaMalloc(&p, bytes));
+            SGB_CUDA(cudaMemset(p, 0, bytes));
+            frees.push_back(p);
+            return p;
+        };
+        auto* K = static_cast<__nv_bfloat16*>(dmal(slots * d * 2));
+        auto* V = static_cast<__nv_bfloat16*>(dmal(slots * d * 2));
+        SGB_CUDA(cudaMemset(K, 0x3c, slots * d * 2));
+        SGB_CUDA(cudaMemset(V, 0x3c, slots * d * 2));
+        auto* q = static_cast<float*>(dmal(static_cast<size_t>(B) * d * 4));
+        auto* ao = static_cast<__nv_bfloat16*>(dmal(static_cast<size_t>(B) * d * 2));
+        const int ns = sgb::attn_splits_for(ctx + 1);
+        sgb::AttnScratch sc{static_cast<float*>(dmal(static_cast<size_t>(B) * d * ns * 4)),
+                            static_cast<float*>(dmal(static_cast<size_t>(B) * H * ns * 8)), nullptr,
+                            static_cast<long long>(B) * H};
+        sc.row_ctr = static_cast<int*>(dmal(sc.ctr_cap * 4));
+        std::vector<long long> base(B), chain(static_cast<size_t>(B) * sgb::kMaxChain, 0);
+        std::vector<int> cl(B, ctx), chl(B, 1);
+        for (int b = 0; b < B; ++b) {
+            base[b] = static_cast<long long>(b) * (ctx + 1);
+            chain[static_cast<size_t>(b) * sgb::kMaxChain] = base[b] + ctx;
+        }
+        auto* dbase = static_cast<long long*>(dmal(B * 8));
+        auto* dchain = static_cast<long long*>(dmal(chain.size() * 8));
+        auto* dcl = static_cast<int*>(dmal(B * 4));
+        auto* dchl = static_cast<int*>(dmal(B * 4));
+        SGB_CUDA(cudaMemcpy(dbase, base.data(), B * 8, cudaMemcpyHostToDevice));
+        SGB_CUDA(cudaMemcpy(dchain, chain.data(), chain.size() * 8, cudaMemcpyHostToDevice));
+        SGB_CUDA(cudaMemcpy(dcl, cl.data(), B * 4, cudaMemcpyHostToDevice));
+        SGB_CUDA(cudaMemcpy(dchl, chl.data(), B * 4, cudaMemcpyHostToDevice));
+        sgb::AttnRowsDev ar{dbase, dcl, dchl, dchain};
+        const double keys = static_cast<double>(B) * (ctx + 1);
+        // the layer's GEMMs, weights in rotating copies (> L2) as in the rollout
+        const int shp[4][2] = {{3 * d, d}, {d, d}, {dff, d}, {d, dff}};
+        const int ncopy = 4;
+        std::vector<sgb::GemmWeight> gw(4 * ncopy);
+        for (int g = 0; g < 4; ++g)
+            for (int c = 0; c < ncopy; ++c) {
+                auto* w = static_cast<__nv_bfloat16*>(dmal(static_cast<size_t>(shp[g][0]) * shp[g][1] * 2));
+                gw[g * ncopy + c].init(w, shp[g][0], shp[g][1]);
+            }
+        const int cap = ((M + 255) / 256) * 256;
+        auto* xa = static_cast<__nv_bfloat16*>(dmal(static_cast<size_t>(cap) * std::max(d, dff) * 2));
+        sgb::GemmAct act_d, act_f;
+        act_d.init(xa, cap, d);
+        act_f.init(xa, cap, dff);
+        auto* yo = static_cast<float*>(dmal(static_cast<size_t>(M) * 3 * std::max(d, dff) * 4));
+        sgb::GemmWorkspace ws;
+        sgb::GemmEpi epi;
+        epi.kind = sgb::kEpiF32;
+        epi.f32 = yo;
+        cudaStream_t s1, s2;
+        SGB_CUDA(cudaStreamCreateWithFlags(&s1, cudaStreamNonBlocking));
+        SGB_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+        cudaEvent_t a, b, j;
+        SGB_CUDA(cudaEventCreate(&a));
+        SGB_CUDA(cudaEventCreate(&b));
+        SGB_CUDA(cudaEventCreate(&j));
+        int rot = 0;
+        auto attn = [&] {
+            sgb::g_attn_sm_cap = attn_cap;
+            sgb::launch_attention(q, K, V, slots, ar, B, H, d, ctx + 1, keys, sc, ao, s1);
+            sgb::g_attn_sm_cap = 0;
+        };
+        auto gemms = [&] {
+            sgb::g_gemm_sm_cap = gemm_cap;
+            for (int g = 0; g < 4; ++g) {
+                epi.ld = shp[g][0];
+                sgb::gemm_run(gw[g * ncopy + rot % ncopy], g == 3 ? act_f : act_d, M, epi, ws, s2, 1);
+            }
+            ++rot;
+            sgb::g_gemm_sm_cap = 0;
+        };
+        auto time = [&](bool ra, bool rg) {
+            for (int w = 0; w < 2; ++w) {
+                if (ra) attn();
+                if (rg) gemms();
+            }
+            SGB_CUDA(cudaDeviceSynchronize());
+            SGB_CUDA(cudaEventRecord(a, s1));
+            SGB_CUDA(cudaStreamWaitEvent(s2, a, 0));
+            for (int i = 0; i < iters; ++i) {
+                if (ra) attn();
+                if (rg) gemms();
+            }
+            SGB_CUDA(cudaEventRecord(j, s2));
+            SGB_CUDA(cudaStreamWaitEvent(s1, j, 0));
+            SGB_CUDA(cudaEventRecord(b, s1));
+            SGB_CUDA(cudaEventSynchronize(b));
+            SGB_KCHECK();
+            float ms = 0.f;
+            SGB_CUDA(cudaEventElapsedTime(&ms, a, b));
+            return static_cast<double>(ms) / iters;
+        };
+        out[0] = time(true, false);
+        out[1] = time(false, true);
+        out[2] = time(true, true);
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        cudaEventDestroy(j);
+        cudaStreamDestroy(s1);
+        cudaStreamDestroy(s2);
+        for (void* p : frees) cudaFree(p);
+    });
+}

@@ -46,6 +46,8 @@
 
 namespace sgb {
 
+int g_gemm_sm_cap = 0;
+
 namespace {
 
 #ifndef SGB_KSUB32
@@ -574,7 +576,7 @@ void launch_bn(const CUtensorMap& w, const CUtensorMap& x, int M, int N, int kbt
                            n_tiles, epi, ws, ctr, 0);
         return;
     }
-    const int grid = std::min(units, kNumSMs);
+    const int grid = std::min(units, g_gemm_sm_cap > 0 ? g_gemm_sm_cap : kNumSMs);
     // L2 prefetch budget for the weight stream of HBM-bound (<= 32-token) tiles, in MB over
     // the whole grid. A/B switch only, off by default: measured at the 7B shape, 48 MB made
     // the one-token QKV GEMM 17.4 -> 19.6 us and the B = 1 AR step 3.19 -> 3.50 ms

@@ -60,6 +60,9 @@ struct GemmWorkspace {
     int ctr_cap = 0;
 };
 
+// persistent-grid caps (0 = all SMs): a launch of a concurrent lane runs on a subset of the SMs
+extern int g_gemm_sm_cap;
+
 CUtensorMap make_kmajor_map(const void* ptr, int rows, int K, int box_rows);
 int gemm_bn_for(int M);
 int gemm_chunk_kb(int N, int K);

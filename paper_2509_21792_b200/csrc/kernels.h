@@ -51,6 +51,7 @@ struct AttnScratch {
     int* row_ctr;     // [ctr_cap], zero between launches
     long long ctr_cap;
 };
+extern int g_attn_sm_cap;  // attention.cu persistent grid cap (0 = every SM, several CTAs each)
 int attn_splits_for(int max_virtual_len);
 // Tiles of rows sharing keys (attention.cu): rows [row0, row0+nrows) read the same keys in
 // 64-key blocks [blo, bhi) -- one row, or up to 8*qw verify rows of one sequence over the
