@@ -432,6 +432,7 @@ def main():
     clocks.start()
     dev_s, wall_s, toks, launches, acc, slots, h2d, d2h = 0.0, 0.0, 0, 0, 0, 0, 0, 0
     spec_steps, upd_s, upd_wall, upd_rows = 0, 0.0, 0.0, 0
+    host_gap, host_enq, n_dec = 0.0, 0.0, 0
     terms = None
     last = None
     hbm0, tf0, _ = measured_peaks()
@@ -457,6 +458,9 @@ def main():
         h2d += r.h2d_bytes
         d2h += r.d2h_bytes
         spec_steps += sum(1 for s in r.steps if s[1] > 1)
+        host_gap += r.host_gap_seconds
+        host_enq += r.host_enqueue_seconds
+        n_dec += len(r.steps)
     clk = clocks.stop()
     # C2: statistics over the data-parallel group (NCCL); times take the max over ranks
     t_max, w_max = dev_s, wall_s
@@ -538,6 +542,14 @@ def main():
     }
     if roof_last:
         line["roofline"]["rollout"] = roof_last
+    if n_dec:
+        # the host side of the step loop (one sync per step): device idle from each step's end to
+        # the next step's first operation, and host time issuing a step -- what a device-resident
+        # (CUDA graph) step loop could remove
+        line["host_loop"] = {"decode_steps": n_dec, "gap_us_per_step": round(1e6 * host_gap / n_dec, 1),
+                             "gap_share_of_device_time": round(host_gap / dev_s, 4),
+                             "enqueue_us_per_step": round(1e6 * host_enq / n_dec, 1),
+                             "device_us_per_step": round(1e6 * (dev_s - upd_s) / n_dec, 1)}
     if w["online"]:
         line["online_draft_step"] = {"device_ms_per_step": round(1e3 * upd_s / args.steps, 2),
                                      "wall_ms_per_step": round(1e3 * upd_wall / args.steps, 2),

@@ -61,6 +61,9 @@ typedef struct sgb_rollout_stats {
     long long target_forwards, draft_forwards, kernel_launches;
     double seconds; /* device time of prefill + step loop, CUDA events (inputs resident) */
     long long h2d_bytes, d2h_bytes; /* host<->device bytes moved by the call */
+    /* host side of the step loop: device idle from a step's end to the next step's first
+     * operation (CUDA events), and host wall time issuing the steps (up to each step's sync) */
+    double host_gap_seconds, host_enqueue_seconds;
 } sgb_rollout_stats;
 
 typedef struct sgb_engine sgb_engine;

@@ -77,7 +77,7 @@ class RolloutStatsC(C.Structure):
     _fields_ = [("total_accepted", C.c_longlong), ("total_verify_slots", C.c_longlong), ("n_steps", C.c_int),
                 ("target_forwards", C.c_longlong), ("draft_forwards", C.c_longlong),
                 ("kernel_launches", C.c_longlong), ("seconds", C.c_double), ("h2d_bytes", C.c_longlong),
-                ("d2h_bytes", C.c_longlong)]
+                ("d2h_bytes", C.c_longlong), ("host_gap_seconds", C.c_double), ("host_enqueue_seconds", C.c_double)]
 
 
 LOGITS_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int),
@@ -206,6 +206,8 @@ class Rollout:
     h2d_bytes: int = 0
     d2h_bytes: int = 0
     step_seconds: Optional[List[float]] = None  # measured device seconds per decode step
+    host_gap_seconds: float = 0.0  # device idle between steps (host planning + launch latency)
+    host_enqueue_seconds: float = 0.0  # host wall time issuing the steps
 
     def tau(self) -> float:
         if self.total_verify_slots == 0:
@@ -390,7 +392,8 @@ class Engine:
             total_accepted=st.total_accepted, total_verify_slots=st.total_verify_slots,
             target_forwards=st.target_forwards, draft_forwards=st.draft_forwards,
             kernel_launches=st.kernel_launches, seconds=st.seconds, h2d_bytes=st.h2d_bytes,
-            d2h_bytes=st.d2h_bytes, step_seconds=step_s[:nst].tolist())
+            d2h_bytes=st.d2h_bytes, step_seconds=step_s[:nst].tolist(), host_gap_seconds=st.host_gap_seconds,
+            host_enqueue_seconds=st.host_enqueue_seconds)
 
     # ---- kernel-class profiler
     def profile(self, on: bool = True):

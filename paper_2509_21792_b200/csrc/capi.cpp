@@ -350,6 +350,8 @@ int sgb_rollout(sgb_engine* e, const int* prompts, const int* prompt_lens, int n
             stats->seconds = r.seconds;
             stats->h2d_bytes = r.h2d_bytes;
             stats->d2h_bytes = r.d2h_bytes;
+            stats->host_gap_seconds = r.host_gap_seconds;
+            stats->host_enqueue_seconds = r.host_enqueue_seconds;
         }
     });
 }

@@ -8,6 +8,7 @@
 // scheduler.cpp:14-54 -- pure integer work that needs the live count B_cur) and reads back
 // one small per-sequence result vector per step.
 #include <algorithm>
+#include <chrono>
 #include <cstdlib>
 #include <cstring>
 #include <thread>
@@ -170,6 +171,7 @@ Engine::Engine(const ModelDims& dims, int draft_layers, int device, int max_seqs
     SGB_CUDA(cudaEventCreate(&ev1_));
     SGB_CUDA(cudaEventCreate(&evs_a_));
     SGB_CUDA(cudaEventCreate(&evs_b_));
+    SGB_CUDA(cudaEventCreate(&evs_c_));
     tlay_ = FlatLayout::target(dims);
     dlay_ = FlatLayout::draft(dims, draft_layers);
 
@@ -340,6 +342,7 @@ Engine::~Engine() {
     if (ev1_) cudaEventDestroy(ev1_);
     if (evs_a_) cudaEventDestroy(evs_a_);
     if (evs_b_) cudaEventDestroy(evs_b_);
+    if (evs_c_) cudaEventDestroy(evs_c_);
     if (st_) cudaStreamDestroy(st_);
 }
 
@@ -1365,6 +1368,7 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
             if (sid_of[s] >= 0 && !fin[s]) live.push_back(s);
         const int B = static_cast<int>(live.size());
         if (B == 0) break;  // (pending groups are admitted at the end of the step that frees regions)
+        const auto t_host0 = std::chrono::steady_clock::now();
         const int eff_b = a.early_term ? B : n_seqs;
         SpecCfg cfg;
         if (a.mode == 0) cfg = SpecCfg{1, 0, 0};
@@ -1398,6 +1402,7 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
             if (k_eff) kstep = k_eff;
         }
         if (vrows > max_rows_) throw std::invalid_argument("generate: verify rows exceed engine max_rows");
+        SGB_CUDA(cudaEventRecord(evs_c_, st_));  // the step's first device operation
         h2d(steps_, hs.data(), B, st_);
         StepStat stat;
         stat.b_cur = B;
@@ -1689,10 +1694,13 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
         d2h(h_result_, result_, 2 * B, st_);
         d2h(h_result_ + 2 * B, err_, 1, st_);
         SGB_CUDA(cudaEventRecord(evs_b_, st_));
+        res.host_enqueue_seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t_host0).count();
         SGB_CUDA(cudaStreamSynchronize(st_));
         {
-            float ms = 0.f;
+            float ms = 0.f, gap = 0.f;
             SGB_CUDA(cudaEventElapsedTime(&ms, evs_a_, evs_b_));
+            SGB_CUDA(cudaEventElapsedTime(&gap, evs_a_, evs_c_));
+            res.host_gap_seconds += gap * 1e-3;
             res.step_seconds.push_back(ms * 1e-3);
             std::swap(evs_a_, evs_b_);
         }

@@ -95,6 +95,10 @@ struct RolloutResult {
     std::vector<double> step_seconds;  // device time of every decode step (CUDA events)
     std::vector<double> step_bytes, step_flops;  // SURVEY §8(d) algorithmic bytes / flops per step
     long long h2d_bytes = 0, d2h_bytes = 0;
+    // host side of the step loop: device idle between a step's end and its successor's first
+    // operation (host planning + launch latency; CUDA events) and host time spent issuing the
+    // steps (wall clock, up to the per-step sync) -- what a device-resident / graph loop could save
+    double host_gap_seconds = 0, host_enqueue_seconds = 0;
     bool waves = false;  // more sequences than KV regions: groups were admitted as regions freed
 };
 
@@ -400,7 +404,7 @@ class Engine {
     void policy_alloc();
     void policy_refresh_ref_weights();
     void wgrad(const __nv_bfloat16* dyT, int N, const __nv_bfloat16* xT, int Kfeat, int Rp, float* grad_dst, int ld);
-    cudaEvent_t ev0_ = nullptr, ev1_ = nullptr, evs_a_ = nullptr, evs_b_ = nullptr;  // rollout / per-step
+    cudaEvent_t ev0_ = nullptr, ev1_ = nullptr, evs_a_ = nullptr, evs_b_ = nullptr, evs_c_ = nullptr;  // rollout / per-step
 };
 
 }  // namespace sgb
