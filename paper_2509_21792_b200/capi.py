@@ -26,6 +26,19 @@ if not os.path.exists(LIB_PATH):
                       "(there is no CPU fallback)")
 
 _lib = C.CDLL(LIB_PATH)
+DEV_LIB_PATH = os.path.join(HERE, "libsgrpo_b200_dev.so")
+_dev_lib = None
+
+
+def _dev():
+    """The test-only library (kernel self-tests, microbenchmarks), loaded on first use."""
+    global _dev_lib
+    if _dev_lib is None:
+        if not os.path.exists(DEV_LIB_PATH):
+            raise ImportError(f"{DEV_LIB_PATH} is missing: build it with `python -m paper_2509_21792_b200.build`")
+        _dev_lib = C.CDLL(DEV_LIB_PATH)
+        _dev_lib.sgb_dev_last_error.restype = C.c_char_p
+    return _dev_lib
 
 
 @dataclass
@@ -92,9 +105,13 @@ EXPORTED = ["sgb_last_error", "sgb_version", "sgb_device_count", "sgb_engine_cre
             "sgb_param_counts", "sgb_upload_target", "sgb_upload_draft", "sgb_download_draft", "sgb_init_random",
             "sgb_cache_reset", "sgb_cache_len", "sgb_cache_read", "sgb_cache_gather_tail", "sgb_forward_target",
             "sgb_forward_draft_rows", "sgb_sample_rows", "sgb_topk_logsoftmax", "sgb_build_tree", "sgb_rollout",
-            "sgb_debug_gemm", "sgb_profile_enable", "sgb_profile_read", "sgb_bench_gemm", "sgb_bench_attention",
-            "sgb_debug_attention", "sgb_debug_tree_attention", "sgb_bench_tree_attention", "sgb_group_advantages", "sgb_target_forward_calls",
-            "sgb_debug_group_advantages", "sgb_allgather_f64", "sgb_detect_knee", "sgb_measure_c_peak"]
+            "sgb_profile_enable", "sgb_profile_read", "sgb_group_advantages", "sgb_target_forward_calls",
+            "sgb_allgather_f64", "sgb_detect_knee", "sgb_measure_c_peak"]
+# test-only self-tests / microbenchmarks of libsgrpo_b200_dev.so (include/sgrpo_b200_dev.h)
+DEV_EXPORTED = ["sgb_dev_last_error", "sgb_debug_group_advantages", "sgb_bench_gemm", "sgb_bench_attention",
+                "sgb_debug_attention", "sgb_debug_tree_attention", "sgb_debug_tree_attention_tree",
+                "sgb_bench_tree_attention_tree", "sgb_debug_attention_decode", "sgb_bench_attention_decode",
+                "sgb_bench_overlap", "sgb_bench_tree_attention", "sgb_debug_gemm"]
 
 KERNEL_CLASSES = ["gemm_tcgen05", "attention", "rowops", "lm_head", "sample", "tree", "kv_commit"]
 
@@ -106,12 +123,21 @@ def _check(rc: int):
         raise _EXC.get(rc, RuntimeError)(_lib.sgb_last_error().decode())
 
 
+def _check_dev(rc: int):
+    if rc != 0:
+        raise _EXC.get(rc, RuntimeError)(_dev().sgb_dev_last_error().decode())
+
+
 def _p(a, ct):
     return None if a is None else a.ctypes.data_as(C.POINTER(ct))
 
 
 def lib():
     return _lib
+
+
+def dev_lib():
+    return _dev()
 
 
 def device_count() -> int:
@@ -129,7 +155,7 @@ def debug_attention(q: np.ndarray, k_rows, v_rows, n_heads: int) -> np.ndarray:
     k = np.ascontiguousarray(np.concatenate(k_rows), np.float32)
     v = np.ascontiguousarray(np.concatenate(v_rows), np.float32)
     out = np.zeros((B, d), np.float32)
-    _check(_lib.sgb_debug_attention(B, _p(nk, C.c_int), n_heads, d // n_heads, _p(q, C.c_float), _p(k, C.c_float),
+    _check_dev(_dev().sgb_debug_attention(B, _p(nk, C.c_int), n_heads, d // n_heads, _p(q, C.c_float), _p(k, C.c_float),
                                     _p(v, C.c_float), _p(out, C.c_float)))
     return out
 
@@ -146,7 +172,7 @@ def debug_tree_attention(ctx_len, parents, q, kctx, vctx, knode, vnode, n_heads:
     f = [np.ascontiguousarray(a, np.float32) for a in (kctx, vctx, knode, vnode)]
     o1 = np.zeros((M, d), np.float32)
     o2 = np.zeros((M, d), np.float32)
-    _check(_lib.sgb_debug_tree_attention(len(cl), _p(cl, C.c_int), _p(nr, C.c_int), _p(par, C.c_int), n_heads,
+    _check_dev(_dev().sgb_debug_tree_attention(len(cl), _p(cl, C.c_int), _p(nr, C.c_int), _p(par, C.c_int), n_heads,
                                          d // n_heads, _p(q, C.c_float), *[_p(a, C.c_float) for a in f],
                                          _p(o1, C.c_float), _p(o2, C.c_float)))
     return o1, o2
@@ -167,7 +193,7 @@ def debug_group_advantages(tokens, prompt_lens, answers, g: int, eps_var: float 
     r = np.zeros(n, np.float64)
     a = np.zeros(n, np.float64)
     v = np.zeros(ng, np.int32)
-    _check(_lib.sgb_debug_group_advantages(_p(tab, C.c_int), _p(lens, C.c_int), _p(pl, C.c_int), ng, g, stride,
+    _check_dev(_dev().sgb_debug_group_advantages(_p(tab, C.c_int), _p(lens, C.c_int), _p(pl, C.c_int), ng, g, stride,
                                            _p(ans, C.c_longlong), C.c_double(eps_var), _p(r, C.c_double),
                                            _p(a, C.c_double), _p(v, C.c_int)))
     return r, a, v
@@ -182,7 +208,7 @@ def debug_gemm(w: np.ndarray, x: np.ndarray, splits: int = 0):
     M = x.shape[0]
     out = np.zeros((M, N), np.float32)
     sp = C.c_int(splits)
-    _check(_lib.sgb_debug_gemm(_p(w, C.c_float), _p(x, C.c_float), M, N, K, _p(out, C.c_float), C.byref(sp)))
+    _check_dev(_dev().sgb_debug_gemm(_p(w, C.c_float), _p(x, C.c_float), M, N, K, _p(out, C.c_float), C.byref(sp)))
     return out, sp.value
 
 
@@ -623,7 +649,7 @@ def debug_tree_attention_tree(ctx_len, parents, q, kctx, vctx, knode, vnode, n_h
     par = np.ascontiguousarray(np.concatenate([np.asarray(p, np.int32) for p in parents]), np.int32)
     q = np.ascontiguousarray(q, np.float32)
     out = np.zeros_like(q)
-    _check(_lib.sgb_debug_tree_attention_tree(len(cl), _p(cl, C.c_int), _p(nr, C.c_int), _p(par, C.c_int), n_heads,
+    _check_dev(_dev().sgb_debug_tree_attention_tree(len(cl), _p(cl, C.c_int), _p(nr, C.c_int), _p(par, C.c_int), n_heads,
                                               q.shape[1] // n_heads, _p(q, C.c_float),
                                               _p(np.ascontiguousarray(kctx, np.float32), C.c_float),
                                               _p(np.ascontiguousarray(vctx, np.float32), C.c_float),
@@ -633,7 +659,7 @@ def debug_tree_attention_tree(ctx_len, parents, q, kctx, vctx, knode, vnode, n_h
     return out
 
 
-EXPORTED += ["sgb_debug_tree_attention_tree", "sgb_bench_tree_attention_tree"]
+
 
 
 def debug_attention_decode(ctx_len, q, kctx, vctx, knode, vnode, n_heads: int):
@@ -641,7 +667,7 @@ def debug_attention_decode(ctx_len, q, kctx, vctx, knode, vnode, n_heads: int):
     cl = np.ascontiguousarray(ctx_len, np.int32)
     q = np.ascontiguousarray(q, np.float32)
     o1, o2 = np.zeros_like(q), np.zeros_like(q)
-    _check(_lib.sgb_debug_attention_decode(len(cl), _p(cl, C.c_int), n_heads, q.shape[1] // n_heads, _p(q, C.c_float),
+    _check_dev(_dev().sgb_debug_attention_decode(len(cl), _p(cl, C.c_int), n_heads, q.shape[1] // n_heads, _p(q, C.c_float),
                                            _p(np.ascontiguousarray(kctx, np.float32), C.c_float),
                                            _p(np.ascontiguousarray(vctx, np.float32), C.c_float),
                                            _p(np.ascontiguousarray(knode, np.float32), C.c_float),
@@ -653,22 +679,22 @@ def debug_attention_decode(ctx_len, q, kctx, vctx, knode, vnode, n_heads: int):
 def bench_attention_decode(B: int, ctx: int, n_heads: int, dh: int = 128, iters: int = 20):
     """ms per launch: (attention.cu rows, tree kernel, cluster decode kernel)."""
     r, t, dd = C.c_double(), C.c_double(), C.c_double()
-    _check(_lib.sgb_bench_attention_decode(B, ctx, n_heads, dh, iters, C.byref(r), C.byref(t), C.byref(dd)))
+    _check_dev(_dev().sgb_bench_attention_decode(B, ctx, n_heads, dh, iters, C.byref(r), C.byref(t), C.byref(dd)))
     return r.value, t.value, dd.value
 
 
-EXPORTED += ["sgb_debug_attention_decode", "sgb_bench_attention_decode"]
+
 
 
 def bench_overlap(B: int, ctx: int, n_heads: int, dff: int, M: int, attn_cap: int, gemm_cap: int, dh: int = 128,
                   iters: int = 20):
     """ms per iteration: (attention alone, layer GEMMs alone, both on two streams)."""
     out = (C.c_double * 3)()
-    _check(_lib.sgb_bench_overlap(B, ctx, n_heads, dh, dff, M, attn_cap, gemm_cap, iters, out))
+    _check_dev(_dev().sgb_bench_overlap(B, ctx, n_heads, dh, dff, M, attn_cap, gemm_cap, iters, out))
     return out[0], out[1], out[2]
 
 
-EXPORTED += ["sgb_bench_overlap"]
+
 
 
 class PolicyTermsC(C.Structure):

@@ -8,7 +8,7 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2509_21792_b200 import capi  # noqa: E402
 
-lib = capi.lib()
+lib = capi.dev_lib()
 out = {"env": {k: v for k, v in os.environ.items() if k.startswith("SGB_")}}
 for (B, N, ctx, H) in [(48, 4, 2200, 32), (1, 211, 640, 28), (16, 13, 1100, 28)]:
     a, b, t = C.c_double(), C.c_double(), C.c_double()

@@ -9,7 +9,7 @@ import sys
 sys.path.insert(0, '.')
 from paper_2509_21792_b200 import capi  # noqa: E402
 
-lib = capi.lib()
+lib = capi.dev_lib()
 # B:ctx[:H] (H heads of 128; default 12 = the c2 width, 28 = c3/c4)
 cases = [tuple(int(x) for x in a.split(':')) for a in sys.argv[1:]] or \
     [(512, 128), (512, 640), (512, 1151), (211, 150), (64, 1151), (16, 150), (8, 1151), (1, 150), (1, 1151),
@@ -20,7 +20,7 @@ for case in cases:
     ms = C.c_double()
     rc = lib.sgb_bench_attention(B, ctx, H, 128, 20, C.byref(ms))
     if rc:
-        print("error", lib.sgb_last_error())
+        print("error", lib.sgb_dev_last_error())
         continue
     t = ms.value * 1e-3
     by = B * (ctx + 1) * H * 128 * 2 * 2

@@ -9,7 +9,7 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2509_21792_b200 import capi  # noqa: E402
 
-lib = capi.lib()
+lib = capi.dev_lib()
 for (B, N, ctx) in [(32, 6, 2048), (48, 4, 2048), (48, 4, 4096), (32, 2, 4096), (64, 3, 1024), (48, 8, 2048)]:
     a, b, t = C.c_double(), C.c_double(), C.c_double()
     lib.sgb_bench_tree_attention(B, N, ctx, 32, 128, 10, C.byref(a), C.byref(b))

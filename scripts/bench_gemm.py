@@ -12,7 +12,7 @@ import sys
 sys.path.insert(0, '.')
 from paper_2509_21792_b200 import capi  # noqa: E402
 
-lib = capi.lib()
+lib = capi.dev_lib()
 shapes = [tuple(int(a) for a in s.split('x')) for s in sys.argv[1:]]
 if not shapes:
     for M in (1, 16, 64, 128, 211, 256, 512):
@@ -23,7 +23,7 @@ for M, N, K in shapes:
         ms = C.c_double()
         rc = lib.sgb_bench_gemm(M, N, K, sp, 30, C.byref(ms))
         if rc:
-            print("error", lib.sgb_last_error())
+            print("error", lib.sgb_dev_last_error())
             continue
         t = ms.value * 1e-3
         by = 2 * N * K + 2 * M * K + 4 * M * N

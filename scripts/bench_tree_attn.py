@@ -11,7 +11,7 @@ import sys
 sys.path.insert(0, '.')
 from paper_2509_21792_b200 import capi  # noqa: E402
 
-lib = capi.lib()
+lib = capi.dev_lib()
 shapes = [(1, 211, 640), (1, 211, 1100), (4, 52, 640), (16, 13, 640), (16, 13, 1100), (64, 3, 640), (105, 2, 640)]
 heads = [(28, 128), (12, 128)]
 iters = 20
@@ -24,7 +24,7 @@ for H, dh in heads:
         a, b = C.c_double(), C.c_double()
         rc = lib.sgb_bench_tree_attention(B, N, ctx, H, dh, iters, C.byref(a), C.byref(b))
         if rc:
-            print(json.dumps(dict(H=H, B=B, N=N, ctx=ctx, err=capi.lib().sgb_last_error().decode())))
+            print(json.dumps(dict(H=H, B=B, N=N, ctx=ctx, err=capi.dev_lib().sgb_dev_last_error().decode())))
             continue
         kv = B * (ctx + N) * d * 4
         fl = 4.0 * B * N * (ctx + 4) * d

@@ -8,7 +8,7 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2509_21792_b200 import capi  # noqa: E402
 
-lib = capi.lib()
+lib = capi.dev_lib()
 for (B, N, ctx, H, dh) in [(1, 211, 640, 28, 128), (4, 52, 640, 28, 128), (16, 13, 1100, 28, 128),
                            (48, 4, 2200, 32, 128), (1, 211, 640, 12, 128), (64, 3, 640, 12, 128)]:
     a, b, t = C.c_double(), C.c_double(), C.c_double()

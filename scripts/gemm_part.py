@@ -6,7 +6,7 @@ import sys
 sys.path.insert(0, '.')
 from paper_2509_21792_b200 import capi  # noqa: E402
 
-lib = capi.lib()
+lib = capi.dev_lib()
 for M in (65, 128, 160, 211, 256, 384, 512):
     for N, K in ((1536, 1536), (1536, 8960), (3584, 3584), (3584, 18944)):
         r = {}

@@ -7,7 +7,7 @@ import sys
 sys.path.insert(0, '.')
 from paper_2509_21792_b200 import capi  # noqa: E402
 
-lib = capi.lib()
+lib = capi.dev_lib()
 for K in (512, 1536, 4096, 8960):
     for tiles in (1, 8, 37, 74, 148):
         ms = C.c_double()

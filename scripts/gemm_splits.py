@@ -1,7 +1,7 @@
 import ctypes as C, json, sys
 sys.path.insert(0, '.')
 from paper_2509_21792_b200 import capi
-lib = capi.lib()
+lib = capi.dev_lib()
 for M, N, K in [(1, 10752, 3584), (1, 3584, 18944), (1, 3584, 3584), (1, 18944, 3584), (1, 4608, 1536), (1, 8960, 1536), (1, 1536, 8960), (8, 10752, 3584), (8, 3584, 18944)]:
     row = []
     for sp in (1, 2, 3, 4, 5, 6, 8, 12):

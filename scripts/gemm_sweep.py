@@ -8,7 +8,7 @@ import sys
 sys.path.insert(0, '.')
 from paper_2509_21792_b200 import capi  # noqa: E402
 
-lib = capi.lib()
+lib = capi.dev_lib()
 var = os.path.basename(os.environ.get("SGB_LIB", "default"))
 tot = {}
 for M in (1, 16, 160, 211, 512):

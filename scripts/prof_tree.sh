@@ -9,7 +9,7 @@ sys.path.insert(0, ".")
 from paper_2509_21792_b200 import capi
 B, N, ctx, H = (int(x) for x in sys.argv[1:5])
 t = C.c_double()
-capi.lib().sgb_bench_tree_attention_tree(B, N, ctx, H, 128, 3, C.byref(t))
+capi.dev_lib().sgb_bench_tree_attention_tree(B, N, ctx, H, 128, 3, C.byref(t))
 print(t.value)
 PY
 for shape in "1 211 640 28" "48 4 2200 32"; do

@@ -35,6 +35,24 @@ def test_library_exports_every_declared_symbol():
     assert lib.sgb_version() == 1
 
 
+DEV_HEADER = os.path.join(ROOT, "include", "sgrpo_b200_dev.h")
+
+
+def test_test_only_entry_points_live_outside_the_product_library():
+    """Kernel self-tests and microbenchmarks are in libsgrpo_b200_dev.so (sgrpo_b200_dev.h),
+    not in the drop-in library."""
+    from paper_2509_21792_b200 import capi
+    src = open(DEV_HEADER).read()
+    dev = sorted(set(re.findall(r"\b(?:int|const char\*)\s+(sgb_\w+)\s*\(", src)))
+    assert "sgb_bench_gemm" in dev and "sgb_debug_attention" in dev
+    assert not set(dev) & set(declared())
+    assert sorted(capi.DEV_EXPORTED) == dev
+    dl = C.CDLL(capi.DEV_LIB_PATH)
+    assert all(hasattr(dl, n) for n in dev)
+    prod = C.CDLL(capi.LIB_PATH)
+    assert not any(hasattr(prod, n) for n in dev if n != "sgb_dev_last_error")
+
+
 def test_no_cpu_fallback_without_gpu():
     from paper_2509_21792_b200 import capi
     try:
