@@ -67,7 +67,7 @@ def launch_list(path):
         if d["Metric Name"] != "gpu__time_duration.sum":
             continue
         v = float(d["Metric Value"].replace(",", ""))
-        v *= {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(d["Metric Unit"], 1.0)
+        v *= {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(d["Metric Unit"], 1.0)
         name = d["Kernel Name"].split("(")[0].replace("void ", "").replace("(anonymous namespace)::", "")
         recs[d["ID"]] = (name, v)
     agg = collections.defaultdict(lambda: [0, 0.0])
