@@ -40,14 +40,17 @@ for B in [int(x) for x in (args or ["1", "4", "16", "64"])]:
         rp = eng.generate(pr, 1, mode=mode, **kw)
         eng.profile(False)
         prof = eng.read_profile(reset=True)
-        # prefill alone (no decode step), profiled: subtracted so the classes are decode-only
+        # prefill alone (no decode step), profiled: subtracted so the classes are decode-only;
+        # with --ctx also the first decode step (the draft's catch-up over the long prompt)
+        base_new = 2 if ctx_arg else 1
         eng.profile(True)
-        eng.generate(pr, 1, mode=mode, **dict(kw, max_new_tokens=1))
+        eng.generate(pr, 1, mode=mode, **dict(kw, max_new_tokens=base_new))
         eng.profile(False)
         pre = eng.read_profile(reset=True)
         n = len(r.steps)
         dec_s = sum(r.step_seconds) if r.step_seconds else r.seconds
-        cls = {k: round((v["ms"] - pre.get(k, {}).get("ms", 0.0)) / n, 3) for k, v in prof.items()}
+        cls = {k: round((v["ms"] - pre.get(k, {}).get("ms", 0.0)) / max(1, n - (base_new - 1)), 3)
+               for k, v in prof.items()}
         med = sorted(r.step_seconds)[n // 2] if r.step_seconds else dec_s / n
         # median: with --ctx the first speculative step carries the draft's catch-up over the whole
         # long prompt (a prefill-like cost the real workloads' 128-token prompts do not have)
