@@ -24,6 +24,9 @@
 // attention.cu's boundary tiles), its key rows gathered per lane by ldmatrix addresses: prefix
 // keys from the staged ring, path keys from the node table.
 #include <algorithm>
+#include <array>
+#include <cstdlib>
+#include <vector>
 #include <cfloat>
 
 #include <cooperative_groups.h>
@@ -43,6 +46,10 @@ constexpr int kTBlock = kAttnBlock;  // 64 keys per softmax partial
 constexpr int kTChunk = 16;          // keys per staged chunk
 constexpr int kTMaxWarps = 8;        // consumer warps (8 query rows each)
 constexpr int kTSmem = 227 * 1024;
+#ifndef SGB_TREE_ONE_WARP_CTAS
+#define SGB_TREE_ONE_WARP_CTAS 7
+#endif
+constexpr int kTOneWarpCtas = SGB_TREE_ONE_WARP_CTAS;  // CTAs per SM of the one-warp tree kernel
 
 SGB_DEV void ldsm_x4(uint32_t addr, uint32_t* r) {
     asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -84,8 +91,11 @@ SGB_DEV uint32_t ring_addr(uint32_t stage, int kr, int dd) {
     return stage + static_cast<uint32_t>(box * 2048 + kr * 128 + ((u ^ (kr & 7)) << 4));
 }
 
-template <int DH>
-__global__ void __launch_bounds__(32 * (kTMaxWarps + 1), 1)
+// MAXW: the consumer warps a launch may use. The one-warp instantiation (tiles of <= 8 rows, the
+// c5 verify shape: 4 rows per sequence) is register-capped so that 7 CTAs fit an SM (with 168
+// registers 6 did, and 1,024 CTAs took 1.15 waves); the code and so the bits are the same
+template <int DH, int MAXW>
+__global__ void __launch_bounds__(32 * (MAXW + 1), MAXW == 1 ? kTOneWarpCtas : 1)
     tree_attn_kernel(const float* __restrict__ q, const __grid_constant__ CUtensorMap kmap,
                      const __grid_constant__ CUtensorMap vmap, long long layer_row0, const __nv_bfloat16* __restrict__ K,
                      const __nv_bfloat16* __restrict__ V, AttnRowsDev rows, const TreeGroupDev* __restrict__ groups,
@@ -663,11 +673,42 @@ void launch_tree_impl(const float* q, const CUtensorMap& kmap, const CUtensorMap
     if (smem > static_cast<size_t>(kTSmem)) throw std::invalid_argument("tree attention: tree too large for shared memory");
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(tree_attn_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTSmem);
+        cudaFuncSetAttribute(tree_attn_kernel<DH, kTMaxWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTSmem);
+        cudaFuncSetAttribute(tree_attn_kernel<DH, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTSmem);
         attr = true;
     }
-    launch_pdl(tree_attn_kernel<DH>, dim3(n_tiles, H), dim3(32 * (W + 1)), smem, st, q, kmap, vmap, layer_row0, K, V,
-               rows, groups, tiles, d, nst, max_nodes, 1.0f / sqrtf(static_cast<float>(DH)), out);
+    static const int one_warp = [] {
+        const char* v = getenv("SGB_TREE_ONE_WARP");  // A/B: 0 = never, 1 = always (W == 1), -1 = by waves
+        return v ? atoi(v) : -1;
+    }();
+    // the register-capped one-warp variant fits more CTAs per SM but runs each CTA ~1.25-1.5x
+    // slower (spills, shared bandwidth): measured (profiles/r02_tree_onewarp_ab.txt) it pays only
+    // when it saves a whole wave (c5 verify at B = 32: 1,024 CTAs, 2 waves -> 1: 0.254 -> 0.191 ms
+    // per layer; at B = 48, 2 waves either way: 0.275 -> 0.344), so it is taken when it does
+    bool use_one = false;
+    if (W == 1 && one_warp != 0) {
+        use_one = one_warp > 0;
+        if (one_warp < 0) {
+            static std::vector<std::array<int, 3>> occ_cache;  // (smem, CTAs/SM 8-warp, CTAs/SM one-warp)
+            std::array<int, 3>* hit = nullptr;
+            for (auto& c : occ_cache)
+                if (c[0] == static_cast<int>(smem)) hit = &c;
+            if (!hit) {
+                int a = 0, b = 0;
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, tree_attn_kernel<DH, kTMaxWarps>, 64, smem);
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, tree_attn_kernel<DH, 1>, 64, smem);
+                occ_cache.push_back({static_cast<int>(smem), std::max(1, a), std::max(1, b)});
+                hit = &occ_cache.back();
+            }
+            const long long ctas = static_cast<long long>(n_tiles) * H;
+            const long long wa = (ctas + 148LL * (*hit)[1] - 1) / (148LL * (*hit)[1]);
+            const long long wb = (ctas + 148LL * (*hit)[2] - 1) / (148LL * (*hit)[2]);
+            use_one = wb < wa;
+        }
+    }
+    auto kern = use_one ? tree_attn_kernel<DH, 1> : tree_attn_kernel<DH, kTMaxWarps>;
+    launch_pdl(kern, dim3(n_tiles, H), dim3(32 * (W + 1)), smem, st, q, kmap, vmap, layer_row0, K, V, rows, groups,
+               tiles, d, nst, max_nodes, 1.0f / sqrtf(static_cast<float>(DH)), out);
 }
 
 }  // namespace

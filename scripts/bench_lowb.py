@@ -4,7 +4,7 @@ second, profiled run gives the per-class split (events around every launch infla
 times are the engine's per-decode-step CUDA-event times (prefill excluded); the class split
 subtracts a profiled prefill-only run.
 
-    python scripts/bench_lowb.py [B ...] [--ncu] [--config=c3|c3r|c5] [--vanilla] [--ctx=N]
+    python scripts/bench_lowb.py [B ...] [--ncu] [--config=c3|c3r|c5] [--vanilla] [--ctx=N] [--cpeak=C]
       (--ncu: one short run per mode, for ncu; --vanilla: AR steps only)
 """
 import json
@@ -20,6 +20,7 @@ conf = next((a.split("=", 1)[1] for a in sys.argv[1:] if a.startswith("--config=
 modes = ("vanilla",) if "--vanilla" in sys.argv else ("vanilla", "adaptive_spec")
 w = dict(WORKLOADS[conf])
 ctx_arg = next((int(a.split("=", 1)[1]) for a in sys.argv[1:] if a.startswith("--ctx=")), 0)
+c_peak = next((int(a.split("=", 1)[1]) for a in sys.argv[1:] if a.startswith("--cpeak=")), 211)
 if ctx_arg:
     w["P"] = ctx_arg  # long prompts stand in for a long generated context
 w["new"] = 64  # the engine's max_seq_len = P + new: keep the KV store small
@@ -30,7 +31,7 @@ prompts = make_prompts(w, 0)
 for B in [int(x) for x in (args or ["1", "4", "16", "64"])]:
     pr = prompts[:B]
     for mode in modes:
-        kw = dict(c_peak=211, temperature=w.get("temp", 0.0), seed=7, max_new_tokens=8 if ncu else 48,
+        kw = dict(c_peak=c_peak, temperature=w.get("temp", 0.0), seed=7, max_new_tokens=8 if ncu else 48,
                   want_features=False, acceptance=w.get("acceptance", "strict"))
         eng.generate(pr, 1, mode=mode, **kw)  # warm
         if ncu:
