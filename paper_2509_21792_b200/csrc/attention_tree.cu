@@ -26,6 +26,7 @@
 #include <algorithm>
 #include <array>
 #include <cstdlib>
+#include <mutex>
 #include <vector>
 #include <cfloat>
 
@@ -689,20 +690,24 @@ void launch_tree_impl(const float* q, const CUtensorMap& kmap, const CUtensorMap
     if (W == 1 && one_warp != 0) {
         use_one = one_warp > 0;
         if (one_warp < 0) {
+            static std::mutex mu;
             static std::vector<std::array<int, 3>> occ_cache;  // (smem, CTAs/SM 8-warp, CTAs/SM one-warp)
-            std::array<int, 3>* hit = nullptr;
-            for (auto& c : occ_cache)
-                if (c[0] == static_cast<int>(smem)) hit = &c;
-            if (!hit) {
-                int a = 0, b = 0;
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, tree_attn_kernel<DH, kTMaxWarps>, 64, smem);
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, tree_attn_kernel<DH, 1>, 64, smem);
-                occ_cache.push_back({static_cast<int>(smem), std::max(1, a), std::max(1, b)});
-                hit = &occ_cache.back();
+            std::array<int, 3> occ{0, 0, 0};
+            {
+                std::lock_guard<std::mutex> lock(mu);
+                for (const auto& c : occ_cache)
+                    if (c[0] == static_cast<int>(smem)) occ = c;
+                if (occ[1] == 0) {
+                    int a = 0, b = 0;
+                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, tree_attn_kernel<DH, kTMaxWarps>, 64, smem);
+                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, tree_attn_kernel<DH, 1>, 64, smem);
+                    occ = {static_cast<int>(smem), std::max(1, a), std::max(1, b)};
+                    occ_cache.push_back(occ);
+                }
             }
             const long long ctas = static_cast<long long>(n_tiles) * H;
-            const long long wa = (ctas + 148LL * (*hit)[1] - 1) / (148LL * (*hit)[1]);
-            const long long wb = (ctas + 148LL * (*hit)[2] - 1) / (148LL * (*hit)[2]);
+            const long long wa = (ctas + 148LL * occ[1] - 1) / (148LL * occ[1]);
+            const long long wb = (ctas + 148LL * occ[2] - 1) / (148LL * occ[2]);
             use_one = wb < wa;
         }
     }
