@@ -24,7 +24,8 @@ int sgb_bench_attention(int B, int ctx, int H, int dh, int iters, double* ms_out
 int sgb_debug_attention(int B, const int* n_keys, int H, int dh, const float* q, const float* k, const float* v,
                         float* out);
 
-/* The same on host token tables ([n_groups*g][stride], lens / prompt_lens per sequence). */
+/* sgb_group_advantages (sgrpo_b200.h) on host token tables ([n_groups*g][stride], lens / prompt_lens
+ * per sequence). */
 int sgb_debug_group_advantages(const int* tokens, const int* lens, const int* prompt_lens, int n_groups, int g,
                                int stride, const long long* answers, double eps_var, double* rewards,
                                double* advantages, int* valid);
