@@ -9,6 +9,7 @@
 // one small per-sequence result vector per step.
 #include <algorithm>
 #include <chrono>
+#include <optional>
 #include <cstdlib>
 #include <cstring>
 #include <thread>
@@ -1120,6 +1121,7 @@ void Engine::reject_alloc() {
 
 // ------------------------------------------------------------------ the rollout
 RolloutResult Engine::rollout(const RolloutArgs& a) {
+    NvtxRange nv_rollout("sgb rollout");
     const ModelDims& mc = dims_;
     const int d = mc.d, V = mc.vocab, T = mc.max_seq;
     // validation (scheduler.cpp:240-249)
@@ -1327,6 +1329,7 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
 
     // admit pending query groups into free region blocks, then prefill them
     auto admit = [&]() {
+        NvtxRange nv_admit("sgb admit + prefill");
         std::vector<std::pair<int, int>> adm;
         for (int gs = 0; gs < n_gslots && next_group < P; ++gs) {
             if (gslot_group[gs] >= 0) continue;
@@ -1369,6 +1372,7 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
         const int B = static_cast<int>(live.size());
         if (B == 0) break;  // (pending groups are admitted at the end of the step that frees regions)
         const auto t_host0 = std::chrono::steady_clock::now();
+        NvtxRange nv_step("sgb step");
         const int eff_b = a.early_term ? B : n_seqs;
         SpecCfg cfg;
         if (a.mode == 0) cfg = SpecCfg{1, 0, 0};
@@ -1411,6 +1415,7 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
         stat.l_draft = cfg.l_draft;
         stat.rows = vrows;
 
+        std::optional<NvtxRange> nv_phase(std::in_place, n_spec > 0 ? "sgb draft" : "sgb plan");
         if (n_spec > 0) {
             // ---- draft catch-up over committed pairs (t_j, f_{j-1}), j = dft_len+1..p (scheduler.cpp:137-157)
             struct CU {
@@ -1588,6 +1593,8 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
         }
 
         // ---- rerank + mask -> verify rows; one batched target forward (scheduler.cpp:208-217)
+        nv_phase.reset();
+        nv_phase.emplace("sgb verify");
         int pe0 = pbeg();
         launch_tree_select(B, steps_, ss_, tr_, rows_, tkv_.seq_stride, tkv_.scratch_base, nullptr, err_, st_);
         pend(kClsTree, pe0, 0, 0);
@@ -1675,6 +1682,8 @@ RolloutResult Engine::rollout(const RolloutArgs& a) {
         forward(f);
         res.target_forwards++;
         // ---- acceptance, walk, commit (scheduler.cpp:219-231)
+        nv_phase.reset();
+        nv_phase.emplace("sgb accept");
         pe0 = pbeg();
         launch_emit(logits_, V, nullptr, rows_.seed, rows_.key_pos, vrows, a.temperature, emitted_, err_, rsc_, st_);
         count(emit_launches(a.temperature) - 1);

@@ -154,6 +154,7 @@ void Engine::policy_refresh_ref_weights() {
 }
 
 Engine::PolicyTerms Engine::policy_update(const PolicyArgs& A) {
+    NvtxRange nv("sgb policy_update");
     if (!target_ready_) throw std::runtime_error("weights not uploaded");
     policy_alloc();
     Pol& p = pol_;

@@ -182,6 +182,7 @@ void Engine::wgrad(const __nv_bfloat16* dyT, int N, const __nv_bfloat16* xT, int
 }
 
 Engine::DraftLossTerms Engine::draft_update(const DraftUpdateArgs& A) {
+    NvtxRange nv("sgb draft_update");
     if (!target_ready_ || !draft_ready_) throw std::runtime_error("weights not uploaded");
     train_alloc();
     Train& t = tr2_;

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <stdexcept>
 #include <string>
@@ -26,6 +27,15 @@ struct CudaError : std::runtime_error {
 inline void cuda_check(cudaError_t e, const char* what) {
     if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
 }
+
+// NVTX ranges around the engine's phases (rollout, prefill, step, draft, verify, accept,
+// draft / policy update): visible in Nsight Systems / Compute timelines, a no-op without a tool
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 #define SGB_CUDA(x) ::sgb::cuda_check((x), #x)
 #define SGB_KCHECK() ::sgb::cuda_check(cudaGetLastError(), "kernel launch")
