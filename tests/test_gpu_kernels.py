@@ -47,6 +47,22 @@ def test_gemm_batch_invariance():
             assert np.array_equal(part, full[:m]), (m, s)
 
 
+@pytest.mark.parametrize("tiles", [84, 96, 112])
+def test_gemm_wide_single_chunk_batch_invariance(tiles):
+    """Single-chunk weights of 84-112 tiles (the 7B / 8B QKV and w1 shapes) at every token-tile
+    width (16 .. 256-token tiles, partial tiles): every row's bits equal the same row computed at
+    any other row count."""
+    c = capi()
+    rng = np.random.default_rng(tiles)
+    N, K = 128 * tiles, 256
+    w = rng.standard_normal((N, K)).astype(np.float32) * 0.05
+    x = rng.standard_normal((300, K)).astype(np.float32)
+    full, _ = c.debug_gemm(w, x)
+    for m in (1, 16, 129, 160, 192, 211, 240, 256):
+        part, _ = c.debug_gemm(w, x[:m])
+        assert np.array_equal(part, full[:m]), m
+
+
 def test_forward_target_matches_oracle():
     e, m, _ = make_engine(SMALL)
     toks = [2, 9, 4, 13, 6, 3, 7, 12, 200, 31]
