@@ -128,8 +128,11 @@ __global__ void __launch_bounds__(kRowThreads) embed_ln_kernel(const int* __rest
 
 // x = (mode==0 ? 0 : x) + sum_s P[s][r] (+ pos_emb[pos[r]]); then LN -> a (bf16) / y (fp32).
 // FR: chunks loaded in the first round (with the residual row); CPR per later round.
-template <int PER, int FR = 4>
-__global__ void __launch_bounds__(kRowThreads)
+// LATE: gamma / beta read at the end (block_ln, identical bits) instead of held in registers from
+// before the PDL wait, and two CTAs per SM: for launches of many waves of rows at d >= 3584, where
+// the register-resident variant (142-167 registers) runs one CTA per SM
+template <int PER, int FR = 4, bool LATE = false>
+__global__ void __launch_bounds__(kRowThreads, LATE ? 2 : 1)
     reduce_residual_ln_kernel(const float* __restrict__ P, int S, int M, int d, float* __restrict__ x, int accumulate,
                               const float* __restrict__ pos_emb, const int* __restrict__ positions,
                               const float* __restrict__ g, const float* __restrict__ b, __nv_bfloat16* __restrict__ a,
@@ -138,8 +141,8 @@ __global__ void __launch_bounds__(kRowThreads)
     // LN parameters are weights, never written by the previous kernel: load them before the
     // PDL wait, so that a one-row launch (the decode tail) pays one dependent round trip for
     // partials + residual instead of four
-    float gs[PER], bs[PER];
-    if (g) {
+    float gs[LATE ? 1 : PER], bs[LATE ? 1 : PER];
+    if (g && !LATE) {
 #pragma unroll
         for (int i = 0; i < PER; ++i) {
             const int e = threadIdx.x + i * kRowThreads;
@@ -240,9 +243,14 @@ __global__ void __launch_bounds__(kRowThreads)
             xs[i] = e < d ? x[row + e] : 0.f;  // plain LayerNorm of the residual stream
         }
     }
-    if (g)
-        block_ln_regs<PER>(xs, d, gs, bs, a ? a + static_cast<size_t>(r) * d : nullptr,
-                           y ? y + static_cast<size_t>(r) * d : nullptr, red);
+    if (g) {
+        if constexpr (LATE)
+            block_ln<PER>(xs, d, g, b, a ? a + static_cast<size_t>(r) * d : nullptr,
+                          y ? y + static_cast<size_t>(r) * d : nullptr, red);
+        else
+            block_ln_regs<PER>(xs, d, gs, bs, a ? a + static_cast<size_t>(r) * d : nullptr,
+                               y ? y + static_cast<size_t>(r) * d : nullptr, red);
+    }
 }
 
 __device__ __forceinline__ float gelu_tanh(float x) {
@@ -408,15 +416,28 @@ void launch_reduce_residual_ln(const float* P, int S, int M, int d, float* x, bo
         else launch_pdl(reduce_residual_ln_kernel<6> ARGS);
     }
     else if (d <= 2048) launch_pdl(reduce_residual_ln_kernel<8> ARGS);
-    else if (d <= 3584) {
-        static const int fr14 = [] {
-            const char* v = getenv("SGB_ROW_FR14");  // A/B: 5 = the 7B wo / w2 partials in one trip
-            return v ? atoi(v) : 4;
+    else if (d <= 4096) {
+        // many waves of rows (prefill chunks): the two-CTA-per-SM LATE variant (same bits).
+        // Measured (profiles/r02_row_late_ab.txt, c5 width): 2,048 rows 66.5 -> 51.2 us, but
+        // 151-256 rows 10.7-11.6 -> 14.1-14.5 us, so it starts at 1,024 rows
+        static const int late_env = [] {
+            const char* v = getenv("SGB_ROW_LATE");  // A/B: 0 = never, N = from N rows
+            return v ? atoi(v) : 1024;
         }();
-        if (fr14 >= 5) launch_pdl(reduce_residual_ln_kernel<14, 5> ARGS);
-        else launch_pdl(reduce_residual_ln_kernel<14> ARGS);
+        const bool late = late_env > 0 && M >= late_env;
+        if (d <= 3584) {
+            static const int fr14 = [] {
+                const char* v = getenv("SGB_ROW_FR14");  // A/B: 5 = the 7B wo / w2 partials in one trip
+                return v ? atoi(v) : 4;
+            }();
+            if (late) launch_pdl(reduce_residual_ln_kernel<14, 4, true> ARGS);
+            else if (fr14 >= 5) launch_pdl(reduce_residual_ln_kernel<14, 5> ARGS);
+            else launch_pdl(reduce_residual_ln_kernel<14> ARGS);
+        } else {
+            if (late) launch_pdl(reduce_residual_ln_kernel<16, 4, true> ARGS);
+            else launch_pdl(reduce_residual_ln_kernel<16> ARGS);
+        }
     }
-    else if (d <= 4096) launch_pdl(reduce_residual_ln_kernel<16> ARGS);
     else launch_pdl(reduce_residual_ln_kernel<kMaxPerThread> ARGS);
 #undef ARGS
     SGB_KCHECK();
