@@ -719,6 +719,11 @@ void launch_tree_impl(const float* q, const CUtensorMap& kmap, const CUtensorMap
 }  // namespace
 
 int tree_attn_warps(int max_rows_per_group, int n_groups, int H, int dh, int max_nodes) {
+    static const int w_env = [] {
+        const char* v = getenv("SGB_TREE_W");  // A/B: consumer warps (8-row groups) per tile
+        return v ? atoi(v) : 0;
+    }();
+    if (w_env > 0) return std::min(kTMaxWarps, std::max(1, std::min(w_env, (max_rows_per_group + 7) / 8)));
     // widest tiles (the prefix streams once per tile) unless narrower ones finish in fewer waves
     // (CTAs resident per SM are bounded by the node table + ring in shared memory)
     const size_t tbl = static_cast<size_t>(max_nodes) * (dh * 2 + 16) * 2;
