@@ -20,6 +20,7 @@ unmodified reference sources compiled here) on the host cores.
 from __future__ import annotations
 
 import argparse
+import collections
 import json
 import os
 import statistics
@@ -278,11 +279,14 @@ def per_b_table(rs, ra):
         out = {}
         for (b, n, k, l, acc), sec in zip(r.steps, r.step_seconds):
             lo = 1 << (max(1, b).bit_length() - 1)  # power-of-two bucket [lo, 2lo)
-            e = out.setdefault(lo, [0, 0.0, 0, 0, (n, k, l)])
+            e = out.setdefault(lo, [0, 0.0, 0, 0, collections.Counter()])
             e[0] += 1
             e[1] += sec
             e[2] += acc
             e[3] += b
+            e[4][(n, k, l)] += 1
+        for e in out.values():
+            e[4] = e[4].most_common(1)[0][0]  # the bucket's most frequent (N, K, L) plan
         return out
     bs, ba = buckets(rs), buckets(ra)
     rows = []
