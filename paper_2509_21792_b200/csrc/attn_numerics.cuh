@@ -26,10 +26,14 @@ constexpr int kAttnBlock = 64;  // keys per softmax partial (part of the numeric
 
 SGB_DEV float attn_scale(float dot, float scale) { return __fmul_rn(dot, scale); }
 
+// The per-chunk exponentials use the SFU (__expf: ex2.approx of x * log2 e, ~2 ulp): six per chunk
+// sit on every consumer warp's dependent chain, and the latency-bound small-B kernels run that
+// chain ~50 times per launch. Every inference attention kernel takes them from here, so their
+// bits stay identical to each other (batch invariance); the block merges keep expf.
 // exp(m_old - m_new), 0 for the fresh state
-SGB_DEV float attn_alpha(float m_old, float m_new) { return m_old == -INFINITY ? 0.f : expf(__fsub_rn(m_old, m_new)); }
+SGB_DEV float attn_alpha(float m_old, float m_new) { return m_old == -INFINITY ? 0.f : __expf(__fsub_rn(m_old, m_new)); }
 
-SGB_DEV float attn_p(float s, float m_new) { return expf(__fsub_rn(s, m_new)); }
+SGB_DEV float attn_p(float s, float m_new) { return __expf(__fsub_rn(s, m_new)); }
 
 SGB_DEV float attn_l(float l, float alpha, float psum) { return fmaf(l, alpha, psum); }
 
